@@ -1,0 +1,186 @@
+/*
+ * adafuse_b200.h -- C ABI of the B200-native AdaFuse hot path.
+ *
+ * The reference (`lorafuse`, pure Python/numpy) has no FFI of its own;
+ * the boundary it exposes is its Python call surface.  Each entry point below names the
+ * reference function it replaces (paths relative to /root/reference/pkg/src/lorafuse/).
+ * The Python host (`paper_2603_11873_b200`) binds these with ctypes; INTEGRATION.md shows
+ * the stub a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every device buffer is OWNED BY THE CALLER
+ *     (the library owns only the table objects it creates and their TMA maps);
+ *   - every call returns an int status (AF_OK == 0); no exceptions, no aborts; the
+ *     message of the last failure on this thread is af_last_error();
+ *   - validation happens BEFORE any data is touched (linalg.py:323-325, routing.py:57-62);
+ *   - all work is enqueued on the caller's `stream` (a cudaStream_t passed as void*);
+ *     no call synchronises unless it says so;
+ *   - matrices are row-major; `ld` is the row pitch in ELEMENTS.
+ */
+#ifndef ADAFUSE_B200_H
+#define ADAFUSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AF_ABI_VERSION 1
+
+/* ---- status codes: one per reference exception class (errors.py:8-33) ---- */
+#define AF_OK 0
+#define AF_EVALUE 1      /* ValueError      bad sign / k / enum                       */
+#define AF_EDIM 2        /* DimensionError  shapes disagree, empty table               */
+#define AF_EPRECISION 3  /* PrecisionError  unsupported / mixed dtype tags             */
+#define AF_EALIAS 4      /* AliasingError   two segments share / overlap one target    */
+#define AF_EINPUT 5      /* InputError      token outside the vocabulary               */
+#define AF_ESTATE 6      /* StateError      missing state (no pristine copy, ...)      */
+#define AF_EINDEX 7      /* IndexError      expert id outside the bank                 */
+#define AF_ECUDA 8       /* a CUDA runtime/driver call failed (message has the code)   */
+
+/* ---- element types ---- */
+#define AF_BF16 0
+#define AF_F32 1
+
+/* ---- fused-switch options ---- */
+#define AF_SWITCH_INPLACE 0       /* W <- W + dNew - dOld   (model.py:350-357)            */
+#define AF_SWITCH_FROM_PRISTINE 1 /* W <- W0 + dNew         (refresh, model.py:308-312, fused with the merge) */
+
+#define AF_COMPUTE_AUTO 0  /* library picks FMA or MMA from the effective rank          */
+#define AF_COMPUTE_EXACT 1 /* reference order: per rank (mul, round)(add, round); bit-exact vs linalg.py:338-343 in f32 */
+#define AF_COMPUTE_FMA 2   /* f32 FMA on CUDA cores, repeated experts collapsed         */
+#define AF_COMPUTE_MMA 3   /* B.(g*A) on the tensor pipe: g*A kept f32-accurate as a bf16 hi+lo pair, f32 accumulate */
+
+#define AF_MAX_K 8 /* experts per decision (top-k <= 8) */
+
+/* GEMV epilogues */
+#define AF_EPI_NONE 0
+#define AF_EPI_GELU_RESIDUAL 1 /* out = res + 0.5*y*(1+erf(y/sqrt2))   (model.py:298,305) */
+#define AF_EPI_RESIDUAL 2      /* out = res + y                                          */
+
+/* routing.py:37-46 `GateDecision`, device/host POD form.  ids ordered by descending
+ * logit, ties by ascending index; weights > 0, sum to 1 (f32). */
+typedef struct af_decision {
+    int32_t k;
+    int32_t ids[AF_MAX_K];
+    float weights[AF_MAX_K];
+    int32_t reserved[15]; /* pads the record to 128 bytes */
+} af_decision;
+
+/* linalg.py:183-217 `Segment`, as addresses.  One adapted matrix and the factors that
+ * can update it.  Two uses:
+ *   bank form        (adapters.py:71-109 `ExpertBank`): down = [N][rank][d_in],
+ *                    up = [N][d_out][rank]; the per-token (expert, weight) list selects blocks;
+ *   materialised form (adapters.py:117-162 `ConcatAdapter`): n_experts = 1,
+ *                    down = s x d_in, up = d_out x s, rank = s. */
+typedef struct af_segment_desc {
+    void* target;         /* d_out x d_in, mutated in place (linalg.py:336-343)          */
+    const void* pristine; /* optional untouched copy (model.py:153), same shape/pitch    */
+    const void* down;     /* LoraExpert.down blocks (adapters.py:53)                      */
+    const void* up;       /* LoraExpert.up blocks   (adapters.py:54)                      */
+    int32_t d_out;
+    int32_t d_in;
+    int32_t rank;         /* rows of one down block; 0 is legal (no-op, linalg.py:190)    */
+    int32_t n_experts;
+    int64_t ld_target;    /* elements                                                    */
+    int64_t ld_down;      /* row pitch of a down block (elements)                        */
+    int64_t ld_up;        /* row pitch of an up block (elements)                         */
+    int64_t down_expert_stride; /* elements between consecutive experts' down blocks      */
+    int64_t up_expert_stride;   /* elements between consecutive experts' up blocks        */
+} af_segment_desc;
+
+typedef struct af_table af_table; /* linalg.py:207-231 `SegmentTable`, device resident */
+
+/* ---- library ---- */
+int af_abi_version(void);
+const char* af_last_error(void);
+/* Fills what the caller asks for (any pointer may be NULL). */
+int af_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_bytes);
+/* Number of kernel launches issued by this library since load (bench `gpu_launches`). */
+int64_t af_launch_count(void);
+
+/* ---- segment table: built once at model load -------------------------------------
+ * Replaces: linalg.py:207-231 `SegmentTable` + `.validate()` (shape, precision and
+ * distinct-target checks) and the per-token Segment construction of adapters.py:252-257.
+ * Builds the device-side descriptor table (segments + work units) and one TMA tensor
+ * map per segment.  Errors: AF_EDIM (empty table, bad shapes), AF_EPRECISION (dtype),
+ * AF_EALIAS (two targets overlap). */
+int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t target_dtype,
+                    int32_t factor_dtype, af_table** out);
+int af_table_destroy(af_table* table);
+/* n_units: persistent-kernel work units; fast_path: 1 if the TMA kernel applies. */
+int af_table_info(const af_table* table, int32_t* n_segments, int64_t* target_elems,
+                  int32_t* n_units, int32_t* fast_path);
+/* Device-side validation result of the launches issued on `stream` so far (SYNCHRONISES the
+ * stream): 0, or the AF_E* code a kernel raised because a device-resident decision named an
+ * expert outside the bank (adapters.py:199-200) or carried more than max_k experts; the
+ * offending launch touched nothing.  Reading clears the flag. */
+int af_table_status(af_table* table, void* stream);
+
+/* ---- pre-gating router --------------------------------------------------------------
+ * Replaces: routing.py:49-78 `route` / routing.py:81-89 `pre_gate`, fused with the row
+ * gather of model.py:248-258 `_embed_token` when `token_dev` is given.
+ *   router_w : N x d (bf16 or f32), row-major, read-only
+ *   x        : d-vector (x_dtype); if token_dev != NULL, x is the embedding TABLE and the
+ *              routed vector is row *token_dev of it (token range is the caller's check)
+ *   out_dev  : af_decision in device memory (consumed by af_fused_switch without a host
+ *              round trip); logits_dev optional N floats
+ * Errors: AF_EVALUE when k is outside [1, min(N, AF_MAX_K)] (routing.py:57-58). */
+int af_pregate(const void* router_w, int32_t w_dtype, int32_t n_experts, int32_t d, const void* x,
+               int32_t x_dtype, const int32_t* token_dev, int32_t k, af_decision* out_dev,
+               float* logits_dev, void* stream);
+
+/* ---- fused switch -------------------------------------------------------------------
+ * Replaces: per token, adapters.py:188-211 `concat_gated` x L, adapters.py:214-233
+ * `build_switch` x L and adapters.py:236-258 `merge_all` -> linalg.py:306-346 `sgmm`
+ * (model.py:350-357): ONE persistent launch over every segment of the table.
+ *   prev_dev / cur_dev : device decisions; NULL = empty concat (first token / final
+ *                        unmerge, adapters.py:150-156).
+ *   prev_host/cur_host : alternative host copies (used when the *_dev pointer is NULL
+ *                        and the host pointer is not).
+ *   max_k              : upper bound of k in the device decisions (the model's top_k); sizes the
+ *                        launch.  Ignored for host decisions.
+ *   scale              : LoRA scale folded into every gate (the reference fixes it to 1,
+ *                        SPEC.md:197).
+ * `af_merge` == switch with empty prev; `af_unmerge` == switch with empty cur
+ * (merge_all(sign=-1), adapters.py:236-258; model.py:460-474 `finalize_generation`).
+ * Errors: AF_EVALUE (bad mode/compute), AF_ESTATE (FROM_PRISTINE without pristine),
+ * AF_EINDEX (host decision names an expert outside the bank). */
+int af_fused_switch(af_table* table, const af_decision* prev_dev, const af_decision* cur_dev,
+                    const af_decision* prev_host, const af_decision* cur_host, int32_t max_k,
+                    float scale, int32_t mode, int32_t compute, void* stream);
+int af_merge(af_table* table, const af_decision* dec_dev, const af_decision* dec_host, int32_t max_k,
+             float scale, int32_t compute, void* stream);
+int af_unmerge(af_table* table, const af_decision* dec_dev, const af_decision* dec_host,
+               int32_t max_k, float scale, int32_t compute, void* stream);
+
+/* linalg.py:306-346 `sgmm` on a table of MATERIALISED segments: target += sign * up @ down
+ * for every segment in one launch.  Errors: AF_EVALUE when sign is not +1/-1. */
+int af_sgmm(af_table* table, int32_t sign, int32_t compute, void* stream);
+
+/* model.py:308-312 `_refresh_from_pristine`: live <- pristine for every segment. */
+int af_refresh_from_pristine(af_table* table, void* stream);
+/* model.py:231-236 `max_backbone_deviation`: max |live - pristine| -> *out_dev (f32). */
+int af_max_deviation(af_table* table, float* out_dev, void* stream);
+
+/* ---- bs=1 decode kernels ------------------------------------------------------------
+ * af_gemv  : y = W x, W rows x cols (bf16/f32).  Replaces linalg.py:246-259 `gemm` used as
+ *            the backbone GEMV (model.py:288) with the epilogue of model.py:298-305 fused.
+ *            x and res are f32 vectors; out is f32.  out must not alias x.
+ * af_gemv_t: y = W^T x, W rows x cols, x has `rows` entries, y has `cols`.  Replaces
+ *            model.py:261-263 `_unembed` (x^T (1 x d) @ unembed (d x V)).
+ * af_argmax: lowest index of the maximum (model.py:396 `np.argmax`). */
+int af_gemv(const void* w, int32_t w_dtype, int32_t rows, int32_t cols, int64_t ld, const float* x,
+            float* out, int32_t epilogue, const float* res, void* stream);
+int af_gemv_t(const void* w, int32_t w_dtype, int32_t rows, int32_t cols, int64_t ld, const float* x,
+              float* out, void* stream);
+int af_argmax(const float* v, int32_t n, int32_t* out_dev, void* stream);
+/* model.py:248-258 `_embed_token`: out[0:d] = (f32) table[*token_dev][0:d]. */
+int af_embed(const void* table, int32_t dtype, int32_t d, const int32_t* token_dev, float* out,
+             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAFUSE_B200_H */

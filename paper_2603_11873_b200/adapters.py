@@ -1,0 +1,332 @@
+"""Adapter algebra and the fused switch.
+
+Host-side mirror of /root/reference/pkg/src/lorafuse/adapters.py.  Two forms live here:
+
+* the reference's *materialised* algebra -- ``concat_gated`` / ``build_switch`` / ``merge_all``
+  on ``ConcatAdapter`` objects -- kept with the same names, argument order, provenance and
+  error behaviour so reference-style code and tests run unchanged (one sgmm launch per
+  ``merge_all``);
+* the B200 form the decode loop uses: ``SwitchTable`` -- the device-side descriptor table
+  built ONCE at model load over the resident expert bank -- and ``fused_switch`` /
+  ``merge`` / ``unmerge``, where a per-token decision (expert ids + gate weights, in device
+  memory) selects bank blocks inside the kernel.  Nothing is concatenated, negated or copied
+  per token: the gate is folded into the DOWN rows while they are staged in shared memory
+  (adapters.py:202), previous blocks are negated there (adapters.py:230).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _capi
+from .errors import DeviceError, DimensionError, PrecisionError
+from .linalg import (
+    DEFAULT_TILE,
+    DeviceTable,
+    DispatchRecorder,
+    Matrix,
+    Segment,
+    SegmentTable,
+    TileConfig,
+    _ptr,
+    gemm,
+    sgmm,
+)
+from .routing import DeviceDecision, GateDecision, decision_to_struct
+
+# ---------------------------------------------------------------------------
+# Expert containers (adapters.py:49-109)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True, slots=True)
+class LoraExpert:
+    """One rank-r factor pair for one backbone matrix: down = A (r x d_in), up = B (d_out x r)."""
+
+    down: Matrix
+    up: Matrix
+
+    @property
+    def rank(self) -> int:
+        return self.down.rows
+
+    def validate(self) -> None:
+        if self.down.rows != self.up.cols:
+            raise DimensionError(
+                f"expert rank mismatch: down has {self.down.rows} rows, up has {self.up.cols} columns"
+            )
+        if self.down.rows < 1:
+            raise DimensionError("expert rank must be >= 1")
+        if self.down.precision != self.up.precision:
+            raise PrecisionError("expert factors carry mixed precision tags")
+
+
+@dataclass(frozen=True, slots=True)
+class ExpertBank:
+    """layers[l][i] adapts backbone matrix l; same expert count, rank and shape everywhere."""
+
+    layers: tuple
+
+    @property
+    def n_layers(self) -> int:
+        return len(self.layers)
+
+    @property
+    def n_experts(self) -> int:
+        return len(self.layers[0])
+
+    @property
+    def rank(self) -> int:
+        return self.layers[0][0].rank
+
+    def validate(self) -> None:
+        if not self.layers or not self.layers[0]:
+            raise DimensionError("expert bank has no layers or no experts")
+        n = len(self.layers[0])
+        first = self.layers[0][0]
+        for li, layer in enumerate(self.layers):
+            if len(layer) != n:
+                raise DimensionError(f"layer {li} holds {len(layer)} experts, expected {n}")
+            for expert in layer:
+                expert.validate()
+                if expert.rank != first.rank:
+                    raise DimensionError("experts must share one rank")
+                if expert.down.cols != first.down.cols or expert.up.rows != first.up.rows:
+                    raise DimensionError("experts must share one input/output shape")
+
+
+# ---------------------------------------------------------------------------
+# Concatenated adapters (adapters.py:117-162)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True, slots=True)
+class ConcatAdapter:
+    """Stacked expert blocks for one matrix: down_cat (s x d_in), up_cat (d_out x s);
+    provenance = one (expert_id, gate_weight, sign) per block, gates live in DOWN only."""
+
+    down_cat: Matrix
+    up_cat: Matrix
+    provenance: tuple
+
+    @property
+    def s(self) -> int:
+        return self.down_cat.rows
+
+    @property
+    def d_in(self) -> int:
+        return self.down_cat.cols
+
+    @property
+    def d_out(self) -> int:
+        return self.up_cat.rows
+
+    @classmethod
+    def empty(cls, d_out: int, d_in: int, precision: str = "single", device=None) -> "ConcatAdapter":
+        return cls(
+            down_cat=Matrix.zeros(0, d_in, precision, device),
+            up_cat=Matrix.zeros(d_out, 0, precision, device),
+            provenance=(),
+        )
+
+    def validate(self) -> None:
+        if self.up_cat.cols != self.down_cat.rows:
+            raise DimensionError(
+                f"concat rank mismatch: up_cat has {self.up_cat.cols} columns, "
+                f"down_cat has {self.down_cat.rows} rows"
+            )
+        if self.provenance:
+            block = self.s / len(self.provenance)
+            if block != int(block) or int(block) < 1:
+                raise DimensionError("summed rank does not divide into provenance blocks")
+        elif self.s != 0:
+            raise DimensionError("non-empty concat carries no provenance")
+
+
+# ---------------------------------------------------------------------------
+# Materialised operations (adapters.py:170-258)
+# ---------------------------------------------------------------------------
+
+
+def expert_apply(expert: LoraExpert, x: Matrix, gate_weight: float, recorder: DispatchRecorder) -> Matrix:
+    """gate_weight * up @ (down @ x): the unmerged path, exactly two gemm events
+    (adapters.py:170-185).  Used by prefill and the baseline strategies only."""
+    expert.validate()
+    if x.rows != expert.down.cols or x.cols != 1:
+        raise DimensionError(f"expert expects a {expert.down.cols}x1 input, got {x.rows}x{x.cols}")
+    t = gemm(expert.down, x, recorder, label="adapter")
+    u = gemm(expert.up, t, recorder, label="adapter")
+    return Matrix(u.data * float(gate_weight), u.precision)
+
+
+def concat_gated(bank_layer, gate: GateDecision) -> ConcatAdapter:
+    """Stack one matrix's chosen experts into a gated block pair (adapters.py:188-211).
+
+    DOWN blocks are scaled by their gate weight in f32 -- the stacked factors are therefore
+    "single" even over a bf16 bank -- UP blocks are stacked unscaled.  No events."""
+    if len(gate.expert_ids) == 0:
+        raise ValueError("gate decision selects no experts")
+    experts = []
+    for expert_id in gate.expert_ids:
+        if not 0 <= expert_id < len(bank_layer):
+            raise IndexError(f"expert id {expert_id} outside bank of {len(bank_layer)}")
+        experts.append(bank_layer[expert_id])
+    down_blocks = [e.down.data.float() * float(w) for e, w in zip(experts, gate.weights)]
+    up_blocks = [e.up.data.float() for e in experts]
+    return ConcatAdapter(
+        down_cat=Matrix(torch.cat(down_blocks, dim=0), "single"),
+        up_cat=Matrix(torch.cat(up_blocks, dim=1), "single"),
+        provenance=tuple((int(i), float(w), 1) for i, w in zip(gate.expert_ids, gate.weights)),
+    )
+
+
+def build_switch(prev: ConcatAdapter, cur: ConcatAdapter) -> ConcatAdapter:
+    """[previous (DOWN negated) | current] in one concat (adapters.py:214-233)."""
+    prev.validate()
+    cur.validate()
+    if prev.d_in != cur.d_in or prev.d_out != cur.d_out:
+        raise DimensionError(
+            f"switch halves disagree on shape: {prev.d_out}x{prev.d_in} vs {cur.d_out}x{cur.d_in}"
+        )
+    if prev.down_cat.precision != cur.down_cat.precision:
+        raise PrecisionError("switch halves carry mixed precision tags")
+    precision = cur.down_cat.precision
+    dev = cur.down_cat.data.device
+    down = torch.cat([-prev.down_cat.data.to(dev), cur.down_cat.data], dim=0)
+    up = torch.cat([prev.up_cat.data.to(dev), cur.up_cat.data], dim=1)
+    provenance = tuple((i, w, -sign) for i, w, sign in prev.provenance) + cur.provenance
+    return ConcatAdapter(Matrix(down, precision), Matrix(up, precision), provenance)
+
+
+def merge_all(backbone, concats, sign: int, recorder: DispatchRecorder, tile: TileConfig = DEFAULT_TILE, *, compute: str = "exact") -> None:
+    """backbone[l] += sign * up_cat[l] @ down_cat[l] for all l in ONE launch and one sgmm
+    event labelled "switch" (adapters.py:236-258)."""
+    if len(backbone) != len(concats):
+        raise DimensionError(f"{len(backbone)} backbone matrices but {len(concats)} concats")
+    table = SegmentTable([Segment(down=c.down_cat, up=c.up_cat, target=f) for f, c in zip(backbone, concats)])
+    sgmm(table, sign, recorder, tile=tile, label="switch", compute=compute)
+
+
+# ---------------------------------------------------------------------------
+# The resident form: descriptor table over the expert bank
+# ---------------------------------------------------------------------------
+
+_MODES = {"inplace": _capi.AF_SWITCH_INPLACE, "from_pristine": _capi.AF_SWITCH_FROM_PRISTINE}
+
+
+class SwitchTable:
+    """Device-side descriptor table (the GPU form of linalg.py:207-231 `SegmentTable`) over
+    every adapted matrix and its slice of the expert bank.  Built once at model load.
+
+    targets[i]  : Matrix d_out x d_in (mutated in place by every switch)
+    pristine[i] : Matrix of the same shape, or None for all i
+    downs[i]    : tensor [N][r][d_in]   (LoraExpert.down of each expert, adapters.py:53)
+    ups[i]      : tensor [N][d_out][r]  (LoraExpert.up,   adapters.py:54)
+    """
+
+    def __init__(self, targets, downs, ups, pristine=None):
+        if not targets:
+            raise DimensionError("segment table is empty")
+        if not (len(targets) == len(downs) == len(ups)) or (pristine is not None and len(pristine) != len(targets)):
+            raise DimensionError("targets, banks and pristine copies must have one entry per segment")
+        descs = []
+        tprec = targets[0].precision
+        fprec = {torch.bfloat16: "bf16", torch.float32: "single"}.get(downs[0].dtype)
+        if fprec is None:
+            raise PrecisionError(f"unsupported bank dtype {downs[0].dtype}")
+        self.flops_per_rank = 0
+        self.factor_elems_per_rank = 0
+        self.target_bytes = 0
+        for i, (tgt, dn, up) in enumerate(zip(targets, downs, ups)):
+            if dn.dim() != 3 or up.dim() != 3:
+                raise DimensionError(f"segment {i}: banks must be [N][r][d_in] and [N][d_out][r]")
+            n, r, d_in = (int(v) for v in dn.shape)
+            if tuple(up.shape) != (n, tgt.rows, r) or d_in != tgt.cols:
+                raise DimensionError(
+                    f"segment {i}: target is {tgt.rows}x{tgt.cols}, bank blocks are {tuple(up.shape)} / {tuple(dn.shape)}"
+                )
+            if tgt.precision != tprec or dn.dtype != downs[0].dtype or up.dtype != downs[0].dtype:
+                raise PrecisionError("segments of one table carry mixed precision tags")
+            if not (tgt.data.is_cuda and dn.is_cuda and up.is_cuda):
+                raise DeviceError("operand is not on a CUDA device: the B200 path has no CPU fallback")
+            if not (dn.is_contiguous() and up.is_contiguous()):
+                raise DimensionError(f"segment {i}: bank tensors must be contiguous")
+            pr = pristine[i] if pristine is not None else None
+            if pr is not None and (pr.rows != tgt.rows or pr.cols != tgt.cols or pr.precision != tgt.precision):
+                raise DimensionError(f"segment {i}: pristine copy does not match its target")
+            descs.append(
+                _capi.SegmentDesc(
+                    target=_ptr(tgt.data), pristine=_ptr(pr.data) if pr is not None else 0,
+                    down=_ptr(dn), up=_ptr(up), d_out=tgt.rows, d_in=tgt.cols, rank=r, n_experts=n,
+                    ld_target=tgt.cols, ld_down=d_in, ld_up=r, down_expert_stride=r * d_in, up_expert_stride=tgt.rows * r,
+                )
+            )
+            self.flops_per_rank += 2 * tgt.rows * tgt.cols
+            self.factor_elems_per_rank += tgt.rows + tgt.cols
+            self.target_bytes += tgt.rows * tgt.cols * tgt.itemsize
+        self.rank = int(downs[0].shape[1])
+        self.n_experts = min(int(d.shape[0]) for d in downs)
+        self.factor_itemsize = downs[0].element_size()
+        self.device_table = DeviceTable(descs, tprec, fprec, keepalive=(targets, downs, ups, pristine))
+        self.n_segments = len(targets)
+        self._dev_scalar = None
+
+    # -- accounting (identical formulas to linalg.py:293-303) --
+    def switch_flops(self, s: int) -> int:
+        return self.flops_per_rank * s
+
+    def switch_bytes(self, s: int) -> int:
+        return 2 * self.target_bytes + s * self.factor_elems_per_rank * self.factor_itemsize
+
+    def info(self) -> dict:
+        return self.device_table.info()
+
+    def status(self) -> None:
+        self.device_table.status()
+
+    @staticmethod
+    def _split(dec):
+        """-> (device pointer or None, host struct or None)"""
+        if dec is None:
+            return None, None
+        if isinstance(dec, DeviceDecision):
+            return dec.ptr, None
+        if isinstance(dec, GateDecision):
+            return None, decision_to_struct(dec)
+        raise TypeError(f"decision must be a GateDecision, a DeviceDecision or None, got {type(dec).__name__}")
+
+    def switch(self, prev, cur, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace", compute: str = "auto") -> None:
+        """W <- W + delta(cur) - delta(prev) on every segment, one launch (model.py:350-357)."""
+        if mode not in _MODES:
+            raise ValueError(f"unknown switch mode {mode!r}")
+        if compute not in _capi.COMPUTE_MODES:
+            raise ValueError(f"unknown compute mode {compute!r}")
+        pd, ph = self._split(prev)
+        cd, ch = self._split(cur)
+        _capi.check(
+            _capi.lib().af_fused_switch(
+                self.device_table.handle, pd, cd, ph, ch, int(max_k), float(scale), _MODES[mode],
+                _capi.COMPUTE_MODES[compute], _capi.stream_ptr(),
+            )
+        )
+
+    def merge(self, dec, **kw) -> None:
+        """merge_all(sign=+1) of one decision (adapters.py:236-258)."""
+        self.switch(None, dec, **kw)
+
+    def unmerge(self, dec, **kw) -> None:
+        """merge_all(sign=-1): model.py:460-474 `finalize_generation` in one launch."""
+        self.switch(dec, None, **kw)
+
+    def refresh(self) -> None:
+        """model.py:308-312 `_refresh_from_pristine`."""
+        _capi.check(_capi.lib().af_refresh_from_pristine(self.device_table.handle, _capi.stream_ptr()))
+
+    def max_deviation(self) -> float:
+        """model.py:231-236 `max_backbone_deviation` (synchronises)."""
+        if self._dev_scalar is None:
+            self._dev_scalar = torch.zeros(1, dtype=torch.float32, device="cuda")
+        _capi.check(_capi.lib().af_max_deviation(self.device_table.handle, _ptr(self._dev_scalar), _capi.stream_ptr()))
+        return float(self._dev_scalar.item())

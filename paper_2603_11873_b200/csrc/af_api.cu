@@ -1,0 +1,583 @@
+// af_api.cu -- the C ABI of include/adafuse_b200.h: validation, descriptor tables, TMA maps,
+// kernel selection and launches.  No torch types anywhere; every device buffer belongs to the
+// caller.  Citations are relative to /root/reference/pkg/src/lorafuse/.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "af_decode.cuh"
+#include "af_llama.cuh"
+#include "af_switch_mma.cuh"
+
+namespace af {
+
+std::string& last_error_slot() {
+    static thread_local std::string slot;
+    return slot;
+}
+int fail(int code, const std::string& msg) {
+    last_error_slot() = msg;
+    return code;
+}
+std::atomic<long long> g_launches{0};
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline size_t esize(int dtype) { return dtype == AF_BF16 ? 2 : 4; }
+
+// ---- driver entry point for cuTensorMapEncodeTiled (no link-time libcuda dependency) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+static int make_map(CUtensorMap* out, const void* base, int rows, int cols, long long ld, int box_cols, int box_rows,
+                    CUtensorMapSwizzle swz) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return fail(AF_ECUDA, "cuTensorMapEncodeTiled entry point not found");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(AF_ECUDA, "cuTensorMapEncodeTiled failed with code " + std::to_string((int)r));
+    return AF_OK;
+}
+
+struct DeviceInfo {
+    int sm_count = 0, cc_major = 0, cc_minor = 0;
+    long long l2 = 0;
+    int max_smem_optin = 0;
+    bool ok = false;
+};
+static const DeviceInfo& device_info() {
+    static thread_local DeviceInfo info;
+    static thread_local int cached_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return info;
+    if (info.ok && dev == cached_dev) return info;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return info;
+    info.sm_count = prop.multiProcessorCount;
+    info.cc_major = prop.major;
+    info.cc_minor = prop.minor;
+    info.l2 = prop.l2CacheSize;
+    info.max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    info.ok = true;
+    cached_dev = dev;
+    return info;
+}
+
+}  // namespace af
+
+using namespace af;
+
+// linalg.py:207-231 `SegmentTable`, device resident.
+struct af_table {
+    int n_segments = 0;
+    int target_dtype = AF_BF16, factor_dtype = AF_BF16;
+    std::vector<af_segment_desc> segs;
+    SegDev* d_segs = nullptr;
+    UnitDev* d_units = nullptr;
+    int n_units = 0;
+    CUtensorMap* d_maps = nullptr;  // [5][n_segments]: fma live, fma pristine, mma-ld live, mma-ld pristine, mma-st live
+    int* d_err = nullptr;
+    bool fast_fma = false, fast_mma = false, has_pristine = false;
+    int max_rank = 0, min_experts = 0;
+    long long target_elems = 0;
+    int sm_count = 0;
+};
+
+extern "C" {
+
+int af_abi_version(void) { return AF_ABI_VERSION; }
+const char* af_last_error(void) { return last_error_slot().c_str(); }
+
+int af_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_bytes) {
+    const DeviceInfo& d = device_info();
+    if (!d.ok) return fail(AF_ECUDA, "no CUDA device");
+    if (sm_count) *sm_count = d.sm_count;
+    if (cc_major) *cc_major = d.cc_major;
+    if (cc_minor) *cc_minor = d.cc_minor;
+    if (l2_bytes) *l2_bytes = d.l2;
+    return AF_OK;
+}
+
+int64_t af_launch_count(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------------ table ----
+
+int af_table_destroy(af_table* t) {
+    if (!t) return AF_OK;
+    if (t->d_segs) cudaFree(t->d_segs);
+    if (t->d_units) cudaFree(t->d_units);
+    if (t->d_maps) cudaFree(t->d_maps);
+    if (t->d_err) cudaFree(t->d_err);
+    delete t;
+    return AF_OK;
+}
+
+int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t target_dtype, int32_t factor_dtype,
+                    af_table** out) {
+    if (!out) return fail(AF_EVALUE, "out is NULL");
+    *out = nullptr;
+    // ---- validation first, nothing touched (linalg.py:219-228, 199-205) ----
+    if (n_segments < 1 || !segments) return fail(AF_EDIM, "segment table is empty");
+    if ((target_dtype != AF_BF16 && target_dtype != AF_F32) || (factor_dtype != AF_BF16 && factor_dtype != AF_F32))
+        return fail(AF_EPRECISION, "unknown precision tag");
+    const size_t te = esize(target_dtype);
+    for (int i = 0; i < n_segments; ++i) {
+        const af_segment_desc& s = segments[i];
+        if (s.d_out < 0 || s.d_in < 0 || s.rank < 0 || s.n_experts < 1)
+            return fail(AF_EDIM, "segment " + std::to_string(i) + ": negative extent or empty bank");
+        if (s.d_out > 0 && s.d_in > 0 && !s.target) return fail(AF_EDIM, "segment " + std::to_string(i) + ": target is NULL");
+        if (s.ld_target < s.d_in) return fail(AF_EDIM, "segment " + std::to_string(i) + ": target pitch below d_in");
+        if (s.rank > 0 && (s.ld_down < s.d_in || s.ld_up < s.rank))
+            return fail(AF_EDIM, "segment " + std::to_string(i) + ": factor pitch below its row length");
+        if (s.rank > 0 && s.d_out > 0 && s.d_in > 0 && (!s.down || !s.up))
+            return fail(AF_EDIM, "segment " + std::to_string(i) + ": factor pointer is NULL");
+    }
+    {  // distinct, non-overlapping targets (linalg.py:222-228 keyed on identity; here on address ranges)
+        struct Range {
+            uintptr_t lo, hi;
+            int idx;
+        };
+        std::vector<Range> rs;
+        for (int i = 0; i < n_segments; ++i) {
+            const af_segment_desc& s = segments[i];
+            if (s.d_out == 0 || s.d_in == 0) continue;
+            const uintptr_t lo = reinterpret_cast<uintptr_t>(s.target);
+            const uintptr_t hi = lo + ((uintptr_t)(s.d_out - 1) * (uintptr_t)s.ld_target + (uintptr_t)s.d_in) * te;
+            rs.push_back({lo, hi, i});
+        }
+        std::sort(rs.begin(), rs.end(), [](const Range& a, const Range& b) { return a.lo < b.lo; });
+        for (size_t i = 1; i < rs.size(); ++i)
+            if (rs[i].lo < rs[i - 1].hi)
+                return fail(AF_EALIAS, "segments " + std::to_string(rs[i - 1].idx) + " and " + std::to_string(rs[i].idx) +
+                                           " share one target matrix");
+    }
+    const DeviceInfo& dinfo = device_info();
+    if (!dinfo.ok) return fail(AF_ECUDA, "no CUDA device");
+
+    af_table* t = new af_table();
+    t->n_segments = n_segments;
+    t->target_dtype = target_dtype;
+    t->factor_dtype = factor_dtype;
+    t->segs.assign(segments, segments + n_segments);
+    t->sm_count = dinfo.sm_count;
+    t->has_pristine = true;
+    t->min_experts = segments[0].n_experts;
+    bool fma_ok = (target_dtype == AF_BF16), mma_ok = (target_dtype == AF_BF16 && factor_dtype == AF_BF16);
+    std::vector<SegDev> hs(n_segments);
+    long long total_tiles = 0;
+    for (int i = 0; i < n_segments; ++i) {
+        const af_segment_desc& s = segments[i];
+        SegDev& d = hs[i];
+        d.target = s.target;
+        d.pristine = s.pristine;
+        d.down = s.down;
+        d.up = s.up;
+        d.d_out = s.d_out;
+        d.d_in = s.d_in;
+        d.rank = s.rank;
+        d.n_experts = s.n_experts;
+        d.ld_target = s.ld_target;
+        d.ld_down = s.ld_down;
+        d.ld_up = s.ld_up;
+        d.down_estride = s.down_expert_stride;
+        d.up_estride = s.up_expert_stride;
+        if (!s.pristine) t->has_pristine = false;
+        t->max_rank = std::max(t->max_rank, s.rank);
+        t->min_experts = std::min(t->min_experts, s.n_experts);
+        t->target_elems += (long long)s.d_out * s.d_in;
+        total_tiles += (long long)((s.d_out + kTM - 1) / kTM) * ((s.d_in + kTN - 1) / kTN);
+        // TMA: 16-byte aligned base and row pitch
+        const bool tma_ok = s.d_out > 0 && s.d_in > 0 && (reinterpret_cast<uintptr_t>(s.target) % 16 == 0) &&
+                            (s.ld_target % 8 == 0) &&
+                            (!s.pristine || reinterpret_cast<uintptr_t>(s.pristine) % 16 == 0);
+        if (!tma_ok) fma_ok = mma_ok = false;
+        // tensor path: dense UP rows (ld_up == rank), rank a multiple of 8, 16-byte aligned factor blocks
+        const bool fac_ok = s.rank > 0 && s.rank % 8 == 0 && s.ld_up == s.rank && (s.up_expert_stride % 8 == 0) &&
+                            (reinterpret_cast<uintptr_t>(s.up) % 16 == 0) && (s.ld_down % 8 == 0) &&
+                            (s.down_expert_stride % 8 == 0) && (reinterpret_cast<uintptr_t>(s.down) % 16 == 0);
+        if (!fac_ok) mma_ok = false;
+    }
+    t->fast_fma = fma_ok;
+    t->fast_mma = mma_ok;
+
+    // ---- work units: column strips of kTN columns cut into runs of row tiles ----
+    // Static round-robin schedule over the persistent grid: aim for ~32 units per SM so the
+    // tail imbalance stays below ~3 %, but keep runs long enough to amortise the slab staging.
+    long long per_unit = total_tiles / ((long long)std::max(1, t->sm_count) * 32);
+    per_unit = std::max(1LL, std::min(64LL, per_unit));
+    std::vector<UnitDev> units;
+    for (int i = 0; i < n_segments; ++i) {
+        const af_segment_desc& s = segments[i];
+        if (s.d_out == 0 || s.d_in == 0) continue;
+        const int rows_per_unit = (int)per_unit * kTM;
+        for (int c0 = 0; c0 < s.d_in; c0 += kTN)
+            for (int r0 = 0; r0 < s.d_out; r0 += rows_per_unit)
+                units.push_back({i, r0, std::min(rows_per_unit, s.d_out - r0), c0});
+    }
+    t->n_units = (int)units.size();
+
+    cudaError_t e = cudaMalloc(&t->d_segs, sizeof(SegDev) * n_segments);
+    if (e == cudaSuccess) e = cudaMemcpy(t->d_segs, hs.data(), sizeof(SegDev) * n_segments, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && t->n_units) e = cudaMalloc(&t->d_units, sizeof(UnitDev) * units.size());
+    if (e == cudaSuccess && t->n_units)
+        e = cudaMemcpy(t->d_units, units.data(), sizeof(UnitDev) * units.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&t->d_err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(t->d_err, 0, sizeof(int));
+    if (e != cudaSuccess) {
+        af_table_destroy(t);
+        return fail(AF_ECUDA, std::string("table upload: ") + cudaGetErrorString(e));
+    }
+    if (t->fast_fma) {
+        std::vector<CUtensorMap> maps((size_t)5 * n_segments);
+        for (int i = 0; i < n_segments; ++i) {
+            const af_segment_desc& s = segments[i];
+            const void* pr = s.pristine ? s.pristine : s.target;
+            int rc = make_map(&maps[0 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kTN, kTM, CU_TENSOR_MAP_SWIZZLE_NONE);
+            if (!rc) rc = make_map(&maps[1 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kTN, kTM, CU_TENSOR_MAP_SWIZZLE_NONE);
+            if (!rc) rc = make_map(&maps[2 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kBoxCols, kTM, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (!rc) rc = make_map(&maps[3 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kBoxCols, kTM, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (!rc) rc = make_map(&maps[4 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kBoxCols, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (rc) {
+                af_table_destroy(t);
+                return rc;
+            }
+        }
+        e = cudaMalloc(&t->d_maps, sizeof(CUtensorMap) * maps.size());
+        if (e == cudaSuccess) e = cudaMemcpy(t->d_maps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            af_table_destroy(t);
+            return fail(AF_ECUDA, std::string("tensor map upload: ") + cudaGetErrorString(e));
+        }
+    }
+    *out = t;
+    return AF_OK;
+}
+
+int af_table_info(const af_table* t, int32_t* n_segments, int64_t* target_elems, int32_t* n_units, int32_t* fast_path) {
+    if (!t) return fail(AF_EVALUE, "table is NULL");
+    if (n_segments) *n_segments = t->n_segments;
+    if (target_elems) *target_elems = t->target_elems;
+    if (n_units) *n_units = t->n_units;
+    if (fast_path) *fast_path = (t->fast_fma ? 1 : 0) | (t->fast_mma ? 2 : 0);
+    return AF_OK;
+}
+
+int af_table_status(af_table* t, void* stream) {
+    if (!t) return fail(AF_EVALUE, "table is NULL");
+    int flag = 0;
+    AF_CUDA_TRY(cudaMemcpyAsync(&flag, t->d_err, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream)));
+    AF_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+    if (flag) {
+        AF_CUDA_TRY(cudaMemsetAsync(t->d_err, 0, sizeof(int), as_stream(stream)));
+        return fail(flag, flag == AF_EINDEX ? "a device decision names an expert outside the bank"
+                                            : "a device decision carries more experts than max_k");
+    }
+    return AF_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ switch launch ----
+
+namespace af {
+
+template <int KS>
+static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
+    using L = MmaLayout<KS>;
+    static bool configured = false;
+    if (!configured) {
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        configured = true;
+    }
+    switch_mma_kernel<KS><<<grid, kConsumers + 32, L::total, st>>>(mp);
+    AF_LAUNCH_CHECK("switch_mma_kernel");
+    return AF_OK;
+}
+
+template <typename FT, bool EXACT, bool F2>
+static int launch_tma(const SwitchParams& p, int grid, cudaStream_t st) {
+    static bool configured = false;
+    const int smem = (int)sizeof(SwitchSmem) + 128;
+    if (!configured) {
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_tma_kernel<FT, EXACT, F2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured = true;
+    }
+    switch_tma_kernel<FT, EXACT, F2><<<grid, kConsumers + 32, smem, st>>>(p);
+    AF_LAUNCH_CHECK("switch_tma_kernel");
+    return AF_OK;
+}
+
+template <bool EXACT>
+static int launch_any(const af_table* t, const SwitchParams& p, int grid, cudaStream_t st) {
+    if (t->target_dtype == AF_BF16 && t->factor_dtype == AF_BF16)
+        switch_any_kernel<__nv_bfloat16, __nv_bfloat16, EXACT><<<grid, kTN, 0, st>>>(p);
+    else if (t->target_dtype == AF_BF16)
+        switch_any_kernel<__nv_bfloat16, float, EXACT><<<grid, kTN, 0, st>>>(p);
+    else if (t->factor_dtype == AF_BF16)
+        switch_any_kernel<float, __nv_bfloat16, EXACT><<<grid, kTN, 0, st>>>(p);
+    else
+        switch_any_kernel<float, float, EXACT><<<grid, kTN, 0, st>>>(p);
+    AF_LAUNCH_CHECK("switch_any_kernel");
+    return AF_OK;
+}
+
+static int check_host_decision(const af_table* t, const af_decision* d, const char* which) {
+    if (!d) return AF_OK;
+    if (d->k < 0 || d->k > AF_MAX_K) return fail(AF_EVALUE, std::string(which) + " decision: k outside [0, AF_MAX_K]");
+    for (int j = 0; j < d->k; ++j)
+        if (d->ids[j] < 0 || d->ids[j] >= t->min_experts)
+            return fail(AF_EINDEX, std::string(which) + " decision: expert id " + std::to_string(d->ids[j]) +
+                                       " outside bank of " + std::to_string(t->min_experts));
+    return AF_OK;
+}
+
+// Common launcher.  host_plan_override != nullptr: af_sgmm (materialised segments).
+static int run_switch(af_table* t, const af_decision* prev_dev, const af_decision* cur_dev, const af_decision* prev_host,
+                      const af_decision* cur_host, int max_k, float scale, int mode, int compute,
+                      const Plan* host_plan_override, cudaStream_t st) {
+    if (!t) return fail(AF_EVALUE, "table is NULL");
+    if (mode != AF_SWITCH_INPLACE && mode != AF_SWITCH_FROM_PRISTINE) return fail(AF_EVALUE, "unknown switch mode");
+    if (compute < AF_COMPUTE_AUTO || compute > AF_COMPUTE_MMA) return fail(AF_EVALUE, "unknown compute mode");
+    if (mode == AF_SWITCH_FROM_PRISTINE && !t->has_pristine)
+        return fail(AF_ESTATE, "FROM_PRISTINE needs a pristine copy of every segment");
+    const bool use_dev = (prev_dev || cur_dev) && !host_plan_override;
+    if (use_dev && ((prev_host && !prev_dev) || (cur_host && !cur_dev)))
+        return fail(AF_EVALUE, "decisions must be all device-resident or all host-resident");
+    if (use_dev && (max_k < 1 || max_k > AF_MAX_K)) return fail(AF_EVALUE, "max_k outside [1, AF_MAX_K]");
+    const bool exact = compute == AF_COMPUTE_EXACT;
+
+    SwitchParams p{};
+    p.segs = t->d_segs;
+    p.units = t->d_units;
+    p.n_units = t->n_units;
+    p.from_pristine = mode == AF_SWITCH_FROM_PRISTINE;
+    p.prev_dev = prev_dev;
+    p.cur_dev = cur_dev;
+    p.use_dev = use_dev ? 1 : 0;
+    p.scale = scale;
+    p.n_experts_limit = t->min_experts;
+    p.err_flag = t->d_err;
+    int n_blocks_bound;
+    if (host_plan_override) {
+        p.host_plan = *host_plan_override;
+        n_blocks_bound = p.host_plan.n_blocks;
+    } else if (!use_dev) {
+        int rc = check_host_decision(t, prev_host, "previous");
+        if (!rc) rc = check_host_decision(t, cur_host, "current");
+        if (rc) return rc;
+        build_plan(p.host_plan, p.from_pristine ? nullptr : prev_host, cur_host, scale, exact, t->min_experts);
+        n_blocks_bound = p.host_plan.n_blocks;
+        if (n_blocks_bound == 0 && !p.from_pristine) return AF_OK;  // nothing changes: no launch
+    } else {
+        n_blocks_bound = (p.from_pristine || !prev_dev ? 0 : max_k) + (cur_dev ? max_k : 0);
+    }
+    p.max_blocks = std::min(n_blocks_bound, kMaxBlocks);
+    if (t->n_units == 0) return AF_OK;
+    const int s_bound = n_blocks_bound * t->max_rank;
+
+    const bool want_mma = compute == AF_COMPUTE_MMA || compute == AF_COMPUTE_AUTO;
+    const bool mma_fits = t->fast_mma && s_bound <= kMmaMaxKS * 16;
+    if (compute == AF_COMPUTE_MMA && !mma_fits)
+        return fail(AF_EVALUE, "tensor path needs bf16 targets and factors, rank % 8 == 0, 16-byte aligned rows and "
+                               "at most 64 stacked ranks");
+    const int S = t->n_segments;
+    if (want_mma && mma_fits) {
+        MmaParams mp{};
+        mp.base = p;
+        mp.tmaps_ld = t->d_maps + (size_t)(p.from_pristine ? 3 : 2) * S;
+        mp.tmaps_st = t->d_maps + (size_t)4 * S;
+        const int grid = std::min(t->n_units, t->sm_count);
+        const int ks = std::max(1, (s_bound + 15) / 16);
+        switch (ks) {
+            case 1: return launch_mma<1>(mp, grid, st);
+            case 2: return launch_mma<2>(mp, grid, st);
+            case 3: return launch_mma<3>(mp, grid, st);
+            default: return launch_mma<4>(mp, grid, st);
+        }
+    }
+    if (t->fast_fma) {
+        p.tmaps_src = t->d_maps + (size_t)(p.from_pristine ? 1 : 0) * S;
+        p.tmaps_dst = t->d_maps;
+        const int grid = std::min(t->n_units, t->sm_count);
+        if (t->factor_dtype == AF_BF16)
+            return exact ? launch_tma<__nv_bfloat16, true, false>(p, grid, st) : launch_tma<__nv_bfloat16, false, true>(p, grid, st);
+        return exact ? launch_tma<float, true, false>(p, grid, st) : launch_tma<float, false, true>(p, grid, st);
+    }
+    const int grid = std::min(t->n_units, t->sm_count * 8);
+    return exact ? launch_any<true>(t, p, grid, st) : launch_any<false>(t, p, grid, st);
+}
+
+}  // namespace af
+
+extern "C" {
+
+int af_fused_switch(af_table* table, const af_decision* prev_dev, const af_decision* cur_dev, const af_decision* prev_host,
+                    const af_decision* cur_host, int32_t max_k, float scale, int32_t mode, int32_t compute, void* stream) {
+    return run_switch(table, prev_dev, cur_dev, prev_host, cur_host, max_k, scale, mode, compute, nullptr, as_stream(stream));
+}
+
+int af_merge(af_table* table, const af_decision* dec_dev, const af_decision* dec_host, int32_t max_k, float scale,
+             int32_t compute, void* stream) {
+    return run_switch(table, nullptr, dec_dev, nullptr, dec_host, max_k, scale, AF_SWITCH_INPLACE, compute, nullptr,
+                      as_stream(stream));
+}
+
+int af_unmerge(af_table* table, const af_decision* dec_dev, const af_decision* dec_host, int32_t max_k, float scale,
+               int32_t compute, void* stream) {
+    return run_switch(table, dec_dev, nullptr, dec_host, nullptr, max_k, scale, AF_SWITCH_INPLACE, compute, nullptr,
+                      as_stream(stream));
+}
+
+int af_sgmm(af_table* table, int32_t sign, int32_t compute, void* stream) {
+    if (sign != 1 && sign != -1) return fail(AF_EVALUE, "sign must be +1 or -1");  // linalg.py:323-324
+    if (!table) return fail(AF_EVALUE, "table is NULL");
+    Plan plan{};
+    plan.n_blocks = 1;
+    plan.expert[0] = 0;
+    if (compute == AF_COMPUTE_EXACT) {
+        plan.weight[0] = 1.0f;            // 1 * down is exact; the sign is applied as `block -= outer`
+        plan.negate[0] = sign < 0 ? 1 : 0;
+    } else {
+        plan.weight[0] = (float)sign;
+        plan.negate[0] = 0;
+    }
+    return run_switch(table, nullptr, nullptr, nullptr, nullptr, 1, 1.0f, AF_SWITCH_INPLACE, compute, &plan, as_stream(stream));
+}
+
+int af_refresh_from_pristine(af_table* t, void* stream) {
+    if (!t) return fail(AF_EVALUE, "table is NULL");
+    if (!t->has_pristine) return fail(AF_ESTATE, "no pristine copy registered");
+    const size_t es = esize(t->target_dtype);
+    for (const af_segment_desc& s : t->segs) {
+        if (s.d_out == 0 || s.d_in == 0) continue;
+        AF_CUDA_TRY(cudaMemcpy2DAsync(s.target, s.ld_target * es, s.pristine, s.ld_target * es, (size_t)s.d_in * es,
+                                      s.d_out, cudaMemcpyDeviceToDevice, as_stream(stream)));
+    }
+    return AF_OK;
+}
+
+int af_max_deviation(af_table* t, float* out_dev, void* stream) {
+    if (!t || !out_dev) return fail(AF_EVALUE, "NULL argument");
+    if (!t->has_pristine) return fail(AF_ESTATE, "no pristine copy registered");
+    cudaStream_t st = as_stream(stream);
+    AF_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(float), st));
+    for (const af_segment_desc& s : t->segs) {
+        if (s.d_out == 0 || s.d_in == 0) continue;
+        const long long n = (long long)s.d_out * s.d_in;
+        const int grid = (int)std::min<long long>((n + 1023) / 1024, (long long)t->sm_count * 8);
+        if (t->target_dtype == AF_BF16)
+            max_dev_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(s.target),
+                                                               reinterpret_cast<const __nv_bfloat16*>(s.pristine), s.d_out,
+                                                               s.d_in, s.ld_target, reinterpret_cast<unsigned*>(out_dev));
+        else
+            max_dev_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(s.target),
+                                                       reinterpret_cast<const float*>(s.pristine), s.d_out, s.d_in,
+                                                       s.ld_target, reinterpret_cast<unsigned*>(out_dev));
+        AF_LAUNCH_CHECK("max_dev_kernel");
+    }
+    return AF_OK;
+}
+
+// ------------------------------------------------------------------ router ----
+
+int af_pregate(const void* router_w, int32_t w_dtype, int32_t n_experts, int32_t d, const void* x, int32_t x_dtype,
+               const int32_t* token_dev, int32_t k, af_decision* out_dev, float* logits_dev, void* stream) {
+    // routing.py:57-58: k first
+    if (n_experts < 1 || n_experts > kRouterMaxExperts) return fail(AF_EDIM, "router supports 1..256 experts");
+    if (k < 1 || k > n_experts) return fail(AF_EVALUE, "k=" + std::to_string(k) + " must be in [1, " + std::to_string(n_experts) + "]");
+    if (k > AF_MAX_K) return fail(AF_EVALUE, "k exceeds AF_MAX_K");
+    if (d < 1) return fail(AF_EDIM, "hidden size must be positive");
+    if (!router_w || !x || !out_dev) return fail(AF_EVALUE, "NULL argument");
+    cudaStream_t st = as_stream(stream);
+#define AF_PREGATE(WT, XT)                                                                                           \
+    pregate_kernel<WT, XT><<<1, kRouterThreads, 0, st>>>(reinterpret_cast<const WT*>(router_w), n_experts, d,          \
+                                                         reinterpret_cast<const XT*>(x), token_dev, k, out_dev, logits_dev)
+    if (w_dtype == AF_BF16 && x_dtype == AF_BF16) AF_PREGATE(__nv_bfloat16, __nv_bfloat16);
+    else if (w_dtype == AF_BF16 && x_dtype == AF_F32) AF_PREGATE(__nv_bfloat16, float);
+    else if (w_dtype == AF_F32 && x_dtype == AF_BF16) AF_PREGATE(float, __nv_bfloat16);
+    else if (w_dtype == AF_F32 && x_dtype == AF_F32) AF_PREGATE(float, float);
+    else return fail(AF_EPRECISION, "unknown precision tag");
+#undef AF_PREGATE
+    AF_LAUNCH_CHECK("pregate_kernel");
+    return AF_OK;
+}
+
+// ------------------------------------------------------------------ decode ----
+
+int af_gemv(const void* w, int32_t w_dtype, int32_t rows, int32_t cols, int64_t ld, const float* x, float* out,
+            int32_t epilogue, const float* res, void* stream) {
+    if (rows < 0 || cols < 0 || ld < cols) return fail(AF_EDIM, "bad GEMV shape");
+    if (epilogue < AF_EPI_NONE || epilogue > AF_EPI_RESIDUAL) return fail(AF_EVALUE, "unknown epilogue");
+    if (epilogue != AF_EPI_NONE && !res) return fail(AF_EVALUE, "epilogue needs a residual vector");
+    if (w_dtype != AF_BF16 && w_dtype != AF_F32) return fail(AF_EPRECISION, "unknown precision tag");
+    if (rows == 0) return AF_OK;
+    if (out == x) return fail(AF_EALIAS, "GEMV output aliases its input");
+    const DeviceInfo& di = device_info();
+    const int smem = cols * 4;
+    if (smem > di.max_smem_optin) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
+    cudaStream_t st = as_stream(stream);
+    const int rows_per_cta = (kGemvThreads / 32) * kRowsPerWarp;
+    const int grid = std::max(1, std::min((rows + rows_per_cta - 1) / rows_per_cta, di.sm_count * 8));
+    if (w_dtype == AF_BF16) {
+        if (smem > 48 * 1024) AF_CUDA_TRY(cudaFuncSetAttribute(gemv_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        gemv_kernel<__nv_bfloat16><<<grid, kGemvThreads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(w), rows, cols, ld, x, out, epilogue, res);
+    } else {
+        if (smem > 48 * 1024) AF_CUDA_TRY(cudaFuncSetAttribute(gemv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        gemv_kernel<float><<<grid, kGemvThreads, smem, st>>>(reinterpret_cast<const float*>(w), rows, cols, ld, x, out, epilogue, res);
+    }
+    AF_LAUNCH_CHECK("gemv_kernel");
+    return AF_OK;
+}
+
+int af_gemv_t(const void* w, int32_t w_dtype, int32_t rows, int32_t cols, int64_t ld, const float* x, float* out,
+              void* stream) {
+    if (rows < 0 || cols < 0 || ld < cols) return fail(AF_EDIM, "bad GEMV shape");
+    if (w_dtype != AF_BF16 && w_dtype != AF_F32) return fail(AF_EPRECISION, "unknown precision tag");
+    if (cols == 0) return AF_OK;
+    cudaStream_t st = as_stream(stream);
+    const int grid = (cols + kGemvTCols - 1) / kGemvTCols;
+    if (w_dtype == AF_BF16)
+        gemv_t_kernel<__nv_bfloat16><<<grid, kGemvTThreads, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(w), rows, cols, ld, x, out);
+    else
+        gemv_t_kernel<float><<<grid, kGemvTThreads, 0, st>>>(reinterpret_cast<const float*>(w), rows, cols, ld, x, out);
+    AF_LAUNCH_CHECK("gemv_t_kernel");
+    return AF_OK;
+}
+
+int af_argmax(const float* v, int32_t n, int32_t* out_dev, void* stream) {
+    if (n < 1 || !v || !out_dev) return fail(AF_EDIM, "argmax of an empty vector");
+    argmax_kernel<<<1, 1024, 0, as_stream(stream)>>>(v, n, out_dev);
+    AF_LAUNCH_CHECK("argmax_kernel");
+    return AF_OK;
+}
+
+int af_embed(const void* table, int32_t dtype, int32_t d, const int32_t* token_dev, float* out, void* stream) {
+    if (d < 1 || !table || !token_dev || !out) return fail(AF_EDIM, "bad embed arguments");
+    const int grid = std::max(1, std::min((d + 255) / 256, 64));
+    if (dtype == AF_BF16)
+        embed_kernel<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(table), d, token_dev, out);
+    else if (dtype == AF_F32)
+        embed_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const float*>(table), d, token_dev, out);
+    else
+        return fail(AF_EPRECISION, "unknown precision tag");
+    AF_LAUNCH_CHECK("embed_kernel");
+    return AF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,308 @@
+// af_switch_mma.cuh -- fused switching kernel, HBM-bound variant.
+//
+// Same contract as af_switch.cuh (adapters.py:188-258 + linalg.py:306-346 in one persistent
+// launch) but the rank-s micro product  D = sum_b g_b * B_b A_b  is issued on the tensor pipe
+// (mma.sync m16n8k16, bf16 in, f32 accumulate) so the CUDA cores only do the W + D add and
+// the bf16 rounding.  On fp32 FMA the steady switch (s = 2kr = 32) needs 104 TFLOP/s to keep
+// up with HBM -- above the FMA peak of the chip; here the math is ~15 % of
+// the tile time and the kernel is bound by the W stream.
+//
+// Gate weights stay f32: the gated DOWN row v = g * a (one f32 multiply, adapters.py:202) is
+// split into v = hi + lo + O(2^-17 |v|) with hi, lo bf16, and D = U.hi + U.lo accumulates in
+// f32 (products of two bf16 values are exact in f32).
+//
+// Data movement per 64 x 256 tile of W (one pipeline stage):
+//   W   : 4 TMA boxes of 64 rows x 64 cols (128-byte swizzle) global -> smem, updated in place
+//         in smem with ldmatrix / stmatrix, then one TMA store per consumer warp (32 x 64).
+//   UP  : one 1-D bulk copy per block (64 rows x r bf16 are contiguous in the bank).
+//   DOWN: gated hi/lo slab [2 * S_pad][256 (+8 pad)] bf16, staged once per unit (column strip).
+#pragma once
+
+#include "af_switch.cuh"
+
+namespace af {
+
+constexpr int kBoxCols = 64;                      // 128-byte swizzle span in bf16
+constexpr int kBoxes = kTN / kBoxCols;            // 4 boxes per tile
+constexpr int kBoxBytes = kTM * kBoxCols * 2;     // 8 KB
+constexpr int kWStageBytes = kTM * kTN * 2;       // 32 KB
+constexpr int kDownPitch = kTN + 8;               // elements; +16 B keeps ldmatrix conflict free
+constexpr int kMmaWarps = kConsumers / 32;        // 8 consumer warps
+constexpr int kMmaMaxKS = 4;                      // k-steps of 16 ranks: S <= 64
+
+template <int KS>
+struct MmaLayout {
+    static constexpr int s_pad = KS * 16;
+    static constexpr int stages = (KS <= 3) ? 4 : 3;
+    static constexpr int up_stage_bytes = kTM * s_pad * 2;
+    static constexpr int down_bytes = 2 * s_pad * kDownPitch * 2;
+    // offsets from the 1024-aligned base
+    static constexpr int off_w = 0;
+    static constexpr int off_up = off_w + stages * kWStageBytes;
+    static constexpr int off_down = off_up + stages * up_stage_bytes;
+    static constexpr int off_bar = off_down + down_bytes;          // full[stages], empty[stages]
+    static constexpr int off_plan = off_bar + 2 * 8 * 4 /*room for 4 stages*/;
+    static constexpr int total = off_plan + (int)sizeof(Plan) + 1024 /*alignment slack*/;
+};
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void stmatrix_x4(uint32_t addr, const uint32_t (&r)[4]) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3])
+                 : "memory");
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// 1-D bulk copy global -> smem, completes on bar (bytes % 16 == 0, both sides 16-byte aligned).
+__device__ __forceinline__ void bulk_load_1d(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_addr(uint32_t smem_dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_dst), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_addr(const void* tmap, int c0, int c1, uint32_t smem_src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap), "r"(c0),
+                 "r"(c1), "r"(smem_src)
+                 : "memory");
+}
+
+struct MmaParams {
+    SwitchParams base;
+    const CUtensorMap* tmaps_ld;   // per segment: 64 x 64 swizzled box on the source (live or pristine)
+    const CUtensorMap* tmaps_st;   // per segment: 32 x 64 swizzled box on the live matrix
+};
+
+// Gated DOWN slab for one unit: rows [0, S) hold hi(g*a), rows [s_pad, s_pad+S) hold lo; the
+// padding rows up to s_pad are zero.  16-byte global loads, 16-byte smem stores.
+template <int KS>
+__device__ __forceinline__ void fill_down_hilo(unsigned char* down_smem, const SegDev& sg, const Plan& plan, int S,
+                                               int col0, int tid) {
+    constexpr int s_pad = KS * 16;
+    constexpr int chunks_per_row = kTN / 8;
+    const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(sg.down);
+    const int r = sg.rank;
+    for (int i = tid; i < s_pad * chunks_per_row; i += kConsumers) {
+        const int q = i / chunks_per_row;
+        const int c = (i % chunks_per_row) * 8;
+        uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
+        if (q < S && col0 + c < sg.d_in) {
+            const int b = q / r, qr = q % r;
+            const __nv_bfloat16* src =
+                base + (long long)plan.expert[b] * sg.down_estride + (long long)qr * sg.ld_down + col0 + c;
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
+            const float w = plan.weight[b];
+            const uint32_t in[4] = {v.x, v.y, v.z, v.w};
+            uint32_t oh[4], ol[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float f0 = __fmul_rn(w, bf16lo_to_f32(in[j]));  // adapters.py:202 (f32 gate folding)
+                const float f1 = __fmul_rn(w, bf16hi_to_f32(in[j]));
+                const uint32_t h = pack_bf16x2(f0, f1);
+                oh[j] = h;
+                ol[j] = pack_bf16x2(f0 - bf16lo_to_f32(h), f1 - bf16hi_to_f32(h));
+            }
+            hi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+            lo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+        }
+        *reinterpret_cast<uint4*>(down_smem + ((size_t)q * kDownPitch + c) * 2) = hi;
+        *reinterpret_cast<uint4*>(down_smem + ((size_t)(s_pad + q) * kDownPitch + c) * 2) = lo;
+    }
+}
+
+template <int KS>
+__global__ void __launch_bounds__(kConsumers + 32, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
+    using L = MmaLayout<KS>;
+    constexpr int kSt = L::stages;
+    extern __shared__ unsigned char smem_dyn[];
+    const SwitchParams& p = mp.base;
+    // 128-byte swizzle needs 1024-byte aligned boxes
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::off_bar);
+    uint64_t* empty = full + 4;
+    Plan& plan = *reinterpret_cast<Plan*>(sm + L::off_plan);
+    const int tid = threadIdx.x;
+
+    if (tid == 0) {
+        for (int s = 0; s < kSt; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kMmaWarps);
+        }
+        fence_mbar_init();
+        if (p.use_dev)
+            build_plan(plan, p.from_pristine ? nullptr : p.prev_dev, p.cur_dev, p.scale, false, p.n_experts_limit);
+        else
+            plan = p.host_plan;
+        if (!plan_usable(p, plan, p.prev_dev, p.cur_dev)) plan.n_blocks = -1;
+    }
+    __syncthreads();
+    const int n_blocks = plan.n_blocks;
+    if (n_blocks < 0) return;                       // unusable decision: flagged, nothing touched
+    if (n_blocks == 0 && !p.from_pristine) return;  // unchanged decision: nothing to move
+
+    const uint32_t w_base = smem_u32(sm + L::off_w);
+    const uint32_t up_base = smem_u32(sm + L::off_up);
+
+    if (tid >= kConsumers) {
+        // ============ producer: W boxes by TMA, UP blocks by 1-D bulk copies ============
+        if (tid == kConsumers) {
+            TileIter ti;
+            ti.init(p);
+            SegDev sg;
+            int cur_seg = -1;
+            for (int it = 0; ti.valid(p); ++it) {
+                const int stage = it % kSt;
+                const uint32_t ph = (it / kSt) & 1;
+                if (ti.un.seg != cur_seg) {
+                    cur_seg = ti.un.seg;
+                    sg = p.segs[cur_seg];
+                }
+                const int rows_here = min(kTM, sg.d_out - ti.m0);
+                const uint32_t up_blk_bytes = (uint32_t)rows_here * sg.rank * 2;
+                mbar_wait(&empty[stage], ph ^ 1);
+                mbar_expect_tx(&full[stage], kWStageBytes + n_blocks * up_blk_bytes);
+                const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
+#pragma unroll
+                for (int b = 0; b < kBoxes; ++b)
+                    tma_load_2d_addr(w_base + stage * kWStageBytes + b * kBoxBytes, tm, ti.un.col0 + b * kBoxCols, ti.m0,
+                                     &full[stage]);
+                const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
+                for (int b = 0; b < n_blocks; ++b)
+                    bulk_load_1d(up_base + stage * L::up_stage_bytes + b * (kTM * sg.rank * 2),
+                                 upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * sg.rank,
+                                 up_blk_bytes, &full[stage]);
+                ti.next(p);
+            }
+        }
+        return;
+    }
+
+    // ================================ consumers ====================================
+    const int lane = tid & 31, warp = tid >> 5;
+    const int mi = lane >> 3, rr = lane & 7;       // ldmatrix: lane supplies row rr of matrix mi
+    const int wrow0 = (warp & 1) * 32;             // this warp: rows [wrow0, wrow0+32) ...
+    const int wbox = warp >> 1;                    // ... of box wbox (64 columns)
+    unsigned char* down_smem = sm + L::off_down;
+    const uint32_t down_base = smem_u32(down_smem);
+
+    TileIter ti;
+    ti.init(p);
+    bool new_unit = true;
+    SegDev sg;
+    int S = 0, ks = 0;
+    int prev_stage = -1;
+    for (int it = 0; ti.valid(p); ++it) {
+        const int stage = it % kSt;
+        const uint32_t ph = (it / kSt) & 1;
+        if (new_unit) {
+            sg = p.segs[ti.un.seg];
+            S = n_blocks * sg.rank;
+            ks = (S + 15) >> 4;
+            named_bar_sync(1, kConsumers);  // every warp is done with the previous slab
+            fill_down_hilo<KS>(down_smem, sg, plan, S, ti.un.col0, tid);
+            named_bar_sync(1, kConsumers);  // slab visible
+        }
+        const int m0 = ti.m0;
+        const UnitDev un = ti.un;
+        new_unit = ti.next(p);
+
+        mbar_wait(&full[stage], ph);
+        const uint32_t w_stage = w_base + stage * kWStageBytes + wbox * kBoxBytes;
+        const uint32_t up_stage = up_base + stage * L::up_stage_bytes;
+
+        // ---- A fragments (UP rows of this warp), kept in registers for the whole tile ----
+        uint32_t afrag[2][KS][4];
+#pragma unroll
+        for (int j = 0; j < KS; ++j) {
+            if (j < ks) {
+                const int k0 = 16 * j + (mi >> 1) * 8;  // first rank of the 8x8 matrix this lane addresses
+                const bool live = k0 < S;
+                const int kk = live ? k0 : 0;
+                const int b = kk / sg.rank, kin = kk % sg.rank;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int row = wrow0 + mt * 16 + (mi & 1) * 8 + rr;
+                    ldmatrix_x4(afrag[mt][j], up_stage + ((b * kTM + row) * sg.rank + kin) * 2);
+                    if (16 * j + 8 >= S) {  // ranks past S are padding: their UP columns must read as 0
+                        afrag[mt][j][2] = 0u;
+                        afrag[mt][j][3] = 0u;
+                    }
+                }
+            }
+        }
+
+        // ---- four n16 chunks of the warp's 32 x 64 region ----
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+            float acc[2][2][4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+            const int ncol = wbox * kBoxCols + c4 * 16 + (mi >> 1) * 8;  // slab column this lane addresses
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {  // hi rows then lo rows of the slab
+#pragma unroll
+                for (int j = 0; j < KS; ++j) {
+                    if (j < ks) {
+                        const int krow = half * L::s_pad + 16 * j + (mi & 1) * 8 + rr;
+                        uint32_t bf[4];
+                        ldmatrix_x4_trans(bf, down_base + (krow * kDownPitch + ncol) * 2);
+#pragma unroll
+                        for (int mt = 0; mt < 2; ++mt) {
+                            mma_bf16_16816(acc[mt][0], afrag[mt][j], bf[0], bf[1]);
+                            mma_bf16_16816(acc[mt][1], afrag[mt][j], bf[2], bf[3]);
+                        }
+                    }
+                }
+            }
+            // W + D, rounded RNE to bf16, written back in place (swizzled smem)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int row = wrow0 + mt * 16 + (mi & 1) * 8 + rr;
+                const int chunk = c4 * 2 + (mi >> 1);
+                const uint32_t addr = w_stage + row * 128 + ((chunk ^ (row & 7)) << 4);
+                uint32_t wv[4];
+                ldmatrix_x4(wv, addr);
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const uint32_t a = wv[nt * 2], b2 = wv[nt * 2 + 1];
+                    wv[nt * 2] = pack_bf16x2(bf16lo_to_f32(a) + acc[mt][nt][0], bf16hi_to_f32(a) + acc[mt][nt][1]);
+                    wv[nt * 2 + 1] = pack_bf16x2(bf16lo_to_f32(b2) + acc[mt][nt][2], bf16hi_to_f32(b2) + acc[mt][nt][3]);
+                }
+                stmatrix_x4(addr, wv);
+            }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d_addr(mp.tmaps_st + un.seg, un.col0 + wbox * kBoxCols, m0 + wrow0, w_stage + wrow0 * 128);
+            bulk_commit();
+            bulk_wait_read<1>();  // this warp's store of the previous tile has drained its smem
+            if (prev_stage >= 0) mbar_arrive(&empty[prev_stage]);
+            prev_stage = stage;
+        }
+    }
+    if (lane == 0) bulk_wait_all<0>();
+}
+
+}  // namespace af
