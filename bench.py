@@ -1,0 +1,348 @@
+"""Contract benchmark of the AdaFuse hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload llama2-7b]
+
+A "step" is one decoded token of a bs=1 sequence through the whole hot path: pre-gate on the
+token's embedding row, ONE fused switch over all 7 x L adapted matrices (a teacher-forced token
+stream makes every step really switch), the merged-path forward (plain GEMVs
+over the live bf16 weights, GQA attention over the KV cache), lm_head and argmax.
+
+  value        tokens/s with every per-step input already in HBM (forced token stream on the
+               device, the step replayed as one CUDA graph), max over ranks.
+  e2e          the same metric through the public API `LlamaEngine.decode_step(token)`: the
+               consumed token comes from pinned host memory every step (4 B H2D) and the next
+               token is read back (4 B D2H).
+  roofline     the fused-switch kernel: algorithmic bytes / its average launch
+               duration, CUDA events on the launching stream inside the e2e timed region,
+               against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline the CPU oracle port (oracle/, reference algorithm restated in C) timed on this
+               box's host cores on a bounded sample (whole layers), scaled to tokens/s.
+
+`--impl reference` times that CPU port alone (the reference itself is pure Python and does not
+exist on the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "bs=1 decode tok/s with a fused switch every token (switch us/token and HBM GB/s in extra keys)"
+UNIT = "tokens/s"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        return float(json.load(open(path))["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ CPU arm ----
+
+
+def cpu_sample(cfg_kw: dict, budget_s: float = 15.0, max_layers: int | None = None):
+    """Time the oracle port (reference algorithm, f32 arithmetic on bf16 weights) on whole
+    layers of the workload: per layer the steady switch of its 7 matrices (s = 2kr) and the 7
+    backbone GEMVs.  Returns (seconds per token extrapolated to all layers, layers timed, threads)."""
+    from oracle import oracle as orc
+
+    d, ffn, L = cfg_kw["hidden"], cfg_kw["ffn"], cfg_kw["layers"]
+    hd = d // cfg_kw["n_heads"]
+    kv = cfg_kw["n_kv_heads"] * hd
+    n, r, k = cfg_kw["experts"], cfg_kw["rank"], cfg_kw["top_k"]
+    shapes = [(d, d), (kv, d), (kv, d), (d, d), (ffn, d), (ffn, d), (d, ffn)]
+    rng = np.random.Generator(np.random.PCG64(0))
+    segs = []
+    for d_out, d_in in shapes:
+        w = orc.to_bf16_bits((rng.random((d_out, d_in), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(d_in)))
+        dn = orc.to_bf16_bits((rng.random((n, r, d_in), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(d_in)))
+        up = orc.to_bf16_bits((rng.random((n, d_out, r), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(r)))
+        segs.append((w, dn, up, rng.random(d_in, dtype=np.float32)))
+    prev = (tuple(range(k)), tuple([1.0 / k] * k))
+    cur = (tuple(range(k, 2 * k)), tuple([1.0 / k] * k))
+    done, t_total = 0, 0.0
+    cap = max_layers or L
+    while done < cap and (done == 0 or t_total + t_total / done <= budget_s):
+        t0 = time.perf_counter()
+        for w, dn, up, x in segs:
+            orc.switch_segment_bf16(w, dn, up, prev, cur)
+            orc.gemv_bf16(w, x)
+        t_total += time.perf_counter() - t0
+        prev, cur = cur, prev
+        done += 1
+    return t_total / done * L, done, orc.num_threads()
+
+
+def run_reference_arm(args, cfg_kw):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per_step_budget = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    vals, layers_timed, threads = [], 0, 1
+    for i in range(args.warmup + args.steps):
+        sec_per_token, layers_timed, threads = cpu_sample(cfg_kw, budget_s=per_step_budget, max_layers=4)
+        if i >= args.warmup:
+            vals.append(sec_per_token)
+    sec = statistics.mean(vals)
+    v = 1.0 / sec
+    sample = f"{layers_timed} of {cfg_kw['layers']} layers per step (steady switch s=2kr + 7 GEMVs each), scaled to all layers"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16 storage, f32 accumulate", "data": "synthetic",
+        "config": {"workload": args.workload, "note": "CPU port of the reference algorithm (oracle/liboracle.so, OpenMP); "
+                   "the reference package itself is pure Python and is not present on the GPU box"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ clocks ----
+
+
+class ClockSampler:
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [c for c in sm if mx and c > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU arm ----
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="llama2-7b")
+    ap.add_argument("--switch-mode", default="inplace", choices=["inplace", "from_pristine"])
+    ap.add_argument("--compute", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2603_11873_b200 import llama
+
+    cfg_kw = dict(llama.PRESETS[args.workload])
+    if args.impl == "reference":
+        run_reference_arm(args, cfg_kw)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_11873_b200 import _capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    max_seq = 2 * (args.steps + args.warmup) + 16
+    cfg = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
+                       compute=args.compute, keep_pristine=True)
+    eng = llama.LlamaEngine(cfg, init="device")
+    info = eng.table.info()
+    forced = np.random.Generator(np.random.PCG64(cfg.seed + 1)).integers(0, cfg.vocab, 4096)
+    peak, peak_kind = load_peaks()
+
+    def timed(fn, n):
+        """n calls of fn bracketed by barrier + synchronize, device time by CUDA events."""
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # ---------------- (1) e2e: public API, host token in / next token out, eager launches ----
+    eng.reset(forced=forced)
+    pinned = torch.from_numpy(forced.astype(np.int32)).pin_memory()
+    switch_events = []
+    orig_switch = eng._switch_for_step
+
+    def instrumented_switch(with_prev):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        orig_switch(with_prev)
+        b.record()
+        switch_events.append((a, b))
+
+    step_i = [0]
+
+    def api_step():
+        i = step_i[0]
+        eng.token_dev.copy_(pinned[i:i + 1], non_blocking=True)      # H2D of the step's input
+        eng._step_body(eng.have_prev)
+        eng.have_prev = True
+        _ = int(eng.next_dev.item())                                   # D2H of the step's result
+        step_i[0] = i + 1
+
+    for _ in range(args.warmup):
+        api_step()
+    eng._switch_for_step = instrumented_switch
+    launches0 = _capi.launch_count()
+    sampler = ClockSampler(local_rank)
+    e2e_ms = timed(api_step, args.steps)
+    launches_e2e = _capi.launch_count() - launches0
+    eng._switch_for_step = orig_switch
+    sw_ms = [a.elapsed_time(b) for a, b in switch_events]
+    switch_ms = statistics.mean(sw_ms)
+    e2e_value = args.steps / (e2e_ms / 1e3)
+
+    # ---------------- (2) value: inputs resident, the step replayed as one CUDA graph ----
+    graph_ok = world == 1
+    if graph_ok:
+        eng.capture()
+        for _ in range(args.warmup):
+            eng.replay()
+        dev_ms = timed(eng.replay, args.steps)
+        launches_per_step = launches_e2e // args.steps
+    else:
+        def dev_step():
+            eng._step_body(True)
+        for _ in range(args.warmup):
+            dev_step()
+        dev_ms = timed(dev_step, args.steps)
+        launches_per_step = launches_e2e // args.steps
+    clocks = sampler.stop()
+    value = args.steps / (dev_ms / 1e3)
+    eng.table.status()
+
+    # ---------------- (3) the adapter-free backbone with the same kernels (decode only) ----
+    def decode_only():
+        eng.forward()
+        eng._advance()
+
+    if graph_ok:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                decode_only()
+        torch.cuda.current_stream().wait_stream(side)
+        eng.pos_dev.fill_(8)
+        for _ in range(3):
+            g.replay()
+        eng.pos_dev.fill_(8)
+        dec_ms = timed(g.replay, min(args.steps, 30))
+        dec_n = min(args.steps, 30)
+    else:
+        eng.pos_dev.fill_(8)
+        dec_n = min(args.steps, 30)
+        dec_ms = timed(decode_only, dec_n)
+    decode_only_tok_s = dec_n / (dec_ms / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    sw_bytes = cfg.switch_bytes(steady=True)
+    achieved = sw_bytes / (switch_ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16 storage, f32 accumulate", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: Llama-shaped bf16, {cfg.experts} experts rank {cfg.rank} top-{cfg.top_k} on q/k/v/o/gate/up/down, "
+                               f"bs=1 decode, teacher-forced tokens, switch every token ({cfg.switch_mode})",
+                   "parallelism": f"tp{world}", "l2": "inputs larger than L2 (weights 13 GB >> 126 MB), no flush needed",
+                   "segments": info["n_segments"], "work_units": info["n_units"], "compute": args.compute},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4,
+                "ms_per_step": e2e_ms / args.steps},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "launches_per_step": int(launches_per_step),
+        "clocks": clocks,
+        "switch_us_per_token": switch_ms * 1e3,
+        "switch_hbm_gbs": achieved,
+        "decode_only_tok_s": decode_only_tok_s,
+        "decode_only_hbm_gbs": cfg.decode_bytes() * decode_only_tok_s / 1e9,
+        "roofline": {"bound": "hbm", "kernel": "switch_mma_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                     "bytes_per_launch": sw_bytes, "avg_launch_ms": switch_ms, "min_launch_ms": min(sw_ms), "traffic": None},
+    }
+    traffic_path = os.path.join(ROOT, "profiles", "switch_traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            tr = json.load(open(traffic_path))
+            if tr.get("workload") == args.workload:
+                out["roofline"]["traffic"] = tr.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            pass
+    if not args.no_cpu_baseline:
+        sec_per_token, layers_timed, threads = cpu_sample(cfg_kw, budget_s=15.0)
+        out["cpu_baseline"] = {
+            "value": 1.0 / sec_per_token, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{layers_timed} of {cfg_kw['layers']} layers (steady switch s=2kr + 7 GEMVs per layer) on the oracle port, "
+                      f"scaled to all layers; host has {os.cpu_count()} logical cores",
+        }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,40 @@ int af_argmax(const float* v, int32_t n, int32_t* out_dev, void* stream);
 int af_embed(const void* table, int32_t dtype, int32_t d, const int32_t* token_dev, float* out,
              void* stream);
 
+/* ---- Llama-shaped block, bs=1 (BASELINE.json configs 2-5) ----------------------------
+ * The reference's layer is x + gelu(W x) (model.py:266-305); the metric's configurations are
+ * Llama-shaped, for which the reference has no dataflow.  These are the
+ * merged-path forward of model.py:367-371 for that block: plain GEMVs over the live weights
+ * with the small ops fused in.
+ *
+ * af_gemv_fused : out = epilogue(W . prologue(x)); W rows x cols bf16 (cols % 8 == 0).
+ *    prologue AF_PRO_RMSNORM : x * rsqrt(mean(x^2) + eps) * norm_w        (x has cols entries)
+ *    prologue AF_PRO_SILU_MUL: silu(x[c]) * x[cols + c]                   (x has 2*cols entries)
+ *    epilogue as af_gemv.
+ * af_attn_decode: RoPE(q, k) at position *pos_dev, append k/v to the bf16 cache, single-query
+ *    GQA attention over positions 0..*pos_dev.  qkv = [q | k | v] f32, caches
+ *    [n_kv][max_seq][head_dim] bf16, cos/sin [max_seq][head_dim/2] f32.
+ * af_argmax_val : argmax + the winning value, index shifted by index_offset (vocab-parallel
+ *    lm_head).
+ * af_step_advance: end-of-step bookkeeping in one launch so a decode step is a static CUDA
+ *    graph: prev <- cur decision, *pos += 1, *step += 1, history[step] = *next,
+ *    *token = forced ? forced[(step+1) % n_forced] : *next.  Any pointer may be NULL. */
+#define AF_PRO_NONE 0
+#define AF_PRO_RMSNORM 1
+#define AF_PRO_SILU_MUL 2
+int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const float* x, float* out,
+                  int32_t prologue, const float* norm_w, float eps, int32_t epilogue, const float* res,
+                  void* stream);
+int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table,
+                   const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
+                   int32_t head_dim, int32_t max_seq, float* out, void* stream);
+int af_argmax_val(const float* v, int32_t n, int32_t index_offset, int32_t* out_idx_dev,
+                  float* out_val_dev, void* stream);
+int af_step_advance(af_decision* prev_dev, const af_decision* cur_dev, int32_t* pos_dev,
+                    int32_t* step_dev, int32_t* token_dev, const int32_t* next_dev,
+                    const int32_t* forced_dev, int32_t n_forced, int32_t* history_dev,
+                    int32_t n_history, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,7 +95,12 @@ SIGNATURES = {
     "af_gemv_t": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i64, _vp, _vp, _vp]),
     "af_argmax": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "af_embed": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
+    "af_gemv_fused": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, _vp, _i32, _vp, _f32, _i32, _vp, _vp]),
+    "af_attn_decode": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "af_argmax_val": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
+    "af_step_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp]),
 }
+AF_PRO_NONE, AF_PRO_RMSNORM, AF_PRO_SILU_MUL = 0, 1, 2
 
 _lib = None
 

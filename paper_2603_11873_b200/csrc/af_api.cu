@@ -580,4 +580,67 @@ int af_embed(const void* table, int32_t dtype, int32_t d, const int32_t* token_d
     return AF_OK;
 }
 
+// ------------------------------------------------------------------ Llama block ----
+
+int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const float* x, float* out, int32_t prologue,
+                  const float* norm_w, float eps, int32_t epilogue, const float* res, void* stream) {
+    if (rows < 0 || cols < 1 || ld < cols) return fail(AF_EDIM, "bad GEMV shape");
+    if (cols % 8 != 0 || ld % 8 != 0 || (reinterpret_cast<uintptr_t>(w) & 15) != 0)
+        return fail(AF_EDIM, "fused GEMV needs 16-byte aligned bf16 rows (cols % 8 == 0)");
+    if (prologue < AF_PRO_NONE || prologue > AF_PRO_SILU_MUL) return fail(AF_EVALUE, "unknown prologue");
+    if (prologue == AF_PRO_RMSNORM && !norm_w) return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
+    if (epilogue < AF_EPI_NONE || epilogue > AF_EPI_RESIDUAL) return fail(AF_EVALUE, "unknown epilogue");
+    if (epilogue != AF_EPI_NONE && !res) return fail(AF_EVALUE, "epilogue needs a residual vector");
+    if (!w || !x || !out) return fail(AF_EVALUE, "NULL argument");
+    if (out == x) return fail(AF_EALIAS, "GEMV output aliases its input");
+    if (rows == 0) return AF_OK;
+    const DeviceInfo& di = device_info();
+    const int smem = cols * 4;
+    if (smem + 1024 > di.max_smem_optin) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
+    static int configured_smem = 48 * 1024;
+    if (smem > configured_smem) {
+        AF_CUDA_TRY(cudaFuncSetAttribute(gemv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured_smem = smem;
+    }
+    const int rows_per_cta = (kGemvFThreads / 32) * kGemvFRows;
+    // resident CTAs per SM are bounded by the staged vector; keep every SM busy with >= 2 waves of rows
+    const int per_sm = std::max(1, std::min(8, (di.max_smem_optin) / (smem + 2048)));
+    const int grid = std::max(1, std::min((rows + rows_per_cta - 1) / rows_per_cta, di.sm_count * per_sm));
+    gemv_fused_kernel<<<grid, kGemvFThreads, smem, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(w), rows, cols,
+                                                                         ld, x, out, prologue, norm_w, eps, epilogue, res);
+    AF_LAUNCH_CHECK("gemv_fused_kernel");
+    return AF_OK;
+}
+
+int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table, const float* sin_table,
+                   const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t max_seq,
+                   float* out, void* stream) {
+    if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads != 0) return fail(AF_EDIM, "heads must be a multiple of kv heads");
+    if (head_dim < 2 || head_dim % 2 != 0 || head_dim > kAttnMaxHd) return fail(AF_EDIM, "head_dim must be even and <= 256");
+    if (max_seq < 1) return fail(AF_EDIM, "max_seq must be positive");
+    if (!qkv || !k_cache || !v_cache || !cos_table || !sin_table || !pos_dev || !out) return fail(AF_EVALUE, "NULL argument");
+    attn_decode_kernel<<<n_heads, kAttnThreads, 0, as_stream(stream)>>>(
+        qkv, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache), cos_table, sin_table,
+        pos_dev, n_heads, n_kv_heads, head_dim, max_seq, 1.0f / sqrtf((float)head_dim), out);
+    AF_LAUNCH_CHECK("attn_decode_kernel");
+    return AF_OK;
+}
+
+int af_argmax_val(const float* v, int32_t n, int32_t index_offset, int32_t* out_idx_dev, float* out_val_dev, void* stream) {
+    if (n < 1 || !v || !out_idx_dev) return fail(AF_EDIM, "argmax of an empty vector");
+    argmax_val_kernel<<<1, 1024, 0, as_stream(stream)>>>(v, n, index_offset, out_idx_dev, out_val_dev);
+    AF_LAUNCH_CHECK("argmax_val_kernel");
+    return AF_OK;
+}
+
+int af_step_advance(af_decision* prev_dev, const af_decision* cur_dev, int32_t* pos_dev, int32_t* step_dev,
+                    int32_t* token_dev, const int32_t* next_dev, const int32_t* forced_dev, int32_t n_forced,
+                    int32_t* history_dev, int32_t n_history, void* stream) {
+    if (!step_dev || !token_dev || !next_dev) return fail(AF_EVALUE, "NULL argument");
+    step_advance_kernel<<<1, 32, 0, as_stream(stream)>>>(prev_dev, cur_dev, pos_dev, step_dev, token_dev, next_dev, forced_dev,
+                                                         n_forced, history_dev, n_history);
+    AF_LAUNCH_CHECK("step_advance_kernel");
+    return AF_OK;
+}
+
 }  // extern "C"

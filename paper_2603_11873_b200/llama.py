@@ -1,0 +1,530 @@
+"""Llama-shaped AdaFuse decode engine (BASELINE.json configs 2-5).
+
+The reference's decoder has one adapted d x d matrix per layer (model.py:3-7); the
+configurations the headline metric is quoted on adapt q/k/v/o/gate/up/down of a Llama block.
+This module is the same per-token hot path -- model.py:332-371 `_merged_pass`:
+
+    pre-gate once per token on the embedding row  ->  ONE fused switch over all 7 x L
+    adapted matrices  ->  plain backbone GEMVs  ->  lm_head  ->  argmax
+
+on those shapes.  Everything per token stays on the device and is a fixed launch sequence,
+so a whole step is captured once in a CUDA graph and replayed.
+
+Tensor parallelism: q/k/v/gate/up are column-parallel (d_out split), o/down
+row-parallel (d_in split); each rank builds the descriptor table over ITS shard and runs the
+identical switch kernel -- no data-path collective in the switch; the routing decision is
+computed on rank 0 and broadcast (one 128-byte NCCL broadcast per token).  The decode GEMVs
+need the usual two all-reduces per layer and an (value, index) all-gather for the
+vocab-parallel lm_head.
+"""
+
+from __future__ import annotations
+
+import math
+import zlib
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _capi
+from .adapters import SwitchTable
+from .errors import ConfigError, InputError, StateError
+from .linalg import DispatchRecorder, Matrix, _ptr
+from .routing import DECISION_BYTES, DeviceDecision, GateDecision
+
+SEGMENT_NAMES = ("q", "k", "v", "o", "gate", "up", "down")
+_COLUMN_PARALLEL = ("q", "k", "v", "gate", "up")
+
+
+@dataclass(frozen=True, slots=True)
+class LlamaConfig:
+    layers: int = 2
+    hidden: int = 256
+    ffn: int = 512
+    n_heads: int = 4
+    n_kv_heads: int = 2
+    vocab: int = 512
+    experts: int = 8
+    rank: int = 8
+    top_k: int = 2
+    rope_theta: float = 10000.0
+    rms_eps: float = 1e-5
+    max_seq: int = 256
+    seed: int = 0
+    tp_size: int = 1
+    tp_rank: int = 0
+    compute: str = "auto"
+    switch_mode: str = "inplace"     # or "from_pristine"
+    adapters: bool = True            # False = adapter-free backbone (the reference's BASE strategy)
+    keep_pristine: bool = True
+
+    def validate(self) -> None:
+        for name in ("layers", "hidden", "ffn", "n_heads", "n_kv_heads", "vocab", "experts", "rank", "top_k", "max_seq", "tp_size"):
+            v = getattr(self, name)
+            if not isinstance(v, int) or isinstance(v, bool) or v < 1:
+                raise ValueError(f"{name} must be a positive integer, got {v!r}")
+        if self.hidden % self.n_heads or self.n_heads % self.n_kv_heads:
+            raise ValueError("hidden must divide into heads, heads into kv heads")
+        if (self.hidden // self.n_heads) % 2 or self.hidden // self.n_heads > 256:
+            raise ValueError("head_dim must be even and <= 256")
+        if self.top_k > self.experts or self.top_k > _capi.AF_MAX_K:
+            raise ValueError(f"top_k={self.top_k} exceeds experts={self.experts} or {_capi.AF_MAX_K}")
+        if self.rank > self.hidden:
+            raise ValueError(f"rank={self.rank} exceeds hidden={self.hidden}")
+        if not 0 <= self.tp_rank < self.tp_size:
+            raise ValueError("tp_rank outside [0, tp_size)")
+        if self.n_kv_heads % self.tp_size or self.ffn % self.tp_size or self.vocab % self.tp_size:
+            raise ValueError("kv heads, ffn and vocab must divide by tp_size")
+        if (self.ffn // self.tp_size) % 8 or self.hidden % 8:
+            raise ValueError("hidden and the local ffn width must be multiples of 8 (16-byte bf16 rows)")
+        if self.compute not in _capi.COMPUTE_MODES:
+            raise ValueError(f"unknown compute mode {self.compute!r}")
+        if self.switch_mode not in ("inplace", "from_pristine"):
+            raise ValueError(f"unknown switch mode {self.switch_mode!r}")
+        if self.switch_mode == "from_pristine" and not self.keep_pristine:
+            raise ValueError("from_pristine needs keep_pristine")
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.n_heads
+
+    def segment_shapes(self) -> dict:
+        """Local (per-rank) d_out x d_in of the seven adapted matrices of one layer."""
+        d, hd, tp = self.hidden, self.head_dim, self.tp_size
+        q, kv, f = self.n_heads // tp * hd, self.n_kv_heads // tp * hd, self.ffn // tp
+        return {"q": (q, d), "k": (kv, d), "v": (kv, d), "o": (d, q), "gate": (f, d), "up": (f, d), "down": (d, f)}
+
+    def full_segment_shapes(self) -> dict:
+        return replace(self, tp_size=1, tp_rank=0).segment_shapes()
+
+    def switch_bytes(self, steady: bool = True) -> int:
+        """Algorithmic bytes of one switch on this rank."""
+        s = (2 if steady and self.switch_mode == "inplace" else 1) * self.top_k * self.rank
+        return self.layers * sum(4 * o * i + 2 * s * (o + i) for o, i in self.segment_shapes().values())
+
+    def decode_bytes(self) -> int:
+        """Bytes one decode forward must read on this rank: every W once + lm_head."""
+        w = self.layers * sum(2 * o * i for o, i in self.segment_shapes().values())
+        return w + 2 * (self.vocab // self.tp_size) * self.hidden
+
+
+PRESETS = {
+    # BASELINE.json configs[1..4]
+    "llama2-7b": dict(layers=32, hidden=4096, ffn=11008, n_heads=32, n_kv_heads=32, vocab=32000, experts=8, rank=8, top_k=2),
+    "llama3-8b": dict(layers=32, hidden=4096, ffn=14336, n_heads=32, n_kv_heads=8, vocab=128256, experts=16, rank=16, top_k=2,
+                      rope_theta=500000.0),
+    "llama2-13b": dict(layers=40, hidden=5120, ffn=13824, n_heads=40, n_kv_heads=40, vocab=32000, experts=8, rank=8, top_k=2),
+    "llama2-70b": dict(layers=80, hidden=8192, ffn=28672, n_heads=64, n_kv_heads=8, vocab=32000, experts=8, rank=32, top_k=4),
+    "tiny": dict(layers=2, hidden=256, ffn=512, n_heads=4, n_kv_heads=2, vocab=512, experts=8, rank=8, top_k=2),
+}
+
+
+def preset(name: str, **overrides) -> LlamaConfig:
+    if name not in PRESETS:
+        raise ConfigError(f"unknown preset {name!r}; known: {sorted(PRESETS)}")
+    cfg = LlamaConfig(**{**PRESETS[name], **overrides})
+    cfg.validate()
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# Synthetic weights
+# ---------------------------------------------------------------------------
+
+
+def tensor_seed(seed: int, name: str) -> int:
+    return (zlib.crc32(name.encode()) ^ (seed * 0x9E3779B1)) & 0xFFFFFFFF
+
+
+def host_tensor(cfg: LlamaConfig, name: str, shape, fan_in: int) -> np.ndarray:
+    """Full (unsharded) tensor `name`: PCG64(seed ^ crc(name)), uniform +-1/sqrt(fan_in)
+    (the reference's distribution, model.py:184-189), drawn in f64, cast to f32.  Keyed by
+    NAME so any rank -- and the CPU oracle -- regenerates exactly the slice it needs."""
+    rng = np.random.Generator(np.random.PCG64(tensor_seed(cfg.seed, name)))
+    b = 1.0 / math.sqrt(fan_in)
+    return rng.uniform(-b, b, size=shape).astype(np.float32)
+
+
+def shard_rows(a, tp, rank):
+    n = a.shape[-2] // tp
+    return a[..., rank * n:(rank + 1) * n, :]
+
+
+def shard_cols(a, tp, rank):
+    n = a.shape[-1] // tp
+    return a[..., rank * n:(rank + 1) * n]
+
+
+def host_weights(cfg: LlamaConfig) -> dict:
+    """All weights of THIS rank as f32 host arrays (small configs / parity runs)."""
+    full = cfg.full_segment_shapes()
+    tp, rk = cfg.tp_size, cfg.tp_rank
+    hd = cfg.head_dim
+    out = {
+        "embed": host_tensor(cfg, "embed", (cfg.vocab, cfg.hidden), cfg.hidden),
+        "router": host_tensor(cfg, "router", (cfg.experts, cfg.hidden), cfg.hidden),
+        "lm_head": shard_rows(host_tensor(cfg, "lm_head", (cfg.vocab, cfg.hidden), cfg.hidden), tp, rk),
+        "final_norm": 1.0 + 0.1 * host_tensor(cfg, "final_norm", (cfg.hidden,), 1),
+        "layers": [],
+    }
+    for li in range(cfg.layers):
+        lw = {"attn_norm": 1.0 + 0.1 * host_tensor(cfg, f"l{li}.attn_norm", (cfg.hidden,), 1),
+              "ffn_norm": 1.0 + 0.1 * host_tensor(cfg, f"l{li}.ffn_norm", (cfg.hidden,), 1)}
+        for name in SEGMENT_NAMES:
+            d_out, d_in = full[name]
+            w = host_tensor(cfg, f"l{li}.{name}.w", (d_out, d_in), d_in)
+            dn = host_tensor(cfg, f"l{li}.{name}.down", (cfg.experts, cfg.rank, d_in), d_in)
+            up = host_tensor(cfg, f"l{li}.{name}.up", (cfg.experts, d_out, cfg.rank), cfg.rank)
+            if name in _COLUMN_PARALLEL:   # split d_out: shard W rows and UP rows, replicate DOWN
+                w, up = shard_rows(w, tp, rk), shard_rows(up, tp, rk)
+            else:                          # split d_in: shard W cols and DOWN cols, replicate UP
+                w, dn = shard_cols(w, tp, rk), shard_cols(dn, tp, rk)
+            lw[name] = {"w": np.ascontiguousarray(w), "down": np.ascontiguousarray(dn), "up": np.ascontiguousarray(up)}
+        out["layers"].append(lw)
+    _ = hd
+    return out
+
+
+def rope_tables(cfg: LlamaConfig):
+    half = cfg.head_dim // 2
+    inv = cfg.rope_theta ** (-np.arange(half, dtype=np.float64) * 2.0 / cfg.head_dim)
+    ang = np.arange(cfg.max_seq, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# Collectives (only where the path has a real exchange)
+# ---------------------------------------------------------------------------
+
+
+class Collectives:
+    """torch.distributed plumbing of the TP path.  With tp_size == 1 every method is a no-op."""
+
+    def __init__(self, group=None, tp_size: int = 1):
+        self.group = group
+        self.tp_size = tp_size
+        if tp_size > 1:
+            import torch.distributed as dist
+
+            if not dist.is_initialized():
+                raise StateError("tp_size > 1 needs torch.distributed to be initialised")
+            self.dist = dist
+
+    def broadcast_decision(self, buf: torch.Tensor) -> None:
+        """The ONLY collective of the switch path: rank 0's 128-byte decision record."""
+        if self.tp_size > 1:
+            self.dist.broadcast(buf, src=self.dist.get_global_rank(self.group, 0) if self.group is not None else 0, group=self.group)
+
+    def all_reduce_sum(self, t: torch.Tensor) -> None:
+        if self.tp_size > 1:
+            self.dist.all_reduce(t, group=self.group)
+
+    def argmax_pairs(self, val: torch.Tensor, idx: torch.Tensor, out_idx: torch.Tensor) -> None:
+        """Vocab-parallel argmax: gather (value, index) pairs, keep the largest value, lowest
+        index on ties (model.py:396)."""
+        if self.tp_size == 1:
+            return
+        pair = torch.stack([val.view(1), idx.view(1).to(torch.float32)], dim=1)  # idx < 2^24 is exact in f32
+        gathered = [torch.empty_like(pair) for _ in range(self.tp_size)]
+        self.dist.all_gather(gathered, pair, group=self.group)
+        allp = torch.cat(gathered, dim=0)
+        best = torch.max(allp[:, 0])
+        cand = torch.where(allp[:, 0] == best, allp[:, 1], torch.full_like(allp[:, 1], float("inf")))
+        out_idx.copy_(torch.min(cand).to(torch.int32).view(1))
+
+
+class NoPeers(Collectives):
+    """Exchange layer of a shard inspected in isolation (switch-only use: nothing to exchange)."""
+
+    def __init__(self):
+        self.group, self.tp_size = None, 1
+
+
+# ---------------------------------------------------------------------------
+# Engine
+# ---------------------------------------------------------------------------
+
+
+class LlamaEngine:
+    """Resident weights, expert bank, descriptor table, KV cache and the captured decode step."""
+
+    def __init__(self, cfg: LlamaConfig, init: str = "host", device=None, group=None, comm=None):
+        cfg.validate()
+        torch_ = _capi.require_cuda()
+        self.cfg = cfg
+        self.dev = torch_.device(device) if device is not None else torch_.device("cuda", torch_.cuda.current_device())
+        # `comm` lets a caller supply the exchange layer (tests build one shard with no peers)
+        self.comm = comm if comm is not None else Collectives(group, cfg.tp_size)
+        self.recorder = DispatchRecorder()
+        d, hd = cfg.hidden, cfg.head_dim
+        shp = cfg.segment_shapes()
+        self.q_rows, self.kv_rows, self.ffn_local = shp["q"][0], shp["k"][0], shp["gate"][0]
+        self.heads_local, self.kv_local = self.q_rows // hd, self.kv_rows // hd
+        self.vocab_local = cfg.vocab // cfg.tp_size
+        bf = torch.bfloat16
+        dev = self.dev
+        if init not in ("host", "device"):
+            raise ValueError("init must be 'host' (PCG64, reproducible on the CPU oracle) or 'device' (throughput runs)")
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(cfg.seed * 1000003 + cfg.tp_rank)
+
+        def dev_uniform(shape, fan_in, dtype=bf):
+            t = torch.empty(shape, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=gen)
+            return t.mul_(fan_in ** -0.5).to(dtype)
+
+        hw = host_weights(cfg) if init == "host" else None
+
+        def put(a, dtype=bf):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype).contiguous()
+
+        self.embed = Matrix(put(hw["embed"]) if hw else dev_uniform((cfg.vocab, d), d), "bf16")
+        self.router = Matrix(put(hw["router"]) if hw else dev_uniform((cfg.experts, d), d), "bf16")
+        self.lm_head = Matrix(put(hw["lm_head"]) if hw else dev_uniform((self.vocab_local, d), d), "bf16")
+        self.final_norm = put(hw["final_norm"], torch.float32) if hw else torch.ones(d, dtype=torch.float32, device=dev)
+        self.wqkv, self.wo, self.wgu, self.wdown = [], [], [], []
+        self.attn_norm, self.ffn_norm = [], []
+        targets, downs, ups = [], [], []
+        for li in range(cfg.layers):
+            qkv = torch.empty((self.q_rows + 2 * self.kv_rows, d), dtype=bf, device=dev)
+            gu = torch.empty((2 * self.ffn_local, d), dtype=bf, device=dev)
+            wo = torch.empty((d, self.q_rows), dtype=bf, device=dev)
+            wdn = torch.empty((d, self.ffn_local), dtype=bf, device=dev)
+            views = {
+                "q": qkv[: self.q_rows], "k": qkv[self.q_rows: self.q_rows + self.kv_rows], "v": qkv[self.q_rows + self.kv_rows:],
+                "o": wo, "gate": gu[: self.ffn_local], "up": gu[self.ffn_local:], "down": wdn,
+            }
+            for name in SEGMENT_NAMES:
+                d_out, d_in = shp[name]
+                if hw:
+                    views[name].copy_(put(hw["layers"][li][name]["w"]))
+                    dn, up = put(hw["layers"][li][name]["down"]), put(hw["layers"][li][name]["up"])
+                else:
+                    views[name].copy_(dev_uniform((d_out, d_in), cfg.full_segment_shapes()[name][1]))
+                    dn = dev_uniform((cfg.experts, cfg.rank, d_in), cfg.full_segment_shapes()[name][1])
+                    up = dev_uniform((cfg.experts, d_out, cfg.rank), cfg.rank)
+                targets.append(Matrix(views[name], "bf16"))
+                downs.append(dn)
+                ups.append(up)
+            self.wqkv.append(qkv)
+            self.wo.append(wo)
+            self.wgu.append(gu)
+            self.wdown.append(wdn)
+            self.attn_norm.append(put(hw["layers"][li]["attn_norm"], torch.float32) if hw else torch.ones(d, dtype=torch.float32, device=dev))
+            self.ffn_norm.append(put(hw["layers"][li]["ffn_norm"], torch.float32) if hw else torch.ones(d, dtype=torch.float32, device=dev))
+        self.targets, self.bank_down, self.bank_up = targets, downs, ups
+        self.pristine = [t.copy() for t in targets] if (cfg.adapters and cfg.keep_pristine) else None
+        self.table = SwitchTable(targets, downs, ups, pristine=self.pristine) if cfg.adapters else None
+        cos, sin = rope_tables(cfg)
+        self.cos, self.sin = put(cos, torch.float32), put(sin, torch.float32)
+        self.k_cache = [torch.zeros((self.kv_local, cfg.max_seq, hd), dtype=bf, device=dev) for _ in range(cfg.layers)]
+        self.v_cache = [torch.zeros((self.kv_local, cfg.max_seq, hd), dtype=bf, device=dev) for _ in range(cfg.layers)]
+        # per-step device state
+        f32 = torch.float32
+        self.x = [torch.zeros(d, dtype=f32, device=dev) for _ in range(2)]
+        self.qkv_buf = torch.zeros(self.q_rows + 2 * self.kv_rows, dtype=f32, device=dev)
+        self.attn_buf = torch.zeros(self.q_rows, dtype=f32, device=dev)
+        self.gu_buf = torch.zeros(2 * self.ffn_local, dtype=f32, device=dev)
+        self.logits = torch.zeros(self.vocab_local, dtype=f32, device=dev)
+        self.token_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.next_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.next_val = torch.zeros(1, dtype=f32, device=dev)
+        self.pos_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.cur = DeviceDecision(dev)
+        self.prev = DeviceDecision(dev)
+        self.have_prev = False
+        self.history = torch.zeros(cfg.max_seq, dtype=torch.int32, device=dev)
+        self.forced_dev = None
+        self._graphs = {}
+
+    # -- the pieces of one step ---------------------------------------------------------
+
+    def _check(self, status):
+        _capi.check(status)
+
+    def pregate(self) -> DeviceDecision:
+        """Pre-gate on the embedding row of *token_dev (model.py:342-343), then broadcast."""
+        cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
+        if cfg.tp_rank == 0 or cfg.tp_size == 1:
+            self._check(L.af_pregate(_ptr(self.router.data), _capi.AF_BF16, cfg.experts, cfg.hidden, _ptr(self.embed.data),
+                                     _capi.AF_BF16, _ptr(self.token_dev), cfg.top_k, self.cur.ptr, None, st))
+        self.comm.broadcast_decision(self.cur.buf)
+        return self.cur
+
+    def fused_switch(self, prev, cur, **kw) -> None:
+        """W <- W + delta(cur) - delta(prev) over all 7 x L local shards, one launch."""
+        if self.table is None:
+            raise StateError("this engine was built without adapters")
+        kw.setdefault("max_k", self.cfg.top_k)
+        kw.setdefault("compute", self.cfg.compute)
+        self.table.switch(prev, cur, **kw)
+
+    def merge(self, dec, **kw) -> None:
+        self.fused_switch(None, dec, **kw)
+
+    def unmerge(self, dec, **kw) -> None:
+        self.fused_switch(dec, None, **kw)
+
+    def _switch_for_step(self, with_prev: bool) -> None:
+        if self.cfg.switch_mode == "from_pristine":
+            self.fused_switch(None, self.cur, mode="from_pristine")
+        else:
+            self.fused_switch(self.prev if with_prev else None, self.cur)
+
+    def forward(self) -> None:
+        """Merged-path forward of one token (model.py:367-371 on the Llama block)."""
+        cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
+        d, eps = cfg.hidden, cfg.rms_eps
+        tp = cfg.tp_size
+        res_epi = _capi.AF_EPI_RESIDUAL if (tp == 1 or cfg.tp_rank == 0) else _capi.AF_EPI_NONE
+        xa, xb = self.x
+        self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
+        for li in range(cfg.layers):
+            self._check(L.af_gemv_fused(_ptr(self.wqkv[li]), self.q_rows + 2 * self.kv_rows, d, d, _ptr(xa), _ptr(self.qkv_buf),
+                                        _capi.AF_PRO_RMSNORM, _ptr(self.attn_norm[li]), eps, _capi.AF_EPI_NONE, None, st))
+            self._check(L.af_attn_decode(_ptr(self.qkv_buf), _ptr(self.k_cache[li]), _ptr(self.v_cache[li]), _ptr(self.cos),
+                                         _ptr(self.sin), _ptr(self.pos_dev), self.heads_local, self.kv_local, cfg.head_dim,
+                                         cfg.max_seq, _ptr(self.attn_buf), st))
+            self._check(L.af_gemv_fused(_ptr(self.wo[li]), d, self.q_rows, self.q_rows, _ptr(self.attn_buf), _ptr(xb),
+                                        _capi.AF_PRO_NONE, None, 0.0, res_epi, _ptr(xa) if res_epi else None, st))
+            self.comm.all_reduce_sum(xb)
+            self._check(L.af_gemv_fused(_ptr(self.wgu[li]), 2 * self.ffn_local, d, d, _ptr(xb), _ptr(self.gu_buf),
+                                        _capi.AF_PRO_RMSNORM, _ptr(self.ffn_norm[li]), eps, _capi.AF_EPI_NONE, None, st))
+            self._check(L.af_gemv_fused(_ptr(self.wdown[li]), d, self.ffn_local, self.ffn_local, _ptr(self.gu_buf), _ptr(xa),
+                                        _capi.AF_PRO_SILU_MUL, None, 0.0, res_epi, _ptr(xb) if res_epi else None, st))
+            self.comm.all_reduce_sum(xa)
+        self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),
+                                    _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))
+        self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, cfg.tp_rank * self.vocab_local, _ptr(self.next_dev),
+                                    _ptr(self.next_val), st))
+        self.comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
+
+    def _advance(self) -> None:
+        L, st = _capi.lib(), _capi.stream_ptr()
+        forced = self.forced_dev
+        self._check(L.af_step_advance(self.prev.ptr if self.cfg.adapters else None, self.cur.ptr if self.cfg.adapters else None,
+                                      _ptr(self.pos_dev), _ptr(self.step_dev), _ptr(self.token_dev), _ptr(self.next_dev),
+                                      _ptr(forced) if forced is not None else None, int(forced.numel()) if forced is not None else 0,
+                                      _ptr(self.history), int(self.history.numel()), st))
+
+    def _step_body(self, with_prev: bool) -> None:
+        if self.cfg.adapters:
+            self.pregate()
+            self._switch_for_step(with_prev)
+        self.forward()
+        self._advance()
+
+    # -- public stepping ---------------------------------------------------------------------
+
+    def reset(self, first_token: int = 0, forced=None) -> None:
+        """Start a new sequence: position 0, weights back to pristine, optional teacher-forced
+        token stream (consumed instead of the greedy feedback)."""
+        if not 0 <= int(first_token) < self.cfg.vocab:
+            raise InputError(f"token {first_token!r} outside vocab of {self.cfg.vocab}")
+        if self.table is not None and self.have_prev:
+            if self.pristine is not None:
+                self.table.refresh()
+            else:
+                self.unmerge(self.prev)
+        self.have_prev = False
+        self.pos_dev.zero_()
+        self.step_dev.zero_()
+        if forced is not None:
+            forced = np.asarray(forced, dtype=np.int64)
+            if forced.size == 0 or forced.min() < 0 or forced.max() >= self.cfg.vocab:
+                raise InputError("teacher-forced stream is empty or leaves the vocabulary")
+            self.forced_dev = torch.from_numpy(forced.astype(np.int32)).to(self.dev)
+            first_token = int(forced[0])
+        else:
+            self.forced_dev = None
+        self.token_dev.fill_(int(first_token))
+        self._graphs = {}
+
+    def decode_step(self, token: int | None = None) -> int:
+        """One eager decode step through the public API: the consumed token comes from the host
+        (4 bytes H2D), the next token is read back (4 bytes D2H)."""
+        if token is not None:
+            if not 0 <= int(token) < self.cfg.vocab:
+                raise InputError(f"token {token!r} outside vocab of {self.cfg.vocab}")
+            self.token_dev.copy_(torch.tensor([int(token)], dtype=torch.int32).pin_memory(), non_blocking=True)
+        if int(self.pos_dev.item()) >= self.cfg.max_seq:
+            raise StateError("KV cache is full")
+        self._step_body(self.have_prev)
+        self.have_prev = self.cfg.adapters
+        return int(self.next_dev.item())
+
+    def capture(self) -> None:
+        """Capture the steady-state step (switch with a previous decision) as a CUDA graph."""
+        if not self.have_prev and self.cfg.adapters and self.cfg.switch_mode == "inplace":
+            raise StateError("run one eager decode_step first: the steady graph unmerges a previous decision")
+        if self.cfg.tp_size > 1:
+            raise StateError("graph capture is single-rank; TP steps run eagerly")
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                self._step_body(True)
+        torch.cuda.current_stream().wait_stream(side)
+        self._graphs["steady"] = g
+
+    def replay(self) -> None:
+        self._graphs["steady"].replay()
+
+    def steps_done(self) -> int:
+        return int(self.step_dev.item())
+
+    def tokens(self, n: int | None = None) -> list:
+        n = self.steps_done() if n is None else n
+        return [int(v) for v in self.history[:n].cpu().numpy()]
+
+    def generate(self, prompt, n_new: int, use_graph: bool = True) -> list:
+        """Greedy generation: the prompt is consumed token by token along the same merged path
+        (token-level pre-gating makes merged == unmerged, PAPER Eq. 2-4), then n_new tokens."""
+        prompt = [int(t) for t in prompt]
+        if not prompt:
+            raise InputError("prompt must contain at least one token")
+        if n_new < 1:
+            raise InputError(f"n_new must be >= 1, got {n_new}")
+        if len(prompt) + n_new > self.cfg.max_seq:
+            raise InputError("prompt + n_new exceeds max_seq")
+        self.reset(prompt[0])
+        out = []
+        nxt = None
+        for t in prompt:
+            nxt = self.decode_step(t)
+        out.append(nxt)
+        remaining = n_new - 1
+        if remaining and use_graph and self.cfg.tp_size == 1:
+            self.capture()
+            for _ in range(remaining):
+                self.replay()
+            torch.cuda.synchronize()
+            out = out + self.tokens()[len(prompt):]
+        else:
+            for _ in range(remaining):
+                out.append(self.decode_step())
+        self.finalize()
+        return out
+
+    def finalize(self) -> None:
+        """model.py:460-474: take the last delta out again."""
+        if self.table is not None and self.have_prev:
+            if self.cfg.switch_mode == "from_pristine":
+                self.table.refresh()
+            else:
+                self.unmerge(self.prev)
+            self.have_prev = False
+
+    def max_backbone_deviation(self) -> float:
+        if self.table is None or self.pristine is None:
+            raise StateError("no pristine copy kept")
+        return self.table.max_deviation()
+
+    def decision(self) -> GateDecision:
+        return self.cur.to_host()
+
+
+_ = DECISION_BYTES

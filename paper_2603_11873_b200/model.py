@@ -65,6 +65,7 @@ class ModelConfig:
     strategy: Strategy = Strategy.PRE_GATED_FUSED
     refresh_every: int = 0
     compute: str = "auto"
+    switch_mode: str = "inplace"   # "inplace": W <- W + dNew - dOld; "from_pristine": W <- W0 + dNew (no drift)
 
     def validate(self) -> None:
         for name in ("layers", "hidden", "vocab", "experts", "rank", "top_k"):
@@ -89,12 +90,15 @@ class ModelConfig:
             raise ValueError("seed must be an integer")
         if self.compute not in _capi.COMPUTE_MODES:
             raise ValueError(f"unknown compute mode {self.compute!r}")
+        if self.switch_mode not in ("inplace", "from_pristine"):
+            raise ValueError(f"unknown switch mode {self.switch_mode!r}")
 
     def to_dict(self) -> dict:
         return {
             "layers": self.layers, "hidden": self.hidden, "vocab": self.vocab, "experts": self.experts,
             "rank": self.rank, "top_k": self.top_k, "precision": self.precision, "seed": self.seed,
             "strategy": self.strategy.value, "refresh_every": self.refresh_every, "compute": self.compute,
+            "switch_mode": self.switch_mode,
         }
 
     @classmethod
@@ -328,7 +332,11 @@ def _merged_pass(model: DecoderModel, state: DecodeState, token: int, recorder: 
     if config.refresh_every > 0 and state.tokens_done > 0 and state.tokens_done % config.refresh_every == 0:
         _refresh_from_pristine(model, state)
     prev = state.prev_decision
-    if strategy is Strategy.PRE_GATED_FUSED:
+    if strategy is Strategy.PRE_GATED_FUSED and config.switch_mode == "from_pristine":
+        # same HBM traffic (read W0, write W), half the stacked rank, and no bf16 re-rounding drift
+        model.table.switch(None, cur, max_k=config.top_k, compute=config.compute, mode="from_pristine")
+        _switch_event(model, config.top_k, recorder)
+    elif strategy is Strategy.PRE_GATED_FUSED:
         model.table.switch(prev, cur, max_k=config.top_k, compute=config.compute)
         _switch_event(model, (config.top_k if prev is not None else 0) + config.top_k, recorder)
     else:  # PRE_GATED_SIMPLE_MERGE: unmerge then merge (model.py:358-365), two launches
@@ -415,7 +423,10 @@ def finalize_generation(model: DecoderModel, state: DecodeState, recorder: Dispa
     if state.prev_decision is None:
         return
     config = model.config
-    model.table.unmerge(state.prev_decision, max_k=config.top_k, compute=config.compute)
+    if config.switch_mode == "from_pristine" and config.strategy is Strategy.PRE_GATED_FUSED:
+        model.table.refresh()
+    else:
+        model.table.unmerge(state.prev_decision, max_k=config.top_k, compute=config.compute)
     s = config.top_k * config.rank
     for f in model.backbone:
         recorder.record("gemm", flops=2 * f.rows * s * f.cols,

@@ -1,0 +1,140 @@
+"""Llama-shaped engine on the GPU against the CPU restatement (oracle/llama_oracle.py):
+router ids bit-exact, merged weights of all 7 x L segments within 1 bf16 ulp, logits within
+1e-2 relative; eager steps == captured-graph steps; TP shards == slices of the full model."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import llama_oracle as lo
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def llama():
+    from paper_2603_11873_b200 import llama
+
+    return llama
+
+
+def _bits(t):
+    return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16).copy()
+
+
+def _oracle_for(eng, llama):
+    cfg = eng.cfg
+    names = llama.SEGMENT_NAMES
+    layers = []
+    for li in range(cfg.layers):
+        lw = {"attn_norm": eng.attn_norm[li].cpu().numpy(), "ffn_norm": eng.ffn_norm[li].cpu().numpy()}
+        for j, name in enumerate(names):
+            i = li * len(names) + j
+            lw[name] = {"bits": _bits(eng.targets[i].data), "down": _bits(eng.bank_down[i]), "up": _bits(eng.bank_up[i])}
+        layers.append(lw)
+    w = {"embed": eng.embed.numpy(), "router": eng.router.numpy(), "lm_head": eng.lm_head.numpy(),
+         "final_norm": eng.final_norm.cpu().numpy(), "layers": layers}
+    return lo.LlamaOracle(w, hidden=cfg.hidden, n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads, top_k=cfg.top_k,
+                          rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps, max_seq=cfg.max_seq)
+
+
+@pytest.mark.parametrize("switch_mode", ["inplace", "from_pristine"])
+def test_decode_steps_against_oracle(llama, switch_mode):
+    cfg = llama.preset("tiny", switch_mode=switch_mode, max_seq=32)
+    eng = llama.LlamaEngine(cfg, init="host")
+    assert eng.table.info()["tensor_path"]
+    ora = _oracle_for(eng, llama)
+    pristine = [{n: ora.w["layers"][li][n]["bits"].copy() for n in llama.SEGMENT_NAMES} for li in range(cfg.layers)]
+    forced = np.random.Generator(np.random.PCG64(11)).integers(0, cfg.vocab, 10)
+    eng.reset(forced=forced)
+    for step, tkn in enumerate(forced):
+        before = [{n: ora.w["layers"][li][n]["bits"].copy() for n in llama.SEGMENT_NAMES} for li in range(cfg.layers)]
+        nxt = eng.decode_step()
+        eng.table.status()
+        ids, wts = ora.route(tkn)
+        dec = eng.decision()
+        assert dec.expert_ids == ids, f"step {step}"
+        np.testing.assert_allclose(dec.weights, wts, rtol=2e-6)
+        ora.switch((ids, wts), from_pristine=(switch_mode == "from_pristine"), pristine=pristine)
+        for li in range(cfg.layers):
+            for j, name in enumerate(llama.SEGMENT_NAMES):
+                got = _bits(eng.targets[li * 7 + j].data)
+                ref_before = pristine[li][name] if switch_mode == "from_pristine" else before[li][name]
+                worst, nd = orc.merge_error_in_ulps(got, ora.w["layers"][li][name]["bits"], ref_before)
+                assert worst <= 1.0, f"step {step} layer {li} {name}: {nd} diffs, max {worst} ulp"
+                ora.w["layers"][li][name]["bits"][...] = got      # oracle follows the GPU's live weights
+        o_next, o_logits, o_hidden = ora.forward(tkn)
+        got_logits = eng.logits.cpu().numpy()
+        scale = np.max(np.abs(o_logits))
+        assert np.max(np.abs(got_logits - o_logits)) <= 1e-2 * scale, f"step {step}"
+        top2 = np.sort(o_logits)[-2:]
+        if top2[1] - top2[0] > 2e-2 * scale:
+            assert nxt == o_next
+    assert eng.steps_done() == len(forced)
+    eng.finalize()
+    assert eng.max_backbone_deviation() < 0.02
+
+
+def test_graph_replay_equals_eager(llama):
+    cfg = llama.preset("tiny", max_seq=48)
+    forced = np.random.Generator(np.random.PCG64(12)).integers(0, cfg.vocab, 20)
+    a = llama.LlamaEngine(cfg, init="host")
+    a.reset(forced=forced)
+    for _ in range(20):
+        a.decode_step()
+    eager = a.tokens()
+    b = llama.LlamaEngine(cfg, init="host")
+    b.reset(forced=forced)
+    b.decode_step()
+    b.capture()
+    for _ in range(19):
+        b.replay()
+    torch.cuda.synchronize()
+    assert b.tokens() == eager
+    for ta, tb in zip(a.targets, b.targets):
+        assert torch.equal(ta.data, tb.data)
+
+
+def test_generate_and_base_engine(llama):
+    cfg = llama.preset("tiny", max_seq=64)
+    eng = llama.LlamaEngine(cfg, init="host")
+    toks = eng.generate([5, 17, 300], 12)
+    assert len(toks) == 12 and all(0 <= t < cfg.vocab for t in toks)
+    assert toks == eng.generate([5, 17, 300], 12, use_graph=False)      # deterministic, graph == eager
+    assert eng.max_backbone_deviation() < 0.02
+    base = llama.LlamaEngine(llama.preset("tiny", max_seq=64, adapters=False), init="host")
+    bt = base.generate([5, 17, 300], 12)
+    assert len(bt) == 12
+    with pytest.raises(Exception):
+        base.fused_switch(None, None)
+    with pytest.raises(ValueError):
+        llama.preset("tiny", n_kv_heads=3)
+
+
+def test_tp_shards_are_slices_of_the_full_switch(llama):
+    """a rank's switch over its shard equals the same slice of the unsharded
+    switch bit for bit (each element's arithmetic is independent of the sharding)."""
+    full_cfg = llama.preset("tiny", max_seq=8, compute="fma")
+    full = llama.LlamaEngine(full_cfg, init="host")
+    dec_a = full.cur.__class__.from_host(llama.GateDecision((1, 6), (0.75, 0.25)))
+    dec_b = full.cur.__class__.from_host(llama.GateDecision((6, 3), (0.5, 0.5)))
+    full.merge(dec_a)
+    full.fused_switch(dec_a, dec_b)
+    for rank in range(2):
+        cfg = llama.preset("tiny", max_seq=8, compute="fma", tp_size=2, tp_rank=rank)
+        one = llama.LlamaEngine(cfg, init="host", comm=llama.NoPeers())   # one shard, no peers: table only
+        one.merge(dec_a)
+        one.fused_switch(dec_a, dec_b)
+        shp = cfg.segment_shapes()
+        for li in range(cfg.layers):
+            for j, name in enumerate(llama.SEGMENT_NAMES):
+                i = li * 7 + j
+                fw = full.targets[i].data
+                if name in ("q", "k", "v", "gate", "up"):
+                    n = shp[name][0]
+                    want = fw[rank * n:(rank + 1) * n]
+                else:
+                    n = shp[name][1]
+                    want = fw[:, rank * n:(rank + 1) * n]
+                assert torch.equal(one.targets[i].data, want), f"rank {rank} layer {li} {name}"

