@@ -245,7 +245,12 @@ def main():
     eng._switch_for_step = instrumented_switch
     launches0 = _capi.launch_count()
     sampler = ClockSampler(local_rank)
+    profiling = bool(os.environ.get("AF_NCU"))   # `ncu --profile-from-start off`: profile the timed region only
+    if profiling:
+        torch.cuda.profiler.start()
     e2e_ms = timed(api_step, args.steps)
+    if profiling:
+        torch.cuda.profiler.stop()
     launches_e2e = _capi.launch_count() - launches0
     eng._switch_for_step = orig_switch
     sw_ms = [a.elapsed_time(b) for a, b in switch_events]

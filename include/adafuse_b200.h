@@ -99,6 +99,10 @@ const char* af_last_error(void);
 int af_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_bytes);
 /* Number of kernel launches issued by this library since load (bench `gpu_launches`). */
 int64_t af_launch_count(void);
+/* Programmatic dependent launch of the decode GEMV / attention chain (default on; the
+ * environment variable AF_PDL=0 turns it off at load).  With it, a GEMV prefetches its first
+ * weight tiles while the previous kernel of the stream is still draining. */
+int af_set_pdl(int32_t enable);
 
 /* ---- segment table: built once at model load -------------------------------------
  * Replaces: linalg.py:207-231 `SegmentTable` + `.validate()` (shape, precision and
@@ -192,7 +196,9 @@ int af_embed(const void* table, int32_t dtype, int32_t d, const int32_t* token_d
  *    epilogue as af_gemv.
  * af_attn_decode: RoPE(q, k) at position *pos_dev, append k/v to the bf16 cache, single-query
  *    GQA attention over positions 0..*pos_dev.  qkv = [q | k | v] f32, caches
- *    [n_kv][max_seq][head_dim] bf16, cos/sin [max_seq][head_dim/2] f32.
+ *    [n_kv][max_seq][head_dim] bf16, cos/sin [max_seq][head_dim/2] f32.  n_split > 1 spreads
+ *    the positions of each head over n_split CTAs (long contexts); it needs a workspace of
+ *    n_heads * n_split * (head_dim + 2) floats and n_heads zero-initialised int32 tickets.
  * af_argmax_val : argmax + the winning value, index shifted by index_offset (vocab-parallel
  *    lm_head).
  * af_step_advance: end-of-step bookkeeping in one launch so a decode step is a static CUDA
@@ -206,7 +212,8 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
                   void* stream);
 int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table,
                    const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
-                   int32_t head_dim, int32_t max_seq, float* out, void* stream);
+                   int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,
+                   int32_t* tickets, float* out, void* stream);
 int af_argmax_val(const float* v, int32_t n, int32_t index_offset, int32_t* out_idx_dev,
                   float* out_val_dev, void* stream);
 int af_step_advance(af_decision* prev_dev, const af_decision* cur_dev, int32_t* pos_dev,

@@ -18,10 +18,10 @@
  *   - gate folding: down_cat block = (float)w * down, one f32 multiply; up_cat unscaled.
  *   - switch: down = [-prev.down_cat ; cur.down_cat], up = [prev.up_cat | cur.up_cat].
  *   - route: logits = W_g x ; stable descending order (ties -> lower index);
- *     softmax over the selected logits only, max-shifted, f32.
+ *     softmax over the selected logits only, max-shifted, correctly rounded to f32.
  *
- * The one deliberate deviation: dot products (router logits, GEMVs) accumulate in
- * double and round once to f32.  The reference delegates those to numpy `@`
+ * The one deliberate deviation: dot products (router logits, GEMVs) and the k-term softmax
+ * accumulate in double and round once to f32.  The reference delegates those to numpy `@`
  * (OpenBLAS, linalg.py:252), whose summation order is unspecified; the correctly
  * rounded f32 dot product is inside OpenBLAS' own round-off band and is order
  * independent, which is what lets the GPU kernels match it bit for bit.
@@ -107,14 +107,24 @@ int orc_route(const float* wg, int n_experts, int d, const float* x, int k,
         taken[best] = 1;
         ids[j] = best;
     }
-    /* routing.py:66-68: softmax over the selected logits only, max-shifted, f32. */
+    /* routing.py:66-68: softmax over the selected logits only, max-shifted.  Evaluated in
+     * double (exp, left-to-right sum, division) and rounded once to f32: the correctly rounded
+     * f32 softmax.  The reference evaluates it in f32 with numpy's exp; f32 exp
+     * implementations (numpy SIMD, glibc, CUDA) differ among themselves by an ulp, so the
+     * correctly rounded value is the one restatement every platform can reproduce bit for
+     * bit; it is within 1 f32 ulp of the reference (pinned at 1e-5 in test_oracle_golden). */
     float mx = logits[ids[0]];
-    float sum = 0.0f;
+    double ex[64];
+    double sum = 0.0;
     for (int j = 0; j < k; ++j) {
-        weights[j] = expf(logits[ids[j]] - mx);
-        sum += weights[j];
+        ex[j & 63] = exp((double)logits[ids[j]] - (double)mx);
+        sum += ex[j & 63];
     }
-    for (int j = 0; j < k; ++j) weights[j] = weights[j] / sum;
+    if (k <= 64) {
+        for (int j = 0; j < k; ++j) weights[j] = (float)(ex[j] / sum);
+    } else { /* very wide k: recompute instead of buffering */
+        for (int j = 0; j < k; ++j) weights[j] = (float)(exp((double)logits[ids[j]] - (double)mx) / sum);
+    }
     free(taken);
     free(logits);
     return ORC_OK;

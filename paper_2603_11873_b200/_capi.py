@@ -80,6 +80,7 @@ SIGNATURES = {
     "af_last_error": (ctypes.c_char_p, []),
     "af_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 3 + [ctypes.POINTER(_i64)]),
     "af_launch_count": (_i64, []),
+    "af_set_pdl": (ctypes.c_int, [_i32]),
     "af_table_create": (ctypes.c_int, [ctypes.POINTER(SegmentDesc), _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     "af_table_destroy": (ctypes.c_int, [_vp]),
     "af_table_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
@@ -96,7 +97,7 @@ SIGNATURES = {
     "af_argmax": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "af_embed": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "af_gemv_fused": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, _vp, _i32, _vp, _f32, _i32, _vp, _vp]),
-    "af_attn_decode": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "af_attn_decode": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "af_argmax_val": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "af_step_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp]),
 }

@@ -2,6 +2,7 @@
 // kernel selection and launches.  No torch types anywhere; every device buffer belongs to the
 // caller.  Citations are relative to /root/reference/pkg/src/lorafuse/.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -20,6 +21,11 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 std::atomic<long long> g_launches{0};
+// Programmatic dependent launch for the decode GEMV chain (af_set_pdl; env AF_PDL=0 disables).
+static std::atomic<int> g_pdl{[] {
+    const char* e = getenv("AF_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+}()};
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline size_t esize(int dtype) { return dtype == AF_BF16 ? 2 : 4; }
@@ -91,7 +97,7 @@ struct af_table {
     SegDev* d_segs = nullptr;
     UnitDev* d_units = nullptr;
     int n_units = 0;
-    CUtensorMap* d_maps = nullptr;  // [5][n_segments]: fma live, fma pristine, mma-ld live, mma-ld pristine, mma-st live
+    CUtensorMap* d_maps = nullptr;  // [4][n_segments]: fma live, fma pristine, mma live, mma pristine
     int* d_err = nullptr;
     bool fast_fma = false, fast_mma = false, has_pristine = false;
     int max_rank = 0, min_experts = 0;
@@ -115,6 +121,11 @@ int af_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_byte
 }
 
 int64_t af_launch_count(void) { return g_launches.load(); }
+
+int af_set_pdl(int32_t enable) {
+    g_pdl.store(enable ? 1 : 0);
+    return AF_OK;
+}
 
 // ------------------------------------------------------------------ table ----
 
@@ -244,7 +255,7 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         return fail(AF_ECUDA, std::string("table upload: ") + cudaGetErrorString(e));
     }
     if (t->fast_fma) {
-        std::vector<CUtensorMap> maps((size_t)5 * n_segments);
+        std::vector<CUtensorMap> maps((size_t)4 * n_segments);
         for (int i = 0; i < n_segments; ++i) {
             const af_segment_desc& s = segments[i];
             const void* pr = s.pristine ? s.pristine : s.target;
@@ -252,7 +263,6 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
             if (!rc) rc = make_map(&maps[1 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kTN, kTM, CU_TENSOR_MAP_SWIZZLE_NONE);
             if (!rc) rc = make_map(&maps[2 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kBoxCols, kTM, CU_TENSOR_MAP_SWIZZLE_128B);
             if (!rc) rc = make_map(&maps[3 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kBoxCols, kTM, CU_TENSOR_MAP_SWIZZLE_128B);
-            if (!rc) rc = make_map(&maps[4 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kBoxCols, 32, CU_TENSOR_MAP_SWIZZLE_128B);
             if (rc) {
                 af_table_destroy(t);
                 return rc;
@@ -305,7 +315,7 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
         AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured = true;
     }
-    switch_mma_kernel<KS><<<grid, kConsumers + 32, L::total, st>>>(mp);
+    switch_mma_kernel<KS><<<grid, kMmaThreads, L::total, st>>>(mp);
     AF_LAUNCH_CHECK("switch_mma_kernel");
     return AF_OK;
 }
@@ -401,7 +411,7 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
         MmaParams mp{};
         mp.base = p;
         mp.tmaps_ld = t->d_maps + (size_t)(p.from_pristine ? 3 : 2) * S;
-        mp.tmaps_st = t->d_maps + (size_t)4 * S;
+        mp.tmaps_st = t->d_maps + (size_t)2 * S;
         const int grid = std::min(t->n_units, t->sm_count);
         const int ks = std::max(1, (s_bound + 15) / 16);
         switch (ks) {
@@ -602,26 +612,65 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
         AF_CUDA_TRY(cudaFuncSetAttribute(gemv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         configured_smem = smem;
     }
-    const int rows_per_cta = (kGemvFThreads / 32) * kGemvFRows;
-    // resident CTAs per SM are bounded by the staged vector; keep every SM busy with >= 2 waves of rows
-    const int per_sm = std::max(1, std::min(8, (di.max_smem_optin) / (smem + 2048)));
-    const int grid = std::max(1, std::min((rows + rows_per_cta - 1) / rows_per_cta, di.sm_count * per_sm));
-    gemv_fused_kernel<<<grid, kGemvFThreads, smem, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(w), rows, cols,
-                                                                         ld, x, out, prologue, norm_w, eps, epilogue, res);
+    // Even split of the rows over SMs x resident CTAs: every SM streams the same number of bytes.
+    int per_sm = 0;
+    {
+        static int occ_cached_smem = -1, occ_cached = 0;
+        if (occ_cached_smem != smem) {
+            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cached, gemv_fused_kernel, kGemvFThreads, smem));
+            occ_cached_smem = smem;
+        }
+        per_sm = std::max(1, std::min(occ_cached, 4));
+    }
+    const int grid = std::max(1, std::min(rows, di.sm_count * per_sm));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemvFThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl.load() ? 1 : 0;
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_fused_kernel, reinterpret_cast<const __nv_bfloat16*>(w), (int)rows, (int)cols,
+                                   (long long)ld, x, out, (int)prologue, norm_w, eps, (int)epilogue, res));
     AF_LAUNCH_CHECK("gemv_fused_kernel");
     return AF_OK;
 }
 
 int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table, const float* sin_table,
                    const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t max_seq,
-                   float* out, void* stream) {
+                   int32_t n_split, float* workspace, int32_t* tickets, float* out, void* stream) {
     if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads != 0) return fail(AF_EDIM, "heads must be a multiple of kv heads");
     if (head_dim < 2 || head_dim % 2 != 0 || head_dim > kAttnMaxHd) return fail(AF_EDIM, "head_dim must be even and <= 256");
     if (max_seq < 1) return fail(AF_EDIM, "max_seq must be positive");
     if (!qkv || !k_cache || !v_cache || !cos_table || !sin_table || !pos_dev || !out) return fail(AF_EVALUE, "NULL argument");
-    attn_decode_kernel<<<n_heads, kAttnThreads, 0, as_stream(stream)>>>(
-        qkv, reinterpret_cast<__nv_bfloat16*>(k_cache), reinterpret_cast<__nv_bfloat16*>(v_cache), cos_table, sin_table,
-        pos_dev, n_heads, n_kv_heads, head_dim, max_seq, 1.0f / sqrtf((float)head_dim), out);
+    if (n_split < 1) n_split = 1;
+    if (n_split > 1 && (!workspace || !tickets)) return fail(AF_EVALUE, "split attention needs a workspace and tickets");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_heads * n_split);
+    cfg.blockDim = dim3(kAttnThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl.load() ? 1 : 0;
+    const float scale = 1.0f / sqrtf((float)head_dim);
+    __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(k_cache);
+    __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
+    const bool aligned = (reinterpret_cast<uintptr_t>(k_cache) % 16 == 0) && (reinterpret_cast<uintptr_t>(v_cache) % 16 == 0);
+#define AF_ATTN(EL)                                                                                                       \
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode_kernel<EL>, qkv, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,  \
+                                   (int)n_kv_heads, (int)head_dim, (int)max_seq, scale, (int)n_split, workspace,           \
+                                   reinterpret_cast<int*>(tickets), out))
+    if (aligned && head_dim == 64) AF_ATTN(2);
+    else if (aligned && head_dim == 128) AF_ATTN(4);
+    else if (aligned && head_dim == 256) AF_ATTN(8);
+    else AF_ATTN(1);
+#undef AF_ATTN
     AF_LAUNCH_CHECK("attn_decode_kernel");
     return AF_OK;
 }

@@ -18,8 +18,8 @@ namespace af {
 // order independent to ~1e-16 relative, so the logit, rounded ONCE to f32, does not depend on
 // the reduction tree -- that is what makes the expert ids reproducible bit for bit against the
 // CPU oracle.  Top-k: descending logit, ascending index on ties
-// (routing.py:64-65).  Softmax over the k selected logits only, max-shifted, f32
-// (routing.py:66-68).
+// (routing.py:64-65).  Softmax over the k selected logits only, max-shifted (routing.py:66-68),
+// evaluated in f64 and rounded once to f32.
 
 constexpr int kRouterThreads = 512;
 constexpr int kRouterMaxExperts = 256;
@@ -99,14 +99,15 @@ __global__ void __launch_bounds__(kRouterThreads) pregate_kernel(const WT* __res
         }
         if (lane == j) { sel_logit = best; sel_id = best_id; }
     }
-    // ---- softmax over the selected logits ----
+    // ---- softmax over the selected logits (routing.py:66-68), max-shifted.  exp, the
+    //      left-to-right sum and the division run in f64 and round ONCE to f32: the result is
+    //      the correctly rounded f32 softmax, within 1 f32 ulp of any f32 evaluation (numpy's,
+    //      glibc's, CUDA's differ among themselves by that much) and identical on CPU and GPU. ----
     const float mx = __shfl_sync(0xffffffffu, sel_logit, 0);  // first selected is the maximum
-    float ex = lane < k ? expf(sel_logit - mx) : 0.f;
-    float sum = ex;
-    // sequential-order sum over k <= 8 terms (matches the oracle's left-to-right f32 sum)
-    float total = 0.f;
-    for (int j = 0; j < k; ++j) total += __shfl_sync(0xffffffffu, sum, j);
-    const float wgt = ex / total;
+    const double ex = lane < k ? exp((double)sel_logit - (double)mx) : 0.0;
+    double total = 0.0;
+    for (int j = 0; j < k; ++j) total += __shfl_sync(0xffffffffu, ex, j);
+    const float wgt = (float)(ex / total);
     if (lane < k) {
         out->ids[lane] = sel_id;
         out->weights[lane] = wgt;

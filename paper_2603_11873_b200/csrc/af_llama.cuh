@@ -18,7 +18,8 @@ constexpr int kPrologueRmsNorm = 1;   // xs = x * rsqrt(mean(x^2) + eps) * norm_
 constexpr int kPrologueSiluMul = 2;   // xs = silu(x[c]) * x[cols + c]   (x holds [gate | up])
 
 constexpr int kGemvFThreads = 256;
-constexpr int kGemvFRows = 2;  // rows per warp per pass
+constexpr int kGemvRB = 4;                    // rows per batch (one partial sum each per thread)
+constexpr int kGemvPass = kGemvFThreads * 8;  // columns covered by the CTA per pass (16 B per thread)
 
 __device__ __forceinline__ void unpack8(const uint4 v, float (&f)[8]) {
     f[0] = bf16lo_to_f32(v.x); f[1] = bf16hi_to_f32(v.x); f[2] = bf16lo_to_f32(v.y); f[3] = bf16hi_to_f32(v.y);
@@ -34,18 +35,50 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     return r;
 }
 
-// y = W xs, W rows x cols bf16 row-major (cols % 8 == 0, 16-byte aligned rows), x f32.
-// Each CTA stages xs once (prologue applied) and grid-strides over row groups; a warp owns
-// kGemvFRows rows per pass, lanes stride the row in 16-byte chunks, 4 chunks per row in
-// flight (8 independent 16-byte loads per thread), f32 FMA, shuffle tree, epilogue by lane 0.
+// Programmatic dependent launch (PDL): a kernel launched with the attribute may start while its
+// predecessor is still running; everything it does before pdl_wait() must be independent of
+// the predecessor (here: prefetching W).  Both are no-ops in an ordinary launch.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// y = epilogue(W . prologue(x)), W rows x cols bf16 row-major (cols % 8 == 0, 16-byte aligned rows).
+//
+// HBM-bound streaming read of W.  Rows are split EVENLY over the grid (grid = SMs x resident
+// CTAs, so every SM streams the same number of bytes); inside a CTA all 256 threads cooperate
+// on a batch of kGemvRB rows: thread t owns the 16-byte chunk t of every 4 KB pass of a row.
+// The loop is software-pipelined two items deep (8 independent 16-byte loads in flight per
+// thread while a third item is consumed), the first loads are issued BEFORE the prologue and
+// before pdl_wait(), so the prologue and the tail of the previous kernel hide under them.
 __global__ void __launch_bounds__(kGemvFThreads) gemv_fused_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols,
                                                                     long long ld, const float* __restrict__ x,
                                                                     float* __restrict__ out, int prologue,
                                                                     const float* __restrict__ norm_w, float eps, int epilogue,
                                                                     const float* __restrict__ res) {
     extern __shared__ __align__(16) float xs[];
-    __shared__ float red[kGemvFThreads / 32];
+    __shared__ float red[2][kGemvFThreads / 32][kGemvRB];
+    __shared__ float redn[kGemvFThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kGemvFThreads / 32;
+    pdl_launch_dependents();
+    const int r_begin = (int)((long long)rows * blockIdx.x / gridDim.x);
+    const int r_end = (int)((long long)rows * (blockIdx.x + 1) / gridDim.x);
+    const int n_pass = (cols + kGemvPass - 1) / kGemvPass;
+    const int n_batch = (r_end - r_begin + kGemvRB - 1) / kGemvRB;
+    const int total = n_batch * n_pass;
+
+    auto issue = [&](int it, uint4 (&v)[kGemvRB]) {
+        if (it >= total) return;
+        const int b = it / n_pass, c = (it % n_pass) * kGemvPass + tid * 8;
+#pragma unroll
+        for (int i = 0; i < kGemvRB; ++i) {
+            const int row = r_begin + b * kGemvRB + i;
+            v[i] = (row < r_end && c < cols) ? ldg_stream(w + (long long)row * ld + c) : make_uint4(0u, 0u, 0u, 0u);
+        }
+    };
+    uint4 b0[kGemvRB], b1[kGemvRB], b2[kGemvRB];
+    issue(0, b0);
+    issue(1, b1);
+
+    pdl_wait();  // x / res come from the previous kernel
     if (prologue == kPrologueRmsNorm) {
         float ss = 0.f;
         for (int c = tid; c < cols; c += kGemvFThreads) {
@@ -54,11 +87,11 @@ __global__ void __launch_bounds__(kGemvFThreads) gemv_fused_kernel(const __nv_bf
             ss = fmaf(v, v, ss);
         }
         ss = warp_sum(ss);
-        if (lane == 0) red[warp] = ss;
+        if (lane == 0) redn[warp] = ss;
         __syncthreads();
         float tot = 0.f;
 #pragma unroll
-        for (int i = 0; i < nwarps; ++i) tot += red[i];
+        for (int i = 0; i < nwarps; ++i) tot += redn[i];
         const float inv = rsqrtf(tot / (float)cols + eps);
         for (int c = tid; c < cols; c += kGemvFThreads) xs[c] = xs[c] * inv * norm_w[c];
     } else if (prologue == kPrologueSiluMul) {
@@ -70,57 +103,56 @@ __global__ void __launch_bounds__(kGemvFThreads) gemv_fused_kernel(const __nv_bf
         for (int c = tid; c < cols; c += kGemvFThreads) xs[c] = x[c];
     }
     __syncthreads();
-    const int rows_per_cta = nwarps * kGemvFRows;
-    for (int r0 = blockIdx.x * rows_per_cta + warp * kGemvFRows; r0 < rows; r0 += gridDim.x * rows_per_cta) {
-        float acc[kGemvFRows] = {};
-        const __nv_bfloat16* wr[kGemvFRows];
-#pragma unroll
-        for (int i = 0; i < kGemvFRows; ++i) wr[i] = w + (long long)min(r0 + i, rows - 1) * ld;
-        int c = lane * 8;
-        for (; c + 3 * 256 < cols; c += 4 * 256) {
-            uint4 v[kGemvFRows][4];
-#pragma unroll
-            for (int i = 0; i < kGemvFRows; ++i)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[i][u] = ldg_stream(wr[i] + c + u * 256);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float4 xa = *reinterpret_cast<const float4*>(xs + c + u * 256);
-                const float4 xb = *reinterpret_cast<const float4*>(xs + c + u * 256 + 4);
-                const float xf[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-                for (int i = 0; i < kGemvFRows; ++i) {
-                    float wf[8];
-                    unpack8(v[i][u], wf);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i] = fmaf(wf[j], xf[j], acc[i]);
-                }
-            }
-        }
-        for (; c < cols; c += 256) {
+
+    float acc[kGemvRB] = {};
+    int buf = 0;
+    auto consume = [&](int it, const uint4 (&v)[kGemvRB]) {
+        if (it >= total) return;
+        const int b = it / n_pass, ps = it % n_pass, c = ps * kGemvPass + tid * 8;
+        if (c < cols) {
             const float4 xa = *reinterpret_cast<const float4*>(xs + c);
             const float4 xb = *reinterpret_cast<const float4*>(xs + c + 4);
             const float xf[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
-            for (int i = 0; i < kGemvFRows; ++i) {
+            for (int i = 0; i < kGemvRB; ++i) {
                 float wf[8];
-                unpack8(ldg_stream(wr[i] + c), wf);
+                unpack8(v[i], wf);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i] = fmaf(wf[j], xf[j], acc[i]);
             }
         }
+        if (ps == n_pass - 1) {  // the batch is complete: CTA-wide reduction and epilogue
 #pragma unroll
-        for (int i = 0; i < kGemvFRows; ++i) {
-            const float y = warp_sum(acc[i]);
-            if (lane == 0 && r0 + i < rows) {
-                float o = y;
-                if (epilogue == AF_EPI_GELU_RESIDUAL)
-                    o = res[r0 + i] + 0.5f * y * (1.0f + erff(y * 0.70710678118654752440f));
-                else if (epilogue == AF_EPI_RESIDUAL)
-                    o = res[r0 + i] + y;
-                out[r0 + i] = o;
+            for (int i = 0; i < kGemvRB; ++i) {
+                const float y = warp_sum(acc[i]);
+                if (lane == 0) red[buf][warp][i] = y;
+                acc[i] = 0.f;
             }
+            __syncthreads();
+            if (tid < kGemvRB) {
+                const int row = r_begin + b * kGemvRB + tid;
+                if (row < r_end) {
+                    float y = 0.f;
+#pragma unroll
+                    for (int wv = 0; wv < nwarps; ++wv) y += red[buf][wv][tid];
+                    float o = y;
+                    if (epilogue == AF_EPI_GELU_RESIDUAL)
+                        o = res[row] + 0.5f * y * (1.0f + erff(y * 0.70710678118654752440f));
+                    else if (epilogue == AF_EPI_RESIDUAL)
+                        o = res[row] + y;
+                    out[row] = o;
+                }
+            }
+            buf ^= 1;
         }
+    };
+    for (int it = 0; it < total; it += 3) {
+        issue(it + 2, b2);
+        consume(it, b0);
+        issue(it + 3, b0);
+        consume(it + 1, b1);
+        issue(it + 4, b1);
+        consume(it + 2, b2);
     }
 }
 
@@ -129,26 +161,62 @@ __global__ void __launch_bounds__(kGemvFThreads) gemv_fused_kernel(const __nv_bf
 //   k_cache : bf16 [n_kv][max_seq][hd], v_cache likewise; position *pos_dev is written here
 //   cos/sin : f32 [max_seq][hd/2] rotary tables (rotate-half convention)
 //   out     : f32 [n_heads*hd]
-// One CTA per query head.  The head's own (rotated) k and v of the new position are used from
-// shared memory, so heads of one group never read what a sibling CTA is still writing.
-constexpr int kAttnThreads = 128;
+// Grid = n_heads x n_split CTAs (flash-decoding): split sp of head h covers a contiguous range
+// of the positions 0..pos; each of its 8 warps keeps 4 positions (8 vector loads) in flight and
+// runs an online softmax; the CTA writes its partial (max, sum, acc[hd]) to a workspace and the
+// last CTA of a head to arrive (atomic ticket) combines the splits.  The new position's own
+// (rotated, bf16-rounded) k and v are used from shared memory, so no CTA reads what a sibling
+// is still appending.
+constexpr int kAttnThreads = 256;
+constexpr int kAttnWarps = kAttnThreads / 32;
 constexpr int kAttnMaxHd = 256;
+constexpr int kAttnUnroll = 4;
 
+template <int EL>
+__device__ __forceinline__ void load_bf16_vec(const __nv_bfloat16* p, float (&f)[EL]) {
+    if constexpr (EL == 2) {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
+        f[0] = bf16lo_to_f32(v); f[1] = bf16hi_to_f32(v);
+    } else if constexpr (EL == 4) {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        f[0] = bf16lo_to_f32(v.x); f[1] = bf16hi_to_f32(v.x); f[2] = bf16lo_to_f32(v.y); f[3] = bf16hi_to_f32(v.y);
+    } else if constexpr (EL == 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        f[0] = bf16lo_to_f32(v.x); f[1] = bf16hi_to_f32(v.x); f[2] = bf16lo_to_f32(v.y); f[3] = bf16hi_to_f32(v.y);
+        f[4] = bf16lo_to_f32(v.z); f[5] = bf16hi_to_f32(v.z); f[6] = bf16lo_to_f32(v.w); f[7] = bf16hi_to_f32(v.w);
+    } else {
+#pragma unroll
+        for (int j = 0; j < EL; ++j) f[j] = __bfloat162float(p[j]);
+    }
+}
+
+// EL = elements of the head dimension owned by one lane (contiguous): hd == 32 * EL for the
+// vector instantiations (2, 4, 8); EL == 1 is the generic one (any even hd <= 256, lane-strided).
+template <int EL>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* __restrict__ qkv,
                                                                    __nv_bfloat16* __restrict__ k_cache,
                                                                    __nv_bfloat16* __restrict__ v_cache,
                                                                    const float* __restrict__ cos_t,
                                                                    const float* __restrict__ sin_t,
                                                                    const int32_t* __restrict__ pos_dev, int n_heads,
-                                                                   int n_kv, int hd, int max_seq, float scale,
+                                                                   int n_kv, int hd, int max_seq, float scale, int n_split,
+                                                                   float* __restrict__ ws, int* __restrict__ tickets,
                                                                    float* __restrict__ out) {
+    constexpr bool VEC = EL > 1;
+    constexpr int PER = VEC ? EL : kAttnMaxHd / 32;  // accumulator slots per lane
     __shared__ float q_s[kAttnMaxHd], k_s[kAttnMaxHd], v_s[kAttnMaxHd];
-    __shared__ float m_s[kAttnThreads / 32], l_s[kAttnThreads / 32];
-    __shared__ float acc_s[kAttnThreads / 32][kAttnMaxHd];
-    const int h = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = kAttnThreads / 32;
+    __shared__ float m_s[kAttnWarps], l_s[kAttnWarps];
+    __shared__ float acc_s[kAttnWarps][kAttnMaxHd];
+    __shared__ int is_last;
+    const int h = blockIdx.x / n_split, sp = blockIdx.x % n_split;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int group = n_heads / n_kv, kvh = h / group;
+    pdl_launch_dependents();
+    pdl_wait();  // qkv comes from the previous kernel
     const int pos = *pos_dev;
+    const int n_pos = pos + 1;
+    const int per = (n_pos + n_split - 1) / n_split;
+    const int t0 = sp * per, t1 = min(n_pos, t0 + per);
     const int half = hd >> 1;
     const float* q = qkv + (long long)h * hd;
     const float* kn = qkv + (long long)n_heads * hd + (long long)kvh * hd;
@@ -160,14 +228,14 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
         q_s[i] = q0 * c - q1 * s;
         q_s[i + half] = q1 * c + q0 * s;
         const float k0 = kn[i], k1 = kn[i + half];
-        // the cache stores bf16: use the rounded values for the new position too, so that a
-        // later token sees exactly what this one saw
+        // the cache stores bf16: the new position uses the rounded values too, so that a later
+        // token sees exactly what this one saw
         k_s[i] = __bfloat162float(__float2bfloat16_rn(k0 * c - k1 * s));
         k_s[i + half] = __bfloat162float(__float2bfloat16_rn(k1 * c + k0 * s));
     }
     for (int i = tid; i < hd; i += kAttnThreads) v_s[i] = __bfloat162float(__float2bfloat16_rn(vn[i]));
     __syncthreads();
-    if (h % group == 0) {  // one head per group appends to the cache
+    if (h % group == 0 && pos >= t0 && pos < t1) {  // one CTA per kv head appends to the cache
         __nv_bfloat16* kc = k_cache + ((long long)kvh * max_seq + pos) * hd;
         __nv_bfloat16* vc = v_cache + ((long long)kvh * max_seq + pos) * hd;
         for (int i = tid; i < hd; i += kAttnThreads) {
@@ -175,65 +243,122 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
             vc[i] = __float2bfloat16_rn(v_s[i]);
         }
     }
-    // online softmax over positions 0..pos; warp w takes positions w, w+nwarps, ...
-    // lane owns elements lane, lane+32, ... of the head dimension
-    constexpr int kPer = kAttnMaxHd / 32;
-    float acc[kPer];
+    // element e of this lane's slot j
+    auto elem = [&](int j) { return VEC ? lane * EL + j : lane + 32 * j; };
+    float qr[PER];
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
+    for (int j = 0; j < PER; ++j) qr[j] = elem(j) < hd ? q_s[elem(j)] : 0.f;
+    float acc[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) acc[j] = 0.f;
     float m = -INFINITY, l = 0.f;
-    for (int t = warp; t <= pos; t += nwarps) {
-        float dot = 0.f;
-        float vv[kPer];
-        if (t == pos) {
+    const __nv_bfloat16* kbase = k_cache + (long long)kvh * max_seq * hd;
+    const __nv_bfloat16* vbase = v_cache + (long long)kvh * max_seq * hd;
+    for (int tb = t0 + warp; tb < t1; tb += kAttnWarps * kAttnUnroll) {
+        float kf[kAttnUnroll][PER], vf[kAttnUnroll][PER];
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                const int i = lane + 32 * j;
-                if (i < hd) {
-                    dot = fmaf(q_s[i], k_s[i], dot);
-                    vv[j] = v_s[i];
+        for (int u = 0; u < kAttnUnroll; ++u) {
+            const int t = tb + u * kAttnWarps;
+            if (t < t1 && t != pos) {
+                if constexpr (VEC) {
+                    load_bf16_vec<EL>(kbase + (long long)t * hd + lane * EL, kf[u]);
+                    load_bf16_vec<EL>(vbase + (long long)t * hd + lane * EL, vf[u]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) {
+                        const int e = lane + 32 * j;
+                        kf[u][j] = e < hd ? __bfloat162float(kbase[(long long)t * hd + e]) : 0.f;
+                        vf[u][j] = e < hd ? __bfloat162float(vbase[(long long)t * hd + e]) : 0.f;
+                    }
                 }
-            }
-        } else {
-            const __nv_bfloat16* kc = k_cache + ((long long)kvh * max_seq + t) * hd;
-            const __nv_bfloat16* vc = v_cache + ((long long)kvh * max_seq + t) * hd;
+            } else {
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                const int i = lane + 32 * j;
-                if (i < hd) {
-                    dot = fmaf(q_s[i], __bfloat162float(kc[i]), dot);
-                    vv[j] = __bfloat162float(vc[i]);
+                for (int j = 0; j < PER; ++j) {
+                    const bool ok = t == pos && elem(j) < hd;
+                    kf[u][j] = ok ? k_s[elem(j)] : 0.f;
+                    vf[u][j] = ok ? v_s[elem(j)] : 0.f;
                 }
             }
         }
-        dot = warp_sum(dot) * scale;
-        const float m_new = fmaxf(m, dot);
-        const float corr = expf(m - m_new);  // exp(-inf) = 0 on the first position
-        const float p = expf(dot - m_new);
-        l = l * corr + p;
 #pragma unroll
-        for (int j = 0; j < kPer; ++j)
-            if (lane + 32 * j < hd) acc[j] = acc[j] * corr + p * vv[j];
-        m = m_new;
+        for (int u = 0; u < kAttnUnroll; ++u) {
+            const int t = tb + u * kAttnWarps;
+            float dot = 0.f;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) dot = fmaf(qr[j], kf[u][j], dot);
+            dot = warp_sum(dot) * scale;
+            if (t < t1) {  // warp-uniform
+                const float m_new = fmaxf(m, dot);
+                const float corr = expf(m - m_new);  // exp(-inf) = 0 on the first position
+                const float pw = expf(dot - m_new);
+                l = l * corr + pw;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) acc[j] = acc[j] * corr + pw * vf[u][j];
+                m = m_new;
+            }
+        }
     }
     if (lane == 0) {
         m_s[warp] = m;
         l_s[warp] = l;
     }
 #pragma unroll
-    for (int j = 0; j < kPer; ++j)
-        if (lane + 32 * j < hd) acc_s[warp][lane + 32 * j] = acc[j];
+    for (int j = 0; j < PER; ++j)
+        if (elem(j) < hd) acc_s[warp][elem(j)] = acc[j];
     __syncthreads();
+    // ---- merge the warps of this CTA ----
     float mm = -INFINITY;
-    for (int wv = 0; wv < nwarps; ++wv) mm = fmaxf(mm, m_s[wv]);
+#pragma unroll
+    for (int wv = 0; wv < kAttnWarps; ++wv) mm = fmaxf(mm, m_s[wv]);
     float ll = 0.f;
-    for (int wv = 0; wv < nwarps; ++wv) ll += (m_s[wv] == -INFINITY) ? 0.f : l_s[wv] * expf(m_s[wv] - mm);
+#pragma unroll
+    for (int wv = 0; wv < kAttnWarps; ++wv) ll += (m_s[wv] == -INFINITY) ? 0.f : l_s[wv] * expf(m_s[wv] - mm);
+    if (n_split == 1) {
+        for (int i = tid; i < hd; i += kAttnThreads) {
+            float o = 0.f;
+#pragma unroll
+            for (int wv = 0; wv < kAttnWarps; ++wv)
+                if (m_s[wv] != -INFINITY) o += acc_s[wv][i] * expf(m_s[wv] - mm);
+            out[(long long)h * hd + i] = o / ll;
+        }
+        return;
+    }
+    // ---- partial of this split -> workspace; the last CTA of the head combines ----
+    float* my = ws + ((long long)h * n_split + sp) * (hd + 2);
     for (int i = tid; i < hd; i += kAttnThreads) {
         float o = 0.f;
-        for (int wv = 0; wv < nwarps; ++wv)
+#pragma unroll
+        for (int wv = 0; wv < kAttnWarps; ++wv)
             if (m_s[wv] != -INFINITY) o += acc_s[wv][i] * expf(m_s[wv] - mm);
-        out[(long long)h * hd + i] = o / ll;
+        my[2 + i] = o;
     }
+    if (tid == 0) {
+        my[0] = mm;
+        my[1] = ll;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = (atomicAdd(&tickets[h], 1) == n_split - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const float* hp = ws + (long long)h * n_split * (hd + 2);
+    float gm = -INFINITY;
+    for (int s2 = 0; s2 < n_split; ++s2) gm = fmaxf(gm, __ldcg(hp + (long long)s2 * (hd + 2)));
+    float gl = 0.f;
+    for (int s2 = 0; s2 < n_split; ++s2) {
+        const float pm = __ldcg(hp + (long long)s2 * (hd + 2));
+        if (pm != -INFINITY) gl += __ldcg(hp + (long long)s2 * (hd + 2) + 1) * expf(pm - gm);
+    }
+    for (int i = tid; i < hd; i += kAttnThreads) {
+        float o = 0.f;
+        for (int s2 = 0; s2 < n_split; ++s2) {
+            const float pm = __ldcg(hp + (long long)s2 * (hd + 2));
+            if (pm != -INFINITY) o += __ldcg(hp + (long long)s2 * (hd + 2) + 2 + i) * expf(pm - gm);
+        }
+        out[(long long)h * hd + i] = o / gl;
+    }
+    if (tid == 0) tickets[h] = 0;  // ready for the next launch (graph replay)
 }
 
 // argmax with the winning value (vocab-parallel lm_head: ranks exchange (value, index)).

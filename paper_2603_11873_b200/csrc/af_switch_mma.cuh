@@ -27,22 +27,25 @@ constexpr int kBoxes = kTN / kBoxCols;            // 4 boxes per tile
 constexpr int kBoxBytes = kTM * kBoxCols * 2;     // 8 KB
 constexpr int kWStageBytes = kTM * kTN * 2;       // 32 KB
 constexpr int kDownPitch = kTN + 8;               // elements; +16 B keeps ldmatrix conflict free
-constexpr int kMmaWarps = kConsumers / 32;        // 8 consumer warps
+constexpr int kMmaWarps = 16;                     // consumer warps: 4 row groups (m16) x 4 boxes
+constexpr int kMmaConsumers = kMmaWarps * 32;     // 512 threads
+constexpr int kMmaThreads = kMmaConsumers + 64;   // + producer warp (TMA loads) + storer warp (TMA stores)
 constexpr int kMmaMaxKS = 4;                      // k-steps of 16 ranks: S <= 64
 
 template <int KS>
 struct MmaLayout {
     static constexpr int s_pad = KS * 16;
-    static constexpr int stages = (KS <= 3) ? 4 : 3;
+    static constexpr int stages = KS == 1 ? 6 : (KS == 2 ? 5 : (KS == 3 ? 4 : 3));
     static constexpr int up_stage_bytes = kTM * s_pad * 2;
     static constexpr int down_bytes = 2 * s_pad * kDownPitch * 2;
     // offsets from the 1024-aligned base
     static constexpr int off_w = 0;
     static constexpr int off_up = off_w + stages * kWStageBytes;
     static constexpr int off_down = off_up + stages * up_stage_bytes;
-    static constexpr int off_bar = off_down + down_bytes;          // full[stages], empty[stages]
-    static constexpr int off_plan = off_bar + 2 * 8 * 4 /*room for 4 stages*/;
+    static constexpr int off_bar = off_down + down_bytes;          // full[8], computed[8], empty[8]
+    static constexpr int off_plan = off_bar + 3 * 8 * 8;
     static constexpr int total = off_plan + (int)sizeof(Plan) + 1024 /*alignment slack*/;
+    static_assert(total <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
@@ -87,7 +90,7 @@ __device__ __forceinline__ void tma_store_2d_addr(const void* tmap, int c0, int 
 struct MmaParams {
     SwitchParams base;
     const CUtensorMap* tmaps_ld;   // per segment: 64 x 64 swizzled box on the source (live or pristine)
-    const CUtensorMap* tmaps_st;   // per segment: 32 x 64 swizzled box on the live matrix
+    const CUtensorMap* tmaps_st;   // per segment: the same box shape on the live matrix
 };
 
 // Gated DOWN slab for one unit: rows [0, S) hold hi(g*a), rows [s_pad, s_pad+S) hold lo; the
@@ -99,7 +102,7 @@ __device__ __forceinline__ void fill_down_hilo(unsigned char* down_smem, const S
     constexpr int chunks_per_row = kTN / 8;
     const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(sg.down);
     const int r = sg.rank;
-    for (int i = tid; i < s_pad * chunks_per_row; i += kConsumers) {
+    for (int i = tid; i < s_pad * chunks_per_row; i += kMmaConsumers) {
         const int q = i / chunks_per_row;
         const int c = (i % chunks_per_row) * 8;
         uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
@@ -127,8 +130,15 @@ __device__ __forceinline__ void fill_down_hilo(unsigned char* down_smem, const S
     }
 }
 
+// Warp roles (all walk the same static tile sequence):
+//   warps 0..15  consumers: wait full[stage] -> W + U.(hi+lo) in place in smem -> arrive computed[stage]
+//   warp 16      producer : wait empty[stage] -> TMA loads of the W boxes + bulk copies of the UP blocks
+//   warp 17      storer   : wait computed[stage] -> TMA stores of the tile -> wait until the stores have
+//                           read shared memory -> arrive empty[stage]
+// A stage is handed back to the producer as soon as its stores have drained shared memory, so
+// stages-1 tiles of loads are in flight while one tile is being updated.
 template <int KS>
-__global__ void __launch_bounds__(kConsumers + 32, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
+__global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
     using L = MmaLayout<KS>;
     constexpr int kSt = L::stages;
     extern __shared__ unsigned char smem_dyn[];
@@ -136,14 +146,16 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) switch_mma_kernel(const __
     // 128-byte swizzle needs 1024-byte aligned boxes
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::off_bar);
-    uint64_t* empty = full + 4;
+    uint64_t* computed = full + 8;
+    uint64_t* empty = full + 16;
     Plan& plan = *reinterpret_cast<Plan*>(sm + L::off_plan);
     const int tid = threadIdx.x;
 
     if (tid == 0) {
         for (int s = 0; s < kSt; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kMmaWarps);
+            mbar_init(&computed[s], kMmaWarps);
+            mbar_init(&empty[s], 1);
         }
         fence_mbar_init();
         if (p.use_dev)
@@ -159,10 +171,11 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) switch_mma_kernel(const __
 
     const uint32_t w_base = smem_u32(sm + L::off_w);
     const uint32_t up_base = smem_u32(sm + L::off_up);
+    const int warp = tid >> 5, lane = tid & 31;
 
-    if (tid >= kConsumers) {
+    if (warp == kMmaWarps) {
         // ============ producer: W boxes by TMA, UP blocks by 1-D bulk copies ============
-        if (tid == kConsumers) {
+        if (lane == 0) {
             TileIter ti;
             ti.init(p);
             SegDev sg;
@@ -193,12 +206,33 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) switch_mma_kernel(const __
         }
         return;
     }
+    if (warp == kMmaWarps + 1) {
+        // ============ storer: whole tile back to global, then hand the stage back ============
+        if (lane == 0) {
+            TileIter ti;
+            ti.init(p);
+            for (int it = 0; ti.valid(p); ++it) {
+                const int stage = it % kSt;
+                const uint32_t ph = (it / kSt) & 1;
+                mbar_wait(&computed[stage], ph);
+                const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
+#pragma unroll
+                for (int b = 0; b < kBoxes; ++b)
+                    tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
+                bulk_commit();
+                bulk_wait_read<0>();  // the stores have drained this stage's shared memory
+                mbar_arrive(&empty[stage]);
+                ti.next(p);
+            }
+            bulk_wait_all<0>();  // global writes complete before the CTA retires
+        }
+        return;
+    }
 
     // ================================ consumers ====================================
-    const int lane = tid & 31, warp = tid >> 5;
     const int mi = lane >> 3, rr = lane & 7;       // ldmatrix: lane supplies row rr of matrix mi
-    const int wrow0 = (warp & 1) * 32;             // this warp: rows [wrow0, wrow0+32) ...
-    const int wbox = warp >> 1;                    // ... of box wbox (64 columns)
+    const int wrow0 = (warp & 3) * 16;             // this warp: rows [wrow0, wrow0+16) ...
+    const int wbox = warp >> 2;                    // ... of box wbox (64 columns)
     unsigned char* down_smem = sm + L::off_down;
     const uint32_t down_base = smem_u32(down_smem);
 
@@ -206,103 +240,76 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) switch_mma_kernel(const __
     ti.init(p);
     bool new_unit = true;
     SegDev sg;
-    int S = 0, ks = 0;
-    int prev_stage = -1;
+    int S = 0;
     for (int it = 0; ti.valid(p); ++it) {
         const int stage = it % kSt;
         const uint32_t ph = (it / kSt) & 1;
         if (new_unit) {
             sg = p.segs[ti.un.seg];
             S = n_blocks * sg.rank;
-            ks = (S + 15) >> 4;
-            named_bar_sync(1, kConsumers);  // every warp is done with the previous slab
+            named_bar_sync(1, kMmaConsumers);  // every warp is done with the previous slab
             fill_down_hilo<KS>(down_smem, sg, plan, S, ti.un.col0, tid);
-            named_bar_sync(1, kConsumers);  // slab visible
+            named_bar_sync(1, kMmaConsumers);  // slab visible
         }
-        const int m0 = ti.m0;
-        const UnitDev un = ti.un;
         new_unit = ti.next(p);
 
         mbar_wait(&full[stage], ph);
         const uint32_t w_stage = w_base + stage * kWStageBytes + wbox * kBoxBytes;
         const uint32_t up_stage = up_base + stage * L::up_stage_bytes;
 
-        // ---- A fragments (UP rows of this warp), kept in registers for the whole tile ----
-        uint32_t afrag[2][KS][4];
+        // ---- A fragments (UP rows of this warp), kept in registers for the whole tile.  Ranks
+        //      past S are padding: their UP columns read as 0 (the slab rows are 0 as well). ----
+        uint32_t afrag[KS][4];
+        {
+            const int row = wrow0 + (mi & 1) * 8 + rr;
 #pragma unroll
-        for (int j = 0; j < KS; ++j) {
-            if (j < ks) {
+            for (int j = 0; j < KS; ++j) {
                 const int k0 = 16 * j + (mi >> 1) * 8;  // first rank of the 8x8 matrix this lane addresses
-                const bool live = k0 < S;
-                const int kk = live ? k0 : 0;
+                const int kk = k0 < S ? k0 : 0;
                 const int b = kk / sg.rank, kin = kk % sg.rank;
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const int row = wrow0 + mt * 16 + (mi & 1) * 8 + rr;
-                    ldmatrix_x4(afrag[mt][j], up_stage + ((b * kTM + row) * sg.rank + kin) * 2);
-                    if (16 * j + 8 >= S) {  // ranks past S are padding: their UP columns must read as 0
-                        afrag[mt][j][2] = 0u;
-                        afrag[mt][j][3] = 0u;
-                    }
-                }
+                ldmatrix_x4(afrag[j], up_stage + ((b * kTM + row) * sg.rank + kin) * 2);
+                if (16 * j >= S) afrag[j][0] = afrag[j][1] = 0u;
+                if (16 * j + 8 >= S) afrag[j][2] = afrag[j][3] = 0u;
             }
         }
-
-        // ---- four n16 chunks of the warp's 32 x 64 region ----
+        const int wrow = wrow0 + (mi & 1) * 8 + rr;  // W row this lane addresses in ldmatrix/stmatrix
+        // ---- four n16 chunks of the warp's 16 x 64 region ----
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
-            float acc[2][2][4];
+            float acc[2][4];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+            for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+                for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
             const int ncol = wbox * kBoxCols + c4 * 16 + (mi >> 1) * 8;  // slab column this lane addresses
+            const int chunk = c4 * 2 + (mi >> 1);
+            const uint32_t waddr = w_stage + wrow * 128 + ((chunk ^ (wrow & 7)) << 4);
+            uint32_t wv[4];
+            ldmatrix_x4(wv, waddr);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {  // hi rows then lo rows of the slab
 #pragma unroll
                 for (int j = 0; j < KS; ++j) {
-                    if (j < ks) {
-                        const int krow = half * L::s_pad + 16 * j + (mi & 1) * 8 + rr;
-                        uint32_t bf[4];
-                        ldmatrix_x4_trans(bf, down_base + (krow * kDownPitch + ncol) * 2);
-#pragma unroll
-                        for (int mt = 0; mt < 2; ++mt) {
-                            mma_bf16_16816(acc[mt][0], afrag[mt][j], bf[0], bf[1]);
-                            mma_bf16_16816(acc[mt][1], afrag[mt][j], bf[2], bf[3]);
-                        }
-                    }
+                    const int krow = half * L::s_pad + 16 * j + (mi & 1) * 8 + rr;
+                    uint32_t bf[4];
+                    ldmatrix_x4_trans(bf, down_base + (krow * kDownPitch + ncol) * 2);
+                    mma_bf16_16816(acc[0], afrag[j], bf[0], bf[1]);
+                    mma_bf16_16816(acc[1], afrag[j], bf[2], bf[3]);
                 }
             }
             // W + D, rounded RNE to bf16, written back in place (swizzled smem)
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                const int row = wrow0 + mt * 16 + (mi & 1) * 8 + rr;
-                const int chunk = c4 * 2 + (mi >> 1);
-                const uint32_t addr = w_stage + row * 128 + ((chunk ^ (row & 7)) << 4);
-                uint32_t wv[4];
-                ldmatrix_x4(wv, addr);
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    const uint32_t a = wv[nt * 2], b2 = wv[nt * 2 + 1];
-                    wv[nt * 2] = pack_bf16x2(bf16lo_to_f32(a) + acc[mt][nt][0], bf16hi_to_f32(a) + acc[mt][nt][1]);
-                    wv[nt * 2 + 1] = pack_bf16x2(bf16lo_to_f32(b2) + acc[mt][nt][2], bf16hi_to_f32(b2) + acc[mt][nt][3]);
-                }
-                stmatrix_x4(addr, wv);
+            for (int nt = 0; nt < 2; ++nt) {
+                const uint32_t a = wv[nt * 2], b2 = wv[nt * 2 + 1];
+                wv[nt * 2] = pack_bf16x2(bf16lo_to_f32(a) + acc[nt][0], bf16hi_to_f32(a) + acc[nt][1]);
+                wv[nt * 2 + 1] = pack_bf16x2(bf16lo_to_f32(b2) + acc[nt][2], bf16hi_to_f32(b2) + acc[nt][3]);
             }
+            stmatrix_x4(waddr, wv);
         }
-        fence_proxy_async_smem();
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA store
         __syncwarp();
-        if (lane == 0) {
-            tma_store_2d_addr(mp.tmaps_st + un.seg, un.col0 + wbox * kBoxCols, m0 + wrow0, w_stage + wrow0 * 128);
-            bulk_commit();
-            bulk_wait_read<1>();  // this warp's store of the previous tile has drained its smem
-            if (prev_stage >= 0) mbar_arrive(&empty[prev_stage]);
-            prev_stage = stage;
-        }
+        if (lane == 0) mbar_arrive(&computed[stage]);
     }
-    if (lane == 0) bulk_wait_all<0>();
 }
 
 }  // namespace af

@@ -58,6 +58,7 @@ class LlamaConfig:
     switch_mode: str = "inplace"     # or "from_pristine"
     adapters: bool = True            # False = adapter-free backbone (the reference's BASE strategy)
     keep_pristine: bool = True
+    attn_splits: int = 0             # CTAs per head in decode attention; 0 = auto (1 up to 512 positions)
 
     def validate(self) -> None:
         for name in ("layers", "hidden", "ffn", "n_heads", "n_kv_heads", "vocab", "experts", "rank", "top_k", "max_seq", "tp_size"):
@@ -335,6 +336,11 @@ class LlamaEngine:
         self.prev = DeviceDecision(dev)
         self.have_prev = False
         self.history = torch.zeros(cfg.max_seq, dtype=torch.int32, device=dev)
+        sm_count = _capi.device_info()["sm_count"]
+        self.attn_splits = cfg.attn_splits if cfg.attn_splits > 0 else (
+            1 if cfg.max_seq <= 512 else max(1, min(16, -(-sm_count // self.heads_local))))
+        self.attn_ws = torch.zeros(self.heads_local * self.attn_splits * (hd + 2), dtype=f32, device=dev)
+        self.attn_tickets = torch.zeros(self.heads_local, dtype=torch.int32, device=dev)
         self.forced_dev = None
         self._graphs = {}
 
@@ -385,7 +391,8 @@ class LlamaEngine:
                                         _capi.AF_PRO_RMSNORM, _ptr(self.attn_norm[li]), eps, _capi.AF_EPI_NONE, None, st))
             self._check(L.af_attn_decode(_ptr(self.qkv_buf), _ptr(self.k_cache[li]), _ptr(self.v_cache[li]), _ptr(self.cos),
                                          _ptr(self.sin), _ptr(self.pos_dev), self.heads_local, self.kv_local, cfg.head_dim,
-                                         cfg.max_seq, _ptr(self.attn_buf), st))
+                                         cfg.max_seq, self.attn_splits, _ptr(self.attn_ws), _ptr(self.attn_tickets),
+                                         _ptr(self.attn_buf), st))
             self._check(L.af_gemv_fused(_ptr(self.wo[li]), d, self.q_rows, self.q_rows, _ptr(self.attn_buf), _ptr(xb),
                                         _capi.AF_PRO_NONE, None, 0.0, res_epi, _ptr(xa) if res_epi else None, st))
             self.comm.all_reduce_sum(xb)

@@ -96,6 +96,28 @@ def test_graph_replay_equals_eager(llama):
         assert torch.equal(ta.data, tb.data)
 
 
+def test_split_attention_and_pdl_do_not_change_results(llama):
+    """flash-decoding split over CTAs and programmatic dependent launch are schedule changes only."""
+    from paper_2603_11873_b200 import _capi
+
+    forced = np.random.Generator(np.random.PCG64(13)).integers(0, 512, 24)
+    outs = []
+    for splits, pdl in ((1, 1), (3, 1), (1, 0), (5, 0)):
+        _capi.check(_capi.lib().af_set_pdl(pdl))
+        eng = llama.LlamaEngine(llama.preset("tiny", max_seq=40, attn_splits=splits), init="host")
+        eng.reset(forced=forced)
+        logits = []
+        for _ in range(24):
+            eng.decode_step()
+            logits.append(eng.logits.cpu().numpy().copy())
+        outs.append((eng.tokens(), np.stack(logits)))
+    _capi.check(_capi.lib().af_set_pdl(1))
+    for toks, lg in outs[1:]:
+        np.testing.assert_allclose(lg, outs[0][1], rtol=1e-4, atol=1e-5)
+    assert outs[2][0] == outs[0][0]          # PDL on/off: bit-identical schedule-independent arithmetic
+    assert np.array_equal(outs[2][1], outs[0][1])
+
+
 def test_generate_and_base_engine(llama):
     cfg = llama.preset("tiny", max_seq=64)
     eng = llama.LlamaEngine(cfg, init="host")
