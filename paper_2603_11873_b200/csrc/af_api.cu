@@ -261,8 +261,8 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
             const void* pr = s.pristine ? s.pristine : s.target;
             int rc = make_map(&maps[0 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kTN, kTM, CU_TENSOR_MAP_SWIZZLE_NONE);
             if (!rc) rc = make_map(&maps[1 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kTN, kTM, CU_TENSOR_MAP_SWIZZLE_NONE);
-            if (!rc) rc = make_map(&maps[2 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kBoxCols, kTM, CU_TENSOR_MAP_SWIZZLE_128B);
-            if (!rc) rc = make_map(&maps[3 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kBoxCols, kTM, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (!rc) rc = make_map(&maps[2 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kBoxCols, kMR, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (!rc) rc = make_map(&maps[3 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kBoxCols, kMR, CU_TENSOR_MAP_SWIZZLE_128B);
             if (rc) {
                 af_table_destroy(t);
                 return rc;
@@ -605,27 +605,28 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
     if (out == x) return fail(AF_EALIAS, "GEMV output aliases its input");
     if (rows == 0) return AF_OK;
     const DeviceInfo& di = device_info();
-    const int smem = cols * 4;
-    if (smem + 1024 > di.max_smem_optin) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
-    static int configured_smem = 48 * 1024;
+    const int xs_bytes = cols * 4;
+    // 16 KB stages beside the staged vector.  The footprint is held to half an SM when possible so
+    // that, under programmatic dependent launch, the next GEMV's CTA is co-resident with this one
+    // and fills its ring while this kernel drains.
+    const int half_sm = (di.max_smem_optin - 2048) / 2;
+    int n_stages = (half_sm - xs_bytes) / kGvStage;
+    if (n_stages < 3) n_stages = (di.max_smem_optin - 2048 - xs_bytes) / kGvStage;
+    n_stages = std::min(n_stages, kGvMaxStages);
+    if (n_stages < 2) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
+    if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (norm_w && (reinterpret_cast<uintptr_t>(norm_w) & 15) != 0) || cols % 4 != 0)
+        return fail(AF_EDIM, "fused GEMV needs 16-byte aligned f32 vectors");
+    const int smem = n_stages * kGvStage + xs_bytes;
+    static int configured_smem = 0;
     if (smem > configured_smem) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(gemv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        AF_CUDA_TRY(cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         configured_smem = smem;
     }
-    // Even split of the rows over SMs x resident CTAs: every SM streams the same number of bytes.
-    int per_sm = 0;
-    {
-        static int occ_cached_smem = -1, occ_cached = 0;
-        if (occ_cached_smem != smem) {
-            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cached, gemv_fused_kernel, kGemvFThreads, smem));
-            occ_cached_smem = smem;
-        }
-        per_sm = std::max(1, std::min(occ_cached, 4));
-    }
-    const int grid = std::max(1, std::min(rows, di.sm_count * per_sm));
+    // Even split of the rows over one persistent CTA per SM (fewer when there are fewer row groups).
+    const int grid = std::max(1, std::min((rows + kGvWarps - 1) / kGvWarps, di.sm_count));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kGemvFThreads);
+    cfg.blockDim = dim3(kGvThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = as_stream(stream);
     cudaLaunchAttribute attr[1];
@@ -633,9 +634,9 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = g_pdl.load() ? 1 : 0;
-    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_fused_kernel, reinterpret_cast<const __nv_bfloat16*>(w), (int)rows, (int)cols,
-                                   (long long)ld, x, out, (int)prologue, norm_w, eps, (int)epilogue, res));
-    AF_LAUNCH_CHECK("gemv_fused_kernel");
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_tma_kernel, reinterpret_cast<const __nv_bfloat16*>(w), (int)rows, (int)cols,
+                                   (long long)ld, x, out, (int)prologue, norm_w, eps, (int)epilogue, res, n_stages));
+    AF_LAUNCH_CHECK("gemv_tma_kernel");
     return AF_OK;
 }
 

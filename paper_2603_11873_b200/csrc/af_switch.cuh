@@ -344,7 +344,8 @@ __device__ __forceinline__ void tile_update(SwitchSmem& sm, int stage, int n_ran
 
 // Tile iterator over this CTA's static schedule: units blockIdx.x, +gridDim.x, ...; inside a
 // unit, kTM-row tiles top to bottom.  Producer and consumers walk the same sequence.
-struct TileIter {
+template <int STEP>
+struct TileIterT {
     int u, m0, row_end;
     UnitDev un;
     __device__ __forceinline__ bool valid(const SwitchParams& p) const { return u < p.n_units; }
@@ -361,13 +362,14 @@ struct TileIter {
     }
     // returns true when the step crossed into a new unit
     __device__ __forceinline__ bool next(const SwitchParams& p) {
-        m0 += kTM;
+        m0 += STEP;
         if (m0 < row_end) return false;
         u += gridDim.x;
         load_unit(p);
         return true;
     }
 };
+using TileIter = TileIterT<kTM>;
 
 // Vectorised UP staging: one 16-byte chunk = 8 consecutive ranks of one (row, block).
 // Eligible when every block's rows are 16-byte aligned and rank % 8 == 0 (bf16 banks).

@@ -11,41 +11,48 @@
 // split into v = hi + lo + O(2^-17 |v|) with hi, lo bf16, and D = U.hi + U.lo accumulates in
 // f32 (products of two bf16 values are exact in f32).
 //
-// Data movement per 64 x 256 tile of W (one pipeline stage):
-//   W   : 4 TMA boxes of 64 rows x 64 cols (128-byte swizzle) global -> smem, updated in place
-//         in smem with ldmatrix / stmatrix, then one TMA store per consumer warp (32 x 64).
-//   UP  : one 1-D bulk copy per block (64 rows x r bf16 are contiguous in the bank).
-//   DOWN: gated hi/lo slab [2 * S_pad][256 (+8 pad)] bf16, staged once per unit (column strip).
+// Data movement per 32 x 256 tile of W (one pipeline stage, 16 KB):
+//   W   : 4 TMA boxes of 32 rows x 64 cols (128-byte swizzle) global -> smem, updated in place
+//         in smem with ldmatrix / stmatrix, then 4 TMA box stores by a dedicated storer warp.
+//   UP  : one 1-D bulk copy per block (32 rows x r bf16 are contiguous in the bank).
+//   DOWN: gated hi/lo slab [2 * S_pad][256 (+8 pad)] bf16, staged once per unit (column strip);
+//         each consumer warp owns 16 columns of the strip and keeps its B fragments of the slab
+//         in registers for the whole unit, so the slab is read once per unit, not once per tile.
 #pragma once
 
 #include "af_switch.cuh"
 
 namespace af {
 
+constexpr int kMR = 32;                           // tile rows of the tensor path
 constexpr int kBoxCols = 64;                      // 128-byte swizzle span in bf16
 constexpr int kBoxes = kTN / kBoxCols;            // 4 boxes per tile
-constexpr int kBoxBytes = kTM * kBoxCols * 2;     // 8 KB
-constexpr int kWStageBytes = kTM * kTN * 2;       // 32 KB
+constexpr int kBoxBytes = kMR * kBoxCols * 2;     // 4 KB
+constexpr int kWStageBytes = kMR * kTN * 2;       // 16 KB
 constexpr int kDownPitch = kTN + 8;               // elements; +16 B keeps ldmatrix conflict free
-constexpr int kMmaWarps = 16;                     // consumer warps: 4 row groups (m16) x 4 boxes
+constexpr int kMmaWarps = 16;                     // consumer warps: one n16 column slice each
 constexpr int kMmaConsumers = kMmaWarps * 32;     // 512 threads
 constexpr int kMmaThreads = kMmaConsumers + 64;   // + producer warp (TMA loads) + storer warp (TMA stores)
 constexpr int kMmaMaxKS = 4;                      // k-steps of 16 ranks: S <= 64
+constexpr int kMmaMaxStages = 12;
+constexpr int kStoreDepth = 2;                    // tile stores that may still be reading smem
 
 template <int KS>
 struct MmaLayout {
     static constexpr int s_pad = KS * 16;
-    static constexpr int stages = KS == 1 ? 6 : (KS == 2 ? 5 : (KS == 3 ? 4 : 3));
-    static constexpr int up_stage_bytes = kTM * s_pad * 2;
+    static constexpr int up_stage_bytes = kMR * s_pad * 2;
     static constexpr int down_bytes = 2 * s_pad * kDownPitch * 2;
+    static constexpr int fixed = down_bytes + 3 * 8 * 16 + (int)sizeof(Plan) + 1024 /*alignment slack*/ + 256;
+    static constexpr int by_smem = (227 * 1024 - fixed) / (kWStageBytes + up_stage_bytes);
+    static constexpr int stages = by_smem < kMmaMaxStages ? by_smem : kMmaMaxStages;
     // offsets from the 1024-aligned base
     static constexpr int off_w = 0;
     static constexpr int off_up = off_w + stages * kWStageBytes;
     static constexpr int off_down = off_up + stages * up_stage_bytes;
-    static constexpr int off_bar = off_down + down_bytes;          // full[8], computed[8], empty[8]
-    static constexpr int off_plan = off_bar + 3 * 8 * 8;
+    static constexpr int off_bar = off_down + down_bytes;          // full[16], computed[16], empty[16]
+    static constexpr int off_plan = off_bar + 3 * 8 * 16;
     static constexpr int total = off_plan + (int)sizeof(Plan) + 1024 /*alignment slack*/;
-    static_assert(total <= 227 * 1024, "shared memory budget");
+    static_assert(stages >= 4 && total <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
@@ -94,33 +101,52 @@ struct MmaParams {
 };
 
 // Gated DOWN slab for one unit: rows [0, S) hold hi(g*a), rows [s_pad, s_pad+S) hold lo; the
-// padding rows up to s_pad are zero.  16-byte global loads, 16-byte smem stores.
+// padding rows up to s_pad are zero.  Staging is split in two so the global-load latency hides
+// under a whole unit of tiles: down_prefetch() issues this thread's 16-byte loads of the NEXT
+// unit's DOWN rows into registers, down_commit() folds the gate (one f32 multiply,
+// adapters.py:202), splits into bf16 hi + lo and writes the slab.
 template <int KS>
-__device__ __forceinline__ void fill_down_hilo(unsigned char* down_smem, const SegDev& sg, const Plan& plan, int S,
-                                               int col0, int tid) {
-    constexpr int s_pad = KS * 16;
+__device__ __forceinline__ void down_prefetch(uint4 (&regs)[KS], const SegDev& sg, const Plan& plan, int S, int col0,
+                                              int tid) {
     constexpr int chunks_per_row = kTN / 8;
     const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(sg.down);
     const int r = sg.rank;
-    for (int i = tid; i < s_pad * chunks_per_row; i += kMmaConsumers) {
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+        const int i = tid + j * kMmaConsumers;
+        const int q = i / chunks_per_row;
+        const int c = (i % chunks_per_row) * 8;
+        regs[j] = make_uint4(0u, 0u, 0u, 0u);
+        if (q < S && col0 + c < sg.d_in) {
+            const int b = q / r, qr = q % r;
+            regs[j] = __ldg(reinterpret_cast<const uint4*>(base + (long long)plan.expert[b] * sg.down_estride +
+                                                           (long long)qr * sg.ld_down + col0 + c));
+        }
+    }
+}
+
+template <int KS>
+__device__ __forceinline__ void down_commit(unsigned char* down_smem, const uint4 (&regs)[KS], int rank, const Plan& plan,
+                                            int S, int tid) {
+    constexpr int s_pad = KS * 16;
+    constexpr int chunks_per_row = kTN / 8;
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+        const int i = tid + j * kMmaConsumers;
         const int q = i / chunks_per_row;
         const int c = (i % chunks_per_row) * 8;
         uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
-        if (q < S && col0 + c < sg.d_in) {
-            const int b = q / r, qr = q % r;
-            const __nv_bfloat16* src =
-                base + (long long)plan.expert[b] * sg.down_estride + (long long)qr * sg.ld_down + col0 + c;
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
-            const float w = plan.weight[b];
-            const uint32_t in[4] = {v.x, v.y, v.z, v.w};
+        if (q < S) {
+            const float w = plan.weight[q / rank];
+            const uint32_t in[4] = {regs[j].x, regs[j].y, regs[j].z, regs[j].w};
             uint32_t oh[4], ol[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float f0 = __fmul_rn(w, bf16lo_to_f32(in[j]));  // adapters.py:202 (f32 gate folding)
-                const float f1 = __fmul_rn(w, bf16hi_to_f32(in[j]));
+            for (int e = 0; e < 4; ++e) {
+                const float f0 = __fmul_rn(w, bf16lo_to_f32(in[e]));
+                const float f1 = __fmul_rn(w, bf16hi_to_f32(in[e]));
                 const uint32_t h = pack_bf16x2(f0, f1);
-                oh[j] = h;
-                ol[j] = pack_bf16x2(f0 - bf16lo_to_f32(h), f1 - bf16hi_to_f32(h));
+                oh[e] = h;
+                ol[e] = pack_bf16x2(f0 - bf16lo_to_f32(h), f1 - bf16hi_to_f32(h));
             }
             hi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
             lo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
@@ -130,13 +156,14 @@ __device__ __forceinline__ void fill_down_hilo(unsigned char* down_smem, const S
     }
 }
 
+using MmaIter = TileIterT<kMR>;
+
 // Warp roles (all walk the same static tile sequence):
 //   warps 0..15  consumers: wait full[stage] -> W + U.(hi+lo) in place in smem -> arrive computed[stage]
 //   warp 16      producer : wait empty[stage] -> TMA loads of the W boxes + bulk copies of the UP blocks
-//   warp 17      storer   : wait computed[stage] -> TMA stores of the tile -> wait until the stores have
-//                           read shared memory -> arrive empty[stage]
-// A stage is handed back to the producer as soon as its stores have drained shared memory, so
-// stages-1 tiles of loads are in flight while one tile is being updated.
+//   warp 17      storer   : wait computed[stage] -> TMA stores of the tile; a stage goes back to the
+//                           producer once its stores have read shared memory (kStoreDepth newer
+//                           stores may still be draining)
 template <int KS>
 __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
     using L = MmaLayout<KS>;
@@ -146,8 +173,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     // 128-byte swizzle needs 1024-byte aligned boxes
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::off_bar);
-    uint64_t* computed = full + 8;
-    uint64_t* empty = full + 16;
+    uint64_t* computed = full + 16;
+    uint64_t* empty = full + 32;
     Plan& plan = *reinterpret_cast<Plan*>(sm + L::off_plan);
     const int tid = threadIdx.x;
 
@@ -176,7 +203,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     if (warp == kMmaWarps) {
         // ============ producer: W boxes by TMA, UP blocks by 1-D bulk copies ============
         if (lane == 0) {
-            TileIter ti;
+            MmaIter ti;
             ti.init(p);
             SegDev sg;
             int cur_seg = -1;
@@ -187,7 +214,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                     cur_seg = ti.un.seg;
                     sg = p.segs[cur_seg];
                 }
-                const int rows_here = min(kTM, sg.d_out - ti.m0);
+                const int rows_here = min(kMR, sg.d_out - ti.m0);
                 const uint32_t up_blk_bytes = (uint32_t)rows_here * sg.rank * 2;
                 mbar_wait(&empty[stage], ph ^ 1);
                 mbar_expect_tx(&full[stage], kWStageBytes + n_blocks * up_blk_bytes);
@@ -198,7 +225,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                                      &full[stage]);
                 const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
                 for (int b = 0; b < n_blocks; ++b)
-                    bulk_load_1d(up_base + stage * L::up_stage_bytes + b * (kTM * sg.rank * 2),
+                    bulk_load_1d(up_base + stage * L::up_stage_bytes + b * (kMR * sg.rank * 2),
                                  upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * sg.rank,
                                  up_blk_bytes, &full[stage]);
                 ti.next(p);
@@ -209,9 +236,10 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     if (warp == kMmaWarps + 1) {
         // ============ storer: whole tile back to global, then hand the stage back ============
         if (lane == 0) {
-            TileIter ti;
+            MmaIter ti;
             ti.init(p);
-            for (int it = 0; ti.valid(p); ++it) {
+            int it = 0;
+            for (; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
                 mbar_wait(&computed[stage], ph);
@@ -220,8 +248,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                 for (int b = 0; b < kBoxes; ++b)
                     tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
                 bulk_commit();
-                bulk_wait_read<0>();  // the stores have drained this stage's shared memory
-                mbar_arrive(&empty[stage]);
+                bulk_wait_read<kStoreDepth>();  // the stores of tile it - kStoreDepth have drained their stage
+                if (it >= kStoreDepth) mbar_arrive(&empty[(it - kStoreDepth) % kSt]);
                 ti.next(p);
             }
             bulk_wait_all<0>();  // global writes complete before the CTA retires
@@ -231,72 +259,82 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
 
     // ================================ consumers ====================================
     const int mi = lane >> 3, rr = lane & 7;       // ldmatrix: lane supplies row rr of matrix mi
-    const int wrow0 = (warp & 3) * 16;             // this warp: rows [wrow0, wrow0+16) ...
-    const int wbox = warp >> 2;                    // ... of box wbox (64 columns)
+    const int wbox = warp >> 2;                    // this warp: 16 columns = chunks (warp & 3) * 2 + {0, 1} of box wbox
+    const int wchunk = (warp & 3) * 2 + (mi >> 1);
+    const int ncol = warp * 16 + (mi >> 1) * 8;    // slab column this lane addresses
     unsigned char* down_smem = sm + L::off_down;
     const uint32_t down_base = smem_u32(down_smem);
 
-    TileIter ti;
+    MmaIter ti;
     ti.init(p);
+    if (!ti.valid(p)) return;
+    SegDev sg = p.segs[ti.un.seg];
+    int S = n_blocks * sg.rank;
+    uint4 dn_regs[KS];
+    down_prefetch<KS>(dn_regs, sg, plan, S, ti.un.col0, tid);
+    down_commit<KS>(down_smem, dn_regs, sg.rank, plan, S, tid);
+    named_bar_sync(1, kMmaConsumers);  // first slab visible
     bool new_unit = true;
-    SegDev sg;
-    int S = 0;
+    uint32_t bfr[2][KS][4];
+    SegDev sg_next = sg;
+    int S_next = 0;
+    bool have_next = false;
     for (int it = 0; ti.valid(p); ++it) {
         const int stage = it % kSt;
         const uint32_t ph = (it / kSt) & 1;
         if (new_unit) {
-            sg = p.segs[ti.un.seg];
-            S = n_blocks * sg.rank;
-            named_bar_sync(1, kMmaConsumers);  // every warp is done with the previous slab
-            fill_down_hilo<KS>(down_smem, sg, plan, S, ti.un.col0, tid);
-            named_bar_sync(1, kMmaConsumers);  // slab visible
+            // B fragments of this unit's slab -> registers (kept for every tile of the unit)
+#pragma unroll
+            for (int half = 0; half < 2; ++half)
+#pragma unroll
+                for (int j = 0; j < KS; ++j) {
+                    const int krow = half * L::s_pad + 16 * j + (mi & 1) * 8 + rr;
+                    ldmatrix_x4_trans(bfr[half][j], down_base + (krow * kDownPitch + ncol) * 2);
+                }
+            // start fetching the NEXT unit's DOWN rows; they are committed to the slab at its start
+            const int un = ti.u + gridDim.x;
+            have_next = un < p.n_units;
+            if (have_next) {
+                const UnitDev nu = p.units[un];
+                sg_next = p.segs[nu.seg];
+                S_next = n_blocks * sg_next.rank;
+                down_prefetch<KS>(dn_regs, sg_next, plan, S_next, nu.col0, tid);
+            }
         }
         new_unit = ti.next(p);
 
         mbar_wait(&full[stage], ph);
         const uint32_t w_stage = w_base + stage * kWStageBytes + wbox * kBoxBytes;
         const uint32_t up_stage = up_base + stage * L::up_stage_bytes;
-
-        // ---- A fragments (UP rows of this warp), kept in registers for the whole tile.  Ranks
-        //      past S are padding: their UP columns read as 0 (the slab rows are 0 as well). ----
-        uint32_t afrag[KS][4];
-        {
-            const int row = wrow0 + (mi & 1) * 8 + rr;
+#pragma unroll
+        for (int mt = 0; mt < kMR / 16; ++mt) {
+            const int row = mt * 16 + (mi & 1) * 8 + rr;  // tile row this lane addresses
+            const uint32_t waddr = w_stage + row * 128 + ((wchunk ^ (row & 7)) << 4);
+            uint32_t wv[4];
+            ldmatrix_x4(wv, waddr);
+            // A fragments (UP rows); ranks past S are padding and read as 0 (the slab rows are 0 too)
+            uint32_t afrag[KS][4];
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
                 const int k0 = 16 * j + (mi >> 1) * 8;  // first rank of the 8x8 matrix this lane addresses
                 const int kk = k0 < S ? k0 : 0;
                 const int b = kk / sg.rank, kin = kk % sg.rank;
-                ldmatrix_x4(afrag[j], up_stage + ((b * kTM + row) * sg.rank + kin) * 2);
+                ldmatrix_x4(afrag[j], up_stage + ((b * kMR + row) * sg.rank + kin) * 2);
                 if (16 * j >= S) afrag[j][0] = afrag[j][1] = 0u;
                 if (16 * j + 8 >= S) afrag[j][2] = afrag[j][3] = 0u;
             }
-        }
-        const int wrow = wrow0 + (mi & 1) * 8 + rr;  // W row this lane addresses in ldmatrix/stmatrix
-        // ---- four n16 chunks of the warp's 16 x 64 region ----
-#pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
             float acc[2][4];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-            const int ncol = wbox * kBoxCols + c4 * 16 + (mi >> 1) * 8;  // slab column this lane addresses
-            const int chunk = c4 * 2 + (mi >> 1);
-            const uint32_t waddr = w_stage + wrow * 128 + ((chunk ^ (wrow & 7)) << 4);
-            uint32_t wv[4];
-            ldmatrix_x4(wv, waddr);
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {  // hi rows then lo rows of the slab
+            for (int half = 0; half < 2; ++half)
 #pragma unroll
                 for (int j = 0; j < KS; ++j) {
-                    const int krow = half * L::s_pad + 16 * j + (mi & 1) * 8 + rr;
-                    uint32_t bf[4];
-                    ldmatrix_x4_trans(bf, down_base + (krow * kDownPitch + ncol) * 2);
-                    mma_bf16_16816(acc[0], afrag[j], bf[0], bf[1]);
-                    mma_bf16_16816(acc[1], afrag[j], bf[2], bf[3]);
+                    mma_bf16_16816(acc[0], afrag[j], bfr[half][j][0], bfr[half][j][1]);
+                    mma_bf16_16816(acc[1], afrag[j], bfr[half][j][2], bfr[half][j][3]);
                 }
-            }
             // W + D, rounded RNE to bf16, written back in place (swizzled smem)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
@@ -309,6 +347,14 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA store
         __syncwarp();
         if (lane == 0) mbar_arrive(&computed[stage]);
+
+        if (new_unit && have_next) {
+            named_bar_sync(1, kMmaConsumers);  // every warp holds its B fragments: the slab may be rewritten
+            sg = sg_next;
+            S = S_next;
+            down_commit<KS>(down_smem, dn_regs, sg.rank, plan, S, tid);
+            named_bar_sync(1, kMmaConsumers);  // next slab visible
+        }
     }
 }
 

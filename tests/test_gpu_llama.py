@@ -53,6 +53,7 @@ def test_decode_steps_against_oracle(llama, switch_mode):
         nxt = eng.decode_step()
         eng.table.status()
         ids, wts = ora.route(tkn)
+        prev_dec = ora.prev
         dec = eng.decision()
         assert dec.expert_ids == ids, f"step {step}"
         np.testing.assert_allclose(dec.weights, wts, rtol=2e-6)
@@ -61,7 +62,11 @@ def test_decode_steps_against_oracle(llama, switch_mode):
             for j, name in enumerate(llama.SEGMENT_NAMES):
                 got = _bits(eng.targets[li * 7 + j].data)
                 ref_before = pristine[li][name] if switch_mode == "from_pristine" else before[li][name]
-                worst, nd = orc.merge_error_in_ulps(got, ora.w["layers"][li][name]["bits"], ref_before)
+                mid = ref_before.copy()
+                if switch_mode == "inplace":
+                    seg = ora.w["layers"][li][name]
+                    orc.switch_segment_bf16(mid, seg["down"], seg["up"], prev_dec, None)
+                worst, nd = orc.merge_error_in_ulps(got, ora.w["layers"][li][name]["bits"], ref_before, mid)
                 assert worst <= 1.0, f"step {step} layer {li} {name}: {nd} diffs, max {worst} ulp"
                 ora.w["layers"][li][name]["bits"][...] = got      # oracle follows the GPU's live weights
         o_next, o_logits, o_hidden = ora.forward(tkn)

@@ -87,6 +87,7 @@ def test_forced_stream_against_oracle_stepwise(af, compute):
     for step, tkn in enumerate(forced):
         logits = []
         before = [b.copy() for b in om.backbone_bits]
+        prev_dec = ostate.prev
         nxt, _ = af.decode_step(model, state, int(tkn), rec, logits_out=logits)
         o_next, o_logits, o_dec = orc.toy_decode_step(om, ostate, int(tkn), storage="bf16")
         dec = state.prev_decision.to_host()
@@ -98,7 +99,9 @@ def test_forced_stream_against_oracle_stepwise(af, compute):
                 worst, ndiff = orc.max_ulp_diff_bf16(got, om.backbone_bits[li])
                 assert worst == 0, f"step {step} layer {li}: {ndiff} diffs, max {worst} ulp"
             else:
-                worst, ndiff = orc.merge_error_in_ulps(got, om.backbone_bits[li], before[li])
+                mid = before[li].copy()
+                orc.switch_segment_bf16(mid, orc.to_bf16_bits(om.down_bank[li]), orc.to_bf16_bits(om.up_bank[li]), prev_dec, None)
+                worst, ndiff = orc.merge_error_in_ulps(got, om.backbone_bits[li], before[li], mid)
                 assert worst <= 1.0, f"step {step} layer {li}: {ndiff} diffs, max {worst} ulp"
             om.backbone_bits[li][...] = got              # oracle follows the GPU's live weights
         scale = np.max(np.abs(o_logits))
