@@ -103,6 +103,11 @@ int64_t af_launch_count(void);
  * environment variable AF_PDL=0 turns it off at load).  With it, a GEMV prefetches its first
  * weight tiles while the previous kernel of the stream is still draining. */
 int af_set_pdl(int32_t enable);
+/* Streaming strategy of af_gemv_fused: 0 = through registers (LDG.128), 1..4 = through a
+ * shared-memory ring filled by 1-D bulk copies (copy size / producer threads: 2 KB x1, 2 KB x2,
+ * 4 KB x1, 4 KB x2); full_sm != 0 lets the ring take the whole SM instead of half of it.
+ * Results are identical up to f32 summation order.  Env: AF_GEMV, AF_GEMV_FULL_SM. */
+int af_set_gemv_variant(int32_t variant, int32_t full_sm);
 
 /* ---- segment table: built once at model load -------------------------------------
  * Replaces: linalg.py:207-231 `SegmentTable` + `.validate()` (shape, precision and

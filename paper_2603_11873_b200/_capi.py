@@ -81,6 +81,7 @@ SIGNATURES = {
     "af_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 3 + [ctypes.POINTER(_i64)]),
     "af_launch_count": (_i64, []),
     "af_set_pdl": (ctypes.c_int, [_i32]),
+    "af_set_gemv_variant": (ctypes.c_int, [_i32, _i32]),
     "af_table_create": (ctypes.c_int, [ctypes.POINTER(SegmentDesc), _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     "af_table_destroy": (ctypes.c_int, [_vp]),
     "af_table_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),

@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = nvcc_path()
     if nvcc is None:
         raise RuntimeError("nvcc not found: cannot build libadafuse_b200.so")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB + ".tmp", os.path.join(CSRC, "af_api.cu")]
+    extra = os.environ.get("AF_NVCC_EXTRA", "").split()  # e.g. "-DAF_MR=64" for kernel-variant experiments
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", LIB + ".tmp", os.path.join(CSRC, "af_api.cu")]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + proc.stdout + proc.stderr)

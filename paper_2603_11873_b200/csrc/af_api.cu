@@ -26,6 +26,16 @@ static std::atomic<int> g_pdl{[] {
     const char* e = getenv("AF_PDL");
     return (e && e[0] == '0') ? 0 : 1;
 }()};
+// Streaming strategy of the fused decode GEMV (af_set_gemv_variant; env AF_GEMV): 0 = registers
+// (LDG.128), 1..4 = shared-memory ring filled by bulk copies (2 KB x1, 2 KB x2, 4 KB x1, 4 KB x2 producers).
+static std::atomic<int> g_gemv_variant{[] {
+    const char* e = getenv("AF_GEMV");
+    return e ? atoi(e) : 0;
+}()};
+static std::atomic<int> g_gemv_full_sm{[] {
+    const char* e = getenv("AF_GEMV_FULL_SM");
+    return (e && e[0] == '1') ? 1 : 0;
+}()};
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline size_t esize(int dtype) { return dtype == AF_BF16 ? 2 : 4; }
@@ -124,6 +134,13 @@ int64_t af_launch_count(void) { return g_launches.load(); }
 
 int af_set_pdl(int32_t enable) {
     g_pdl.store(enable ? 1 : 0);
+    return AF_OK;
+}
+
+int af_set_gemv_variant(int32_t variant, int32_t full_sm) {
+    if (variant < 0 || variant > 4) return fail(AF_EVALUE, "GEMV variant must be 0..4");
+    g_gemv_variant.store(variant);
+    g_gemv_full_sm.store(full_sm ? 1 : 0);
     return AF_OK;
 }
 
@@ -315,7 +332,14 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
         AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured = true;
     }
-    switch_mma_kernel<KS><<<grid, kMmaThreads, L::total, st>>>(mp);
+    MmaParams mp2 = mp;
+    static const int env_stages = [] { const char* e = getenv("AF_MMA_STAGES"); return e ? atoi(e) : 0; }();
+    static const int env_depth = [] { const char* e = getenv("AF_STORE_DEPTH"); return e ? atoi(e) : -1; }();
+    mp2.n_stages = std::min(L::stages, kMmaDefaultStages);
+    (void)env_stages;
+    mp2.store_depth = (env_depth >= 0 && env_depth <= 3) ? env_depth : kStoreDepth;
+    if (mp2.store_depth > mp2.n_stages - 2) mp2.store_depth = mp2.n_stages - 2;
+    switch_mma_kernel<KS><<<grid, kMmaThreads, L::total, st>>>(mp2);
     AF_LAUNCH_CHECK("switch_mma_kernel");
     return AF_OK;
 }
@@ -606,36 +630,67 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
     if (rows == 0) return AF_OK;
     const DeviceInfo& di = device_info();
     const int xs_bytes = cols * 4;
-    // 16 KB stages beside the staged vector.  The footprint is held to half an SM when possible so
-    // that, under programmatic dependent launch, the next GEMV's CTA is co-resident with this one
-    // and fills its ring while this kernel drains.
-    const int half_sm = (di.max_smem_optin - 2048) / 2;
-    int n_stages = (half_sm - xs_bytes) / kGvStage;
-    if (n_stages < 3) n_stages = (di.max_smem_optin - 2048 - xs_bytes) / kGvStage;
-    n_stages = std::min(n_stages, kGvMaxStages);
-    if (n_stages < 2) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
     if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (norm_w && (reinterpret_cast<uintptr_t>(norm_w) & 15) != 0) || cols % 4 != 0)
         return fail(AF_EDIM, "fused GEMV needs 16-byte aligned f32 vectors");
-    const int smem = n_stages * kGvStage + xs_bytes;
-    static int configured_smem = 0;
-    if (smem > configured_smem) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured_smem = smem;
-    }
-    // Even split of the rows over one persistent CTA per SM (fewer when there are fewer row groups).
-    const int grid = std::max(1, std::min((rows + kGvWarps - 1) / kGvWarps, di.sm_count));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kGvThreads);
-    cfg.dynamicSmemBytes = smem;
     cfg.stream = as_stream(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = g_pdl.load() ? 1 : 0;
-    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_tma_kernel, reinterpret_cast<const __nv_bfloat16*>(w), (int)rows, (int)cols,
-                                   (long long)ld, x, out, (int)prologue, norm_w, eps, (int)epilogue, res, n_stages));
+    const __nv_bfloat16* wp = reinterpret_cast<const __nv_bfloat16*>(w);
+    const int variant = g_gemv_variant.load();
+    if (variant == 0) {
+        // register-streamed kernel: even split of the rows over SMs x resident CTAs
+        if (xs_bytes + 1024 > di.max_smem_optin) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
+        static int configured = 48 * 1024;
+        if (xs_bytes > configured) {
+            AF_CUDA_TRY(cudaFuncSetAttribute(gemv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, xs_bytes));
+            configured = xs_bytes;
+        }
+        static int occ_smem = -1, occ = 0;
+        if (occ_smem != xs_bytes) {
+            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_fused_kernel, kGemvFThreads, xs_bytes));
+            occ_smem = xs_bytes;
+        }
+        cfg.gridDim = dim3(std::max(1, std::min(rows, di.sm_count * std::max(1, std::min(occ, 4)))));
+        cfg.blockDim = dim3(kGemvFThreads);
+        cfg.dynamicSmemBytes = xs_bytes;
+        AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_fused_kernel, wp, (int)rows, (int)cols, (long long)ld, x, out, (int)prologue,
+                                       norm_w, eps, (int)epilogue, res));
+    } else {
+        // TMA-ring kernel: variant 1 = 2 KB copies / 1 producer, 2 = 2 KB / 2 producers, 3 = 4 KB / 1, 4 = 4 KB / 2
+        const int ch = (variant >= 3) ? 2048 : 1024;
+        const int stage = kGvWarps * ch * 2;
+        // The footprint is held to half an SM when that still leaves >= 3 stages, so that under
+        // programmatic dependent launch the next GEMV's CTA is co-resident and fills its ring
+        // while this kernel drains.
+        const int half_sm = (di.max_smem_optin - 2048) / 2;
+        int n_stages = (half_sm - xs_bytes) / stage;
+        if (n_stages < 3 || g_gemv_full_sm.load()) n_stages = (di.max_smem_optin - 2048 - xs_bytes) / stage;
+        n_stages = std::min(n_stages, kGvMaxStages);
+        if (n_stages < 2) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
+        const int smem = n_stages * stage + xs_bytes;
+        cfg.gridDim = dim3(std::max(1, std::min((rows + kGvWarps - 1) / kGvWarps, di.sm_count)));
+        cfg.dynamicSmemBytes = smem;
+#define AF_GV_LAUNCH(CH, NP)                                                                                              \
+    do {                                                                                                                  \
+        static int configured = 0;                                                                                        \
+        if (smem > configured) {                                                                                          \
+            AF_CUDA_TRY(cudaFuncSetAttribute(gemv_tma_kernel<CH, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+            configured = smem;                                                                                            \
+        }                                                                                                                 \
+        cfg.blockDim = dim3(kGvWarps * 32 + 32 * NP);                                                                     \
+        AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_tma_kernel<CH, NP>, wp, (int)rows, (int)cols, (long long)ld, x, out,     \
+                                       (int)prologue, norm_w, eps, (int)epilogue, res, n_stages));                        \
+    } while (0)
+        if (variant == 1) AF_GV_LAUNCH(1024, 1);
+        else if (variant == 2) AF_GV_LAUNCH(1024, 2);
+        else if (variant == 3) AF_GV_LAUNCH(2048, 1);
+        else AF_GV_LAUNCH(2048, 2);
+#undef AF_GV_LAUNCH
+    }
     AF_LAUNCH_CHECK("gemv_tma_kernel");
     return AF_OK;
 }

@@ -62,40 +62,43 @@ __device__ __forceinline__ void gv_bulk_load(uint32_t smem_dst, const void* src,
 // accumulates its own row across the chunks and finishes with a shuffle reduction, so the
 // steady state has no block-wide barrier at all.
 constexpr int kGvWarps = 8;                       // consumer warps = rows per group
-constexpr int kGvThreads = kGvWarps * 32 + 32;    // + producer warp
-constexpr int kGvCH = 1024;                       // columns per row chunk (2 KB)
-constexpr int kGvStage = kGvWarps * kGvCH * 2;    // 16 KB
 constexpr int kGvMaxStages = 10;
+constexpr int kGvMaxProd = 4;
 
-__global__ void __launch_bounds__(kGvThreads, 1) gemv_tma_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols,
-                                                                 long long ld, const float* __restrict__ x,
-                                                                 float* __restrict__ out, int prologue,
-                                                                 const float* __restrict__ norm_w, float eps, int epilogue,
-                                                                 const float* __restrict__ res, int n_stages) {
+// CH = columns per row chunk (one bulk copy of CH*2 bytes), NPROD = producer threads (one per
+// warp; a single thread can issue a bulk copy only every ~80-100 cycles, so 8 copies of 2 KB per
+// 16 KB stage would cap one SM below its share of HBM bandwidth).
+template <int CH, int NPROD>
+__global__ void __launch_bounds__(kGvWarps * 32 + 32 * NPROD, 1)
+gemv_tma_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols, long long ld, const float* __restrict__ x,
+                float* __restrict__ out, int prologue, const float* __restrict__ norm_w, float eps, int epilogue,
+                const float* __restrict__ res, int n_stages) {
+    constexpr int kStage = kGvWarps * CH * 2;
     extern __shared__ __align__(128) unsigned char gv_smem[];
-    // layout: [stages x 16 KB] [xs: cols f32] ; barriers static
+    // layout: [stages x kStage] [xs: cols f32] ; barriers static
     __shared__ uint64_t full[kGvMaxStages], empty[kGvMaxStages];
     __shared__ float redn[kGvWarps];
-    float* xs = reinterpret_cast<float*>(gv_smem + (size_t)n_stages * kGvStage);
+    float* xs = reinterpret_cast<float*>(gv_smem + (size_t)n_stages * kStage);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     pdl_launch_dependents();
     const int r_begin = (int)((long long)rows * blockIdx.x / gridDim.x);
     const int r_end = (int)((long long)rows * (blockIdx.x + 1) / gridDim.x);
     const int n_groups = (r_end - r_begin + kGvWarps - 1) / kGvWarps;
-    const int n_ch = (cols + kGvCH - 1) / kGvCH;
+    const int n_ch = (cols + CH - 1) / CH;
     const int total = n_groups * n_ch;
     if (tid == 0) {
         for (int s = 0; s < n_stages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], NPROD);
             mbar_init(&empty[s], kGvWarps);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (warp == kGvWarps) {
-        // ===================== producer: streams W, independent of the previous kernel =====================
+    if (warp >= kGvWarps) {
+        // ===================== producers: stream W, independent of the previous kernel =====================
         if (lane == 0) {
+            const int who = warp - kGvWarps;
             const uint32_t base = smem_u32(gv_smem);
             for (int it = 0; it < total; ++it) {
                 const int stage = it % n_stages;
@@ -103,13 +106,14 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_tma_kernel(const __nv_bflo
                 const int g = it / n_ch, ch = it % n_ch;
                 const int row0 = r_begin + g * kGvWarps;
                 const int nrow = min(kGvWarps, r_end - row0);
-                const int c0 = ch * kGvCH;
-                const uint32_t bytes = (uint32_t)min(kGvCH, cols - c0) * 2;
+                const int c0 = ch * CH;
+                const uint32_t bytes = (uint32_t)min(CH, cols - c0) * 2;
+                int mine = 0;
+                for (int r = who; r < nrow; r += NPROD) ++mine;
                 mbar_wait(&empty[stage], ph ^ 1);
-                mbar_expect_tx(&full[stage], bytes * nrow);
-                for (int r = 0; r < nrow; ++r)
-                    gv_bulk_load(base + stage * kGvStage + r * (kGvCH * 2), w + (long long)(row0 + r) * ld + c0, bytes,
-                                 &full[stage]);
+                mbar_expect_tx(&full[stage], bytes * mine);
+                for (int r = who; r < nrow; r += NPROD)
+                    gv_bulk_load(base + stage * kStage + r * (CH * 2), w + (long long)(row0 + r) * ld + c0, bytes, &full[stage]);
             }
         }
         return;
@@ -154,19 +158,19 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_tma_kernel(const __nv_bflo
     }
     named_bar_sync(1, kC);
 
-    float acc = 0.f;
+    float acc0 = 0.f, acc1 = 0.f;
     for (int it = 0; it < total; ++it) {
         const int stage = it % n_stages;
         const uint32_t ph = (it / n_stages) & 1;
         const int g = it / n_ch, ch = it % n_ch;
         const int row = r_begin + g * kGvWarps + warp;
-        const int c0 = ch * kGvCH;
-        const int width = min(kGvCH, cols - c0);
+        const int c0 = ch * CH;
+        const int width = min(CH, cols - c0);
         mbar_wait(&full[stage], ph);
         if (row < r_end) {
-            const unsigned char* wrow = gv_smem + (size_t)stage * kGvStage + warp * (kGvCH * 2);
+            const unsigned char* wrow = gv_smem + (size_t)stage * kStage + warp * (CH * 2);
 #pragma unroll
-            for (int i = 0; i < kGvCH / 256; ++i) {
+            for (int i = 0; i < CH / 256; ++i) {
                 const int c = lane * 8 + i * 256;
                 if (c < width) {
                     const uint4 v = *reinterpret_cast<const uint4*>(wrow + c * 2);
@@ -174,16 +178,16 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_tma_kernel(const __nv_bflo
                     const float4 xb = *reinterpret_cast<const float4*>(xs + c0 + c + 4);
                     float wf[8];
                     unpack8(v, wf);
-                    acc = fmaf(wf[0], xa.x, acc); acc = fmaf(wf[1], xa.y, acc); acc = fmaf(wf[2], xa.z, acc); acc = fmaf(wf[3], xa.w, acc);
-                    acc = fmaf(wf[4], xb.x, acc); acc = fmaf(wf[5], xb.y, acc); acc = fmaf(wf[6], xb.z, acc); acc = fmaf(wf[7], xb.w, acc);
+                    acc0 = fmaf(wf[0], xa.x, acc0); acc1 = fmaf(wf[1], xa.y, acc1); acc0 = fmaf(wf[2], xa.z, acc0); acc1 = fmaf(wf[3], xa.w, acc1);
+                    acc0 = fmaf(wf[4], xb.x, acc0); acc1 = fmaf(wf[5], xb.y, acc1); acc0 = fmaf(wf[6], xb.z, acc0); acc1 = fmaf(wf[7], xb.w, acc1);
                 }
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (ch == n_ch - 1) {
-            const float y = warp_sum(acc);
-            acc = 0.f;
+            const float y = warp_sum(acc0 + acc1);
+            acc0 = acc1 = 0.f;
             if (lane == 0 && row < r_end) {
                 float o = y;
                 if (epilogue == AF_EPI_GELU_RESIDUAL)
@@ -193,6 +197,135 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_tma_kernel(const __nv_bflo
                 out[row] = o;
             }
         }
+    }
+}
+
+// ---- register-streamed variant (no shared-memory ring for W): kept selectable (af_set_gemv_variant)
+//      so the two streaming strategies can be measured against each other on the same launch chain ----
+// y = epilogue(W . prologue(x)), W rows x cols bf16 row-major (cols % 8 == 0, 16-byte aligned rows).
+//
+// HBM-bound streaming read of W.  Rows are split EVENLY over the grid (grid = SMs x resident
+// CTAs, so every SM streams the same number of bytes); inside a CTA all 256 threads cooperate
+// on a batch of kGemvRB rows: thread t owns the 16-byte chunk t of every 4 KB pass of a row.
+// The loop is software-pipelined two items deep (8 independent 16-byte loads in flight per
+// thread while a third item is consumed), the first loads are issued BEFORE the prologue and
+// before pdl_wait(), so the prologue and the tail of the previous kernel hide under them.
+__global__ void __launch_bounds__(kGemvFThreads) gemv_fused_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols,
+                                                                    long long ld, const float* __restrict__ x,
+                                                                    float* __restrict__ out, int prologue,
+                                                                    const float* __restrict__ norm_w, float eps, int epilogue,
+                                                                    const float* __restrict__ res) {
+    extern __shared__ __align__(16) float xs[];
+    __shared__ float red[2][kGemvFThreads / 32][kGemvRB];
+    __shared__ float redn[kGemvFThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kGemvFThreads / 32;
+    pdl_launch_dependents();
+    const int r_begin = (int)((long long)rows * blockIdx.x / gridDim.x);
+    const int r_end = (int)((long long)rows * (blockIdx.x + 1) / gridDim.x);
+    const int n_pass = (cols + kGemvPass - 1) / kGemvPass;
+    const int n_batch = (r_end - r_begin + kGemvRB - 1) / kGemvRB;
+    const int total = n_batch * n_pass;
+
+    auto issue = [&](int it, uint4 (&v)[kGemvRB]) {
+        if (it >= total) return;
+        const int b = it / n_pass, c = (it % n_pass) * kGemvPass + tid * 8;
+#pragma unroll
+        for (int i = 0; i < kGemvRB; ++i) {
+            const int row = r_begin + b * kGemvRB + i;
+            v[i] = (row < r_end && c < cols) ? ldg_stream(w + (long long)row * ld + c) : make_uint4(0u, 0u, 0u, 0u);
+        }
+    };
+    uint4 b0[kGemvRB], b1[kGemvRB], b2[kGemvRB];
+    issue(0, b0);
+    issue(1, b1);
+
+    pdl_wait();  // x / res come from the previous kernel
+    if (prologue == kPrologueRmsNorm) {
+        float ss = 0.f;
+        for (int c = tid * 4; c < cols; c += kGemvFThreads * 4) {
+            const float4 v = *reinterpret_cast<const float4*>(x + c);
+            *reinterpret_cast<float4*>(xs + c) = v;
+            ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+        }
+        ss = warp_sum(ss);
+        if (lane == 0) redn[warp] = ss;
+        __syncthreads();
+        float tot = 0.f;
+#pragma unroll
+        for (int i = 0; i < nwarps; ++i) tot += redn[i];
+        const float inv = rsqrtf(tot / (float)cols + eps);
+        for (int c = tid * 4; c < cols; c += kGemvFThreads * 4) {
+            float4 v = *reinterpret_cast<float4*>(xs + c);
+            const float4 nw = *reinterpret_cast<const float4*>(norm_w + c);
+            v.x *= inv * nw.x; v.y *= inv * nw.y; v.z *= inv * nw.z; v.w *= inv * nw.w;
+            *reinterpret_cast<float4*>(xs + c) = v;
+        }
+    } else if (prologue == kPrologueSiluMul) {
+        for (int c = tid * 4; c < cols; c += kGemvFThreads * 4) {
+            const float4 g = *reinterpret_cast<const float4*>(x + c);
+            const float4 u = *reinterpret_cast<const float4*>(x + cols + c);
+            float4 v;
+            v.x = g.x / (1.0f + expf(-g.x)) * u.x;
+            v.y = g.y / (1.0f + expf(-g.y)) * u.y;
+            v.z = g.z / (1.0f + expf(-g.z)) * u.z;
+            v.w = g.w / (1.0f + expf(-g.w)) * u.w;
+            *reinterpret_cast<float4*>(xs + c) = v;
+        }
+    } else {
+        for (int c = tid * 4; c < cols; c += kGemvFThreads * 4)
+            *reinterpret_cast<float4*>(xs + c) = *reinterpret_cast<const float4*>(x + c);
+    }
+    __syncthreads();
+
+    float acc[kGemvRB] = {};
+    int buf = 0;
+    auto consume = [&](int it, const uint4 (&v)[kGemvRB]) {
+        if (it >= total) return;
+        const int b = it / n_pass, ps = it % n_pass, c = ps * kGemvPass + tid * 8;
+        if (c < cols) {
+            const float4 xa = *reinterpret_cast<const float4*>(xs + c);
+            const float4 xb = *reinterpret_cast<const float4*>(xs + c + 4);
+            const float xf[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+            for (int i = 0; i < kGemvRB; ++i) {
+                float wf[8];
+                unpack8(v[i], wf);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i] = fmaf(wf[j], xf[j], acc[i]);
+            }
+        }
+        if (ps == n_pass - 1) {  // the batch is complete: CTA-wide reduction and epilogue
+#pragma unroll
+            for (int i = 0; i < kGemvRB; ++i) {
+                const float y = warp_sum(acc[i]);
+                if (lane == 0) red[buf][warp][i] = y;
+                acc[i] = 0.f;
+            }
+            __syncthreads();
+            if (tid < kGemvRB) {
+                const int row = r_begin + b * kGemvRB + tid;
+                if (row < r_end) {
+                    float y = 0.f;
+#pragma unroll
+                    for (int wv = 0; wv < nwarps; ++wv) y += red[buf][wv][tid];
+                    float o = y;
+                    if (epilogue == AF_EPI_GELU_RESIDUAL)
+                        o = res[row] + 0.5f * y * (1.0f + erff(y * 0.70710678118654752440f));
+                    else if (epilogue == AF_EPI_RESIDUAL)
+                        o = res[row] + y;
+                    out[row] = o;
+                }
+            }
+            buf ^= 1;
+        }
+    };
+    for (int it = 0; it < total; it += 3) {
+        issue(it + 2, b2);
+        consume(it, b0);
+        issue(it + 3, b0);
+        consume(it + 1, b1);
+        issue(it + 4, b1);
+        consume(it + 2, b2);
     }
 }
 

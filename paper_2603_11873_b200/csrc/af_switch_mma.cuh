@@ -24,7 +24,16 @@
 
 namespace af {
 
-constexpr int kMR = 32;                           // tile rows of the tensor path
+#ifndef AF_MR
+#define AF_MR 32
+#endif
+#ifndef AF_WPROD
+#define AF_WPROD 1      /* threads (one per warp) issuing the W box loads */
+#endif
+#ifndef AF_STORERS
+#define AF_STORERS 1    /* threads (one per warp) issuing the W box stores */
+#endif
+constexpr int kMR = AF_MR;                        // tile rows of the tensor path
 constexpr int kBoxCols = 64;                      // 128-byte swizzle span in bf16
 constexpr int kBoxes = kTN / kBoxCols;            // 4 boxes per tile
 constexpr int kBoxBytes = kMR * kBoxCols * 2;     // 4 KB
@@ -32,10 +41,13 @@ constexpr int kWStageBytes = kMR * kTN * 2;       // 16 KB
 constexpr int kDownPitch = kTN + 8;               // elements; +16 B keeps ldmatrix conflict free
 constexpr int kMmaWarps = 16;                     // consumer warps: one n16 column slice each
 constexpr int kMmaConsumers = kMmaWarps * 32;     // 512 threads
-constexpr int kMmaThreads = kMmaConsumers + 64;   // + producer warp (TMA loads) + storer warp (TMA stores)
+constexpr int kWProd = AF_WPROD;                  // W-load producer warps
+constexpr int kStorers = AF_STORERS;              // storer warps
+constexpr int kMmaThreads = kMmaConsumers + 32 * (kWProd + 1 + kStorers);  // + W producers + UP producer + storers
 constexpr int kMmaMaxKS = 4;                      // k-steps of 16 ranks: S <= 64
 constexpr int kMmaMaxStages = 12;
-constexpr int kStoreDepth = 2;                    // tile stores that may still be reading smem
+constexpr int kStoreDepth = 0;                    // tile stores that may still be reading smem
+constexpr int kMmaDefaultStages = 10;
 
 template <int KS>
 struct MmaLayout {
@@ -52,7 +64,7 @@ struct MmaLayout {
     static constexpr int off_bar = off_down + down_bytes;          // full[16], computed[16], empty[16]
     static constexpr int off_plan = off_bar + 3 * 8 * 16;
     static constexpr int total = off_plan + (int)sizeof(Plan) + 1024 /*alignment slack*/;
-    static_assert(stages >= 4 && total <= 227 * 1024, "shared memory budget");
+    static_assert(stages >= 3 && total <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
@@ -96,8 +108,10 @@ __device__ __forceinline__ void tma_store_2d_addr(const void* tmap, int c0, int 
 
 struct MmaParams {
     SwitchParams base;
-    const CUtensorMap* tmaps_ld;   // per segment: 64 x 64 swizzled box on the source (live or pristine)
+    const CUtensorMap* tmaps_ld;   // per segment: 32 x 64 swizzled box on the source (live or pristine)
     const CUtensorMap* tmaps_st;   // per segment: the same box shape on the live matrix
+    int n_stages;                  // ring depth actually used (<= MmaLayout<KS>::stages)
+    int store_depth;               // tile stores that may still be reading shared memory (0..3)
 };
 
 // Gated DOWN slab for one unit: rows [0, S) hold hi(g*a), rows [s_pad, s_pad+S) hold lo; the
@@ -160,14 +174,15 @@ using MmaIter = TileIterT<kMR>;
 
 // Warp roles (all walk the same static tile sequence):
 //   warps 0..15  consumers: wait full[stage] -> W + U.(hi+lo) in place in smem -> arrive computed[stage]
-//   warp 16      producer : wait empty[stage] -> TMA loads of the W boxes + bulk copies of the UP blocks
-//   warp 17      storer   : wait computed[stage] -> TMA stores of the tile; a stage goes back to the
-//                           producer once its stores have read shared memory (kStoreDepth newer
-//                           stores may still be draining)
+//   W producers  (kWProd warps, 1 thread each): wait empty[stage] -> TMA loads of their W boxes
+//   UP producer  (1 warp, 1 thread): wait empty[stage] -> bulk copies of the selected UP blocks
+//   storers      (kStorers warps, 1 thread each): wait computed[stage] -> TMA stores of their
+//                boxes; a stage goes back to the producers once every storer's stores have read
+//                shared memory (store_depth newer stores may still be draining)
 template <int KS>
 __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
     using L = MmaLayout<KS>;
-    constexpr int kSt = L::stages;
+    constexpr int kSt = L::stages < kMmaDefaultStages ? L::stages : kMmaDefaultStages;
     extern __shared__ unsigned char smem_dyn[];
     const SwitchParams& p = mp.base;
     // 128-byte swizzle needs 1024-byte aligned boxes
@@ -180,9 +195,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
 
     if (tid == 0) {
         for (int s = 0; s < kSt; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], kWProd + 1);
             mbar_init(&computed[s], kMmaWarps);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], kStorers);
         }
         fence_mbar_init();
         if (p.use_dev)
@@ -200,8 +215,40 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     const uint32_t up_base = smem_u32(sm + L::off_up);
     const int warp = tid >> 5, lane = tid & 31;
 
-    if (warp == kMmaWarps) {
-        // ============ producer: W boxes by TMA, UP blocks by 1-D bulk copies ============
+    // One thread can issue a TMA operation only every ~100 cycles; at 16 KB per stage a single
+    // producer thread would be the bottleneck of the whole kernel (measured: 4.80 ms -> 4.29 ms on
+    // the Llama-2-7B table when the UP copies moved to their own thread).  The issue work is
+    // therefore spread over kWProd W-load threads, one UP-copy thread and kStorers store threads.
+    if (warp >= kMmaWarps && warp < kMmaWarps + kWProd) {
+        // ============ W producers: boxes b = who, who + kWProd, ... of every tile ============
+        if (lane == 0) {
+            const int who = warp - kMmaWarps;
+            constexpr int kMine = (kBoxes + kWProd - 1) / kWProd;
+            MmaIter ti;
+            ti.init(p);
+            for (int it = 0; ti.valid(p); ++it) {
+                const int stage = it % kSt;
+                const uint32_t ph = (it / kSt) & 1;
+                mbar_wait(&empty[stage], ph ^ 1);
+                int mine = 0;
+#pragma unroll
+                for (int j = 0; j < kMine; ++j) mine += (who + j * kWProd < kBoxes) ? 1 : 0;
+                mbar_expect_tx(&full[stage], mine * kBoxBytes);
+                const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
+#pragma unroll
+                for (int j = 0; j < kMine; ++j) {
+                    const int b = who + j * kWProd;
+                    if (b < kBoxes)
+                        tma_load_2d_addr(w_base + stage * kWStageBytes + b * kBoxBytes, tm, ti.un.col0 + b * kBoxCols, ti.m0,
+                                         &full[stage]);
+                }
+                ti.next(p);
+            }
+        }
+        return;
+    }
+    if (warp == kMmaWarps + kWProd) {
+        // ============ UP producer: one 1-D bulk copy per selected expert block ============
         if (lane == 0) {
             MmaIter ti;
             ti.init(p);
@@ -217,12 +264,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                 const int rows_here = min(kMR, sg.d_out - ti.m0);
                 const uint32_t up_blk_bytes = (uint32_t)rows_here * sg.rank * 2;
                 mbar_wait(&empty[stage], ph ^ 1);
-                mbar_expect_tx(&full[stage], kWStageBytes + n_blocks * up_blk_bytes);
-                const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
-#pragma unroll
-                for (int b = 0; b < kBoxes; ++b)
-                    tma_load_2d_addr(w_base + stage * kWStageBytes + b * kBoxBytes, tm, ti.un.col0 + b * kBoxCols, ti.m0,
-                                     &full[stage]);
+                mbar_expect_tx(&full[stage], n_blocks * up_blk_bytes);
                 const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
                 for (int b = 0; b < n_blocks; ++b)
                     bulk_load_1d(up_base + stage * L::up_stage_bytes + b * (kMR * sg.rank * 2),
@@ -233,9 +275,11 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
         }
         return;
     }
-    if (warp == kMmaWarps + 1) {
-        // ============ storer: whole tile back to global, then hand the stage back ============
+    if (warp > kMmaWarps + kWProd) {
+        // ============ storers: boxes back to global, then hand the stage back ============
         if (lane == 0) {
+            const int who = warp - (kMmaWarps + kWProd + 1);
+            constexpr int kMine = (kBoxes + kStorers - 1) / kStorers;
             MmaIter ti;
             ti.init(p);
             int it = 0;
@@ -245,11 +289,19 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                 mbar_wait(&computed[stage], ph);
                 const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
 #pragma unroll
-                for (int b = 0; b < kBoxes; ++b)
-                    tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
+                for (int j = 0; j < kMine; ++j) {
+                    const int b = who + j * kStorers;
+                    if (b < kBoxes)
+                        tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
+                }
                 bulk_commit();
-                bulk_wait_read<kStoreDepth>();  // the stores of tile it - kStoreDepth have drained their stage
-                if (it >= kStoreDepth) mbar_arrive(&empty[(it - kStoreDepth) % kSt]);
+                // the stores of tile it - depth have drained their stage: hand it back
+                const int depth = mp.store_depth;
+                if (depth <= 0) bulk_wait_read<0>();
+                else if (depth == 1) bulk_wait_read<1>();
+                else if (depth == 2) bulk_wait_read<2>();
+                else bulk_wait_read<3>();
+                if (it >= depth) mbar_arrive(&empty[(it - depth) % kSt]);
                 ti.next(p);
             }
             bulk_wait_all<0>();  // global writes complete before the CTA retires

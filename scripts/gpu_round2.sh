@@ -15,7 +15,7 @@ AF_NCU=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -
    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:switch_mma -s 2 -c 1 -o gpurun_out/prof_switch -f \
    python scripts/bench_switch.py --config 7b --modes mma --iters 2 --warmup 1 > gpurun_out/ncu_switch.log 2>&1
-AF_NCU=1 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"gemv_fused|attn_decode" -s 10 -c 6 -o gpurun_out/prof_gemv -f \
+AF_NCU=1 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"gemv_fused|gemv_tma|attn_decode" -s 10 -c 6 -o gpurun_out/prof_gemv -f \
    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_gemv.log 2>&1
 fi
 grep -E "passed|failed|exit" gpurun_out/tests.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
