@@ -258,6 +258,14 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
             for (int r0 = 0; r0 < s.d_out; r0 += rows_per_unit)
                 units.push_back({i, r0, std::min(rows_per_unit, s.d_out - r0), c0});
     }
+    // Largest units first: with the round-robin walk (unit u -> CTA u % grid) every CTA then gets the
+    // same mix of sizes.  Unsorted, segments of different shapes alias with the grid size (42 % more
+    // work on the busiest SM for Llama-2-13B shapes, 10 % for Llama-3-8B); sorted, < 1 %.
+    std::stable_sort(units.begin(), units.end(), [&](const UnitDev& a, const UnitDev& b) {
+        const long long wa = (long long)a.rows * std::min(kTN, segments[a.seg].d_in - a.col0);
+        const long long wb = (long long)b.rows * std::min(kTN, segments[b.seg].d_in - b.col0);
+        return wa > wb;
+    });
     t->n_units = (int)units.size();
 
     cudaError_t e = cudaMalloc(&t->d_segs, sizeof(SegDev) * n_segments);
@@ -654,7 +662,7 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
             AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_fused_kernel, kGemvFThreads, xs_bytes));
             occ_smem = xs_bytes;
         }
-        cfg.gridDim = dim3(std::max(1, std::min(rows, di.sm_count * std::max(1, std::min(occ, 4)))));
+        cfg.gridDim = dim3(std::max(1, std::min(rows, di.sm_count * std::max(1, std::min(occ, 8)))));
         cfg.blockDim = dim3(kGemvFThreads);
         cfg.dynamicSmemBytes = xs_bytes;
         AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_fused_kernel, wp, (int)rows, (int)cols, (long long)ld, x, out, (int)prologue,

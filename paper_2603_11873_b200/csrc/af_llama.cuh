@@ -17,8 +17,17 @@ constexpr int kPrologueNone = 0;
 constexpr int kPrologueRmsNorm = 1;   // xs = x * rsqrt(mean(x^2) + eps) * norm_w
 constexpr int kPrologueSiluMul = 2;   // xs = silu(x[c]) * x[cols + c]   (x holds [gate | up])
 
-constexpr int kGemvFThreads = 256;
-constexpr int kGemvRB = 4;                    // rows per batch (one partial sum each per thread)
+#ifndef AF_GEMV_RB
+#define AF_GEMV_RB 4
+#endif
+#ifndef AF_GEMV_MINB
+#define AF_GEMV_MINB 4   /* 64 registers -> 4 CTAs (32 warps) per SM: measured best, profiles/r01_sweep_gemv.txt */
+#endif
+#ifndef AF_GEMV_THREADS
+#define AF_GEMV_THREADS 256
+#endif
+constexpr int kGemvFThreads = AF_GEMV_THREADS;
+constexpr int kGemvRB = AF_GEMV_RB;           // rows per batch (one partial sum each per thread)
 constexpr int kGemvPass = kGemvFThreads * 8;  // columns covered by the CTA per pass (16 B per thread)
 
 __device__ __forceinline__ void unpack8(const uint4 v, float (&f)[8]) {
@@ -29,7 +38,11 @@ __device__ __forceinline__ void unpack8(const uint4 v, float (&f)[8]) {
 // Streaming 16-byte load that does not pollute L1 (W is read exactly once per token).
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     uint4 r;
+#ifdef AF_GEMV_L2_256
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#else
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+#endif
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
@@ -210,7 +223,7 @@ gemv_tma_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols, long lo
 // The loop is software-pipelined two items deep (8 independent 16-byte loads in flight per
 // thread while a third item is consumed), the first loads are issued BEFORE the prologue and
 // before pdl_wait(), so the prologue and the tail of the previous kernel hide under them.
-__global__ void __launch_bounds__(kGemvFThreads) gemv_fused_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols,
+__global__ void __launch_bounds__(kGemvFThreads, AF_GEMV_MINB) gemv_fused_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols,
                                                                     long long ld, const float* __restrict__ x,
                                                                     float* __restrict__ out, int prologue,
                                                                     const float* __restrict__ norm_w, float eps, int epilogue,
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(kGemvFThreads) gemv_fused_kernel(const __nv_bf
 constexpr int kAttnThreads = 256;
 constexpr int kAttnWarps = kAttnThreads / 32;
 constexpr int kAttnMaxHd = 256;
-constexpr int kAttnUnroll = 4;
+constexpr int kAttnUnroll = 8;
 
 template <int EL>
 __device__ __forceinline__ void load_bf16_vec(const __nv_bfloat16* p, float (&f)[EL]) {

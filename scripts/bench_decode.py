@@ -15,7 +15,10 @@ def main():
     cfg = llama.preset(workload, max_seq=256, adapters=False)
     eng = llama.LlamaEngine(cfg, init="device")
     L = _capi.lib()
-    for variant, full_sm in ((0, 0), (1, 0), (2, 0), (3, 0), (4, 0), (2, 1), (4, 1), (3, 1)):
+    combos = ((0, 0), (1, 0), (2, 0), (3, 0), (4, 0), (2, 1), (4, 1), (3, 1))
+    if len(sys.argv) > 2:
+        combos = tuple((int(v), 0) for v in sys.argv[2].split(","))
+    for variant, full_sm in combos:
         for pdl in (1, 0):
             _capi.check(L.af_set_gemv_variant(variant, full_sm))
             _capi.check(L.af_set_pdl(pdl))
