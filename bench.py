@@ -301,6 +301,25 @@ def main():
         dec_ms = timed(decode_only, dec_n)
     decode_only_tok_s = dec_n / (dec_ms / 1e3)
 
+    # ---------------- (4) context: this box's own copy bandwidth, measured the way MEASURED_PEAKS.json was
+    # (torch b.copy_(a) over 1 Gi bf16 elements, best of 10).  B200s of the pool differ by several per cent.
+    box_copy = None
+    try:
+        a = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
+        b = torch.empty_like(a)
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        box_copy = 2 * a.numel() * 2 / best / 1e6
+        del a, b
+    except RuntimeError:
+        box_copy = None
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -325,6 +344,7 @@ def main():
         "switch_hbm_gbs": achieved,
         "decode_only_tok_s": decode_only_tok_s,
         "decode_only_hbm_gbs": cfg.decode_bytes() * decode_only_tok_s / 1e9,
+        "box_hbm_copy_gbs": box_copy,
         "roofline": {"bound": "hbm", "kernel": "switch_mma_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                      "bytes_per_launch": sw_bytes, "avg_launch_ms": switch_ms, "min_launch_ms": min(sw_ms), "traffic": None},

@@ -37,6 +37,7 @@ static std::atomic<int> g_gemv_full_sm{[] {
     return (e && e[0] == '1') ? 1 : 0;
 }()};
 
+static const bool g_force_hilo = [] { const char* e = getenv("AF_FORCE_HILO"); return e && e[0] == '1'; }();
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline size_t esize(int dtype) { return dtype == AF_BF16 ? 2 : 4; }
 
@@ -107,9 +108,10 @@ struct af_table {
     SegDev* d_segs = nullptr;
     UnitDev* d_units = nullptr;
     int n_units = 0;
-    CUtensorMap* d_maps = nullptr;  // [4][n_segments]: fma live, fma pristine, mma live, mma pristine
+    CUtensorMap* d_maps = nullptr;  // [5][n_segments]: fma live, fma pristine, mma live, mma pristine, UP bank (swizzled)
     int* d_err = nullptr;
     bool fast_fma = false, fast_mma = false, has_pristine = false;
+    bool rank16 = true;  // every segment's rank is a multiple of 16
     int max_rank = 0, min_experts = 0;
     long long target_elems = 0;
     int sm_count = 0;
@@ -240,6 +242,9 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
                             (reinterpret_cast<uintptr_t>(s.up) % 16 == 0) && (s.ld_down % 8 == 0) &&
                             (s.down_expert_stride % 8 == 0) && (reinterpret_cast<uintptr_t>(s.down) % 16 == 0);
         if (!fac_ok) mma_ok = false;
+        // ranks fetched through the swizzled UP map need the bank packed as one [N * d_out][rank] matrix
+        if (up_swizzled(s.rank) && s.up_expert_stride != (long long)s.d_out * s.rank) mma_ok = false;
+        if (s.rank % 16 != 0) t->rank16 = false;
     }
     t->fast_fma = fma_ok;
     t->fast_mma = mma_ok;
@@ -280,7 +285,8 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         return fail(AF_ECUDA, std::string("table upload: ") + cudaGetErrorString(e));
     }
     if (t->fast_fma) {
-        std::vector<CUtensorMap> maps((size_t)4 * n_segments);
+        std::vector<CUtensorMap> maps((size_t)5 * n_segments);
+        std::memset(maps.data(), 0, sizeof(CUtensorMap) * maps.size());
         for (int i = 0; i < n_segments; ++i) {
             const af_segment_desc& s = segments[i];
             const void* pr = s.pristine ? s.pristine : s.target;
@@ -288,6 +294,12 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
             if (!rc) rc = make_map(&maps[1 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kTN, kTM, CU_TENSOR_MAP_SWIZZLE_NONE);
             if (!rc) rc = make_map(&maps[2 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kBoxCols, kMR, CU_TENSOR_MAP_SWIZZLE_128B);
             if (!rc) rc = make_map(&maps[3 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kBoxCols, kMR, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (!rc && t->fast_mma && up_swizzled(s.rank)) {
+                // UP bank of the segment as one [N * d_out][rank] matrix; swizzle span = row bytes
+                const CUtensorMapSwizzle sw = s.rank == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                              : s.rank == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+                rc = make_map(&maps[4 * n_segments + i], s.up, s.n_experts * s.d_out, s.rank, s.rank, s.rank, kMR, sw);
+            }
             if (rc) {
                 af_table_destroy(t);
                 return rc;
@@ -332,12 +344,12 @@ int af_table_status(af_table* t, void* stream) {
 
 namespace af {
 
-template <int KS>
+template <int KS, bool BA>
 static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
-    using L = MmaLayout<KS>;
+    using L = MmaLayout<KS, BA>;
     static bool configured = false;
     if (!configured) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS, BA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured = true;
     }
     MmaParams mp2 = mp;
@@ -346,8 +358,10 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     mp2.n_stages = std::min(L::stages, kMmaDefaultStages);
     (void)env_stages;
     mp2.store_depth = (env_depth >= 0 && env_depth <= 3) ? env_depth : kStoreDepth;
+    static const int env_upsw = [] { const char* e = getenv("AF_UP_SWIZZLE"); return (e && e[0] == '0') ? 0 : 1; }();
+    mp2.up_swizzle_ok = env_upsw;
     if (mp2.store_depth > mp2.n_stages - 2) mp2.store_depth = mp2.n_stages - 2;
-    switch_mma_kernel<KS><<<grid, kMmaThreads, L::total, st>>>(mp2);
+    switch_mma_kernel<KS, BA><<<grid, kMmaThreads, L::total, st>>>(mp2);
     AF_LAUNCH_CHECK("switch_mma_kernel");
     return AF_OK;
 }
@@ -444,13 +458,17 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
         mp.base = p;
         mp.tmaps_ld = t->d_maps + (size_t)(p.from_pristine ? 3 : 2) * S;
         mp.tmaps_st = t->d_maps + (size_t)2 * S;
+        mp.tmaps_up = t->d_maps + (size_t)4 * S;
         const int grid = std::min(t->n_units, t->sm_count);
         const int ks = std::max(1, (s_bound + 15) / 16);
+        // block-accumulate form when every block is a whole number of rank-16 steps and the hi/lo
+        // form would need more than two steps (it doubles the tensor work)
+        const bool ba = t->rank16 && ks > 2 && !g_force_hilo;
         switch (ks) {
-            case 1: return launch_mma<1>(mp, grid, st);
-            case 2: return launch_mma<2>(mp, grid, st);
-            case 3: return launch_mma<3>(mp, grid, st);
-            default: return launch_mma<4>(mp, grid, st);
+            case 1: return launch_mma<1, false>(mp, grid, st);
+            case 2: return launch_mma<2, false>(mp, grid, st);
+            case 3: return ba ? launch_mma<3, true>(mp, grid, st) : launch_mma<3, false>(mp, grid, st);
+            default: return ba ? launch_mma<4, true>(mp, grid, st) : launch_mma<4, false>(mp, grid, st);
         }
     }
     if (t->fast_fma) {
