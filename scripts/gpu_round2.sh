@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 rm -f gpurun_out/tests.log
 nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-for f in tests/test_gpu_router.py tests/test_gpu_switch.py tests/test_gpu_model.py tests/test_gpu_llama.py; do
+for f in tests/test_gpu_router.py tests/test_gpu_switch.py tests/test_gpu_model.py tests/test_gpu_llama.py tests/test_gpu_decode_kernels.py; do
   echo "=== $f" >> gpurun_out/tests.log
   timeout 900 python -m pytest $f -q -m gpu --timeout 600 --timeout-method=thread >> gpurun_out/tests.log 2>&1
   echo "exit $?" >> gpurun_out/tests.log
