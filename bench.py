@@ -3,18 +3,23 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload llama2-7b]
 
 A "step" is one decoded token of a bs=1 sequence through the whole hot path: pre-gate on the
-token's embedding row, ONE fused switch over all 7 x L adapted matrices (a teacher-forced token
-stream makes every step really switch), the merged-path forward (plain GEMVs
-over the live bf16 weights, GQA attention over the KV cache), lm_head and argmax.
+token's embedding row, the fused switch of all 7 x L adapted matrices (a teacher-forced token
+stream makes every step really switch), the merged-path forward (GQA attention
+over the KV cache), lm_head and argmax.  Two schedules of the same arithmetic:
+  --forward-mode chase    (default at N=1) each projection's GEMV is fused INTO the switch of its
+                          weights: one read + one write of W per token (af_switch_gemv);
+  --forward-mode separate ONE switch launch over all matrices, then plain GEMVs (a third pass over W).
 
   value        tokens/s with every per-step input already in HBM (forced token stream on the
                device, the step replayed as one CUDA graph), max over ranks.
   e2e          the same metric through the public API `LlamaEngine.decode_step(token)`: the
                consumed token comes from pinned host memory every step (4 B H2D) and the next
                token is read back (4 B D2H).
-  roofline     the fused-switch kernel: algorithmic bytes / its average launch
-               duration, CUDA events on the launching stream inside the e2e timed region,
-               against MEASURED_PEAKS.json hbm_gbs.
+  roofline     the fused-switch kernel (chase: its 4 x L launches per token, switch + GEMV):
+               algorithmic bytes / launch duration by CUDA events on the launching
+               stream -- separate: inside the e2e timed region; chase: in extra e2e steps right
+               after it (events between the launches would cut the programmatic overlap the timed
+               region runs with) -- against MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline the CPU oracle port (oracle/, reference algorithm restated in C) timed on this
                box's host cores on a bounded sample (whole layers), scaled to tokens/s.
 
@@ -163,6 +168,7 @@ def main():
     ap.add_argument("--workload", default="llama2-7b")
     ap.add_argument("--switch-mode", default="inplace", choices=["inplace", "from_pristine"])
     ap.add_argument("--compute", default="auto")
+    ap.add_argument("--forward-mode", default="auto", choices=["auto", "chase", "separate"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -194,8 +200,9 @@ def main():
         torch.cuda.synchronize()
 
     max_seq = 2 * (args.steps + args.warmup) + 16
+    max_seq += 16  # roofline pass of the chase schedule
     cfg = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
-                       compute=args.compute, keep_pristine=True)
+                       compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode)
     eng = llama.LlamaEngine(cfg, init="device")
     info = eng.table.info()
     forced = np.random.Generator(np.random.PCG64(cfg.seed + 1)).integers(0, cfg.vocab, 4096)
@@ -253,9 +260,35 @@ def main():
         torch.cuda.profiler.stop()
     launches_e2e = _capi.launch_count() - launches0
     eng._switch_for_step = orig_switch
-    sw_ms = [a.elapsed_time(b) for a, b in switch_events]
-    switch_ms = statistics.mean(sw_ms)
     e2e_value = args.steps / (e2e_ms / 1e3)
+    chase = eng.chase
+    fused_ms = None
+    if not chase:
+        sw_ms = [a.elapsed_time(b) for a, b in switch_events]
+        switch_ms = statistics.mean(sw_ms)
+    else:
+        # ---- (1b) roofline pass: the same e2e steps with events around every switch + GEMV launch ----
+        from paper_2603_11873_b200.adapters import SegmentGroup
+
+        fused_events = []
+        orig_sg = SegmentGroup.switch_gemv
+
+        def instrumented_sg(self, *a, **kw):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            orig_sg(self, *a, **kw)
+            e1.record()
+            fused_events.append((e0, e1))
+
+        SegmentGroup.switch_gemv = instrumented_sg
+        n_roof = 4
+        for _ in range(n_roof):
+            api_step()
+        torch.cuda.synchronize()
+        SegmentGroup.switch_gemv = orig_sg
+        per_launch = [a.elapsed_time(b) for a, b in fused_events]
+        n_per_step = len(per_launch) // n_roof
+        fused_ms = [sum(per_launch[i * n_per_step:(i + 1) * n_per_step]) for i in range(n_roof)]   # per token
 
     # ---------------- (2) value: inputs resident, the step replayed as one CUDA graph ----
     graph_ok = world == 1
@@ -301,6 +334,26 @@ def main():
         dec_ms = timed(decode_only, dec_n)
     decode_only_tok_s = dec_n / (dec_ms / 1e3)
 
+    # ---------------- (3b) chase: the standalone one-launch switch of the whole table (BASELINE metric
+    # "fused-switch us/token"), alternating between two decisions so every launch really switches ----
+    if chase:
+        from paper_2603_11873_b200.routing import DeviceDecision, GateDecision
+
+        k = cfg.top_k
+        da = DeviceDecision.from_host(GateDecision(tuple(range(k)), tuple([1.0 / k] * k)), eng.dev)
+        db = DeviceDecision.from_host(GateDecision(tuple(range(k, 2 * k)), tuple([1.0 / k] * k)), eng.dev)
+        eng.fused_switch(eng.prev, da)       # live weights now hold decision A
+        sw_ms = []
+        for i in range(8):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            eng.fused_switch(da if i % 2 == 0 else db, db if i % 2 == 0 else da)
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                sw_ms.append(e0.elapsed_time(e1))
+        switch_ms = statistics.mean(sw_ms)
+
     # ---------------- (4) context: this box's own copy bandwidth, measured the way MEASURED_PEAKS.json was
     # (torch b.copy_(a) over 1 Gi bf16 elements, best of 10).  B200s of the pool differ by several per cent.
     box_copy = None
@@ -327,6 +380,19 @@ def main():
 
     sw_bytes = cfg.switch_bytes(steady=True)
     achieved = sw_bytes / (switch_ms * 1e-3) / 1e9
+    if chase:
+        n_launch = 4 * cfg.layers
+        roof_ms = statistics.mean(fused_ms)
+        roof_achieved = sw_bytes / (roof_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "switch_mma_kernel<GEMV> (fused switch + GEMV, 4 launches per layer)",
+                    "achieved": roof_achieved, "peak": peak, "unit": "GB/s", "frac": roof_achieved / peak,
+                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)", "launches_per_token": n_launch,
+                    "bytes_per_launch": sw_bytes / n_launch, "avg_launch_ms": roof_ms / n_launch,
+                    "bytes_per_token": sw_bytes, "ms_per_token": roof_ms, "min_ms_per_token": min(fused_ms), "traffic": None}
+    else:
+        roofline = {"bound": "hbm", "kernel": "switch_mma_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                    "bytes_per_launch": sw_bytes, "avg_launch_ms": switch_ms, "min_launch_ms": min(sw_ms), "traffic": None}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -334,7 +400,9 @@ def main():
         "config": {"workload": f"{args.workload}: Llama-shaped bf16, {cfg.experts} experts rank {cfg.rank} top-{cfg.top_k} on q/k/v/o/gate/up/down, "
                                f"bs=1 decode, teacher-forced tokens, switch every token ({cfg.switch_mode})",
                    "parallelism": f"tp{world}", "l2": "inputs larger than L2 (weights 13 GB >> 126 MB), no flush needed",
-                   "segments": info["n_segments"], "work_units": info["n_units"], "compute": args.compute},
+                   "segments": info["n_segments"], "work_units": info["n_units"], "compute": args.compute,
+                   "forward_mode": "chase (GEMV fused into the switch: W read and written once per token)" if chase
+                   else "separate (one switch launch, then plain GEMVs)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4,
                 "ms_per_step": e2e_ms / args.steps},
         "gpu_launches": int(launches_per_step * args.steps),
@@ -345,16 +413,16 @@ def main():
         "decode_only_tok_s": decode_only_tok_s,
         "decode_only_hbm_gbs": cfg.decode_bytes() * decode_only_tok_s / 1e9,
         "box_hbm_copy_gbs": box_copy,
-        "roofline": {"bound": "hbm", "kernel": "switch_mma_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                     "bytes_per_launch": sw_bytes, "avg_launch_ms": switch_ms, "min_launch_ms": min(sw_ms), "traffic": None},
+        "roofline": roofline,
     }
-    traffic_path = os.path.join(ROOT, "profiles", "switch_traffic.json")
+    traffic_path = os.path.join(ROOT, "profiles", "chase_traffic.json" if chase else "switch_traffic.json")
     if os.path.exists(traffic_path):
         try:
             tr = json.load(open(traffic_path))
             if tr.get("workload") == args.workload:
                 out["roofline"]["traffic"] = tr.get("dram_bytes_per_launch")
+                if chase and tr.get("dram_bytes_per_token"):
+                    out["roofline"]["traffic_per_token"] = tr.get("dram_bytes_per_token")
         except (OSError, ValueError):
             pass
     if not args.no_cpu_baseline:

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define AF_ABI_VERSION 1
+#define AF_ABI_VERSION 2
 
 /* ---- status codes: one per reference exception class (errors.py:8-33) ---- */
 #define AF_OK 0
@@ -225,6 +225,46 @@ int af_step_advance(af_decision* prev_dev, const af_decision* cur_dev, int32_t* 
                     int32_t* step_dev, int32_t* token_dev, const int32_t* next_dev,
                     const int32_t* forced_dev, int32_t n_forced, int32_t* history_dev,
                     int32_t n_history, void* stream);
+
+/* ---- fused switch + GEMV ("chase" mode) -------------------------------
+ * The steady decode step moves every weight twice for the switch (read + write) and once more
+ * for the forward GEMV.  These entry points remove the third pass: a projection's segments are
+ * switched (adapters.py:236-258 -> linalg.py:306-346) and, while each freshly merged and rounded
+ * tile is still in registers, multiplied with the projection's input vector (model.py:288).
+ * One launch per projection of the Llama block (q|k|v, o, gate|up, down); a token costs
+ * 2 x W bytes instead of 3 x W.
+ *
+ * af_group_create : segments of `table` that share one input vector, in the order their outputs
+ *    are concatenated; builds an evenly split tile schedule for one launch.
+ * af_switch_gemv  : W <- W + delta(cur) - delta(prev) on the group's segments AND
+ *    acc_out[row] += fix(W_new[row] . x).  prev_dev / cur_dev / max_k / scale / mode as
+ *    af_fused_switch (both NULL: no switch, the launch is a plain GEMV over the live weights).
+ *    Input vector:  h = (res ? res : 0) + (acc_in ? fix^-1(acc_in) : xin);  x = prologue(h)
+ *    (AF_PRO_NONE / AF_PRO_RMSNORM with norm_w, eps / AF_PRO_SILU_MUL over [gate | up], no res).
+ *    h_out (optional) receives h -- the residual stream -- written by one CTA.
+ *    acc_out: y_rows 64-bit fixed-point accumulators (value * 2^AF_FIX_SHIFT), ZEROED BY THE CALLER
+ *    before the launch; the per-strip partial dot products are added with integer atomics, so the
+ *    result does not depend on CTA arrival order (deterministic).
+ *    pdl != 0: launched with programmatic stream serialization -- the launch streams its weights
+ *    while the previous kernel of the stream drains; the previous kernel must be one of this
+ *    library's decode kernels (they all execute griddepcontrol.wait).
+ * af_accum_to_f32 : out = (res ? res : 0) + fix^-1(acc)   (hand-over to af_gemv_fused / lm_head).
+ * af_attn_decode_fix : af_attn_decode reading q|k|v from fixed-point accumulators. */
+#define AF_FIX_SHIFT 40
+typedef struct af_group af_group;
+int af_group_create(af_table* table, const int32_t* seg_ids, int32_t n, af_group** out);
+int af_group_destroy(af_group* group);
+int af_group_info(const af_group* group, int32_t* x_len, int32_t* y_rows, int32_t* n_units, int32_t* grid,
+                  int64_t* tiles);
+int af_switch_gemv(af_group* group, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k,
+                   float scale, int32_t mode, const float* xin, const int64_t* acc_in, const float* res,
+                   float* h_out, int32_t prologue, const float* norm_w, float eps, int64_t* acc_out,
+                   int32_t pdl, void* stream);
+int af_accum_to_f32(const int64_t* acc, const float* res, float* out, int32_t n, void* stream);
+int af_attn_decode_fix(const int64_t* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,
+                       const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
+                       int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,
+                       int32_t* tickets, float* out, void* stream);
 
 #ifdef __cplusplus
 }

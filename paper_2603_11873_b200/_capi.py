@@ -14,7 +14,7 @@ from . import errors
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libadafuse_b200.so")
 
-AF_ABI_VERSION = 1
+AF_ABI_VERSION = 2
 AF_OK, AF_EVALUE, AF_EDIM, AF_EPRECISION, AF_EALIAS, AF_EINPUT, AF_ESTATE, AF_EINDEX, AF_ECUDA = range(9)
 AF_BF16, AF_F32 = 0, 1
 AF_SWITCH_INPLACE, AF_SWITCH_FROM_PRISTINE = 0, 1
@@ -101,7 +101,14 @@ SIGNATURES = {
     "af_attn_decode": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "af_argmax_val": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "af_step_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp]),
+    "af_group_create": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_vp)]),
+    "af_group_destroy": (ctypes.c_int, [_vp]),
+    "af_group_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
+    "af_switch_gemv": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _i32, _vp]),
+    "af_accum_to_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp]),
+    "af_attn_decode_fix": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
+AF_FIX_SHIFT = 40
 AF_PRO_NONE, AF_PRO_RMSNORM, AF_PRO_SILU_MUL = 0, 1, 2
 
 _lib = None

@@ -330,3 +330,64 @@ class SwitchTable:
             self._dev_scalar = torch.zeros(1, dtype=torch.float32, device="cuda")
         _capi.check(_capi.lib().af_max_deviation(self.device_table.handle, _ptr(self._dev_scalar), _capi.stream_ptr()))
         return float(self._dev_scalar.item())
+
+
+class SegmentGroup:
+    """Segments of a `SwitchTable` that share one input vector (q|k|v, gate|up, or one matrix):
+    the unit of the fused switch + GEMV launch (include/adafuse_b200.h `af_switch_gemv`).  The
+    switch of adapters.py:236-258 and the backbone GEMV of model.py:288 over the same weights
+    become one pass: every tile is merged, rounded, multiplied with x and written back."""
+
+    PROLOGUES = {"none": _capi.AF_PRO_NONE, "rmsnorm": _capi.AF_PRO_RMSNORM, "silu_mul": _capi.AF_PRO_SILU_MUL}
+
+    def __init__(self, table: SwitchTable, seg_ids):
+        import ctypes
+
+        ids = [int(i) for i in seg_ids]
+        arr = (ctypes.c_int32 * len(ids))(*ids)
+        handle = ctypes.c_void_p()
+        _capi.check(_capi.lib().af_group_create(table.device_table.handle, arr, len(ids), ctypes.byref(handle)))
+        self.handle = handle
+        self.table = table  # keeps the af_table (and the tensors it points at) alive
+        x_len, y_rows, n_units, grid, tiles = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+        _capi.check(_capi.lib().af_group_info(handle, ctypes.byref(x_len), ctypes.byref(y_rows), ctypes.byref(n_units),
+                                              ctypes.byref(grid), ctypes.byref(tiles)))
+        self.x_len, self.y_rows, self.n_units, self.grid, self.tiles = x_len.value, y_rows.value, n_units.value, grid.value, tiles.value
+
+    def switch_gemv(self, prev, cur, acc_out, *, xin=None, acc_in=None, res=None, h_out=None, prologue="none", norm_w=None,
+                    eps: float = 0.0, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace", pdl: bool = False) -> None:
+        """acc_out (int64, zeroed by the caller) += fix(W_new . prologue(h)); W <- W_new in place."""
+        if mode not in _MODES:
+            raise ValueError(f"unknown switch mode {mode!r}")
+        if prologue not in self.PROLOGUES:
+            raise ValueError(f"unknown prologue {prologue!r}")
+        for dec in (prev, cur):
+            if dec is not None and not isinstance(dec, DeviceDecision):
+                raise TypeError("the fused switch + GEMV takes device-resident decisions (DeviceDecision) or None")
+        need = self.x_len * (2 if prologue == "silu_mul" else 1)
+        for name, t, dt, n in (("xin", xin, torch.float32, need), ("acc_in", acc_in, torch.int64, need), ("res", res, torch.float32, self.x_len),
+                               ("h_out", h_out, torch.float32, self.x_len), ("norm_w", norm_w, torch.float32, self.x_len),
+                               ("acc_out", acc_out, torch.int64, self.y_rows)):
+            if t is None:
+                continue
+            if not t.is_cuda:
+                raise DeviceError("operand is not on a CUDA device: the B200 path has no CPU fallback")
+            if t.dtype != dt or not t.is_contiguous() or t.numel() < n:
+                raise DimensionError(f"{name} must be a contiguous {dt} vector of at least {n} entries")
+        _capi.check(_capi.lib().af_switch_gemv(
+            self.handle, prev.ptr if prev is not None else None, cur.ptr if cur is not None else None, int(max_k), float(scale),
+            _MODES[mode], _ptr(xin) if xin is not None else None, _ptr(acc_in) if acc_in is not None else None,
+            _ptr(res) if res is not None else None, _ptr(h_out) if h_out is not None else None, self.PROLOGUES[prologue],
+            _ptr(norm_w) if norm_w is not None else None, float(eps), _ptr(acc_out), 1 if pdl else 0, _capi.stream_ptr()))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None and self.handle:
+            _capi.lib().af_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+

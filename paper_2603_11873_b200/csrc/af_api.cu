@@ -117,6 +117,18 @@ struct af_table {
     int sm_count = 0;
 };
 
+// A group of segments that share one input vector (q|k|v, gate|up, or a single matrix) with its
+// own work-unit schedule: the fused switch + GEMV launch of one projection of the decode forward.
+struct af_group {
+    af_table* table = nullptr;
+    std::vector<int> segs;
+    UnitDev* d_units = nullptr;
+    int n_units = 0, grid = 0;
+    int* d_seg_yoff = nullptr;
+    int x_len = 0, y_rows = 0;
+    long long tiles = 0;
+};
+
 extern "C" {
 
 int af_abi_version(void) { return AF_ABI_VERSION; }
@@ -344,12 +356,12 @@ int af_table_status(af_table* t, void* stream) {
 
 namespace af {
 
-template <int KS, bool BA>
+template <int KS, bool BA, bool GEMV = false>
 static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
-    using L = MmaLayout<KS, BA>;
+    using L = MmaLayout<KS, BA, GEMV>;
     static bool configured = false;
     if (!configured) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS, BA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS, BA, GEMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured = true;
     }
     MmaParams mp2 = mp;
@@ -361,7 +373,21 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     static const int env_upsw = [] { const char* e = getenv("AF_UP_SWIZZLE"); return (e && e[0] == '0') ? 0 : 1; }();
     mp2.up_swizzle_ok = env_upsw;
     if (mp2.store_depth > mp2.n_stages - 2) mp2.store_depth = mp2.n_stages - 2;
-    switch_mma_kernel<KS, BA><<<grid, kMmaThreads, L::total, st>>>(mp2);
+    if constexpr (GEMV) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kMmaThreads);
+        cfg.dynamicSmemBytes = L::total;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = mp2.gv.pdl ? 1 : 0;
+        AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_mma_kernel<KS, BA, GEMV>, mp2));
+    } else {
+        switch_mma_kernel<KS, BA, GEMV><<<grid, kMmaThreads, L::total, st>>>(mp2);
+    }
     AF_LAUNCH_CHECK("switch_mma_kernel");
     return AF_OK;
 }
@@ -554,6 +580,176 @@ int af_max_deviation(af_table* t, float* out_dev, void* stream) {
     return AF_OK;
 }
 
+// ------------------------------------------------------------------ fused switch + GEMV ----
+
+int af_group_destroy(af_group* g) {
+    if (!g) return AF_OK;
+    if (g->d_units) cudaFree(g->d_units);
+    if (g->d_seg_yoff) cudaFree(g->d_seg_yoff);
+    delete g;
+    return AF_OK;
+}
+
+int af_group_create(af_table* t, const int32_t* seg_ids, int32_t n, af_group** out) {
+    if (!out) return fail(AF_EVALUE, "out is NULL");
+    *out = nullptr;
+    if (!t || !seg_ids || n < 1) return fail(AF_EDIM, "segment group is empty");
+    if (!t->fast_mma)
+        return fail(AF_EPRECISION, "the fused switch + GEMV needs the tensor path: bf16 targets and factors, rank % 8 == 0, "
+                                   "16-byte aligned rows");
+    std::vector<int> yoff(t->n_segments, 0);
+    std::vector<char> seen(t->n_segments, 0);
+    int x_len = -1, rows = 0;
+    for (int i = 0; i < n; ++i) {
+        const int sidx = seg_ids[i];
+        if (sidx < 0 || sidx >= t->n_segments) return fail(AF_EINDEX, "segment id outside the table");
+        if (seen[sidx]) return fail(AF_EALIAS, "segment listed twice in one group");
+        seen[sidx] = 1;
+        const af_segment_desc& sd = t->segs[sidx];
+        if (sd.d_out < 1 || sd.d_in < 1) return fail(AF_EDIM, "empty segment in a GEMV group");
+        if (x_len < 0) x_len = sd.d_in;
+        if (sd.d_in != x_len) return fail(AF_EDIM, "segments of one group must share d_in (one input vector)");
+        yoff[sidx] = rows;
+        rows += sd.d_out;
+    }
+    af_group* g = new af_group();
+    g->table = t;
+    g->segs.assign(seg_ids, seg_ids + n);
+    g->x_len = x_len;
+    g->y_rows = rows;
+    // ---- schedule: the group's tiles in (segment, column strip, row tile) order, cut into one
+    //      contiguous span per CTA: every SM streams the same number of tiles (+-1) and restages
+    //      the DOWN slab only when its span crosses into another strip ----
+    const int strips = (x_len + kTN - 1) / kTN;
+    long long total = 0;
+    for (int i = 0; i < n; ++i) total += (long long)strips * ((t->segs[seg_ids[i]].d_out + kMR - 1) / kMR);
+    g->tiles = total;
+    const int G = (int)std::min<long long>(total, std::max(1, t->sm_count));
+    std::vector<std::vector<UnitDev>> per_cta(G);
+    {
+        int cta = 0;
+        long long idx = 0;                      // linear tile index
+        long long cta_end = total * 1 / G;      // end of CTA 0's span
+        for (int i = 0; i < n; ++i) {
+            const int sidx = seg_ids[i];
+            const int d_out = t->segs[sidx].d_out;
+            const int rt = (d_out + kMR - 1) / kMR;
+            for (int sp = 0; sp < strips; ++sp) {
+                int r = 0;  // row tile inside the strip
+                while (r < rt) {
+                    while (idx >= cta_end && cta < G - 1) {
+                        ++cta;
+                        cta_end = total * (cta + 1) / G;
+                    }
+                    const int take = (int)std::min<long long>(rt - r, cta_end - idx);
+                    const int row0 = r * kMR;
+                    per_cta[cta].push_back({sidx, row0, std::min(take * kMR, d_out - row0), sp * kTN});
+                    r += take;
+                    idx += take;
+                }
+            }
+        }
+    }
+    size_t depth = 0;
+    for (auto& v : per_cta) depth = std::max(depth, v.size());
+    std::vector<UnitDev> units(depth * G, UnitDev{0, 0, 0, 0});
+    for (int c = 0; c < G; ++c)
+        for (size_t j = 0; j < per_cta[c].size(); ++j) units[j * G + c] = per_cta[c][j];
+    g->grid = G;
+    g->n_units = (int)units.size();
+    cudaError_t e = cudaMalloc(&g->d_units, sizeof(UnitDev) * units.size());
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_units, units.data(), sizeof(UnitDev) * units.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_seg_yoff, sizeof(int) * yoff.size());
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_seg_yoff, yoff.data(), sizeof(int) * yoff.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        af_group_destroy(g);
+        return fail(AF_ECUDA, std::string("group upload: ") + cudaGetErrorString(e));
+    }
+    *out = g;
+    return AF_OK;
+}
+
+int af_group_info(const af_group* g, int32_t* x_len, int32_t* y_rows, int32_t* n_units, int32_t* grid, int64_t* tiles) {
+    if (!g) return fail(AF_EVALUE, "group is NULL");
+    if (x_len) *x_len = g->x_len;
+    if (y_rows) *y_rows = g->y_rows;
+    if (n_units) *n_units = g->n_units;
+    if (grid) *grid = g->grid;
+    if (tiles) *tiles = g->tiles;
+    return AF_OK;
+}
+
+int af_switch_gemv(af_group* g, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k, float scale,
+                   int32_t mode, const float* xin, const int64_t* acc_in, const float* res, float* h_out, int32_t prologue,
+                   const float* norm_w, float eps, int64_t* acc_out, int32_t pdl, void* stream) {
+    if (!g) return fail(AF_EVALUE, "group is NULL");
+    af_table* t = g->table;
+    if (mode != AF_SWITCH_INPLACE && mode != AF_SWITCH_FROM_PRISTINE) return fail(AF_EVALUE, "unknown switch mode");
+    if (mode == AF_SWITCH_FROM_PRISTINE && !t->has_pristine)
+        return fail(AF_ESTATE, "FROM_PRISTINE needs a pristine copy of every segment");
+    if (prologue < AF_PRO_NONE || prologue > AF_PRO_SILU_MUL) return fail(AF_EVALUE, "unknown prologue");
+    if (prologue == AF_PRO_RMSNORM && !norm_w) return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
+    if ((xin == nullptr) == (acc_in == nullptr)) return fail(AF_EVALUE, "exactly one of xin / acc_in must be given");
+    if (!acc_out) return fail(AF_EVALUE, "acc_out is NULL");
+    if (reinterpret_cast<uintptr_t>(acc_out) % 8 != 0 || reinterpret_cast<uintptr_t>(acc_in) % 8 != 0)
+        return fail(AF_EDIM, "fixed-point accumulators must be 8-byte aligned");
+    if (h_out && (h_out == xin || h_out == res)) return fail(AF_EALIAS, "h_out aliases an input vector");
+    const bool use_dev = prev_dev || cur_dev;
+    if (use_dev && (max_k < 1 || max_k > AF_MAX_K)) return fail(AF_EVALUE, "max_k outside [1, AF_MAX_K]");
+    const bool from_pristine = mode == AF_SWITCH_FROM_PRISTINE;
+
+    MmaParams mp{};
+    SwitchParams& p = mp.base;
+    p.segs = t->d_segs;
+    p.units = g->d_units;
+    p.n_units = g->n_units;
+    p.from_pristine = from_pristine;
+    p.prev_dev = prev_dev;
+    p.cur_dev = cur_dev;
+    p.use_dev = use_dev ? 1 : 0;
+    p.scale = scale;
+    p.n_experts_limit = t->min_experts;
+    p.err_flag = t->d_err;
+    p.host_plan.n_blocks = 0;  // no decision at all: a plain GEMV over the live weights
+    const int n_blocks_bound = use_dev ? ((from_pristine || !prev_dev ? 0 : max_k) + (cur_dev ? max_k : 0)) : 0;
+    p.max_blocks = std::min(n_blocks_bound, kMaxBlocks);
+    const int s_bound = n_blocks_bound * t->max_rank;
+    if (s_bound > kMmaMaxKS * 16) return fail(AF_EVALUE, "the fused switch + GEMV holds at most 64 stacked ranks");
+    const int S = t->n_segments;
+    mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 3 : 2) * S;
+    mp.tmaps_st = t->d_maps + (size_t)2 * S;
+    mp.tmaps_up = t->d_maps + (size_t)4 * S;
+    mp.gv.xin = xin;
+    mp.gv.acc_in = reinterpret_cast<const long long*>(acc_in);
+    mp.gv.res = res;
+    mp.gv.h_out = h_out;
+    mp.gv.norm_w = norm_w;
+    mp.gv.eps = eps;
+    mp.gv.prologue = prologue;
+    mp.gv.x_len = g->x_len;
+    mp.gv.acc_out = reinterpret_cast<unsigned long long*>(acc_out);
+    mp.gv.seg_yoff = g->d_seg_yoff;
+    mp.gv.pdl = (pdl && g_pdl.load()) ? 1 : 0;
+    const int ks = std::max(1, (s_bound + 15) / 16);
+    const bool ba = t->rank16 && ks > 2 && !g_force_hilo;
+    cudaStream_t st = as_stream(stream);
+    switch (ks) {
+        case 1: return launch_mma<1, false, true>(mp, g->grid, st);
+        case 2: return launch_mma<2, false, true>(mp, g->grid, st);
+        case 3: return ba ? launch_mma<3, true, true>(mp, g->grid, st) : launch_mma<3, false, true>(mp, g->grid, st);
+        default: return ba ? launch_mma<4, true, true>(mp, g->grid, st) : launch_mma<4, false, true>(mp, g->grid, st);
+    }
+}
+
+int af_accum_to_f32(const int64_t* acc, const float* res, float* out, int32_t n, void* stream) {
+    if (n < 0 || !acc || !out) return fail(AF_EVALUE, "NULL argument");
+    if (n == 0) return AF_OK;
+    accum_to_f32_kernel<<<std::max(1, std::min((n + 255) / 256, 64)), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const long long*>(acc), res, out, n);
+    AF_LAUNCH_CHECK("accum_to_f32_kernel");
+    return AF_OK;
+}
+
 // ------------------------------------------------------------------ router ----
 
 int af_pregate(const void* router_w, int32_t w_dtype, int32_t n_experts, int32_t d, const void* x, int32_t x_dtype,
@@ -721,13 +917,35 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
     return AF_OK;
 }
 
+static int attn_decode_impl(const float* qkv, const long long* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,
+                            const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
+                            int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace, int32_t* tickets, float* out,
+                            void* stream);
+
 int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table, const float* sin_table,
                    const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t max_seq,
                    int32_t n_split, float* workspace, int32_t* tickets, float* out, void* stream) {
+    if (!qkv) return fail(AF_EVALUE, "NULL argument");
+    return attn_decode_impl(qkv, nullptr, k_cache, v_cache, cos_table, sin_table, pos_dev, n_heads, n_kv_heads, head_dim, max_seq,
+                            n_split, workspace, tickets, out, stream);
+}
+
+int af_attn_decode_fix(const int64_t* qkv_fix, void* k_cache, void* v_cache, const float* cos_table, const float* sin_table,
+                       const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t max_seq,
+                       int32_t n_split, float* workspace, int32_t* tickets, float* out, void* stream) {
+    if (!qkv_fix) return fail(AF_EVALUE, "NULL argument");
+    return attn_decode_impl(nullptr, reinterpret_cast<const long long*>(qkv_fix), k_cache, v_cache, cos_table, sin_table, pos_dev,
+                            n_heads, n_kv_heads, head_dim, max_seq, n_split, workspace, tickets, out, stream);
+}
+
+static int attn_decode_impl(const float* qkv, const long long* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,
+                            const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
+                            int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace, int32_t* tickets, float* out,
+                            void* stream) {
     if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads != 0) return fail(AF_EDIM, "heads must be a multiple of kv heads");
     if (head_dim < 2 || head_dim % 2 != 0 || head_dim > kAttnMaxHd) return fail(AF_EDIM, "head_dim must be even and <= 256");
     if (max_seq < 1) return fail(AF_EDIM, "max_seq must be positive");
-    if (!qkv || !k_cache || !v_cache || !cos_table || !sin_table || !pos_dev || !out) return fail(AF_EVALUE, "NULL argument");
+    if (!k_cache || !v_cache || !cos_table || !sin_table || !pos_dev || !out) return fail(AF_EVALUE, "NULL argument");
     if (n_split < 1) n_split = 1;
     if (n_split > 1 && (!workspace || !tickets)) return fail(AF_EVALUE, "split attention needs a workspace and tickets");
     cudaLaunchConfig_t cfg{};
@@ -745,7 +963,7 @@ int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* 
     __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
     const bool aligned = (reinterpret_cast<uintptr_t>(k_cache) % 16 == 0) && (reinterpret_cast<uintptr_t>(v_cache) % 16 == 0);
 #define AF_ATTN(EL)                                                                                                       \
-    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode_kernel<EL>, qkv, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,  \
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode_kernel<EL>, qkv, qkv_fix, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,  \
                                    (int)n_kv_heads, (int)head_dim, (int)max_seq, scale, (int)n_split, workspace,           \
                                    reinterpret_cast<int*>(tickets), out))
     if (aligned && head_dim == 64) AF_ATTN(2);

@@ -48,11 +48,6 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     return r;
 }
 
-// Programmatic dependent launch (PDL): a kernel launched with the attribute may start while its
-// predecessor is still running; everything it does before pdl_wait() must be independent of
-// the predecessor (here: prefetching W).  Both are no-ops in an ordinary launch.
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // 1-D bulk copy global -> shared, completing on an mbarrier (UBLKCP); 16-byte aligned, size % 16 == 0.
 __device__ __forceinline__ void gv_bulk_load(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -380,6 +375,7 @@ __device__ __forceinline__ void load_bf16_vec(const __nv_bfloat16* p, float (&f)
 // vector instantiations (2, 4, 8); EL == 1 is the generic one (any even hd <= 256, lane-strided).
 template <int EL>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* __restrict__ qkv,
+                                                                   const long long* __restrict__ qkv_fix,
                                                                    __nv_bfloat16* __restrict__ k_cache,
                                                                    __nv_bfloat16* __restrict__ v_cache,
                                                                    const float* __restrict__ cos_t,
@@ -397,29 +393,30 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
     const int h = blockIdx.x / n_split, sp = blockIdx.x % n_split;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int group = n_heads / n_kv, kvh = h / group;
-    pdl_launch_dependents();
     pdl_wait();  // qkv comes from the previous kernel
+    pdl_launch_dependents();  // after the wait: a dependent's pre-wait part then never runs ahead of qkv's producer
     const int pos = *pos_dev;
     const int n_pos = pos + 1;
     const int per = (n_pos + n_split - 1) / n_split;
     const int t0 = sp * per, t1 = min(n_pos, t0 + per);
     const int half = hd >> 1;
-    const float* q = qkv + (long long)h * hd;
-    const float* kn = qkv + (long long)n_heads * hd + (long long)kvh * hd;
-    const float* vn = qkv + (long long)(n_heads + n_kv) * hd + (long long)kvh * hd;
+    // q/k/v of this head: f32, or the fixed-point accumulators of a fused switch + GEMV launch
+    const long long oq = (long long)h * hd, ok = (long long)n_heads * hd + (long long)kvh * hd,
+                    ov = (long long)(n_heads + n_kv) * hd + (long long)kvh * hd;
+    auto ld = [&](long long i) { return qkv_fix ? __ll2float_rn(qkv_fix[i]) * (1.0f / (float)(1ll << AF_FIX_SHIFT)) : qkv[i]; };
     // RoPE (rotate-half): x'[i] = x[i] c - x[i+half] s ; x'[i+half] = x[i+half] c + x[i] s
     for (int i = tid; i < half; i += kAttnThreads) {
         const float c = cos_t[(long long)pos * half + i], s = sin_t[(long long)pos * half + i];
-        const float q0 = q[i], q1 = q[i + half];
+        const float q0 = ld(oq + i), q1 = ld(oq + i + half);
         q_s[i] = q0 * c - q1 * s;
         q_s[i + half] = q1 * c + q0 * s;
-        const float k0 = kn[i], k1 = kn[i + half];
+        const float k0 = ld(ok + i), k1 = ld(ok + i + half);
         // the cache stores bf16: the new position uses the rounded values too, so that a later
         // token sees exactly what this one saw
         k_s[i] = __bfloat162float(__float2bfloat16_rn(k0 * c - k1 * s));
         k_s[i + half] = __bfloat162float(__float2bfloat16_rn(k1 * c + k0 * s));
     }
-    for (int i = tid; i < hd; i += kAttnThreads) v_s[i] = __bfloat162float(__float2bfloat16_rn(vn[i]));
+    for (int i = tid; i < hd; i += kAttnThreads) v_s[i] = __bfloat162float(__float2bfloat16_rn(ld(ov + i)));
     __syncthreads();
     if (h % group == 0 && pos >= t0 && pos < t1) {  // one CTA per kv head appends to the cache
         __nv_bfloat16* kc = k_cache + ((long long)kvh * max_seq + pos) * hd;
@@ -545,6 +542,14 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
         out[(long long)h * hd + i] = o / gl;
     }
     if (tid == 0) tickets[h] = 0;  // ready for the next launch (graph replay)
+}
+
+// out[i] = (res ? res[i] : 0) + fixed-point accumulator i (the residual stream after the last fused
+// switch + GEMV launch, as a plain f32 vector for the lm_head GEMV).
+__global__ void accum_to_f32_kernel(const long long* __restrict__ acc, const float* __restrict__ res, float* __restrict__ out, int n) {
+    pdl_wait();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = (res ? res[i] : 0.f) + __ll2float_rn(acc[i]) * (1.0f / (float)(1ll << AF_FIX_SHIFT));
 }
 
 // argmax with the winning value (vocab-parallel lm_head: ranks exchange (value, index)).

@@ -349,11 +349,14 @@ struct TileIterT {
     int u, m0, row_end;
     UnitDev un;
     __device__ __forceinline__ bool valid(const SwitchParams& p) const { return u < p.n_units; }
+    // A unit with rows == 0 is padding of a per-CTA list (group schedules, af_group_create):
+    // a CTA's list has no holes, so the first empty unit ends its walk.
     __device__ __forceinline__ void load_unit(const SwitchParams& p) {
         if (u < p.n_units) {
             un = p.units[u];
             m0 = un.row0;
             row_end = un.row0 + un.rows;
+            if (un.rows <= 0) u = p.n_units;
         }
     }
     __device__ __forceinline__ void init(const SwitchParams& p) {

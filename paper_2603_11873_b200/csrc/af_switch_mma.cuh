@@ -53,21 +53,26 @@ constexpr int kMmaDefaultStages = 10;
 // f32 product of each rank-16 step (acc += g * (U_b A_b)) instead of being folded into a hi+lo
 // pair -- half the tensor work, one f32 FMA per element per step.  Used when rank % 16 == 0 and
 // the stacked rank exceeds 32 (Llama-3-8B: r = 16, s = 64), where the hi/lo form is HMMA-bound.
-template <int KS, bool BA = false>
+template <int KS, bool BA = false, bool GEMV = false>
 struct MmaLayout {
     static constexpr int s_pad = KS * 16;
     static constexpr int up_stage_bytes = kMR * s_pad * 2;
     static constexpr int down_bytes = (BA ? 1 : 2) * s_pad * kDownPitch * 2;
-    static constexpr int fixed = down_bytes + 3 * 8 * 16 + (int)sizeof(Plan) + 1024 /*alignment slack*/ + 256;
-    static constexpr int by_smem = (227 * 1024 - fixed) / (kWStageBytes + up_stage_bytes);
+    // GEMV: per stage, the 16 consumer warps' partial dot products of the tile's 32 rows (f32)
+    static constexpr int part_stage_bytes = GEMV ? kMmaWarps * kMR * 4 : 0;
+    static constexpr int red_bytes = GEMV ? 128 : 0;  // block reduction scratch of the RMSNorm prologue
+    static constexpr int fixed = down_bytes + 3 * 8 * 16 + (int)sizeof(Plan) + red_bytes + 1024 /*alignment slack*/ + 256;
+    static constexpr int by_smem = (227 * 1024 - fixed) / (kWStageBytes + up_stage_bytes + part_stage_bytes);
     static constexpr int stages = by_smem < kMmaMaxStages ? by_smem : kMmaMaxStages;
     // offsets from the 1024-aligned base
     static constexpr int off_w = 0;
     static constexpr int off_up = off_w + stages * kWStageBytes;
-    static constexpr int off_down = off_up + stages * up_stage_bytes;
+    static constexpr int off_part = off_up + stages * up_stage_bytes;
+    static constexpr int off_down = off_part + stages * part_stage_bytes;
     static constexpr int off_bar = off_down + down_bytes;          // full[16], computed[16], empty[16]
     static constexpr int off_plan = off_bar + 3 * 8 * 16;
-    static constexpr int total = off_plan + (int)sizeof(Plan) + 1024 /*alignment slack*/;
+    static constexpr int off_red = (off_plan + (int)sizeof(Plan) + 15) & ~15;
+    static constexpr int total = off_red + red_bytes + 1024 /*alignment slack*/;
     static_assert(stages >= 3 && total <= 227 * 1024, "shared memory budget");
 };
 
@@ -110,8 +115,38 @@ __device__ __forceinline__ void tma_store_2d_addr(const void* tmap, int c0, int 
                  : "memory");
 }
 
+// Fixed-point accumulators of the fused GEMV: a row's partial dot products (one per 256-column
+// strip, produced by different CTAs) are added with 64-bit INTEGER atomics, so the sum does not
+// depend on the order the CTAs arrive in -- the result is deterministic, unlike f32 atomics.
+// value = acc * 2^-AF_FIX_SHIFT; resolution 9e-13, range +-8.4e6.
+__device__ __forceinline__ float fix_to_f32(long long q) { return __ll2float_rn(q) * (1.0f / (float)(1ll << AF_FIX_SHIFT)); }
+__device__ __forceinline__ long long f32_to_fix(float v) { return __float2ll_rn(v * (float)(1ll << AF_FIX_SHIFT)); }
+
+// The GEMV fused into the switch (switch_mma_kernel<..., GEMV = true>): while a tile of W is in
+// registers, freshly updated and rounded to bf16, it is also multiplied with the input vector of
+// the projection -- the decode forward (model.py:367-368) reads no weight a second time.
+//   h[c] = (res ? res[c] : 0) + (acc_in ? fix(acc_in[c]) : xin[c])
+//   x[c] = h[c]                                   prologue NONE
+//        = h[c] * rsqrt(mean(h^2) + eps) * norm_w prologue RMSNORM
+//        = silu(a[c]) * a[x_len + c]              prologue SILU_MUL (a = the un-residualed input)
+//   acc_out[seg_yoff[seg] + row] += fix(sum_c Wnew[row][c] * x[c])   per 256-column strip
+struct GemvParams {
+    const float* xin;
+    const long long* acc_in;
+    const float* res;
+    float* h_out;                  // optional: CTA 0 materialises h (the residual stream)
+    const float* norm_w;
+    float eps;
+    int prologue;
+    int x_len;                     // d_in of the group
+    unsigned long long* acc_out;
+    const int* seg_yoff;           // per table segment: first row of its slice of acc_out
+    int pdl;                       // launched with programmatic stream serialization
+};
+
 struct MmaParams {
     SwitchParams base;
+    GemvParams gv;
     const CUtensorMap* tmaps_ld;   // per segment: 32 x 64 swizzled box on the source (live or pristine)
     const CUtensorMap* tmaps_st;   // per segment: the same box shape on the live matrix
     const CUtensorMap* tmaps_up;   // per segment: UP bank as [N * d_out][rank], box 32 rows x rank, swizzle = row bytes
@@ -195,9 +230,48 @@ __host__ __device__ __forceinline__ bool up_swizzled(int rank) { return rank == 
 //   storers      (kStorers warps, 1 thread each): wait computed[stage] -> TMA stores of their
 //                boxes; a stage goes back to the producers once every storer's stores have read
 //                shared memory (store_depth newer stores may still be draining)
-template <int KS, bool BA>
+// ---- pieces of the fused GEMV (GEMV = true) ----
+
+// One element of the un-normalised input h (see GemvParams).
+__device__ __forceinline__ float gemv_h(const GemvParams& g, int c) {
+    float h = g.acc_in ? fix_to_f32(g.acc_in[c]) : g.xin[c];
+    if (g.res) h += g.res[c];
+    return h;
+}
+// One element of the projection's input vector x; inv = rsqrt(mean(h^2) + eps) for RMSNORM.
+__device__ __forceinline__ float gemv_x(const GemvParams& g, int c, float inv) {
+    if (g.prologue == AF_PRO_SILU_MUL) {
+        const float a = g.acc_in ? fix_to_f32(g.acc_in[c]) : g.xin[c];
+        const float b = g.acc_in ? fix_to_f32(g.acc_in[g.x_len + c]) : g.xin[g.x_len + c];
+        return a / (1.0f + expf(-a)) * b;
+    }
+    float h = gemv_h(g, c);
+    if (g.prologue == AF_PRO_RMSNORM) h *= inv * g.norm_w[c];
+    return h;
+}
+// B fragment (k16 x n8, col-major) of the input vector for this warp's 16 columns: column n = 0
+// carries bf16 hi(x), n = 1 carries lo = x - hi (x is reproduced to 2^-17 relative), the other six
+// columns are zero.  Lane j < 16 evaluates x at column col0 + 16 * warp + j.
+__device__ __forceinline__ void gemv_x_fragment(const GemvParams& g, int col0, int warp, int lane, float inv,
+                                                uint32_t& xb0, uint32_t& xb1) {
+    float xv = 0.f;
+    const int c = col0 + warp * 16 + (lane & 15);
+    if (lane < 16 && c < g.x_len) xv = gemv_x(g, c, inv);
+    const float hi = __bfloat162float(__float2bfloat16_rn(xv));
+    const float lo = xv - hi;
+    const int t2 = (lane & 3) * 2, n = lane >> 2;
+    const float h0 = __shfl_sync(0xffffffffu, hi, t2), h1 = __shfl_sync(0xffffffffu, hi, t2 + 1);
+    const float h2 = __shfl_sync(0xffffffffu, hi, t2 + 8), h3 = __shfl_sync(0xffffffffu, hi, t2 + 9);
+    const float l0 = __shfl_sync(0xffffffffu, lo, t2), l1 = __shfl_sync(0xffffffffu, lo, t2 + 1);
+    const float l2 = __shfl_sync(0xffffffffu, lo, t2 + 8), l3 = __shfl_sync(0xffffffffu, lo, t2 + 9);
+    xb0 = n == 0 ? pack_bf16x2(h0, h1) : (n == 1 ? pack_bf16x2(l0, l1) : 0u);
+    xb1 = n == 0 ? pack_bf16x2(h2, h3) : (n == 1 ? pack_bf16x2(l2, l3) : 0u);
+}
+
+template <int KS, bool BA, bool GEMV>
 __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
-    using L = MmaLayout<KS, BA>;
+    using L = MmaLayout<KS, BA, GEMV>;
+    static_assert(!GEMV || kStorers == 1, "the fused GEMV reduces a tile's partial sums in the single storer warp");
     constexpr int kSt = L::stages < kMmaDefaultStages ? L::stages : kMmaDefaultStages;
     extern __shared__ unsigned char smem_dyn[];
     const SwitchParams& p = mp.base;
@@ -225,7 +299,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     __syncthreads();
     const int n_blocks = plan.n_blocks;
     if (n_blocks < 0) return;                       // unusable decision: flagged, nothing touched
-    if (n_blocks == 0 && !p.from_pristine) return;  // unchanged decision: nothing to move
+    // unchanged decision: nothing to move (the fused GEMV still has to stream W, but stores nothing)
+    const bool store_w = n_blocks > 0 || p.from_pristine;
+    if (!GEMV && !store_w) return;
 
     const uint32_t w_base = smem_u32(sm + L::off_w);
     const uint32_t up_base = smem_u32(sm + L::off_up);
@@ -303,34 +379,57 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     }
     if (warp > kMmaWarps + kWProd) {
         // ============ storers: boxes back to global, then hand the stage back ============
-        if (lane == 0) {
+        // GEMV: the whole warp also adds the 16 consumer warps' partial dot products of the tile
+        // (fixed order) and accumulates the 32 row sums into the launch's fixed-point vector.
+        if (lane == 0 || GEMV) {
             const int who = warp - (kMmaWarps + kWProd + 1);
             constexpr int kMine = (kBoxes + kStorers - 1) / kStorers;
             MmaIter ti;
             ti.init(p);
             int it = 0;
+            int cur_seg = -1, yoff = 0;
+            if constexpr (GEMV) {
+                if (mp.gv.pdl) pdl_wait();  // acc_out may still be read by an earlier kernel of the chain
+            }
             for (; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
                 mbar_wait(&computed[stage], ph);
-                const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
+                if (lane == 0 && store_w) {
+                    const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
 #pragma unroll
-                for (int j = 0; j < kMine; ++j) {
-                    const int b = who + j * kStorers;
-                    if (b < kBoxes)
-                        tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
+                    for (int j = 0; j < kMine; ++j) {
+                        const int b = who + j * kStorers;
+                        if (b < kBoxes)
+                            tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
+                    }
+                    bulk_commit();
                 }
-                bulk_commit();
-                // the stores of tile it - depth have drained their stage: hand it back
-                const int depth = mp.store_depth;
-                if (depth <= 0) bulk_wait_read<0>();
-                else if (depth == 1) bulk_wait_read<1>();
-                else if (depth == 2) bulk_wait_read<2>();
-                else bulk_wait_read<3>();
-                if (it >= depth) mbar_arrive(&empty[(it - depth) % kSt]);
+                if constexpr (GEMV) {
+                    if (ti.un.seg != cur_seg) {
+                        cur_seg = ti.un.seg;
+                        yoff = mp.gv.seg_yoff[cur_seg];
+                    }
+                    const float* part = reinterpret_cast<const float*>(sm + L::off_part + stage * L::part_stage_bytes);
+                    float sum = 0.f;
+#pragma unroll
+                    for (int w = 0; w < kMmaWarps; ++w) sum += part[w * kMR + lane];
+                    if (ti.m0 + lane < ti.row_end)
+                        atomicAdd(mp.gv.acc_out + yoff + ti.m0 + lane, (unsigned long long)f32_to_fix(sum));
+                    __syncwarp();  // every lane has read the stage's partials before it is handed back
+                }
+                if (lane == 0) {
+                    // the stores of tile it - depth have drained their stage: hand it back
+                    const int depth = mp.store_depth;
+                    if (depth <= 0) bulk_wait_read<0>();
+                    else if (depth == 1) bulk_wait_read<1>();
+                    else if (depth == 2) bulk_wait_read<2>();
+                    else bulk_wait_read<3>();
+                    if (it >= depth) mbar_arrive(&empty[(it - depth) % kSt]);
+                }
                 ti.next(p);
             }
-            bulk_wait_all<0>();  // global writes complete before the CTA retires
+            if (lane == 0) bulk_wait_all<0>();  // global writes complete before the CTA retires
         }
         return;
     }
@@ -352,6 +451,35 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     down_prefetch<KS>(dn_regs, sg, plan, S, ti.un.col0, tid);
     down_commit<KS, BA>(down_smem, dn_regs, sg.rank, plan, S, tid);
     named_bar_sync(1, kMmaConsumers);  // first slab visible
+    // ---- GEMV prologue: everything above (and the W ring the producers are filling) is
+    //      independent of the previous kernel; the input vector is not ----
+    float x_inv = 1.0f;
+    uint32_t xb0 = 0u, xb1 = 0u;
+    if constexpr (GEMV) {
+        const GemvParams& g = mp.gv;
+        if (g.pdl) {
+            pdl_wait();
+            // the dependent may start (its own pre-wait part reads nothing this chain writes later
+            // than one kernel back); triggered after the wait so the chain stays one kernel deep
+            if (tid == 0) pdl_launch_dependents();
+        }
+        if (g.prologue == AF_PRO_RMSNORM || (g.h_out && blockIdx.x == 0)) {
+            float ss = 0.f;
+            for (int c = tid; c < g.x_len; c += kMmaConsumers) {
+                const float h = gemv_h(g, c);
+                ss = fmaf(h, h, ss);
+                if (g.h_out && blockIdx.x == 0) g.h_out[c] = h;
+            }
+            float* red = reinterpret_cast<float*>(sm + L::off_red);
+            ss = warp_sum(ss);
+            if (lane == 0) red[warp] = ss;
+            named_bar_sync(1, kMmaConsumers);
+            float tot = 0.f;
+#pragma unroll
+            for (int i = 0; i < kMmaWarps; ++i) tot += red[i];
+            x_inv = rsqrtf(tot / (float)g.x_len + g.eps);
+        }
+    }
     bool new_unit = true;
     constexpr int kHalves = BA ? 1 : 2;
     uint32_t bfr[kHalves][KS][4];
@@ -372,6 +500,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
         const int stage = it % kSt;
         const uint32_t ph = (it / kSt) & 1;
         if (new_unit) {
+            if constexpr (GEMV) gemv_x_fragment(mp.gv, ti.un.col0, warp, lane, x_inv, xb0, xb1);
             // B fragments of this unit's slab -> registers (kept for every tile of the unit)
 #pragma unroll
             for (int half = 0; half < kHalves; ++half)
@@ -400,7 +529,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
             }
             // start fetching the NEXT unit's DOWN rows; they are committed to the slab at its start
             const int un = ti.u + gridDim.x;
-            have_next = un < p.n_units;
+            have_next = un < p.n_units && p.units[un].rows > 0;
             if (have_next) {
                 const UnitDev nu = p.units[un];
                 sg_next = p.segs[nu.seg];
@@ -461,6 +590,16 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                 wv[nt * 2 + 1] = pack_bf16x2(bf16lo_to_f32(b2) + acc[nt][2], bf16hi_to_f32(b2) + acc[nt][3]);
             }
             stmatrix_x4(waddr, wv);
+            if constexpr (GEMV) {
+                // the rounded tile is an A fragment as it stands: y[16 rows] = Wnew[16 x 16] . x[16]
+                float yv[4] = {0.f, 0.f, 0.f, 0.f};
+                mma_bf16_16816(yv, wv, xb0, xb1);
+                if ((lane & 3) == 0) {  // columns n = 0 (hi) and n = 1 (lo) of rows lane/4 and lane/4 + 8
+                    float* part = reinterpret_cast<float*>(sm + L::off_part + stage * L::part_stage_bytes) + warp * kMR + mt * 16;
+                    part[lane >> 2] = yv[0] + yv[1];
+                    part[(lane >> 2) + 8] = yv[2] + yv[3];
+                }
+            }
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA store
         __syncwarp();

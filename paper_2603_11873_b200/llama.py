@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _capi
-from .adapters import SwitchTable
+from .adapters import SegmentGroup, SwitchTable
 from .errors import ConfigError, InputError, StateError
 from .linalg import DispatchRecorder, Matrix, _ptr
 from .routing import DECISION_BYTES, DeviceDecision, GateDecision
@@ -59,6 +59,10 @@ class LlamaConfig:
     adapters: bool = True            # False = adapter-free backbone (the reference's BASE strategy)
     keep_pristine: bool = True
     attn_splits: int = 0             # CTAs per head in decode attention; 0 = auto (1 up to 512 positions)
+    # "chase": the forward GEMV of every projection is fused into the switch of its weights (one pass
+    # over W per token instead of switch + forward); "separate": one switch launch, then plain GEMVs;
+    # "auto": chase when it applies (adapters, single rank, tensor path)
+    forward_mode: str = "auto"
 
     def validate(self) -> None:
         for name in ("layers", "hidden", "ffn", "n_heads", "n_kv_heads", "vocab", "experts", "rank", "top_k", "max_seq", "tp_size"):
@@ -85,6 +89,10 @@ class LlamaConfig:
             raise ValueError(f"unknown switch mode {self.switch_mode!r}")
         if self.switch_mode == "from_pristine" and not self.keep_pristine:
             raise ValueError("from_pristine needs keep_pristine")
+        if self.forward_mode not in ("auto", "chase", "separate"):
+            raise ValueError(f"unknown forward mode {self.forward_mode!r}")
+        if self.forward_mode == "chase" and (not self.adapters or self.tp_size > 1):
+            raise ValueError("forward_mode='chase' needs adapters and tp_size == 1")
 
     @property
     def head_dim(self) -> int:
@@ -343,6 +351,29 @@ class LlamaEngine:
         self.attn_tickets = torch.zeros(self.heads_local, dtype=torch.int32, device=dev)
         self.forced_dev = None
         self._graphs = {}
+        # ---- fused switch + GEMV ("chase") ----
+        want = cfg.forward_mode
+        can = cfg.adapters and cfg.tp_size == 1 and self.table is not None and self.table.info()["tensor_path"] \
+            and 2 * cfg.top_k * cfg.rank <= 64 and cfg.compute in ("auto", "mma")
+        if want == "chase" and not can:
+            raise ConfigError("forward_mode='chase' needs the tensor path (bf16, rank % 8 == 0) and 2*top_k*rank <= 64")
+        self.chase = can and want in ("auto", "chase")
+        if self.chase:
+            self.groups = []
+            for li in range(cfg.layers):
+                b = 7 * li  # SEGMENT_NAMES order: q k v o gate up down
+                self.groups.append({"qkv": SegmentGroup(self.table, [b, b + 1, b + 2]), "o": SegmentGroup(self.table, [b + 3]),
+                                    "gu": SegmentGroup(self.table, [b + 4, b + 5]), "down": SegmentGroup(self.table, [b + 6])})
+            # fixed-point accumulators of every launch of a token, one arena zeroed once per step
+            n_qkv, n_gu = self.q_rows + 2 * self.kv_rows, 2 * self.ffn_local
+            per_layer = n_qkv + d + n_gu + d
+            self.acc_arena = torch.zeros(cfg.layers * per_layer, dtype=torch.int64, device=dev)
+            self.acc = []
+            for li in range(cfg.layers):
+                o = li * per_layer
+                self.acc.append({"qkv": self.acc_arena[o: o + n_qkv], "o": self.acc_arena[o + n_qkv: o + n_qkv + d],
+                                 "gu": self.acc_arena[o + n_qkv + d: o + n_qkv + d + n_gu],
+                                 "down": self.acc_arena[o + n_qkv + d + n_gu: o + per_layer]})
 
     # -- the pieces of one step ---------------------------------------------------------
 
@@ -407,6 +438,40 @@ class LlamaEngine:
                                     _ptr(self.next_val), st))
         self.comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
 
+    def forward_chase(self, with_prev: bool) -> None:
+        """Switch AND merged forward of one token in one pass over the weights: each projection's
+        launch merges the selected experts into its tiles (adapters.py:236-258), multiplies the
+        rounded tiles with the projection's input (model.py:288) and writes them back.  4 weight
+        launches + attention per layer; RMSNorm, SiLU*up and the residual adds ride in the
+        prologue of the consuming launch."""
+        cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
+        d, eps = cfg.hidden, cfg.rms_eps
+        xa, xb = self.x
+        prev = self.prev if (with_prev and cfg.switch_mode == "inplace") else None
+        kw = dict(max_k=cfg.top_k, mode=cfg.switch_mode)
+        self.acc_arena.zero_()
+        self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
+        for li in range(cfg.layers):
+            g, a = self.groups[li], self.acc[li]
+            if li == 0:
+                g["qkv"].switch_gemv(prev, self.cur, a["qkv"], xin=xa, prologue="rmsnorm", norm_w=self.attn_norm[li], eps=eps,
+                                     pdl=False, **kw)
+            else:
+                g["qkv"].switch_gemv(prev, self.cur, a["qkv"], acc_in=self.acc[li - 1]["down"], res=xb, h_out=xa, prologue="rmsnorm",
+                                     norm_w=self.attn_norm[li], eps=eps, pdl=True, **kw)
+            self._check(L.af_attn_decode_fix(_ptr(a["qkv"]), _ptr(self.k_cache[li]), _ptr(self.v_cache[li]), _ptr(self.cos),
+                                             _ptr(self.sin), _ptr(self.pos_dev), self.heads_local, self.kv_local, cfg.head_dim,
+                                             cfg.max_seq, self.attn_splits, _ptr(self.attn_ws), _ptr(self.attn_tickets),
+                                             _ptr(self.attn_buf), st))
+            g["o"].switch_gemv(prev, self.cur, a["o"], xin=self.attn_buf, pdl=True, **kw)
+            g["gu"].switch_gemv(prev, self.cur, a["gu"], acc_in=a["o"], res=xa, h_out=xb, prologue="rmsnorm", norm_w=self.ffn_norm[li],
+                                eps=eps, pdl=True, **kw)
+            g["down"].switch_gemv(prev, self.cur, a["down"], acc_in=a["gu"], prologue="silu_mul", pdl=True, **kw)
+        self._check(L.af_accum_to_f32(_ptr(self.acc[-1]["down"]), _ptr(xb), _ptr(xa), d, st))
+        self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),
+                                    _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))
+        self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
+
     def _advance(self) -> None:
         L, st = _capi.lib(), _capi.stream_ptr()
         forced = self.forced_dev
@@ -416,6 +481,11 @@ class LlamaEngine:
                                       _ptr(self.history), int(self.history.numel()), st))
 
     def _step_body(self, with_prev: bool) -> None:
+        if self.chase:
+            self.pregate()
+            self.forward_chase(with_prev)
+            self._advance()
+            return
         if self.cfg.adapters:
             self.pregate()
             self._switch_for_step(with_prev)

@@ -39,11 +39,13 @@ def _oracle_for(eng, llama):
                           rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps, max_seq=cfg.max_seq)
 
 
+@pytest.mark.parametrize("forward_mode", ["chase", "separate"])
 @pytest.mark.parametrize("switch_mode", ["inplace", "from_pristine"])
-def test_decode_steps_against_oracle(llama, switch_mode):
-    cfg = llama.preset("tiny", switch_mode=switch_mode, max_seq=32)
+def test_decode_steps_against_oracle(llama, switch_mode, forward_mode):
+    cfg = llama.preset("tiny", switch_mode=switch_mode, max_seq=32, forward_mode=forward_mode)
     eng = llama.LlamaEngine(cfg, init="host")
     assert eng.table.info()["tensor_path"]
+    assert eng.chase == (forward_mode == "chase")
     ora = _oracle_for(eng, llama)
     pristine = [{n: ora.w["layers"][li][n]["bits"].copy() for n in llama.SEGMENT_NAMES} for li in range(cfg.layers)]
     forced = np.random.Generator(np.random.PCG64(11)).integers(0, cfg.vocab, 10)
@@ -81,8 +83,9 @@ def test_decode_steps_against_oracle(llama, switch_mode):
     assert eng.max_backbone_deviation() < 0.02
 
 
-def test_graph_replay_equals_eager(llama):
-    cfg = llama.preset("tiny", max_seq=48)
+@pytest.mark.parametrize("forward_mode", ["chase", "separate"])
+def test_graph_replay_equals_eager(llama, forward_mode):
+    cfg = llama.preset("tiny", max_seq=48, forward_mode=forward_mode)
     forced = np.random.Generator(np.random.PCG64(12)).integers(0, cfg.vocab, 20)
     a = llama.LlamaEngine(cfg, init="host")
     a.reset(forced=forced)
@@ -101,7 +104,8 @@ def test_graph_replay_equals_eager(llama):
         assert torch.equal(ta.data, tb.data)
 
 
-def test_split_attention_and_pdl_do_not_change_results(llama):
+@pytest.mark.parametrize("forward_mode", ["chase", "separate"])
+def test_split_attention_and_pdl_do_not_change_results(llama, forward_mode):
     """flash-decoding split over CTAs and programmatic dependent launch are schedule changes only."""
     from paper_2603_11873_b200 import _capi
 
@@ -109,7 +113,7 @@ def test_split_attention_and_pdl_do_not_change_results(llama):
     outs = []
     for splits, pdl in ((1, 1), (3, 1), (1, 0), (5, 0)):
         _capi.check(_capi.lib().af_set_pdl(pdl))
-        eng = llama.LlamaEngine(llama.preset("tiny", max_seq=40, attn_splits=splits), init="host")
+        eng = llama.LlamaEngine(llama.preset("tiny", max_seq=40, attn_splits=splits, forward_mode=forward_mode), init="host")
         eng.reset(forced=forced)
         logits = []
         for _ in range(24):
@@ -117,8 +121,13 @@ def test_split_attention_and_pdl_do_not_change_results(llama):
             logits.append(eng.logits.cpu().numpy().copy())
         outs.append((eng.tokens(), np.stack(logits)))
     _capi.check(_capi.lib().af_set_pdl(1))
+    # Split attention reorders f32 sums (1e-7 on the attention output).  In the one-pass forward the
+    # activations enter the tensor pipe as bf16 hi + lo pairs -- x is reproduced to 2^-18, by a
+    # rounding that a 1e-7 change re-rolls -- so bf16 roundings of cached k/v flip more often and
+    # the schedules drift apart faster (still 20x inside the 1e-2 logit criterion).
+    atol = 1e-5 if forward_mode == "separate" else 1e-3
     for toks, lg in outs[1:]:
-        np.testing.assert_allclose(lg, outs[0][1], rtol=1e-4, atol=1e-5)
+        np.testing.assert_allclose(lg, outs[0][1], rtol=1e-4, atol=atol)
     assert outs[2][0] == outs[0][0]          # PDL on/off: bit-identical schedule-independent arithmetic
     assert np.array_equal(outs[2][1], outs[0][1])
 
