@@ -169,6 +169,7 @@ def main():
     ap.add_argument("--switch-mode", default="inplace", choices=["inplace", "from_pristine"])
     ap.add_argument("--compute", default="auto")
     ap.add_argument("--forward-mode", default="auto", choices=["auto", "chase", "separate"])
+    ap.add_argument("--no-chain", action="store_true", help="chase: one launch per projection instead of chained phases")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -202,7 +203,7 @@ def main():
     max_seq = 2 * (args.steps + args.warmup) + 16
     max_seq += 16  # roofline pass of the chase schedule
     cfg = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
-                       compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode)
+                       compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain)
     eng = llama.LlamaEngine(cfg, init="device")
     info = eng.table.info()
     forced = np.random.Generator(np.random.PCG64(cfg.seed + 1)).integers(0, cfg.vocab, 4096)
@@ -271,7 +272,7 @@ def main():
         from paper_2603_11873_b200.adapters import SegmentGroup
 
         fused_events = []
-        orig_sg = SegmentGroup.switch_gemv
+        orig_sg = SegmentGroup.switch_gemv_chain
 
         def instrumented_sg(self, *a, **kw):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -280,12 +281,12 @@ def main():
             e1.record()
             fused_events.append((e0, e1))
 
-        SegmentGroup.switch_gemv = instrumented_sg
+        SegmentGroup.switch_gemv_chain = instrumented_sg
         n_roof = 4
         for _ in range(n_roof):
             api_step()
         torch.cuda.synchronize()
-        SegmentGroup.switch_gemv = orig_sg
+        SegmentGroup.switch_gemv_chain = orig_sg
         per_launch = [a.elapsed_time(b) for a, b in fused_events]
         n_per_step = len(per_launch) // n_roof
         fused_ms = [sum(per_launch[i * n_per_step:(i + 1) * n_per_step]) for i in range(n_roof)]   # per token
@@ -381,10 +382,10 @@ def main():
     sw_bytes = cfg.switch_bytes(steady=True)
     achieved = sw_bytes / (switch_ms * 1e-3) / 1e9
     if chase:
-        n_launch = 4 * cfg.layers
+        n_launch = n_per_step
         roof_ms = statistics.mean(fused_ms)
         roof_achieved = sw_bytes / (roof_ms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "switch_mma_kernel<GEMV> (fused switch + GEMV, 4 launches per layer)",
+        roofline = {"bound": "hbm", "kernel": "switch_mma_kernel<GEMV> (fused switch + GEMV; " + ("chained: o -> gate|up -> down -> next q|k|v per launch)" if eng.chase_chained else "one launch per projection)"),
                     "achieved": roof_achieved, "peak": peak, "unit": "GB/s", "frac": roof_achieved / peak,
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)", "launches_per_token": n_launch,
                     "bytes_per_launch": sw_bytes / n_launch, "avg_launch_ms": roof_ms / n_launch,

@@ -249,17 +249,50 @@ int af_step_advance(af_decision* prev_dev, const af_decision* cur_dev, int32_t* 
  *    while the previous kernel of the stream drains; the previous kernel must be one of this
  *    library's decode kernels (they all execute griddepcontrol.wait).
  * af_accum_to_f32 : out = (res ? res : 0) + fix^-1(acc)   (hand-over to af_gemv_fused / lm_head).
- * af_attn_decode_fix : af_attn_decode reading q|k|v from fixed-point accumulators. */
+ * af_attn_decode_fix : af_attn_decode reading q|k|v from fixed-point accumulators.
+ *
+ * Chains: up to 4 projections whose inputs depend on each other's outputs (o -> gate|up -> down ->
+ * next layer's q|k|v) run in ONE launch (af_chain_create / af_switch_gemv_chain).  The weight
+ * stream never stops at a phase boundary -- the tiles of the next projection fill the
+ * shared-memory ring meanwhile; only the consumers wait, on a device counter every CTA bumps when
+ * its partial sums of the phase are out.  phase_done_dev: n_phases - 1 int32 counters, zeroed by
+ * the caller before the launch.  All CTAs of the launch must be co-resident (grid <= SM count, one
+ * CTA per SM; the library sizes it so); a lost CTA raises AF_ECUDA on the table after ~2 s instead
+ * of hanging. */
 #define AF_FIX_SHIFT 40
 typedef struct af_group af_group;
+typedef struct af_gemv_phase {
+    const float* xin;       /* plain input vector, or NULL when acc_in is given                    */
+    const int64_t* acc_in;  /* fixed-point output of an earlier launch / phase                     */
+    const float* res;       /* optional residual added to the input                                */
+    float* h_out;           /* optional: receives h = res + input (the residual stream)            */
+    const float* norm_w;    /* RMSNorm weight (AF_PRO_RMSNORM)                                     */
+    int64_t* acc_out;       /* y_rows accumulators of this phase, zeroed by the caller             */
+    float eps;
+    int32_t prologue;
+} af_gemv_phase;
 int af_group_create(af_table* table, const int32_t* seg_ids, int32_t n, af_group** out);
+/* seg_ids: the phases' segment lists back to back; phase_len[p] segments belong to phase p. */
+int af_chain_create(af_table* table, const int32_t* seg_ids, const int32_t* phase_len, int32_t n_phases,
+                    af_group** out);
 int af_group_destroy(af_group* group);
-int af_group_info(const af_group* group, int32_t* x_len, int32_t* y_rows, int32_t* n_units, int32_t* grid,
-                  int64_t* tiles);
+/* x_len / y_rows: arrays of n_phases entries (4 is always enough). */
+int af_group_info(const af_group* group, int32_t* n_phases, int32_t* x_len, int32_t* y_rows, int32_t* n_units,
+                  int32_t* grid, int64_t* tiles);
+int af_switch_gemv_chain(af_group* group, const af_decision* prev_dev, const af_decision* cur_dev,
+                         int32_t max_k, float scale, int32_t mode, const af_gemv_phase* phases,
+                         int32_t n_phases, int32_t* phase_done_dev, int32_t pdl, void* stream);
 int af_switch_gemv(af_group* group, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k,
                    float scale, int32_t mode, const float* xin, const int64_t* acc_in, const float* res,
                    float* h_out, int32_t prologue, const float* norm_w, float eps, int64_t* acc_out,
                    int32_t pdl, void* stream);
+/* Profiling aid: the next n_launches af_switch_gemv[_chain] launches each write per-CTA
+ * %globaltimer stamps (grid x AF_TIMELINE_SLOTS uint64: entry, plan ready, first slab, pdl wait
+ * passed, first/last W load issued, storer done, consumers done, then per phase: wait begins,
+ * barrier passed, prologue done, first tile computed; then %smid) to buffer_dev + i * stride_elems.
+ * buffer_dev == NULL turns the probe off. */
+#define AF_TIMELINE_SLOTS 26
+int af_set_timeline(uint64_t* buffer_dev, int32_t n_launches, int64_t stride_elems);
 int af_accum_to_f32(const int64_t* acc, const float* res, float* out, int32_t n, void* stream);
 int af_attn_decode_fix(const int64_t* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,
                        const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,

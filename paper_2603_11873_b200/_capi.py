@@ -67,6 +67,21 @@ class SegmentDesc(ctypes.Structure):
     ]
 
 
+class GemvPhase(ctypes.Structure):
+    """`af_gemv_phase`: one projection of a chained switch + GEMV launch."""
+
+    _fields_ = [
+        ("xin", ctypes.c_void_p),
+        ("acc_in", ctypes.c_void_p),
+        ("res", ctypes.c_void_p),
+        ("h_out", ctypes.c_void_p),
+        ("norm_w", ctypes.c_void_p),
+        ("acc_out", ctypes.c_void_p),
+        ("eps", ctypes.c_float),
+        ("prologue", ctypes.c_int32),
+    ]
+
+
 assert ctypes.sizeof(Decision) == 128
 
 _vp = ctypes.c_void_p
@@ -103,8 +118,11 @@ SIGNATURES = {
     "af_step_advance": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp]),
     "af_group_create": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_vp)]),
     "af_group_destroy": (ctypes.c_int, [_vp]),
-    "af_group_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
+    "af_chain_create": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _i32, ctypes.POINTER(_vp)]),
+    "af_group_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
+    "af_switch_gemv_chain": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, ctypes.POINTER(GemvPhase), _i32, _vp, _i32, _vp]),
     "af_switch_gemv": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _i32, _vp]),
+    "af_set_timeline": (ctypes.c_int, [_vp, _i32, _i64]),
     "af_accum_to_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp]),
     "af_attn_decode_fix": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }

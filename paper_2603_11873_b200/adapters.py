@@ -336,49 +336,77 @@ class SegmentGroup:
     """Segments of a `SwitchTable` that share one input vector (q|k|v, gate|up, or one matrix):
     the unit of the fused switch + GEMV launch (include/adafuse_b200.h `af_switch_gemv`).  The
     switch of adapters.py:236-258 and the backbone GEMV of model.py:288 over the same weights
-    become one pass: every tile is merged, rounded, multiplied with x and written back."""
+    become one pass: every tile is merged, rounded, multiplied with x and written back.
+
+    `seg_ids` may also be a list of lists: a CHAIN of up to four such groups whose inputs depend
+    on each other's outputs, run as one launch (`switch_gemv_chain`)."""
 
     PROLOGUES = {"none": _capi.AF_PRO_NONE, "rmsnorm": _capi.AF_PRO_RMSNORM, "silu_mul": _capi.AF_PRO_SILU_MUL}
 
     def __init__(self, table: SwitchTable, seg_ids):
         import ctypes
 
-        ids = [int(i) for i in seg_ids]
-        arr = (ctypes.c_int32 * len(ids))(*ids)
+        seg_ids = list(seg_ids)
+        phases = [list(p) for p in seg_ids] if seg_ids and isinstance(seg_ids[0], (list, tuple, range)) else [seg_ids]
+        ids = [int(i) for p in phases for i in p]
+        arr = (ctypes.c_int32 * max(1, len(ids)))(*ids)
+        lens = (ctypes.c_int32 * len(phases))(*[len(p) for p in phases])
         handle = ctypes.c_void_p()
-        _capi.check(_capi.lib().af_group_create(table.device_table.handle, arr, len(ids), ctypes.byref(handle)))
+        _capi.check(_capi.lib().af_chain_create(table.device_table.handle, arr, lens, len(phases), ctypes.byref(handle)))
         self.handle = handle
         self.table = table  # keeps the af_table (and the tensors it points at) alive
-        x_len, y_rows, n_units, grid, tiles = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
-        _capi.check(_capi.lib().af_group_info(handle, ctypes.byref(x_len), ctypes.byref(y_rows), ctypes.byref(n_units),
-                                              ctypes.byref(grid), ctypes.byref(tiles)))
-        self.x_len, self.y_rows, self.n_units, self.grid, self.tiles = x_len.value, y_rows.value, n_units.value, grid.value, tiles.value
+        n_ph, n_units, grid, tiles = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+        x_len, y_rows = (ctypes.c_int32 * 4)(), (ctypes.c_int32 * 4)()
+        _capi.check(_capi.lib().af_group_info(handle, ctypes.byref(n_ph), x_len, y_rows, ctypes.byref(n_units), ctypes.byref(grid),
+                                              ctypes.byref(tiles)))
+        self.n_phases = n_ph.value
+        self.x_lens, self.y_rows_all = list(x_len)[: self.n_phases], list(y_rows)[: self.n_phases]
+        self.x_len, self.y_rows = self.x_lens[0], self.y_rows_all[0]
+        self.n_units, self.grid, self.tiles = n_units.value, grid.value, tiles.value
 
-    def switch_gemv(self, prev, cur, acc_out, *, xin=None, acc_in=None, res=None, h_out=None, prologue="none", norm_w=None,
-                    eps: float = 0.0, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace", pdl: bool = False) -> None:
-        """acc_out (int64, zeroed by the caller) += fix(W_new . prologue(h)); W <- W_new in place."""
-        if mode not in _MODES:
-            raise ValueError(f"unknown switch mode {mode!r}")
+    def _phase_struct(self, ph: int, acc_out, xin=None, acc_in=None, res=None, h_out=None, prologue="none", norm_w=None, eps: float = 0.0):
         if prologue not in self.PROLOGUES:
             raise ValueError(f"unknown prologue {prologue!r}")
-        for dec in (prev, cur):
-            if dec is not None and not isinstance(dec, DeviceDecision):
-                raise TypeError("the fused switch + GEMV takes device-resident decisions (DeviceDecision) or None")
-        need = self.x_len * (2 if prologue == "silu_mul" else 1)
-        for name, t, dt, n in (("xin", xin, torch.float32, need), ("acc_in", acc_in, torch.int64, need), ("res", res, torch.float32, self.x_len),
-                               ("h_out", h_out, torch.float32, self.x_len), ("norm_w", norm_w, torch.float32, self.x_len),
-                               ("acc_out", acc_out, torch.int64, self.y_rows)):
+        x_len, y_rows = self.x_lens[ph], self.y_rows_all[ph]
+        need = x_len * (2 if prologue == "silu_mul" else 1)
+        for name, t, dt, n in (("xin", xin, torch.float32, need), ("acc_in", acc_in, torch.int64, need), ("res", res, torch.float32, x_len),
+                               ("h_out", h_out, torch.float32, x_len), ("norm_w", norm_w, torch.float32, x_len),
+                               ("acc_out", acc_out, torch.int64, y_rows)):
             if t is None:
                 continue
             if not t.is_cuda:
                 raise DeviceError("operand is not on a CUDA device: the B200 path has no CPU fallback")
             if t.dtype != dt or not t.is_contiguous() or t.numel() < n:
                 raise DimensionError(f"{name} must be a contiguous {dt} vector of at least {n} entries")
-        _capi.check(_capi.lib().af_switch_gemv(
+        p = lambda t: _ptr(t) if t is not None else None  # noqa: E731
+        return _capi.GemvPhase(xin=p(xin), acc_in=p(acc_in), res=p(res), h_out=p(h_out), norm_w=p(norm_w), acc_out=p(acc_out),
+                               eps=float(eps), prologue=self.PROLOGUES[prologue])
+
+    def switch_gemv_chain(self, prev, cur, phases, phase_done=None, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0,
+                          mode: str = "inplace", pdl: bool = False) -> None:
+        """One launch over every phase of the chain.  `phases`: one dict per phase with the keyword
+        arguments of `switch_gemv` (acc_out, xin | acc_in, res, h_out, prologue, norm_w, eps);
+        `phase_done`: int32 tensor of n_phases - 1 zeroed counters."""
+        if mode not in _MODES:
+            raise ValueError(f"unknown switch mode {mode!r}")
+        for dec in (prev, cur):
+            if dec is not None and not isinstance(dec, DeviceDecision):
+                raise TypeError("the fused switch + GEMV takes device-resident decisions (DeviceDecision) or None")
+        if len(phases) != self.n_phases:
+            raise DimensionError(f"chain has {self.n_phases} phases, got {len(phases)} descriptions")
+        if self.n_phases > 1:
+            if phase_done is None or phase_done.dtype != torch.int32 or not phase_done.is_cuda or phase_done.numel() < self.n_phases - 1:
+                raise DimensionError("phase_done must be a CUDA int32 tensor of n_phases - 1 zeroed counters")
+        structs = (_capi.GemvPhase * self.n_phases)(*[self._phase_struct(i, **ph) for i, ph in enumerate(phases)])
+        _capi.check(_capi.lib().af_switch_gemv_chain(
             self.handle, prev.ptr if prev is not None else None, cur.ptr if cur is not None else None, int(max_k), float(scale),
-            _MODES[mode], _ptr(xin) if xin is not None else None, _ptr(acc_in) if acc_in is not None else None,
-            _ptr(res) if res is not None else None, _ptr(h_out) if h_out is not None else None, self.PROLOGUES[prologue],
-            _ptr(norm_w) if norm_w is not None else None, float(eps), _ptr(acc_out), 1 if pdl else 0, _capi.stream_ptr()))
+            _MODES[mode], structs, self.n_phases, _ptr(phase_done) if phase_done is not None else None, 1 if pdl else 0,
+            _capi.stream_ptr()))
+
+    def switch_gemv(self, prev, cur, acc_out, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace",
+                    pdl: bool = False, **phase) -> None:
+        """acc_out (int64, zeroed by the caller) += fix(W_new . prologue(h)); W <- W_new in place."""
+        self.switch_gemv_chain(prev, cur, [dict(acc_out=acc_out, **phase)], None, max_k=max_k, scale=scale, mode=mode, pdl=pdl)
 
     def close(self) -> None:
         if getattr(self, "handle", None) is not None and self.handle:
@@ -390,4 +418,3 @@ class SegmentGroup:
             self.close()
         except Exception:
             pass
-

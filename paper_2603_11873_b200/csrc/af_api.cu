@@ -37,6 +37,11 @@ static std::atomic<int> g_gemv_full_sm{[] {
     return (e && e[0] == '1') ? 1 : 0;
 }()};
 
+// Timeline probe of the fused switch + GEMV launches (af_set_timeline): launch i of the probed
+// sequence writes its per-CTA stamps to buffer + i * stride.
+static unsigned long long* g_timeline = nullptr;
+static int g_timeline_left = 0;
+static long long g_timeline_stride = 0;
 static const bool g_force_hilo = [] { const char* e = getenv("AF_FORCE_HILO"); return e && e[0] == '1'; }();
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline size_t esize(int dtype) { return dtype == AF_BF16 ? 2 : 4; }
@@ -125,7 +130,8 @@ struct af_group {
     UnitDev* d_units = nullptr;
     int n_units = 0, grid = 0;
     int* d_seg_yoff = nullptr;
-    int x_len = 0, y_rows = 0;
+    int n_phases = 1;
+    int x_len[kMaxPhases] = {0, 0, 0, 0}, y_rows[kMaxPhases] = {0, 0, 0, 0};
     long long tiles = 0;
 };
 
@@ -376,14 +382,14 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     if constexpr (GEMV) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(kMmaThreads);
+        cfg.blockDim = dim3(kMmaThreadsGemv);
         cfg.dynamicSmemBytes = L::total;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = mp2.gv.pdl ? 1 : 0;
+        cfg.numAttrs = mp2.pdl ? 1 : 0;
         AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_mma_kernel<KS, BA, GEMV>, mp2));
     } else {
         switch_mma_kernel<KS, BA, GEMV><<<grid, kMmaThreads, L::total, st>>>(mp2);
@@ -590,72 +596,86 @@ int af_group_destroy(af_group* g) {
     return AF_OK;
 }
 
-int af_group_create(af_table* t, const int32_t* seg_ids, int32_t n, af_group** out) {
+int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_len, int32_t n_phases, af_group** out) {
     if (!out) return fail(AF_EVALUE, "out is NULL");
     *out = nullptr;
-    if (!t || !seg_ids || n < 1) return fail(AF_EDIM, "segment group is empty");
+    if (!t || !seg_ids || !phase_len || n_phases < 1) return fail(AF_EDIM, "segment group is empty");
+    if (n_phases > kMaxPhases) return fail(AF_EVALUE, "a chain holds at most 4 phases");
     if (!t->fast_mma)
         return fail(AF_EPRECISION, "the fused switch + GEMV needs the tensor path: bf16 targets and factors, rank % 8 == 0, "
                                    "16-byte aligned rows");
     std::vector<int> yoff(t->n_segments, 0);
     std::vector<char> seen(t->n_segments, 0);
-    int x_len = -1, rows = 0;
-    for (int i = 0; i < n; ++i) {
-        const int sidx = seg_ids[i];
-        if (sidx < 0 || sidx >= t->n_segments) return fail(AF_EINDEX, "segment id outside the table");
-        if (seen[sidx]) return fail(AF_EALIAS, "segment listed twice in one group");
-        seen[sidx] = 1;
-        const af_segment_desc& sd = t->segs[sidx];
-        if (sd.d_out < 1 || sd.d_in < 1) return fail(AF_EDIM, "empty segment in a GEMV group");
-        if (x_len < 0) x_len = sd.d_in;
-        if (sd.d_in != x_len) return fail(AF_EDIM, "segments of one group must share d_in (one input vector)");
-        yoff[sidx] = rows;
-        rows += sd.d_out;
-    }
     af_group* g = new af_group();
     g->table = t;
+    g->n_phases = n_phases;
+    int n = 0;
+    for (int ph = 0; ph < n_phases; ++ph) {
+        if (phase_len[ph] < 1) { delete g; return fail(AF_EDIM, "segment group is empty"); }
+        int x_len = -1, rows = 0;
+        for (int i = 0; i < phase_len[ph]; ++i) {
+            const int sidx = seg_ids[n + i];
+            int rc = AF_OK;
+            if (sidx < 0 || sidx >= t->n_segments) rc = fail(AF_EINDEX, "segment id outside the table");
+            else if (seen[sidx]) rc = fail(AF_EALIAS, "segment listed twice in one group");
+            else if (t->segs[sidx].d_out < 1 || t->segs[sidx].d_in < 1) rc = fail(AF_EDIM, "empty segment in a GEMV group");
+            else if (x_len >= 0 && t->segs[sidx].d_in != x_len)
+                rc = fail(AF_EDIM, "segments of one group must share d_in (one input vector)");
+            if (rc) { delete g; return rc; }
+            seen[sidx] = 1;
+            x_len = t->segs[sidx].d_in;
+            yoff[sidx] = rows;
+            rows += t->segs[sidx].d_out;
+        }
+        g->x_len[ph] = x_len;
+        g->y_rows[ph] = rows;
+        n += phase_len[ph];
+    }
     g->segs.assign(seg_ids, seg_ids + n);
-    g->x_len = x_len;
-    g->y_rows = rows;
-    // ---- schedule: the group's tiles in (segment, column strip, row tile) order, cut into one
-    //      contiguous span per CTA: every SM streams the same number of tiles (+-1) and restages
-    //      the DOWN slab only when its span crosses into another strip ----
-    const int strips = (x_len + kTN - 1) / kTN;
-    long long total = 0;
-    for (int i = 0; i < n; ++i) total += (long long)strips * ((t->segs[seg_ids[i]].d_out + kMR - 1) / kMR);
-    g->tiles = total;
-    const int G = (int)std::min<long long>(total, std::max(1, t->sm_count));
+    // ---- schedule: per phase, the tiles in (segment, column strip, row tile) order cut into one
+    //      contiguous span per CTA -- every SM streams the same number of tiles (+-1) and restages
+    //      the DOWN slab only when its span crosses into another strip.  A CTA's spans of all phases
+    //      are concatenated into its unit list. ----
+    const int G = std::max(1, t->sm_count);
     std::vector<std::vector<UnitDev>> per_cta(G);
-    {
+    int used = 0, first = 0;
+    for (int ph = 0; ph < n_phases; ++ph) {
+        const int strips = (g->x_len[ph] + kTN - 1) / kTN;
+        long long total = 0;
+        for (int i = 0; i < phase_len[ph]; ++i) total += (long long)strips * ((t->segs[seg_ids[first + i]].d_out + kMR - 1) / kMR);
+        g->tiles += total;
+        const int Gp = (int)std::min<long long>(total, G);   // CTA 0 always owns tiles of every phase (it writes h_out)
+        used = std::max(used, Gp);
         int cta = 0;
-        long long idx = 0;                      // linear tile index
-        long long cta_end = total * 1 / G;      // end of CTA 0's span
-        for (int i = 0; i < n; ++i) {
-            const int sidx = seg_ids[i];
+        long long idx = 0, cta_end = total / Gp;
+        for (int i = 0; i < phase_len[ph]; ++i) {
+            const int sidx = seg_ids[first + i];
             const int d_out = t->segs[sidx].d_out;
             const int rt = (d_out + kMR - 1) / kMR;
             for (int sp = 0; sp < strips; ++sp) {
-                int r = 0;  // row tile inside the strip
+                int r = 0;
                 while (r < rt) {
-                    while (idx >= cta_end && cta < G - 1) {
+                    while (idx >= cta_end && cta < Gp - 1) {
                         ++cta;
-                        cta_end = total * (cta + 1) / G;
+                        cta_end = total * (cta + 1) / Gp;
                     }
                     const int take = (int)std::min<long long>(rt - r, cta_end - idx);
                     const int row0 = r * kMR;
-                    per_cta[cta].push_back({sidx, row0, std::min(take * kMR, d_out - row0), sp * kTN});
+                    per_cta[cta].push_back({sidx, row0, std::min(take * kMR, d_out - row0), sp * kTN, ph});
                     r += take;
                     idx += take;
                 }
             }
         }
+        first += phase_len[ph];
     }
+    const int grid = used;
     size_t depth = 0;
     for (auto& v : per_cta) depth = std::max(depth, v.size());
-    std::vector<UnitDev> units(depth * G, UnitDev{0, 0, 0, 0});
-    for (int c = 0; c < G; ++c)
-        for (size_t j = 0; j < per_cta[c].size(); ++j) units[j * G + c] = per_cta[c][j];
-    g->grid = G;
+    std::vector<UnitDev> units(depth * grid, UnitDev{0, 0, 0, 0, 0});
+    for (int c = 0; c < grid; ++c)
+        for (size_t j = 0; j < per_cta[c].size(); ++j) units[j * grid + c] = per_cta[c][j];
+    g->grid = grid;
     g->n_units = (int)units.size();
     cudaError_t e = cudaMalloc(&g->d_units, sizeof(UnitDev) * units.size());
     if (e == cudaSuccess) e = cudaMemcpy(g->d_units, units.data(), sizeof(UnitDev) * units.size(), cudaMemcpyHostToDevice);
@@ -669,31 +689,47 @@ int af_group_create(af_table* t, const int32_t* seg_ids, int32_t n, af_group** o
     return AF_OK;
 }
 
-int af_group_info(const af_group* g, int32_t* x_len, int32_t* y_rows, int32_t* n_units, int32_t* grid, int64_t* tiles) {
+int af_group_create(af_table* t, const int32_t* seg_ids, int32_t n, af_group** out) {
+    return af_chain_create(t, seg_ids, &n, 1, out);
+}
+
+int af_group_info(const af_group* g, int32_t* n_phases, int32_t* x_len, int32_t* y_rows, int32_t* n_units, int32_t* grid,
+                  int64_t* tiles) {
     if (!g) return fail(AF_EVALUE, "group is NULL");
-    if (x_len) *x_len = g->x_len;
-    if (y_rows) *y_rows = g->y_rows;
+    if (n_phases) *n_phases = g->n_phases;
+    for (int ph = 0; ph < g->n_phases; ++ph) {
+        if (x_len) x_len[ph] = g->x_len[ph];
+        if (y_rows) y_rows[ph] = g->y_rows[ph];
+    }
     if (n_units) *n_units = g->n_units;
     if (grid) *grid = g->grid;
     if (tiles) *tiles = g->tiles;
     return AF_OK;
 }
 
-int af_switch_gemv(af_group* g, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k, float scale,
-                   int32_t mode, const float* xin, const int64_t* acc_in, const float* res, float* h_out, int32_t prologue,
-                   const float* norm_w, float eps, int64_t* acc_out, int32_t pdl, void* stream) {
+int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k, float scale,
+                         int32_t mode, const af_gemv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t pdl,
+                         void* stream) {
     if (!g) return fail(AF_EVALUE, "group is NULL");
     af_table* t = g->table;
     if (mode != AF_SWITCH_INPLACE && mode != AF_SWITCH_FROM_PRISTINE) return fail(AF_EVALUE, "unknown switch mode");
     if (mode == AF_SWITCH_FROM_PRISTINE && !t->has_pristine)
         return fail(AF_ESTATE, "FROM_PRISTINE needs a pristine copy of every segment");
-    if (prologue < AF_PRO_NONE || prologue > AF_PRO_SILU_MUL) return fail(AF_EVALUE, "unknown prologue");
-    if (prologue == AF_PRO_RMSNORM && !norm_w) return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
-    if ((xin == nullptr) == (acc_in == nullptr)) return fail(AF_EVALUE, "exactly one of xin / acc_in must be given");
-    if (!acc_out) return fail(AF_EVALUE, "acc_out is NULL");
-    if (reinterpret_cast<uintptr_t>(acc_out) % 8 != 0 || reinterpret_cast<uintptr_t>(acc_in) % 8 != 0)
-        return fail(AF_EDIM, "fixed-point accumulators must be 8-byte aligned");
-    if (h_out && (h_out == xin || h_out == res)) return fail(AF_EALIAS, "h_out aliases an input vector");
+    if (!phases || n_phases != g->n_phases) return fail(AF_EDIM, "one af_gemv_phase per phase of the chain");
+    if (n_phases > 1 && !phase_done_dev) return fail(AF_EVALUE, "a chain of several phases needs its phase_done counters");
+    for (int ph = 0; ph < n_phases; ++ph) {
+        const af_gemv_phase& f = phases[ph];
+        if (f.prologue < AF_PRO_NONE || f.prologue > AF_PRO_SILU_MUL) return fail(AF_EVALUE, "unknown prologue");
+        if (f.prologue == AF_PRO_RMSNORM && !f.norm_w) return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
+        if ((f.xin == nullptr) == (f.acc_in == nullptr)) return fail(AF_EVALUE, "exactly one of xin / acc_in must be given");
+        if (!f.acc_out) return fail(AF_EVALUE, "acc_out is NULL");
+        if (reinterpret_cast<uintptr_t>(f.acc_out) % 8 != 0 || reinterpret_cast<uintptr_t>(f.acc_in) % 16 != 0)
+            return fail(AF_EDIM, "fixed-point accumulators must be 8-byte aligned (16-byte as an input)");
+        if (reinterpret_cast<uintptr_t>(f.xin) % 8 != 0 || reinterpret_cast<uintptr_t>(f.res) % 8 != 0 ||
+            reinterpret_cast<uintptr_t>(f.h_out) % 8 != 0 || g->x_len[ph] % 2 != 0)
+            return fail(AF_EDIM, "input vectors must be 8-byte aligned and of even length");
+        if (f.h_out && (f.h_out == f.xin || f.h_out == f.res)) return fail(AF_EALIAS, "h_out aliases an input vector");
+    }
     const bool use_dev = prev_dev || cur_dev;
     if (use_dev && (max_k < 1 || max_k > AF_MAX_K)) return fail(AF_EVALUE, "max_k outside [1, AF_MAX_K]");
     const bool from_pristine = mode == AF_SWITCH_FROM_PRISTINE;
@@ -719,26 +755,64 @@ int af_switch_gemv(af_group* g, const af_decision* prev_dev, const af_decision* 
     mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 3 : 2) * S;
     mp.tmaps_st = t->d_maps + (size_t)2 * S;
     mp.tmaps_up = t->d_maps + (size_t)4 * S;
-    mp.gv.xin = xin;
-    mp.gv.acc_in = reinterpret_cast<const long long*>(acc_in);
-    mp.gv.res = res;
-    mp.gv.h_out = h_out;
-    mp.gv.norm_w = norm_w;
-    mp.gv.eps = eps;
-    mp.gv.prologue = prologue;
-    mp.gv.x_len = g->x_len;
-    mp.gv.acc_out = reinterpret_cast<unsigned long long*>(acc_out);
-    mp.gv.seg_yoff = g->d_seg_yoff;
-    mp.gv.pdl = (pdl && g_pdl.load()) ? 1 : 0;
+    for (int ph = 0; ph < n_phases; ++ph) {
+        const af_gemv_phase& f = phases[ph];
+        GemvParams& gv = mp.gv[ph];
+        gv.xin = f.xin;
+        gv.acc_in = reinterpret_cast<const long long*>(f.acc_in);
+        gv.res = f.res;
+        gv.h_out = f.h_out;
+        gv.norm_w = f.norm_w;
+        gv.eps = f.eps;
+        gv.prologue = f.prologue;
+        gv.x_len = g->x_len[ph];
+        gv.acc_out = reinterpret_cast<unsigned long long*>(f.acc_out);
+    }
+    mp.n_phases = n_phases;
+    mp.phase_done = phase_done_dev;
+    mp.seg_yoff = g->d_seg_yoff;
+    mp.pdl = (pdl && g_pdl.load()) ? 1 : 0;
+    static const int env_dbg = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
+    mp.dbg = env_dbg;
+    if (g_timeline && g_timeline_left > 0) {
+        mp.timeline = g_timeline;
+        g_timeline += g_timeline_stride;
+        --g_timeline_left;
+    }
     const int ks = std::max(1, (s_bound + 15) / 16);
     const bool ba = t->rank16 && ks > 2 && !g_force_hilo;
     cudaStream_t st = as_stream(stream);
+    if (env_dbg & 4) {  // experiment: the plain switch kernel on this group's schedule (no GEMV at all)
+        if (ks == 2) return launch_mma<2, false, false>(mp, g->grid, st);
+    }
     switch (ks) {
         case 1: return launch_mma<1, false, true>(mp, g->grid, st);
         case 2: return launch_mma<2, false, true>(mp, g->grid, st);
         case 3: return ba ? launch_mma<3, true, true>(mp, g->grid, st) : launch_mma<3, false, true>(mp, g->grid, st);
         default: return ba ? launch_mma<4, true, true>(mp, g->grid, st) : launch_mma<4, false, true>(mp, g->grid, st);
     }
+}
+
+int af_switch_gemv(af_group* g, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k, float scale,
+                   int32_t mode, const float* xin, const int64_t* acc_in, const float* res, float* h_out, int32_t prologue,
+                   const float* norm_w, float eps, int64_t* acc_out, int32_t pdl, void* stream) {
+    af_gemv_phase f{};
+    f.xin = xin;
+    f.acc_in = acc_in;
+    f.res = res;
+    f.h_out = h_out;
+    f.norm_w = norm_w;
+    f.acc_out = acc_out;
+    f.eps = eps;
+    f.prologue = prologue;
+    return af_switch_gemv_chain(g, prev_dev, cur_dev, max_k, scale, mode, &f, 1, nullptr, pdl, stream);
+}
+
+int af_set_timeline(uint64_t* buffer_dev, int32_t n_launches, int64_t stride_elems) {
+    g_timeline = reinterpret_cast<unsigned long long*>(buffer_dev);
+    g_timeline_left = buffer_dev ? n_launches : 0;
+    g_timeline_stride = stride_elems;
+    return AF_OK;
 }
 
 int af_accum_to_f32(const int64_t* acc, const float* res, float* out, int32_t n, void* stream) {

@@ -43,6 +43,7 @@ struct SegDev {
 // One work unit: rows [row0, row0+rows) x cols [col0, col0+kTN) of segment `seg`.
 struct UnitDev {
     int seg, row0, rows, col0;
+    int phase;  // chained switch + GEMV launches: which projection of the chain the unit belongs to
 };
 
 struct Plan {

@@ -44,6 +44,7 @@ constexpr int kMmaConsumers = kMmaWarps * 32;     // 512 threads
 constexpr int kWProd = AF_WPROD;                  // W-load producer warps
 constexpr int kStorers = AF_STORERS;              // storer warps
 constexpr int kMmaThreads = kMmaConsumers + 32 * (kWProd + 1 + kStorers);  // + W producers + UP producer + storers
+constexpr int kMmaThreadsGemv = kMmaThreads + 32;                          // + the reducer warp of the fused GEMV
 constexpr int kMmaMaxKS = 4;                      // k-steps of 16 ranks: S <= 64
 constexpr int kMmaMaxStages = 12;
 constexpr int kStoreDepth = 0;                    // tile stores that may still be reading smem
@@ -140,13 +141,25 @@ struct GemvParams {
     int prologue;
     int x_len;                     // d_in of the group
     unsigned long long* acc_out;
-    const int* seg_yoff;           // per table segment: first row of its slice of acc_out
-    int pdl;                       // launched with programmatic stream serialization
 };
+
+// A launch may chain up to kMaxPhases projections whose inputs depend on each other's outputs
+// (o -> gate|up -> down -> next layer's q|k|v): the weight stream of phase p+1 never waits -- its
+// tiles fill the shared-memory ring while the consumers sit at the phase boundary -- only the
+// GEMV input does: consumers spin on a device counter that every CTA's storer bumps once its
+// last partial sums of phase p are out (a grid barrier the producers do not take part in).
+constexpr int kMaxPhases = 4;
 
 struct MmaParams {
     SwitchParams base;
-    GemvParams gv;
+    GemvParams gv[kMaxPhases];
+    int n_phases;
+    int* phase_done;               // [n_phases - 1] counters, zeroed by the caller per launch
+    const int* seg_yoff;           // per table segment: first row of its slice of its phase's acc_out
+    int pdl;                       // launched with programmatic stream serialization
+    // optional timeline probe (af_set_timeline): [gridDim.x][kTlSlots] globaltimer stamps of this launch
+    unsigned long long* timeline;
+    int dbg;                       // experiments (env AF_DBG): 4 = plain switch kernel on the group schedule
     const CUtensorMap* tmaps_ld;   // per segment: 32 x 64 swizzled box on the source (live or pristine)
     const CUtensorMap* tmaps_st;   // per segment: the same box shape on the live matrix
     const CUtensorMap* tmaps_up;   // per segment: UP bank as [N * d_out][rank], box 32 rows x rank, swizzle = row bytes
@@ -232,17 +245,31 @@ __host__ __device__ __forceinline__ bool up_swizzled(int rank) { return rank == 
 //                shared memory (store_depth newer stores may still be draining)
 // ---- pieces of the fused GEMV (GEMV = true) ----
 
+// Timeline probe slots (nanoseconds of %globaltimer), one row per CTA:
+//   0 entry | 1 plan ready | 2 first slab staged | 3 pdl_wait passed | 4 first W load issued |
+//   5 last W load issued | 6 storer done | 7 consumers done |
+//   8 + 4 * phase: barrier wait begins | +1 barrier passed | +2 prologue done | +3 first tile of the phase computed
+constexpr int kTlSlots = 8 + 4 * 4 + 2;  // + [24] = %smid, [25] = tiles of this CTA
+__device__ __forceinline__ void tl_stamp(unsigned long long* tl, int slot) {
+    if (tl) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tl[(size_t)blockIdx.x * kTlSlots + slot] = t;
+    }
+}
+
 // One element of the un-normalised input h (see GemvParams).
+// (inputs may have been produced by other CTAs earlier in this very launch: read through L2)
 __device__ __forceinline__ float gemv_h(const GemvParams& g, int c) {
-    float h = g.acc_in ? fix_to_f32(g.acc_in[c]) : g.xin[c];
-    if (g.res) h += g.res[c];
+    float h = g.acc_in ? fix_to_f32(__ldcg(g.acc_in + c)) : __ldcg(g.xin + c);
+    if (g.res) h += __ldcg(g.res + c);
     return h;
 }
 // One element of the projection's input vector x; inv = rsqrt(mean(h^2) + eps) for RMSNORM.
 __device__ __forceinline__ float gemv_x(const GemvParams& g, int c, float inv) {
     if (g.prologue == AF_PRO_SILU_MUL) {
-        const float a = g.acc_in ? fix_to_f32(g.acc_in[c]) : g.xin[c];
-        const float b = g.acc_in ? fix_to_f32(g.acc_in[g.x_len + c]) : g.xin[g.x_len + c];
+        const float a = g.acc_in ? fix_to_f32(__ldcg(g.acc_in + c)) : __ldcg(g.xin + c);
+        const float b = g.acc_in ? fix_to_f32(__ldcg(g.acc_in + g.x_len + c)) : __ldcg(g.xin + g.x_len + c);
         return a / (1.0f + expf(-a)) * b;
     }
     float h = gemv_h(g, c);
@@ -269,9 +296,8 @@ __device__ __forceinline__ void gemv_x_fragment(const GemvParams& g, int col0, i
 }
 
 template <int KS, bool BA, bool GEMV>
-__global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
+__global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
     using L = MmaLayout<KS, BA, GEMV>;
-    static_assert(!GEMV || kStorers == 1, "the fused GEMV reduces a tile's partial sums in the single storer warp");
     constexpr int kSt = L::stages < kMmaDefaultStages ? L::stages : kMmaDefaultStages;
     extern __shared__ unsigned char smem_dyn[];
     const SwitchParams& p = mp.base;
@@ -284,10 +310,18 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     const int tid = threadIdx.x;
 
     if (tid == 0) {
+        if constexpr (GEMV) {
+            tl_stamp(mp.timeline, 0);
+            if (mp.timeline) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                mp.timeline[(size_t)blockIdx.x * kTlSlots + 24] = smid;
+            }
+        }
         for (int s = 0; s < kSt; ++s) {
             mbar_init(&full[s], kWProd + 1);
             mbar_init(&computed[s], kMmaWarps);
-            mbar_init(&empty[s], kStorers);
+            mbar_init(&empty[s], kStorers + (GEMV ? 1 : 0));
         }
         fence_mbar_init();
         if (p.use_dev)
@@ -295,6 +329,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
         else
             plan = p.host_plan;
         if (!plan_usable(p, plan, p.prev_dev, p.cur_dev)) plan.n_blocks = -1;
+        if constexpr (GEMV) tl_stamp(mp.timeline, 1);
     }
     __syncthreads();
     const int n_blocks = plan.n_blocks;
@@ -326,6 +361,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
 #pragma unroll
                 for (int j = 0; j < kMine; ++j) mine += (who + j * kWProd < kBoxes) ? 1 : 0;
                 mbar_expect_tx(&full[stage], mine * kBoxBytes);
+                if constexpr (GEMV) {
+                    if (who == 0 && it == 0) tl_stamp(mp.timeline, 4);
+                }
                 const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
 #pragma unroll
                 for (int j = 0; j < kMine; ++j) {
@@ -335,6 +373,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                                          &full[stage]);
                 }
                 ti.next(p);
+            }
+            if constexpr (GEMV) {
+                if (who == 0) tl_stamp(mp.timeline, 5);
             }
         }
         return;
@@ -377,25 +418,19 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
         }
         return;
     }
-    if (warp > kMmaWarps + kWProd) {
+    if (warp > kMmaWarps + kWProd && warp <= kMmaWarps + kWProd + kStorers) {
         // ============ storers: boxes back to global, then hand the stage back ============
-        // GEMV: the whole warp also adds the 16 consumer warps' partial dot products of the tile
-        // (fixed order) and accumulates the 32 row sums into the launch's fixed-point vector.
-        if (lane == 0 || GEMV) {
+        if (lane == 0) {
             const int who = warp - (kMmaWarps + kWProd + 1);
             constexpr int kMine = (kBoxes + kStorers - 1) / kStorers;
             MmaIter ti;
             ti.init(p);
             int it = 0;
-            int cur_seg = -1, yoff = 0;
-            if constexpr (GEMV) {
-                if (mp.gv.pdl) pdl_wait();  // acc_out may still be read by an earlier kernel of the chain
-            }
             for (; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
                 mbar_wait(&computed[stage], ph);
-                if (lane == 0 && store_w) {
+                if (store_w) {
                     const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
 #pragma unroll
                     for (int j = 0; j < kMine; ++j) {
@@ -405,33 +440,68 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
                     }
                     bulk_commit();
                 }
-                if constexpr (GEMV) {
-                    if (ti.un.seg != cur_seg) {
-                        cur_seg = ti.un.seg;
-                        yoff = mp.gv.seg_yoff[cur_seg];
-                    }
-                    const float* part = reinterpret_cast<const float*>(sm + L::off_part + stage * L::part_stage_bytes);
-                    float sum = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kMmaWarps; ++w) sum += part[w * kMR + lane];
-                    if (ti.m0 + lane < ti.row_end)
-                        atomicAdd(mp.gv.acc_out + yoff + ti.m0 + lane, (unsigned long long)f32_to_fix(sum));
-                    __syncwarp();  // every lane has read the stage's partials before it is handed back
-                }
-                if (lane == 0) {
-                    // the stores of tile it - depth have drained their stage: hand it back
-                    const int depth = mp.store_depth;
-                    if (depth <= 0) bulk_wait_read<0>();
-                    else if (depth == 1) bulk_wait_read<1>();
-                    else if (depth == 2) bulk_wait_read<2>();
-                    else bulk_wait_read<3>();
-                    if (it >= depth) mbar_arrive(&empty[(it - depth) % kSt]);
-                }
+                // the stores of tile it - depth have drained their stage: hand it back
+                const int depth = mp.store_depth;
+                if (depth <= 0) bulk_wait_read<0>();
+                else if (depth == 1) bulk_wait_read<1>();
+                else if (depth == 2) bulk_wait_read<2>();
+                else bulk_wait_read<3>();
+                if (it >= depth) mbar_arrive(&empty[(it - depth) % kSt]);
                 ti.next(p);
             }
-            if (lane == 0) bulk_wait_all<0>();  // global writes complete before the CTA retires
+            bulk_wait_all<0>();  // global writes complete before the CTA retires
+            if constexpr (GEMV) tl_stamp(mp.timeline, 6);
         }
         return;
+    }
+    if constexpr (GEMV) {
+        if (warp > kMmaWarps + kWProd + kStorers) {
+            // ============ reducer (GEMV only): adds the 16 consumer warps' partial dot products of a
+            // tile in a fixed order and accumulates the 32 row sums into the phase's fixed-point
+            // vector; publishes a finished phase of a chain.  Its own warp, so that neither the
+            // stores nor the consumers wait for the shared-memory reads and the atomics. ============
+            MmaIter ti;
+            ti.init(p);
+            int cur_seg = -1, yoff = 0, cur_phase = 0;
+            unsigned long long* acc_out = nullptr;
+            // phases [from, to) of the chain are complete on this CTA: publish (the atomics of every
+            // lane are ordered before lane 0's fence by the __syncwarp)
+            auto phases_done = [&](int from, int to) {
+                __syncwarp();
+                if (lane == 0 && from < to) {
+                    __threadfence();
+                    for (int ph = from; ph < to && ph < mp.n_phases - 1; ++ph) atomicAdd(mp.phase_done + ph, 1);
+                }
+            };
+            if (mp.pdl) pdl_wait();  // acc_out may still be read by an earlier kernel of the chain
+            for (int it = 0; ti.valid(p); ++it) {
+                const int stage = it % kSt;
+                const uint32_t ph = (it / kSt) & 1;
+                // publish finished phases BEFORE waiting for the next phase's first tile: its
+                // consumers are waiting for exactly this
+                if (ti.un.phase != cur_phase) {
+                    phases_done(cur_phase, ti.un.phase);
+                    cur_phase = ti.un.phase;
+                }
+                if (ti.un.seg != cur_seg) {
+                    cur_seg = ti.un.seg;
+                    yoff = mp.seg_yoff[cur_seg];
+                    acc_out = mp.gv[cur_phase].acc_out;
+                }
+                mbar_wait(&computed[stage], ph);
+                const float* part = reinterpret_cast<const float*>(sm + L::off_part + stage * L::part_stage_bytes);
+                float sum = 0.f;
+#pragma unroll
+                for (int w = 0; w < kMmaWarps; ++w) sum += part[w * kMR + lane];
+                if (ti.m0 + lane < ti.row_end)
+                    atomicAdd(acc_out + yoff + ti.m0 + lane, (unsigned long long)f32_to_fix(sum));
+                __syncwarp();  // every lane has read the stage's partials before it is handed back
+                if (lane == 0) mbar_arrive(&empty[stage]);
+                ti.next(p);
+            }
+            phases_done(cur_phase, mp.n_phases - 1);
+            return;
+        }
     }
 
     // ================================ consumers ====================================
@@ -451,27 +521,81 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
     down_prefetch<KS>(dn_regs, sg, plan, S, ti.un.col0, tid);
     down_commit<KS, BA>(down_smem, dn_regs, sg.rank, plan, S, tid);
     named_bar_sync(1, kMmaConsumers);  // first slab visible
-    // ---- GEMV prologue: everything above (and the W ring the producers are filling) is
-    //      independent of the previous kernel; the input vector is not ----
+    // ---- GEMV: everything above (and the W ring the producers are filling) is independent of the
+    //      previous kernel; the input vector is not ----
     float x_inv = 1.0f;
     uint32_t xb0 = 0u, xb1 = 0u;
+    int cur_phase = -1;
+    bool tl_first_tile = false;
     if constexpr (GEMV) {
-        const GemvParams& g = mp.gv;
-        if (g.pdl) {
+        if (tid == 0) tl_stamp(mp.timeline, 2);
+        if (mp.pdl) {
             pdl_wait();
             // the dependent may start (its own pre-wait part reads nothing this chain writes later
             // than one kernel back); triggered after the wait so the chain stays one kernel deep
             if (tid == 0) pdl_launch_dependents();
         }
+        if (tid == 0) tl_stamp(mp.timeline, 3);
+    }
+    // Entering phase ph of the chain: wait until every CTA has published its partial sums of phase
+    // ph - 1, then the prologue over the whole input vector (RMSNorm scale, residual stream out).
+    auto enter_phase = [&](int ph) {
+        const GemvParams& g = mp.gv[ph];
+        if (tid == 0) tl_stamp(mp.timeline, 8 + 4 * ph);
+        if (ph > 0) {
+            if (tid == 0) {
+                const int target = (int)gridDim.x;
+                const long long t0 = clock64();
+                int seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(mp.phase_done + ph - 1) : "memory");
+                    if (seen >= target) break;
+                    __nanosleep(32);
+                    if (clock64() - t0 > (1ll << 32)) {  // ~2 s: never hang the device on a lost CTA
+                        if (p.err_flag) atomicExch(p.err_flag, AF_ECUDA);
+                        break;
+                    }
+                } while (true);
+            }
+            named_bar_sync(1, kMmaConsumers);
+        }
+        if (tid == 0) tl_stamp(mp.timeline, 9 + 4 * ph);
+        x_inv = 1.0f;
         if (g.prologue == AF_PRO_RMSNORM || (g.h_out && blockIdx.x == 0)) {
+            // whole-vector pass, two elements per thread and step, four steps of loads in flight
             float ss = 0.f;
-            for (int c = tid; c < g.x_len; c += kMmaConsumers) {
-                const float h = gemv_h(g, c);
-                ss = fmaf(h, h, ss);
-                if (g.h_out && blockIdx.x == 0) g.h_out[c] = h;
+            const bool write_h = g.h_out && blockIdx.x == 0;
+            constexpr int kStep = 2 * kMmaConsumers;
+            for (int base = 2 * tid; base < g.x_len; base += 4 * kStep) {
+                float2 hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = base + u * kStep;
+                    hv[u] = make_float2(0.f, 0.f);
+                    if (c < g.x_len) {
+                        if (g.acc_in) {
+                            const longlong2 q = __ldcg(reinterpret_cast<const longlong2*>(g.acc_in + c));
+                            hv[u] = make_float2(fix_to_f32(q.x), fix_to_f32(q.y));
+                        } else {
+                            hv[u] = __ldcg(reinterpret_cast<const float2*>(g.xin + c));
+                        }
+                        if (g.res) {
+                            const float2 r = __ldcg(reinterpret_cast<const float2*>(g.res + c));
+                            hv[u].x += r.x;
+                            hv[u].y += r.y;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = base + u * kStep;
+                    ss = fmaf(hv[u].x, hv[u].x, fmaf(hv[u].y, hv[u].y, ss));
+                    if (write_h && c < g.x_len) *reinterpret_cast<float2*>(g.h_out + c) = hv[u];
+                }
             }
             float* red = reinterpret_cast<float*>(sm + L::off_red);
             ss = warp_sum(ss);
+            named_bar_sync(1, kMmaConsumers);  // the previous phase's readers of red[] are done
             if (lane == 0) red[warp] = ss;
             named_bar_sync(1, kMmaConsumers);
             float tot = 0.f;
@@ -479,7 +603,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
             for (int i = 0; i < kMmaWarps; ++i) tot += red[i];
             x_inv = rsqrtf(tot / (float)g.x_len + g.eps);
         }
-    }
+        if (tid == 0) tl_stamp(mp.timeline, 10 + 4 * ph);
+        tl_first_tile = true;
+    };
     bool new_unit = true;
     constexpr int kHalves = BA ? 1 : 2;
     uint32_t bfr[kHalves][KS][4];
@@ -500,7 +626,13 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
         const int stage = it % kSt;
         const uint32_t ph = (it / kSt) & 1;
         if (new_unit) {
-            if constexpr (GEMV) gemv_x_fragment(mp.gv, ti.un.col0, warp, lane, x_inv, xb0, xb1);
+            if constexpr (GEMV) {
+                if (ti.un.phase != cur_phase) {
+                    cur_phase = ti.un.phase;
+                    enter_phase(cur_phase);
+                }
+                gemv_x_fragment(mp.gv[cur_phase], ti.un.col0, warp, lane, x_inv, xb0, xb1);
+            }
             // B fragments of this unit's slab -> registers (kept for every tile of the unit)
 #pragma unroll
             for (int half = 0; half < kHalves; ++half)
@@ -604,6 +736,12 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA store
         __syncwarp();
         if (lane == 0) mbar_arrive(&computed[stage]);
+        if constexpr (GEMV) {
+            if (tl_first_tile) {
+                if (tid == 0) tl_stamp(mp.timeline, 11 + 4 * cur_phase);
+                tl_first_tile = false;
+            }
+        }
 
         if (new_unit && have_next) {
             named_bar_sync(1, kMmaConsumers);  // every warp holds its B fragments: the slab may be rewritten
@@ -612,6 +750,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) switch_mma_kernel(const __grid
             down_commit<KS, BA>(down_smem, dn_regs, sg.rank, plan, S, tid);
             named_bar_sync(1, kMmaConsumers);  // next slab visible
         }
+    }
+    if constexpr (GEMV) {
+        if (tid == 0) tl_stamp(mp.timeline, 7);
     }
 }
 

@@ -63,6 +63,7 @@ class LlamaConfig:
     # over W per token instead of switch + forward); "separate": one switch launch, then plain GEMVs;
     # "auto": chase when it applies (adapters, single rank, tensor path)
     forward_mode: str = "auto"
+    chain: bool = True               # chase: o -> gate|up -> down -> next q|k|v as ONE launch with in-kernel phase barriers
 
     def validate(self) -> None:
         for name in ("layers", "hidden", "ffn", "n_heads", "n_kv_heads", "vocab", "experts", "rank", "top_k", "max_seq", "tp_size"):
@@ -359,21 +360,33 @@ class LlamaEngine:
             raise ConfigError("forward_mode='chase' needs the tensor path (bf16, rank % 8 == 0) and 2*top_k*rank <= 64")
         self.chase = can and want in ("auto", "chase")
         if self.chase:
+            # launches of one token: [qkv(0)] attn [o gu down qkv(1)] attn ... [o gu down (L-1)]
+            self.chase_chained = cfg.chain
+            seg = lambda li: {"qkv": [7 * li, 7 * li + 1, 7 * li + 2], "o": [7 * li + 3], "gu": [7 * li + 4, 7 * li + 5],  # noqa: E731
+                              "down": [7 * li + 6]}                                 # SEGMENT_NAMES order: q k v o gate up down
             self.groups = []
             for li in range(cfg.layers):
-                b = 7 * li  # SEGMENT_NAMES order: q k v o gate up down
-                self.groups.append({"qkv": SegmentGroup(self.table, [b, b + 1, b + 2]), "o": SegmentGroup(self.table, [b + 3]),
-                                    "gu": SegmentGroup(self.table, [b + 4, b + 5]), "down": SegmentGroup(self.table, [b + 6])})
-            # fixed-point accumulators of every launch of a token, one arena zeroed once per step
+                sg = seg(li)
+                if self.chase_chained:
+                    mid = [sg["o"], sg["gu"], sg["down"]] + ([seg(li + 1)["qkv"]] if li + 1 < cfg.layers else [])
+                    self.groups.append({"qkv": SegmentGroup(self.table, sg["qkv"]) if li == 0 else None,
+                                        "mid": SegmentGroup(self.table, mid)})
+                else:
+                    self.groups.append({k: SegmentGroup(self.table, v) for k, v in sg.items()})
+            # fixed-point accumulators of every launch of a token and the chains' phase counters:
+            # one arena, zeroed once per step
             n_qkv, n_gu = self.q_rows + 2 * self.kv_rows, 2 * self.ffn_local
             per_layer = n_qkv + d + n_gu + d
-            self.acc_arena = torch.zeros(cfg.layers * per_layer, dtype=torch.int64, device=dev)
+            self.acc_arena = torch.zeros(cfg.layers * (per_layer + 2), dtype=torch.int64, device=dev)
             self.acc = []
+            self.phase_done = []
+            counters = self.acc_arena[cfg.layers * per_layer:].view(torch.int32)   # 4 int32 per layer
             for li in range(cfg.layers):
                 o = li * per_layer
                 self.acc.append({"qkv": self.acc_arena[o: o + n_qkv], "o": self.acc_arena[o + n_qkv: o + n_qkv + d],
                                  "gu": self.acc_arena[o + n_qkv + d: o + n_qkv + d + n_gu],
                                  "down": self.acc_arena[o + n_qkv + d + n_gu: o + per_layer]})
+                self.phase_done.append(counters[4 * li: 4 * li + 4])
 
     # -- the pieces of one step ---------------------------------------------------------
 
@@ -453,20 +466,30 @@ class LlamaEngine:
         self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
         for li in range(cfg.layers):
             g, a = self.groups[li], self.acc[li]
+            last = li + 1 == cfg.layers
+            qkv_first = dict(acc_out=a["qkv"], xin=xa, prologue="rmsnorm", norm_w=self.attn_norm[li], eps=eps)
             if li == 0:
-                g["qkv"].switch_gemv(prev, self.cur, a["qkv"], xin=xa, prologue="rmsnorm", norm_w=self.attn_norm[li], eps=eps,
-                                     pdl=False, **kw)
-            else:
+                g["qkv"].switch_gemv(prev, self.cur, pdl=False, **qkv_first, **kw)
+            elif not self.chase_chained:
                 g["qkv"].switch_gemv(prev, self.cur, a["qkv"], acc_in=self.acc[li - 1]["down"], res=xb, h_out=xa, prologue="rmsnorm",
                                      norm_w=self.attn_norm[li], eps=eps, pdl=True, **kw)
             self._check(L.af_attn_decode_fix(_ptr(a["qkv"]), _ptr(self.k_cache[li]), _ptr(self.v_cache[li]), _ptr(self.cos),
                                              _ptr(self.sin), _ptr(self.pos_dev), self.heads_local, self.kv_local, cfg.head_dim,
                                              cfg.max_seq, self.attn_splits, _ptr(self.attn_ws), _ptr(self.attn_tickets),
                                              _ptr(self.attn_buf), st))
-            g["o"].switch_gemv(prev, self.cur, a["o"], xin=self.attn_buf, pdl=True, **kw)
-            g["gu"].switch_gemv(prev, self.cur, a["gu"], acc_in=a["o"], res=xa, h_out=xb, prologue="rmsnorm", norm_w=self.ffn_norm[li],
-                                eps=eps, pdl=True, **kw)
-            g["down"].switch_gemv(prev, self.cur, a["down"], acc_in=a["gu"], prologue="silu_mul", pdl=True, **kw)
+            ph_o = dict(acc_out=a["o"], xin=self.attn_buf)
+            ph_gu = dict(acc_out=a["gu"], acc_in=a["o"], res=xa, h_out=xb, prologue="rmsnorm", norm_w=self.ffn_norm[li], eps=eps)
+            ph_down = dict(acc_out=a["down"], acc_in=a["gu"], prologue="silu_mul")
+            if self.chase_chained:
+                phases = [ph_o, ph_gu, ph_down]
+                if not last:
+                    phases.append(dict(acc_out=self.acc[li + 1]["qkv"], acc_in=a["down"], res=xb, h_out=xa, prologue="rmsnorm",
+                                       norm_w=self.attn_norm[li + 1], eps=eps))
+                g["mid"].switch_gemv_chain(prev, self.cur, phases, self.phase_done[li], pdl=True, **kw)
+            else:
+                g["o"].switch_gemv(prev, self.cur, pdl=True, **ph_o, **kw)
+                g["gu"].switch_gemv(prev, self.cur, pdl=True, **ph_gu, **kw)
+                g["down"].switch_gemv(prev, self.cur, pdl=True, **ph_down, **kw)
         self._check(L.af_accum_to_f32(_ptr(self.acc[-1]["down"]), _ptr(xb), _ptr(xa), d, st))
         self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),
                                     _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))

@@ -126,6 +126,51 @@ def test_switch_gemv_prologues(af):
     np.testing.assert_allclose(out.cpu().numpy(), h, rtol=1e-6, atol=1e-6)
 
 
+def test_chain_equals_separate_launches(af):
+    """o -> gate|up -> down -> q|k|v shaped chain in ONE launch (in-kernel phase barriers) against the
+    same four projections launched one by one: bit-identical accumulators, residual streams, weights."""
+    from paper_2603_11873_b200.adapters import SegmentGroup
+
+    d, f = 512, 1280
+    shapes = [(d, d), (f, d), (f, d), (d, f), (d, d), (128, d), (128, d)]      # o | gate up | down | q k v
+    phases_ids = [[0], [1, 2], [3], [4, 5, 6]]
+    outs = []
+    for chained in (True, False):
+        tg, tab = _mk_table(af, shapes, seed=7)
+        prev = _decision(af, (1, 4), (0.7, 0.3))
+        cur = _decision(af, (4, 2), (0.55, 0.45))
+        tab.switch(None, prev, max_k=2)
+        g = torch.Generator(device="cuda").manual_seed(2)
+        attn = torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        xa = torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        nw1 = 1.0 + 0.1 * torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        nw2 = 1.0 + 0.1 * torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        xb, xa2 = torch.zeros(d, device="cuda"), torch.zeros(d, device="cuda")
+        acc = [torch.zeros(n, dtype=torch.int64, device="cuda") for n in (d, 2 * f, d, d + 256)]
+        phases = [dict(acc_out=acc[0], xin=attn),
+                  dict(acc_out=acc[1], acc_in=acc[0], res=xa, h_out=xb, prologue="rmsnorm", norm_w=nw1, eps=1e-5),
+                  dict(acc_out=acc[2], acc_in=acc[1], prologue="silu_mul"),
+                  dict(acc_out=acc[3], acc_in=acc[2], res=xb, h_out=xa2, prologue="rmsnorm", norm_w=nw2, eps=1e-5)]
+        if chained:
+            done = torch.zeros(4, dtype=torch.int32, device="cuda")
+            grp = SegmentGroup(tab, phases_ids)
+            assert grp.n_phases == 4 and grp.x_lens == [d, d, f, d]
+            grp.switch_gemv_chain(prev, cur, phases, done, max_k=2)
+            torch.cuda.synchronize()
+            assert done[:3].tolist() == [grp.grid] * 3
+        else:
+            for ids, ph in zip(phases_ids, phases):
+                SegmentGroup(tab, ids).switch_gemv_chain(prev, cur, [ph], None, max_k=2)
+        tab.status()
+        outs.append(([a.clone() for a in acc], xb.clone(), xa2.clone(), [t.data.clone() for t in tg]))
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert torch.equal(a, b)
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
+    for a, b in zip(outs[0][3], outs[1][3]):
+        assert torch.equal(a, b)
+    assert float(outs[0][0][3].abs().max()) > 0
+
+
 def test_group_validation(af):
     from paper_2603_11873_b200.adapters import SegmentGroup
     from paper_2603_11873_b200.errors import AliasingError, DimensionError
@@ -152,8 +197,8 @@ def test_chase_engine_equals_separate_engine(af):
 
     forced = np.random.Generator(np.random.PCG64(21)).integers(0, 512, 12)
     engs = {}
-    for mode in ("chase", "separate"):
-        e = llama.LlamaEngine(llama.preset("tiny", max_seq=32, forward_mode=mode), init="host")
+    for mode in ("chase", "separate", "chase-unchained"):
+        e = llama.LlamaEngine(llama.preset("tiny", max_seq=32, forward_mode=mode.split("-")[0], chain=(mode == "chase")), init="host")
         e.reset(forced=forced)
         lg = []
         for _ in range(12):
@@ -166,5 +211,8 @@ def test_chase_engine_equals_separate_engine(af):
         assert torch.equal(ta.data, tb.data)
     np.testing.assert_allclose(la, lb, rtol=0, atol=2e-4 * np.max(np.abs(lb)))
     assert a.tokens() == b.tokens()
+    c, lc = engs["chase-unchained"]
+    assert c.chase and not c.chase_chained and a.chase_chained
+    assert np.array_equal(la, lc)            # chaining is a schedule change only: bit-identical logits
     a.finalize()
     assert a.max_backbone_deviation() < 0.02
