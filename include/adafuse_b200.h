@@ -291,7 +291,7 @@ int af_switch_gemv(af_group* group, const af_decision* prev_dev, const af_decisi
  * passed, first/last W load issued, storer done, consumers done, then per phase: wait begins,
  * barrier passed, prologue done, first tile computed; then %smid) to buffer_dev + i * stride_elems.
  * buffer_dev == NULL turns the probe off. */
-#define AF_TIMELINE_SLOTS 26
+#define AF_TIMELINE_SLOTS 36
 int af_set_timeline(uint64_t* buffer_dev, int32_t n_launches, int64_t stride_elems);
 int af_accum_to_f32(const int64_t* acc, const float* res, float* out, int32_t n, void* stream);
 int af_attn_decode_fix(const int64_t* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,

@@ -378,6 +378,8 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     mp2.store_depth = (env_depth >= 0 && env_depth <= 3) ? env_depth : kStoreDepth;
     static const int env_upsw = [] { const char* e = getenv("AF_UP_SWIZZLE"); return (e && e[0] == '0') ? 0 : 1; }();
     mp2.up_swizzle_ok = env_upsw;
+    static const int env_dbg2 = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
+    mp2.dbg = env_dbg2 ^ 24;  // bits 8 / 16: L2 evict-first hint on the W loads / stores, on unless AF_DBG flips them
     if (mp2.store_depth > mp2.n_stages - 2) mp2.store_depth = mp2.n_stages - 2;
     if constexpr (GEMV) {
         cudaLaunchConfig_t cfg{};
@@ -601,6 +603,11 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
     *out = nullptr;
     if (!t || !seg_ids || !phase_len || n_phases < 1) return fail(AF_EDIM, "segment group is empty");
     if (n_phases > kMaxPhases) return fail(AF_EVALUE, "a chain holds at most 4 phases");
+    {
+        int total_segs = 0;
+        for (int ph = 0; ph < n_phases; ++ph) total_segs += phase_len[ph] > 0 ? phase_len[ph] : 0;
+        if (total_segs > kSegCache) return fail(AF_EVALUE, "a chain holds at most 12 segments");
+    }
     if (!t->fast_mma)
         return fail(AF_EPRECISION, "the fused switch + GEMV needs the tensor path: bf16 targets and factors, rank % 8 == 0, "
                                    "16-byte aligned rows");
@@ -646,33 +653,57 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
         g->tiles += total;
         const int Gp = (int)std::min<long long>(total, G);   // CTA 0 always owns tiles of every phase (it writes h_out)
         used = std::max(used, Gp);
-        int cta = 0;
-        long long idx = 0, cta_end = total / Gp;
+        // Cost model of a span: its tiles + `penalty` tile-times for every strip boundary inside it
+        // (a unit change restages the gated DOWN slab and refills the per-unit registers: ~4 us
+        // against ~0.85 us per tile, profiles/r01_chase_timeline.txt).  All CTAs meet at the phase
+        // barrier, so spans are cut to equal COST, not equal tile count: the smallest per-CTA
+        // budget that needs at most Gp spans, found by bisection.
+        static const int penalty = [] { const char* e = getenv("AF_UNIT_PENALTY"); return e ? atoi(e) : 4; }();
+        struct Strip { int sidx, slot, sp, rt, d_out; };
+        std::vector<Strip> strips_v;
         for (int i = 0; i < phase_len[ph]; ++i) {
             const int sidx = seg_ids[first + i];
             const int d_out = t->segs[sidx].d_out;
-            const int rt = (d_out + kMR - 1) / kMR;
-            for (int sp = 0; sp < strips; ++sp) {
+            for (int sp = 0; sp < strips; ++sp) strips_v.push_back({sidx, first + i, sp, (d_out + kMR - 1) / kMR, d_out});
+        }
+        auto cut = [&](long long budget, std::vector<std::vector<UnitDev>>* out) -> int {
+            int cta = 0;
+            long long cost = 0;   // cost already in the current span
+            for (const Strip& st : strips_v) {
                 int r = 0;
-                while (r < rt) {
-                    while (idx >= cta_end && cta < Gp - 1) {
+                while (r < st.rt) {
+                    long long room = budget - cost - (cost > 0 ? penalty : 0);   // entering a strip mid-span costs the penalty
+                    if (cost > 0 && room < std::max(1, penalty)) {   // not worth a unit change: close the span, start a new one here
                         ++cta;
-                        cta_end = total * (cta + 1) / Gp;
+                        cost = 0;
+                        continue;
                     }
-                    const int take = (int)std::min<long long>(rt - r, cta_end - idx);
-                    const int row0 = r * kMR;
-                    per_cta[cta].push_back({sidx, row0, std::min(take * kMR, d_out - row0), sp * kTN, ph});
+                    if (room < 1) room = 1;
+                    const int take = (int)std::min<long long>(st.rt - r, room);
+                    if (out) {
+                        const int row0 = r * kMR;
+                        (*out)[std::min(cta, Gp - 1)].push_back({st.sidx, row0, std::min(take * kMR, st.d_out - row0), st.sp * kTN, ph, st.slot});
+                    }
+                    cost += take + (cost > 0 ? penalty : 0);
                     r += take;
-                    idx += take;
                 }
             }
+            return cta + 1;
+        };
+        long long lo = (total + Gp - 1) / Gp, hi = lo + (long long)penalty * 4 + 8;
+        while (cut(hi, nullptr) > Gp) hi *= 2;
+        while (lo < hi) {
+            const long long mid = (lo + hi) / 2;
+            if (cut(mid, nullptr) <= Gp) hi = mid;
+            else lo = mid + 1;
         }
+        cut(lo, &per_cta);
         first += phase_len[ph];
     }
     const int grid = used;
     size_t depth = 0;
     for (auto& v : per_cta) depth = std::max(depth, v.size());
-    std::vector<UnitDev> units(depth * grid, UnitDev{0, 0, 0, 0, 0});
+    std::vector<UnitDev> units(depth * grid, UnitDev{0, 0, 0, 0, 0, 0});
     for (int c = 0; c < grid; ++c)
         for (size_t j = 0; j < per_cta[c].size(); ++j) units[j * grid + c] = per_cta[c][j];
     g->grid = grid;
@@ -771,9 +802,11 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     mp.n_phases = n_phases;
     mp.phase_done = phase_done_dev;
     mp.seg_yoff = g->d_seg_yoff;
+    mp.n_chain_segs = (int)g->segs.size();
+    for (size_t i = 0; i < g->segs.size(); ++i) mp.chain_segs[i] = g->segs[i];
     mp.pdl = (pdl && g_pdl.load()) ? 1 : 0;
     static const int env_dbg = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
-    mp.dbg = env_dbg;
+    mp.dbg = env_dbg ^ 24;
     if (g_timeline && g_timeline_left > 0) {
         mp.timeline = g_timeline;
         g_timeline += g_timeline_stride;

@@ -44,6 +44,7 @@ struct SegDev {
 struct UnitDev {
     int seg, row0, rows, col0;
     int phase;  // chained switch + GEMV launches: which projection of the chain the unit belongs to
+    int slot;   // ... and the segment's position in the chain's segment list (shared-memory descriptor cache)
 };
 
 struct Plan {

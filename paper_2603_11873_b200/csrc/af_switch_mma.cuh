@@ -49,6 +49,9 @@ constexpr int kMmaMaxKS = 4;                      // k-steps of 16 ranks: S <= 6
 constexpr int kMmaMaxStages = 12;
 constexpr int kStoreDepth = 0;                    // tile stores that may still be reading smem
 constexpr int kMmaDefaultStages = 10;
+constexpr int kUnitCache = 24;  // unit descriptors of a CTA cached in shared memory
+constexpr int kSegCache = 12;   // segments of a chain (4 phases x up to 3 matrices)
+constexpr int kXSlots = 4;      // input-vector strips staged per phase (units of one CTA in one phase)
 
 // BA ("block accumulate"): the slab holds the RAW bf16 DOWN rows and the gate is applied to the
 // f32 product of each rank-16 step (acc += g * (U_b A_b)) instead of being folded into a hi+lo
@@ -62,7 +65,9 @@ struct MmaLayout {
     // GEMV: per stage, the 16 consumer warps' partial dot products of the tile's 32 rows (f32)
     static constexpr int part_stage_bytes = GEMV ? kMmaWarps * kMR * 4 : 0;
     static constexpr int red_bytes = GEMV ? 128 : 0;  // block reduction scratch of the RMSNorm prologue
-    static constexpr int fixed = down_bytes + 3 * 8 * 16 + (int)sizeof(Plan) + red_bytes + 1024 /*alignment slack*/ + 256;
+    static constexpr int cache_bytes = kUnitCache * (int)sizeof(UnitDev) + (GEMV ? kSegCache * (int)sizeof(SegDev) : 0);
+    static constexpr int xs_bytes = GEMV ? kXSlots * kTN * 4 : 0;  // staged input-vector strips of the current phase
+    static constexpr int fixed = down_bytes + 3 * 8 * 16 + (int)sizeof(Plan) + red_bytes + cache_bytes + xs_bytes + 1024 /*alignment slack*/ + 256;
     static constexpr int by_smem = (227 * 1024 - fixed) / (kWStageBytes + up_stage_bytes + part_stage_bytes);
     static constexpr int stages = by_smem < kMmaMaxStages ? by_smem : kMmaMaxStages;
     // offsets from the 1024-aligned base
@@ -73,7 +78,10 @@ struct MmaLayout {
     static constexpr int off_bar = off_down + down_bytes;          // full[16], computed[16], empty[16]
     static constexpr int off_plan = off_bar + 3 * 8 * 16;
     static constexpr int off_red = (off_plan + (int)sizeof(Plan) + 15) & ~15;
-    static constexpr int total = off_red + red_bytes + 1024 /*alignment slack*/;
+    static constexpr int off_units = off_red + red_bytes;
+    static constexpr int off_segs = off_units + kUnitCache * (int)sizeof(UnitDev);
+    static constexpr int off_xs = (off_segs + (GEMV ? kSegCache * (int)sizeof(SegDev) : 0) + 15) & ~15;
+    static constexpr int total = off_xs + xs_bytes + 1024 /*alignment slack*/;
     static_assert(stages >= 3 && total <= 227 * 1024, "shared memory budget");
 };
 
@@ -102,6 +110,25 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
 __device__ __forceinline__ void bulk_load_1d(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_dst),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// W is touched once per token and is 100x larger than L2: its tiles are loaded and stored with an
+// evict-first policy so that the stream does not push out what IS reused -- the selected experts'
+// factors (re-read by every column strip), the activation vectors, the accumulators, the code.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t smem_dst, const void* tmap, int c0, int c1, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(smem_dst), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const void* tmap, int c0, int c1, uint32_t smem_src, uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(tmap),
+                 "r"(c0), "r"(c1), "r"(smem_src), "l"(pol)
                  : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_addr(uint32_t smem_dst, const void* tmap, int c0, int c1, uint64_t* bar) {
@@ -156,6 +183,8 @@ struct MmaParams {
     int n_phases;
     int* phase_done;               // [n_phases - 1] counters, zeroed by the caller per launch
     const int* seg_yoff;           // per table segment: first row of its slice of its phase's acc_out
+    int chain_segs[kSegCache];     // table ids of the chain's segments (UnitDev::slot indexes this list)
+    int n_chain_segs;
     int pdl;                       // launched with programmatic stream serialization
     // optional timeline probe (af_set_timeline): [gridDim.x][kTlSlots] globaltimer stamps of this launch
     unsigned long long* timeline;
@@ -174,6 +203,18 @@ struct MmaParams {
 // under a whole unit of tiles: down_prefetch() issues this thread's 16-byte loads of the NEXT
 // unit's DOWN rows into registers, down_commit() folds the gate (one f32 multiply,
 // adapters.py:202), splits into bf16 hi + lo and writes the slab.
+// q / r and q % r for the (usually power-of-two) rank: these sit on the per-unit serial path of
+// every consumer thread, where a generic integer division costs ~40 dependent instructions.
+__device__ __forceinline__ void rank_divmod(int q, int r, int& quo, int& rem) {
+    if ((r & (r - 1)) == 0) {
+        quo = q >> (31 - __clz(r));
+        rem = q & (r - 1);
+    } else {
+        quo = q / r;
+        rem = q % r;
+    }
+}
+
 template <int KS>
 __device__ __forceinline__ void down_prefetch(uint4 (&regs)[KS], const SegDev& sg, const Plan& plan, int S, int col0,
                                               int tid) {
@@ -185,12 +226,25 @@ __device__ __forceinline__ void down_prefetch(uint4 (&regs)[KS], const SegDev& s
         const int i = tid + j * kMmaConsumers;
         const int q = i / chunks_per_row;
         const int c = (i % chunks_per_row) * 8;
-        regs[j] = make_uint4(0u, 0u, 0u, 0u);
-        if (q < S && col0 + c < sg.d_in) {
-            const int b = q / r, qr = q % r;
-            regs[j] = __ldg(reinterpret_cast<const uint4*>(base + (long long)plan.expert[b] * sg.down_estride +
-                                                           (long long)qr * sg.ld_down + col0 + c));
-        }
+        // predicated load inside one asm block: nothing consumes the value here, so the thread does
+        // not wait for it (a C++ `zero; if (ok) load` becomes load + select, which does)
+        const bool ok = q < S && col0 + c < sg.d_in;
+        const int qq = ok ? q : 0;
+        int b, qr;
+        rank_divmod(qq, r, b, qr);
+        const __nv_bfloat16* src = base + (long long)plan.expert[b] * sg.down_estride + (long long)qr * sg.ld_down + col0 + c;
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %5, 0;\n"
+            "mov.b32 %0, 0;\n"
+            "mov.b32 %1, 0;\n"
+            "mov.b32 %2, 0;\n"
+            "mov.b32 %3, 0;\n"
+            "@p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+            "}\n"
+            : "=r"(regs[j].x), "=r"(regs[j].y), "=r"(regs[j].z), "=r"(regs[j].w)
+            : "l"(ok ? src : base), "r"((int)ok));
     }
 }
 
@@ -210,7 +264,9 @@ __device__ __forceinline__ void down_commit(unsigned char* down_smem, const uint
         }
         uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
         if (q < S) {
-            const float w = plan.weight[q / rank];
+            int wb, wr;
+            rank_divmod(q, rank, wb, wr);
+            const float w = plan.weight[wb];
             const uint32_t in[4] = {regs[j].x, regs[j].y, regs[j].z, regs[j].w};
             uint32_t oh[4], ol[4];
 #pragma unroll
@@ -229,7 +285,46 @@ __device__ __forceinline__ void down_commit(unsigned char* down_smem, const uint
     }
 }
 
-using MmaIter = TileIterT<kMR>;
+// Tile walk of the tensor-path kernels: as TileIterT<kMR>, but the CTA's first kUnitCache unit
+// descriptors come from shared memory (copied once at kernel start).  Under load a global read
+// costs ~2 us; a unit change used to pay two of them in a row (unit, then its segment).
+struct MmaIter {
+    int j, u, m0, row_end;
+    UnitDev un;
+    const UnitDev* cache;
+    __device__ __forceinline__ bool valid(const SwitchParams& p) const { return u < p.n_units; }
+    __device__ __forceinline__ UnitDev fetch(const SwitchParams& p, int jj, int uu) const {
+        return jj < kUnitCache ? cache[jj] : p.units[uu];
+    }
+    __device__ __forceinline__ void load_unit(const SwitchParams& p) {
+        if (u < p.n_units) {
+            un = fetch(p, j, u);
+            m0 = un.row0;
+            row_end = un.row0 + un.rows;
+            if (un.rows <= 0) u = p.n_units;
+        }
+    }
+    __device__ __forceinline__ void init(const SwitchParams& p, const UnitDev* c) {
+        cache = c;
+        j = 0;
+        u = blockIdx.x;
+        load_unit(p);
+    }
+    __device__ __forceinline__ bool next(const SwitchParams& p) {
+        m0 += kMR;
+        if (m0 < row_end) return false;
+        u += gridDim.x;
+        ++j;
+        load_unit(p);
+        return true;
+    }
+    // the unit after the current one (rows == 0: none)
+    __device__ __forceinline__ UnitDev peek(const SwitchParams& p) const {
+        const int un2 = u + gridDim.x;
+        if (un2 >= p.n_units) return UnitDev{0, 0, 0, 0, 0, 0};
+        return fetch(p, j + 1, un2);
+    }
+};
 
 // UP rows of 32 / 64 / 128 bytes are fetched through a swizzled 2-D tensor map (swizzle span =
 // row bytes) so that the A-fragment ldmatrix of 8 consecutive rows is bank-conflict free; 16-byte
@@ -249,7 +344,7 @@ __host__ __device__ __forceinline__ bool up_swizzled(int rank) { return rank == 
 //   0 entry | 1 plan ready | 2 first slab staged | 3 pdl_wait passed | 4 first W load issued |
 //   5 last W load issued | 6 storer done | 7 consumers done |
 //   8 + 4 * phase: barrier wait begins | +1 barrier passed | +2 prologue done | +3 first tile of the phase computed
-constexpr int kTlSlots = 8 + 4 * 4 + 2;  // + [24] = %smid, [25] = tiles of this CTA
+constexpr int kTlSlots = 8 + 4 * 4 + 2 + 6 + 4;  // + [24] = %smid; [26..31]: first unit change inside phase 1
 __device__ __forceinline__ void tl_stamp(unsigned long long* tl, int slot) {
     if (tl) {
         unsigned long long t;
@@ -279,11 +374,16 @@ __device__ __forceinline__ float gemv_x(const GemvParams& g, int c, float inv) {
 // B fragment (k16 x n8, col-major) of the input vector for this warp's 16 columns: column n = 0
 // carries bf16 hi(x), n = 1 carries lo = x - hi (x is reproduced to 2^-17 relative), the other six
 // columns are zero.  Lane j < 16 evaluates x at column col0 + 16 * warp + j.
-__device__ __forceinline__ void gemv_x_fragment(const GemvParams& g, int col0, int warp, int lane, float inv,
+// `xs` != nullptr: the strip was staged in shared memory at phase entry (the usual case).
+__device__ __forceinline__ void gemv_x_fragment(const GemvParams& g, const float* xs, int col0, int warp, int lane, float inv,
                                                 uint32_t& xb0, uint32_t& xb1) {
     float xv = 0.f;
     const int c = col0 + warp * 16 + (lane & 15);
-    if (lane < 16 && c < g.x_len) xv = gemv_x(g, c, inv);
+    if (xs) {
+        if (lane < 16) xv = xs[warp * 16 + lane];
+    } else if (lane < 16 && c < g.x_len) {
+        xv = gemv_x(g, c, inv);
+    }
     const float hi = __bfloat162float(__float2bfloat16_rn(xv));
     const float lo = xv - hi;
     const int t2 = (lane & 3) * 2, n = lane >> 2;
@@ -307,7 +407,20 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
     uint64_t* computed = full + 16;
     uint64_t* empty = full + 32;
     Plan& plan = *reinterpret_cast<Plan*>(sm + L::off_plan);
+    UnitDev* unit_cache = reinterpret_cast<UnitDev*>(sm + L::off_units);
+    SegDev* seg_cache = reinterpret_cast<SegDev*>(sm + L::off_segs);
     const int tid = threadIdx.x;
+    // descriptor caches (one global round trip, concurrent with the plan build below)
+    if (tid >= 32 && tid < 32 + kUnitCache) {
+        const int jj = tid - 32;
+        const long long uu = (long long)blockIdx.x + (long long)jj * gridDim.x;
+        unit_cache[jj] = uu < p.n_units ? p.units[uu] : UnitDev{0, 0, 0, 0, 0, 0};
+    }
+    if constexpr (GEMV) {
+        if (tid >= 64 && tid < 64 + mp.n_chain_segs) seg_cache[tid - 64] = p.segs[mp.chain_segs[tid - 64]];
+    }
+    // descriptor of a unit's segment
+    auto seg_of = [&](const UnitDev& un) -> SegDev { return GEMV ? seg_cache[un.slot] : p.segs[un.seg]; };
 
     if (tid == 0) {
         if constexpr (GEMV) {
@@ -351,8 +464,9 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         if (lane == 0) {
             const int who = warp - kMmaWarps;
             constexpr int kMine = (kBoxes + kWProd - 1) / kWProd;
+            const uint64_t pol = l2_evict_first_policy();
             MmaIter ti;
-            ti.init(p);
+            ti.init(p, unit_cache);
             for (int it = 0; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
@@ -368,9 +482,14 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
 #pragma unroll
                 for (int j = 0; j < kMine; ++j) {
                     const int b = who + j * kWProd;
-                    if (b < kBoxes)
-                        tma_load_2d_addr(w_base + stage * kWStageBytes + b * kBoxBytes, tm, ti.un.col0 + b * kBoxCols, ti.m0,
-                                         &full[stage]);
+                    if (b < kBoxes) {
+                        if (mp.dbg & 8)
+                            tma_load_2d_hint(w_base + stage * kWStageBytes + b * kBoxBytes, tm, ti.un.col0 + b * kBoxCols, ti.m0,
+                                             &full[stage], pol);
+                        else
+                            tma_load_2d_addr(w_base + stage * kWStageBytes + b * kBoxBytes, tm, ti.un.col0 + b * kBoxCols, ti.m0,
+                                             &full[stage]);
+                    }
                 }
                 ti.next(p);
             }
@@ -384,7 +503,7 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         // ============ UP producer: one 1-D bulk copy per selected expert block ============
         if (lane == 0) {
             MmaIter ti;
-            ti.init(p);
+            ti.init(p, unit_cache);
             SegDev sg;
             int cur_seg = -1;
             for (int it = 0; ti.valid(p); ++it) {
@@ -392,7 +511,7 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 const uint32_t ph = (it / kSt) & 1;
                 if (ti.un.seg != cur_seg) {
                     cur_seg = ti.un.seg;
-                    sg = p.segs[cur_seg];
+                    sg = seg_of(ti.un);
                 }
                 const int rows_here = min(kMR, sg.d_out - ti.m0);
                 mbar_wait(&empty[stage], ph ^ 1);
@@ -423,8 +542,9 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         if (lane == 0) {
             const int who = warp - (kMmaWarps + kWProd + 1);
             constexpr int kMine = (kBoxes + kStorers - 1) / kStorers;
+            const uint64_t pol = l2_evict_first_policy();
             MmaIter ti;
-            ti.init(p);
+            ti.init(p, unit_cache);
             int it = 0;
             for (; ti.valid(p); ++it) {
                 const int stage = it % kSt;
@@ -436,7 +556,12 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                     for (int j = 0; j < kMine; ++j) {
                         const int b = who + j * kStorers;
                         if (b < kBoxes)
-                            tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
+                        {
+                            if (mp.dbg & 16)
+                                tma_store_2d_hint(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes, pol);
+                            else
+                                tma_store_2d_addr(tm, ti.un.col0 + b * kBoxCols, ti.m0, w_base + stage * kWStageBytes + b * kBoxBytes);
+                        }
                     }
                     bulk_commit();
                 }
@@ -461,7 +586,7 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             // vector; publishes a finished phase of a chain.  Its own warp, so that neither the
             // stores nor the consumers wait for the shared-memory reads and the atomics. ============
             MmaIter ti;
-            ti.init(p);
+            ti.init(p, unit_cache);
             int cur_seg = -1, yoff = 0, cur_phase = 0;
             unsigned long long* acc_out = nullptr;
             // phases [from, to) of the chain are complete on this CTA: publish (the atomics of every
@@ -513,9 +638,9 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
     const uint32_t down_base = smem_u32(down_smem);
 
     MmaIter ti;
-    ti.init(p);
+    ti.init(p, unit_cache);
     if (!ti.valid(p)) return;
-    SegDev sg = p.segs[ti.un.seg];
+    SegDev sg = seg_of(ti.un);
     int S = n_blocks * sg.rank;
     uint4 dn_regs[KS];
     down_prefetch<KS>(dn_regs, sg, plan, S, ti.un.col0, tid);
@@ -525,8 +650,8 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
     //      previous kernel; the input vector is not ----
     float x_inv = 1.0f;
     uint32_t xb0 = 0u, xb1 = 0u;
-    int cur_phase = -1;
-    bool tl_first_tile = false;
+    int cur_phase = -1, phase_j0 = 0;
+    bool tl_first_tile = false, tl_probe = false, tl_probe_done = false;
     if constexpr (GEMV) {
         if (tid == 0) tl_stamp(mp.timeline, 2);
         if (mp.pdl) {
@@ -561,6 +686,31 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         }
         if (tid == 0) tl_stamp(mp.timeline, 9 + 4 * ph);
         x_inv = 1.0f;
+        // Input-vector strips of this CTA's units of the phase (at most kXSlots of them) are staged in
+        // shared memory now: their loads go out together with the whole-vector pass below -- ONE
+        // global round trip (~2 us under load) per phase instead of one more at every unit start.
+        phase_j0 = ti.j;
+        float xr_h[kXSlots / 2], xr_w[kXSlots / 2];   // thread t: column t % 256 of slots t / 256 and t / 256 + 2
+#pragma unroll
+        for (int k2 = 0; k2 < kXSlots / 2; ++k2) {
+            const int slot = (tid >> 8) + 2 * k2;
+            xr_h[k2] = 0.f;
+            xr_w[k2] = 1.f;
+            const int jj = ti.j + slot;
+            const long long uu = (long long)ti.u + (long long)slot * gridDim.x;
+            if (uu < p.n_units) {
+                const UnitDev un2 = ti.fetch(p, jj, (int)uu);
+                const int c = un2.col0 + (tid & 255);
+                if (un2.rows > 0 && un2.phase == ph && c < g.x_len) {
+                    if (g.prologue == AF_PRO_SILU_MUL) {
+                        xr_h[k2] = gemv_x(g, c, 1.0f);
+                    } else {
+                        xr_h[k2] = gemv_h(g, c);
+                        if (g.prologue == AF_PRO_RMSNORM) xr_w[k2] = g.norm_w[c];
+                    }
+                }
+            }
+        }
         if (g.prologue == AF_PRO_RMSNORM || (g.h_out && blockIdx.x == 0)) {
             // whole-vector pass, two elements per thread and step, four steps of loads in flight
             float ss = 0.f;
@@ -603,6 +753,16 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             for (int i = 0; i < kMmaWarps; ++i) tot += red[i];
             x_inv = rsqrtf(tot / (float)g.x_len + g.eps);
         }
+        {
+            float* xs = reinterpret_cast<float*>(sm + L::off_xs);
+#pragma unroll
+            for (int k2 = 0; k2 < kXSlots / 2; ++k2) {
+                float v = xr_h[k2];
+                if (g.prologue == AF_PRO_RMSNORM) v *= x_inv * xr_w[k2];   // same expression as gemv_x
+                xs[((tid >> 8) + 2 * k2) * kTN + (tid & 255)] = v;
+            }
+            named_bar_sync(1, kMmaConsumers);  // strips visible to every consumer warp
+        }
         if (tid == 0) tl_stamp(mp.timeline, 10 + 4 * ph);
         tl_first_tile = true;
     };
@@ -631,7 +791,10 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                     cur_phase = ti.un.phase;
                     enter_phase(cur_phase);
                 }
-                gemv_x_fragment(mp.gv[cur_phase], ti.un.col0, warp, lane, x_inv, xb0, xb1);
+                const int xslot = ti.j - phase_j0;
+                const float* xs = xslot < kXSlots ? reinterpret_cast<const float*>(sm + L::off_xs) + xslot * kTN : nullptr;
+                gemv_x_fragment(mp.gv[cur_phase], xs, ti.un.col0, warp, lane, x_inv, xb0, xb1);
+                if (tl_probe) tl_stamp(mp.timeline, 32);
             }
             // B fragments of this unit's slab -> registers (kept for every tile of the unit)
 #pragma unroll
@@ -645,12 +808,14 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
 #pragma unroll
                 for (int j = 0; j < KS; ++j) gate[j] = (16 * j < S) ? plan.weight[(16 * j) / sg.rank] : 0.f;
             }
+            if (GEMV && tl_probe) tl_stamp(mp.timeline, 33);
             a_mt_stride = 16 * sg.rank * 2;
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
                 const int k0 = 16 * j + (mi >> 1) * 8;  // first rank of the 8x8 matrix this lane addresses
                 const int kk = k0 < S ? k0 : 0;
-                const int b = kk / sg.rank, kin = kk % sg.rank;
+                int b, kin;
+                rank_divmod(kk, sg.rank, b, kin);
                 // 16-byte chunk index inside the row, XOR-swizzled when the block came through the
                 // swizzled tensor map (address bits [4..] ^= bits [7..], span = row bytes)
                 const int span16 = (mp.up_swizzle_ok && up_swizzled(sg.rank)) ? sg.rank / 8 : 1;  // row bytes / 16
@@ -659,19 +824,22 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 a_keep_lo[j] = (16 * j < S) ? 0xffffffffu : 0u;
                 a_keep_hi[j] = (16 * j + 8 < S) ? 0xffffffffu : 0u;
             }
+            if (GEMV && tl_probe) tl_stamp(mp.timeline, 34);
             // start fetching the NEXT unit's DOWN rows; they are committed to the slab at its start
-            const int un = ti.u + gridDim.x;
-            have_next = un < p.n_units && p.units[un].rows > 0;
+            const UnitDev nu = ti.peek(p);
+            have_next = nu.rows > 0;
             if (have_next) {
-                const UnitDev nu = p.units[un];
-                sg_next = p.segs[nu.seg];
+                sg_next = seg_of(nu);
                 S_next = n_blocks * sg_next.rank;
                 down_prefetch<KS>(dn_regs, sg_next, plan, S_next, nu.col0, tid);
             }
+            if (GEMV && tl_probe) tl_stamp(mp.timeline, 35);
         }
         new_unit = ti.next(p);
 
+        if (GEMV && tl_probe) tl_stamp(mp.timeline, 29);
         mbar_wait(&full[stage], ph);
+        if (GEMV && tl_probe) tl_stamp(mp.timeline, 30);
         const uint32_t w_stage = w_base + stage * kWStageBytes + wbox * kBoxBytes + w_off;
         const uint32_t up_stage = up_base + stage * L::up_stage_bytes;
 #pragma unroll
@@ -737,6 +905,10 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         __syncwarp();
         if (lane == 0) mbar_arrive(&computed[stage]);
         if constexpr (GEMV) {
+            if (tl_probe) {
+                tl_stamp(mp.timeline, 31);
+                tl_probe = false;
+            }
             if (tl_first_tile) {
                 if (tid == 0) tl_stamp(mp.timeline, 11 + 4 * cur_phase);
                 tl_first_tile = false;
@@ -744,11 +916,19 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         }
 
         if (new_unit && have_next) {
+            const bool probe = GEMV && tid == 0 && cur_phase == 1 && ti.valid(p) && ti.un.phase == 1 && !tl_probe_done;
+            if (probe) tl_stamp(mp.timeline, 26);
             named_bar_sync(1, kMmaConsumers);  // every warp holds its B fragments: the slab may be rewritten
+            if (probe) tl_stamp(mp.timeline, 27);
             sg = sg_next;
             S = S_next;
             down_commit<KS, BA>(down_smem, dn_regs, sg.rank, plan, S, tid);
             named_bar_sync(1, kMmaConsumers);  // next slab visible
+            if (probe) {
+                tl_stamp(mp.timeline, 28);
+                tl_probe = true;
+                tl_probe_done = true;
+            }
         }
     }
     if constexpr (GEMV) {

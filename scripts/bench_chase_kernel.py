@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("workload", nargs="?", default="llama2-7b")
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--iters", type=int, default=6)
+ap.add_argument("--plain", action="store_true", help="no decisions: the launch is a plain GEMV (reads W once, stores nothing)")
 args = ap.parse_args()
 cfg = llama.preset(args.workload, layers=args.layers, max_seq=16, forward_mode="separate", keep_pristine=False)
 eng = llama.LlamaEngine(cfg, init="device")
@@ -33,11 +34,15 @@ names = {"qkv": ["q", "k", "v"], "o": ["o"], "gu": ["gate", "up"], "down": ["dow
 for gname in ("gu", "qkv", "down", "o"):
     groups = [SegmentGroup(eng.table, [7 * li + j for j in ids[gname]]) for li in range(cfg.layers)]
     nbytes = sum(4 * shp[n][0] * shp[n][1] + 2 * s * (shp[n][0] + shp[n][1]) for n in names[gname])
+    if args.plain:
+        nbytes = sum(2 * shp[n][0] * shp[n][1] for n in names[gname])
     x = torch.randn(groups[0].x_len, device="cuda")
     acc = torch.zeros(groups[0].y_rows, dtype=torch.int64, device="cuda")
     best = 1e9
     for it in range(args.iters):
         prev, cur = (da, db) if it % 2 == 0 else (db, da)
+        if args.plain:
+            prev = cur = None
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -48,4 +53,4 @@ for gname in ("gu", "qkv", "down", "o"):
         if it >= 2:
             best = min(best, e0.elapsed_time(e1))
     us = best * 1e3 / cfg.layers
-    print(f"AF_DBG={os.environ.get('AF_DBG', '0')} group {gname:4s}: {us:7.1f} us per launch, {nbytes / us / 1e3:7.1f} GB/s ({groups[0].tiles} tiles, grid {groups[0].grid})")
+    print(f"AF_DBG={os.environ.get('AF_DBG', '0')}{' plain-GEMV' if args.plain else ''} group {gname:4s}: {us:7.1f} us per launch, {nbytes / us / 1e3:7.1f} GB/s ({groups[0].tiles} tiles, grid {groups[0].grid})")

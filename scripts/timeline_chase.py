@@ -25,7 +25,7 @@ forced = np.random.Generator(np.random.PCG64(1)).integers(0, cfg.vocab, 64)
 eng.reset(forced=forced)
 for _ in range(4):
     eng.decode_step()
-SLOTS = 26
+SLOTS = 36
 n_launch = (cfg.layers + 1) if not args.no_chain else 4 * cfg.layers
 grid = _capi.device_info()["sm_count"]
 buf = torch.zeros(n_launch * grid * SLOTS, dtype=torch.int64, device="cuda")
@@ -39,7 +39,9 @@ torch.cuda.synchronize()
 _capi.check(_capi.lib().af_set_timeline(None, 0, 0))
 print(f"step {e0.elapsed_time(e1):.3f} ms eager, {n_launch} fused launches")
 tl = buf.cpu().numpy().reshape(n_launch, grid, SLOTS).astype(np.float64)
+smid_all = tl[:, :, 24].copy()
 tl[tl == 0] = np.nan
+tl[:, :, 24] = smid_all
 names = ["entry", "plan", "slab0", "pdlwait", "Wld_first", "Wld_last", "storer_done", "cons_done"]
 for ph in range(4):
     names += [f"p{ph}.wait", f"p{ph}.passed", f"p{ph}.prolog", f"p{ph}.tile0"]
@@ -73,5 +75,20 @@ if not args.no_chain:
         print("   slowest CTAs (cta:smid:us):", " ".join(f"{c}:{int(smid[c])}:{mean_per_cta[c]:.1f}" for c in order[-10:]))
         same_sm = np.all(tl[1:-1, :, 24] == smid[None, :])
         print("   CTA -> SM mapping identical in every launch:", bool(same_sm))
+if not args.no_chain:
+    # first unit change inside phase 1 (CTAs whose span crosses a strip boundary)
+    uc = tl[1:-1, :, 26:32]
+    has = ~np.isnan(uc[:, :, 0])
+    if has.any():
+        d = (uc[:, :, 1:] - uc[:, :, :-1]) / 1e3
+        labels = ["wait for all warps", "commit slab + barrier", "new-unit setup", "wait full[stage]", "first tile compute"]
+        for k, lb in enumerate(labels):
+            v = d[:, :, k][has]
+            print(f"unit change: {lb:22s} med {np.nanmedian(v):6.2f}  max {np.nanmax(v):6.2f} us  (n={v.size})")
+        fine = tl[1:-1, :, [28, 32, 33, 34, 35, 29]]
+        df = (fine[:, :, 1:] - fine[:, :, :-1]) / 1e3
+        for k, lb in enumerate(["x fragment", "B fragments (ldmatrix)", "A offsets", "peek + prefetch issue", "ti.next"]):
+            v = df[:, :, k][has]
+            print(f"   setup: {lb:24s} med {np.nanmedian(v):6.2f}  max {np.nanmax(v):6.2f} us")
 t_last = np.nanmax(tl[-1, :, 6])
 print(f"first entry -> last storer done: {(t_last - t_first) / 1e3:.1f} us; sum of launch spans {total_span:.1f} us")
