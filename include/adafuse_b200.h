@@ -279,9 +279,19 @@ int af_group_destroy(af_group* group);
 /* x_len / y_rows: arrays of n_phases entries (4 is always enough). */
 int af_group_info(const af_group* group, int32_t* n_phases, int32_t* x_len, int32_t* y_rows, int32_t* n_units,
                   int32_t* grid, int64_t* tiles);
+/* flags of af_switch_gemv_chain (af_switch_gemv takes AF_CHAIN_PDL as its `pdl` argument) */
+#define AF_CHAIN_PDL 1           /* programmatic stream serialization, see af_switch_gemv          */
+#define AF_CHAIN_PLAN_PREBUILT 2 /* the block list of (prev, cur, scale, mode) was built by          */
+                                 /* af_plan_build earlier on this stream: skip the per-launch build */
 int af_switch_gemv_chain(af_group* group, const af_decision* prev_dev, const af_decision* cur_dev,
                          int32_t max_k, float scale, int32_t mode, const af_gemv_phase* phases,
-                         int32_t n_phases, int32_t* phase_done_dev, int32_t pdl, void* stream);
+                         int32_t n_phases, int32_t* phase_done_dev, int32_t flags, void* stream);
+/* adapters.py:188-233 (`concat_gated` + `build_switch` bookkeeping) once per token: turns the two
+ * device decisions into the table's block list (experts present on both sides collapse to one block
+ * of weight g_new - g_old).  The launches of the token that pass AF_CHAIN_PLAN_PREBUILT read it
+ * instead of rebuilding it; validation errors surface through af_table_status as usual. */
+int af_plan_build(af_table* table, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k,
+                  float scale, int32_t mode, void* stream);
 int af_switch_gemv(af_group* group, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k,
                    float scale, int32_t mode, const float* xin, const int64_t* acc_in, const float* res,
                    float* h_out, int32_t prologue, const float* norm_w, float eps, int64_t* acc_out,
@@ -291,7 +301,7 @@ int af_switch_gemv(af_group* group, const af_decision* prev_dev, const af_decisi
  * passed, first/last W load issued, storer done, consumers done, then per phase: wait begins,
  * barrier passed, prologue done, first tile computed; then %smid) to buffer_dev + i * stride_elems.
  * buffer_dev == NULL turns the probe off. */
-#define AF_TIMELINE_SLOTS 36
+#define AF_TIMELINE_SLOTS 42
 int af_set_timeline(uint64_t* buffer_dev, int32_t n_launches, int64_t stride_elems);
 int af_accum_to_f32(const int64_t* acc, const float* res, float* out, int32_t n, void* stream);
 int af_attn_decode_fix(const int64_t* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,

@@ -312,6 +312,16 @@ class SwitchTable:
             )
         )
 
+    def build_plan(self, prev, cur, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace") -> None:
+        """Once per token: the block list of (prev, cur) for the switch + GEMV launches that pass
+        plan_prebuilt=True (adapters.py:188-233 bookkeeping, on the device)."""
+        for dec in (prev, cur):
+            if dec is not None and not isinstance(dec, DeviceDecision):
+                raise TypeError("build_plan takes device-resident decisions (DeviceDecision) or None")
+        _capi.check(_capi.lib().af_plan_build(self.device_table.handle, prev.ptr if prev is not None else None,
+                                              cur.ptr if cur is not None else None, int(max_k), float(scale), _MODES[mode],
+                                              _capi.stream_ptr()))
+
     def merge(self, dec, **kw) -> None:
         """merge_all(sign=+1) of one decision (adapters.py:236-258)."""
         self.switch(None, dec, **kw)
@@ -383,7 +393,7 @@ class SegmentGroup:
                                eps=float(eps), prologue=self.PROLOGUES[prologue])
 
     def switch_gemv_chain(self, prev, cur, phases, phase_done=None, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0,
-                          mode: str = "inplace", pdl: bool = False) -> None:
+                          mode: str = "inplace", pdl: bool = False, plan_prebuilt: bool = False) -> None:
         """One launch over every phase of the chain.  `phases`: one dict per phase with the keyword
         arguments of `switch_gemv` (acc_out, xin | acc_in, res, h_out, prologue, norm_w, eps);
         `phase_done`: int32 tensor of n_phases - 1 zeroed counters."""
@@ -400,13 +410,14 @@ class SegmentGroup:
         structs = (_capi.GemvPhase * self.n_phases)(*[self._phase_struct(i, **ph) for i, ph in enumerate(phases)])
         _capi.check(_capi.lib().af_switch_gemv_chain(
             self.handle, prev.ptr if prev is not None else None, cur.ptr if cur is not None else None, int(max_k), float(scale),
-            _MODES[mode], structs, self.n_phases, _ptr(phase_done) if phase_done is not None else None, 1 if pdl else 0,
-            _capi.stream_ptr()))
+            _MODES[mode], structs, self.n_phases, _ptr(phase_done) if phase_done is not None else None,
+            (_capi.AF_CHAIN_PDL if pdl else 0) | (_capi.AF_CHAIN_PLAN_PREBUILT if plan_prebuilt else 0), _capi.stream_ptr()))
 
     def switch_gemv(self, prev, cur, acc_out, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace",
-                    pdl: bool = False, **phase) -> None:
+                    pdl: bool = False, plan_prebuilt: bool = False, **phase) -> None:
         """acc_out (int64, zeroed by the caller) += fix(W_new . prologue(h)); W <- W_new in place."""
-        self.switch_gemv_chain(prev, cur, [dict(acc_out=acc_out, **phase)], None, max_k=max_k, scale=scale, mode=mode, pdl=pdl)
+        self.switch_gemv_chain(prev, cur, [dict(acc_out=acc_out, **phase)], None, max_k=max_k, scale=scale, mode=mode, pdl=pdl,
+                               plan_prebuilt=plan_prebuilt)
 
     def close(self) -> None:
         if getattr(self, "handle", None) is not None and self.handle:

@@ -115,6 +115,7 @@ struct af_table {
     int n_units = 0;
     CUtensorMap* d_maps = nullptr;  // [5][n_segments]: fma live, fma pristine, mma live, mma pristine, UP bank (swizzled)
     int* d_err = nullptr;
+    Plan* d_plan = nullptr;         // af_plan_build target
     bool fast_fma = false, fast_mma = false, has_pristine = false;
     bool rank16 = true;  // every segment's rank is a multiple of 16
     int max_rank = 0, min_experts = 0;
@@ -172,6 +173,7 @@ int af_table_destroy(af_table* t) {
     if (t->d_units) cudaFree(t->d_units);
     if (t->d_maps) cudaFree(t->d_maps);
     if (t->d_err) cudaFree(t->d_err);
+    if (t->d_plan) cudaFree(t->d_plan);
     delete t;
     return AF_OK;
 }
@@ -298,6 +300,8 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         e = cudaMemcpy(t->d_units, units.data(), sizeof(UnitDev) * units.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&t->d_err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(t->d_err, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&t->d_plan, sizeof(Plan));
+    if (e == cudaSuccess) e = cudaMemset(t->d_plan, 0, sizeof(Plan));
     if (e != cudaSuccess) {
         af_table_destroy(t);
         return fail(AF_ECUDA, std::string("table upload: ") + cudaGetErrorString(e));
@@ -738,9 +742,30 @@ int af_group_info(const af_group* g, int32_t* n_phases, int32_t* x_len, int32_t*
     return AF_OK;
 }
 
+int af_plan_build(af_table* t, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k, float scale,
+                  int32_t mode, void* stream) {
+    if (!t) return fail(AF_EVALUE, "table is NULL");
+    if (mode != AF_SWITCH_INPLACE && mode != AF_SWITCH_FROM_PRISTINE) return fail(AF_EVALUE, "unknown switch mode");
+    if (max_k < 1 || max_k > AF_MAX_K) return fail(AF_EVALUE, "max_k outside [1, AF_MAX_K]");
+    SwitchParams p{};
+    p.from_pristine = mode == AF_SWITCH_FROM_PRISTINE;
+    p.prev_dev = prev_dev;
+    p.cur_dev = cur_dev;
+    p.use_dev = 1;
+    p.scale = scale;
+    p.n_experts_limit = t->min_experts;
+    p.err_flag = t->d_err;
+    const int bound = (p.from_pristine || !prev_dev ? 0 : max_k) + (cur_dev ? max_k : 0);
+    p.max_blocks = std::min(bound, kMaxBlocks);
+    plan_build_kernel<<<1, 32, 0, as_stream(stream)>>>(p, t->d_plan);
+    AF_LAUNCH_CHECK("plan_build_kernel");
+    return AF_OK;
+}
+
 int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k, float scale,
-                         int32_t mode, const af_gemv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t pdl,
+                         int32_t mode, const af_gemv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t flags,
                          void* stream) {
+    const int pdl = flags & AF_CHAIN_PDL;
     if (!g) return fail(AF_EVALUE, "group is NULL");
     af_table* t = g->table;
     if (mode != AF_SWITCH_INPLACE && mode != AF_SWITCH_FROM_PRISTINE) return fail(AF_EVALUE, "unknown switch mode");
@@ -778,6 +803,7 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     p.n_experts_limit = t->min_experts;
     p.err_flag = t->d_err;
     p.host_plan.n_blocks = 0;  // no decision at all: a plain GEMV over the live weights
+    p.plan_dev = (use_dev && (flags & AF_CHAIN_PLAN_PREBUILT)) ? t->d_plan : nullptr;
     const int n_blocks_bound = use_dev ? ((from_pristine || !prev_dev ? 0 : max_k) + (cur_dev ? max_k : 0)) : 0;
     p.max_blocks = std::min(n_blocks_bound, kMaxBlocks);
     const int s_bound = n_blocks_bound * t->max_rank;

@@ -68,6 +68,7 @@ struct SwitchParams {
     int n_experts_limit;  // smallest bank over the table: ids outside [0, limit) are rejected
     int max_blocks;       // block-list capacity this launch was sized for (kernel variant, smem)
     int* err_flag;        // device word: set to AF_EINDEX / AF_EVALUE when a device decision is unusable
+    const Plan* plan_dev; // block list built once per token by plan_build_kernel (af_plan_build); NULL: build it here
     Plan host_plan;
 };
 
@@ -168,6 +169,16 @@ __host__ __device__ inline void build_plan(Plan& plan, const af_decision* prev, 
         plan.negate[plan.n_blocks] = 0;
         ++plan.n_blocks;
     }
+}
+
+// One launch per token (af_plan_build): the block list every switch + GEMV launch of the token
+// would otherwise rebuild from the two decisions at its start (2.6 us of serial work per launch).
+__global__ void plan_build_kernel(SwitchParams p, Plan* out) {
+    if (threadIdx.x != 0) return;
+    Plan plan;
+    build_plan(plan, p.from_pristine ? nullptr : p.prev_dev, p.cur_dev, p.scale, false, p.n_experts_limit);
+    if (!plan_usable(p, plan, p.prev_dev, p.cur_dev)) plan.n_blocks = -1;
+    *out = plan;
 }
 
 // ---------------------------------------------------------------------------

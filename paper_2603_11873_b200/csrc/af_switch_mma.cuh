@@ -344,7 +344,20 @@ __host__ __device__ __forceinline__ bool up_swizzled(int rank) { return rank == 
 //   0 entry | 1 plan ready | 2 first slab staged | 3 pdl_wait passed | 4 first W load issued |
 //   5 last W load issued | 6 storer done | 7 consumers done |
 //   8 + 4 * phase: barrier wait begins | +1 barrier passed | +2 prologue done | +3 first tile of the phase computed
-constexpr int kTlSlots = 8 + 4 * 4 + 2 + 6 + 4;  // + [24] = %smid; [26..31]: first unit change inside phase 1
+constexpr int kTlSlots = 8 + 4 * 4 + 2 + 6 + 4 + 6;  // [36..41]: cycles spent waiting, per role  // + [24] = %smid; [26..31]: first unit change inside phase 1
+// mbarrier wait that adds the cycles it blocked to `acc` when the timeline probe is on
+__device__ __forceinline__ void mbar_wait_timed(uint64_t* bar, uint32_t parity, bool on, long long& acc) {
+    if (on) {
+        const long long t0 = clock64();
+        mbar_wait(bar, parity);
+        acc += clock64() - t0;
+    } else {
+        mbar_wait(bar, parity);
+    }
+}
+__device__ __forceinline__ void tl_put(unsigned long long* tl, int slot, long long v) {
+    if (tl) tl[(size_t)blockIdx.x * kTlSlots + slot] = (unsigned long long)v;
+}
 __device__ __forceinline__ void tl_stamp(unsigned long long* tl, int slot) {
     if (tl) {
         unsigned long long t;
@@ -437,12 +450,19 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             mbar_init(&empty[s], kStorers + (GEMV ? 1 : 0));
         }
         fence_mbar_init();
-        if (p.use_dev)
-            build_plan(plan, p.from_pristine ? nullptr : p.prev_dev, p.cur_dev, p.scale, false, p.n_experts_limit);
-        else
-            plan = p.host_plan;
-        if (!plan_usable(p, plan, p.prev_dev, p.cur_dev)) plan.n_blocks = -1;
+        if (!p.plan_dev) {
+            if (p.use_dev)
+                build_plan(plan, p.from_pristine ? nullptr : p.prev_dev, p.cur_dev, p.scale, false, p.n_experts_limit);
+            else
+                plan = p.host_plan;
+            if (!plan_usable(p, plan, p.prev_dev, p.cur_dev)) plan.n_blocks = -1;
+        }
         if constexpr (GEMV) tl_stamp(mp.timeline, 1);
+    }
+    if (p.plan_dev) {  // prebuilt by af_plan_build: one global round trip, concurrent with the barrier setup
+        constexpr int kWords = (int)(sizeof(Plan) / 4);
+        if (tid >= 128 && tid < 128 + kWords)
+            reinterpret_cast<int*>(&plan)[tid - 128] = reinterpret_cast<const int*>(p.plan_dev)[tid - 128];
     }
     __syncthreads();
     const int n_blocks = plan.n_blocks;
@@ -465,12 +485,13 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             const int who = warp - kMmaWarps;
             constexpr int kMine = (kBoxes + kWProd - 1) / kWProd;
             const uint64_t pol = l2_evict_first_policy();
+            long long waited = 0;
             MmaIter ti;
             ti.init(p, unit_cache);
             for (int it = 0; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
-                mbar_wait(&empty[stage], ph ^ 1);
+                mbar_wait_timed(&empty[stage], ph ^ 1, GEMV && mp.timeline, waited);
                 int mine = 0;
 #pragma unroll
                 for (int j = 0; j < kMine; ++j) mine += (who + j * kWProd < kBoxes) ? 1 : 0;
@@ -494,7 +515,10 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 ti.next(p);
             }
             if constexpr (GEMV) {
-                if (who == 0) tl_stamp(mp.timeline, 5);
+                if (who == 0) {
+                    tl_stamp(mp.timeline, 5);
+                    tl_put(mp.timeline, 37, waited);
+                }
             }
         }
         return;
@@ -543,13 +567,14 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             const int who = warp - (kMmaWarps + kWProd + 1);
             constexpr int kMine = (kBoxes + kStorers - 1) / kStorers;
             const uint64_t pol = l2_evict_first_policy();
+            long long waited = 0, waited_read = 0;
             MmaIter ti;
             ti.init(p, unit_cache);
             int it = 0;
             for (; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
-                mbar_wait(&computed[stage], ph);
+                mbar_wait_timed(&computed[stage], ph, GEMV && mp.timeline, waited);
                 if (store_w) {
                     const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
 #pragma unroll
@@ -567,15 +592,21 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 }
                 // the stores of tile it - depth have drained their stage: hand it back
                 const int depth = mp.store_depth;
+                const long long tr0 = (GEMV && mp.timeline) ? clock64() : 0;
                 if (depth <= 0) bulk_wait_read<0>();
                 else if (depth == 1) bulk_wait_read<1>();
                 else if (depth == 2) bulk_wait_read<2>();
                 else bulk_wait_read<3>();
+                if (GEMV && mp.timeline) waited_read += clock64() - tr0;
                 if (it >= depth) mbar_arrive(&empty[(it - depth) % kSt]);
                 ti.next(p);
             }
             bulk_wait_all<0>();  // global writes complete before the CTA retires
-            if constexpr (GEMV) tl_stamp(mp.timeline, 6);
+            if constexpr (GEMV) {
+                tl_stamp(mp.timeline, 6);
+                tl_put(mp.timeline, 38, waited);
+                tl_put(mp.timeline, 39, waited_read);
+            }
         }
         return;
     }
@@ -652,6 +683,8 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
     uint32_t xb0 = 0u, xb1 = 0u;
     int cur_phase = -1, phase_j0 = 0;
     bool tl_first_tile = false, tl_probe = false, tl_probe_done = false;
+    long long cons_waited = 0;
+    const long long cons_t0 = clock64();
     if constexpr (GEMV) {
         if (tid == 0) tl_stamp(mp.timeline, 2);
         if (mp.pdl) {
@@ -786,16 +819,6 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         const int stage = it % kSt;
         const uint32_t ph = (it / kSt) & 1;
         if (new_unit) {
-            if constexpr (GEMV) {
-                if (ti.un.phase != cur_phase) {
-                    cur_phase = ti.un.phase;
-                    enter_phase(cur_phase);
-                }
-                const int xslot = ti.j - phase_j0;
-                const float* xs = xslot < kXSlots ? reinterpret_cast<const float*>(sm + L::off_xs) + xslot * kTN : nullptr;
-                gemv_x_fragment(mp.gv[cur_phase], xs, ti.un.col0, warp, lane, x_inv, xb0, xb1);
-                if (tl_probe) tl_stamp(mp.timeline, 32);
-            }
             // B fragments of this unit's slab -> registers (kept for every tile of the unit)
 #pragma unroll
             for (int half = 0; half < kHalves; ++half)
@@ -834,11 +857,24 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 down_prefetch<KS>(dn_regs, sg_next, plan, S_next, nu.col0, tid);
             }
             if (GEMV && tl_probe) tl_stamp(mp.timeline, 35);
+            // The input vector comes LAST: everything above is independent of it, so at a phase
+            // boundary it runs while this CTA's own partial sums are still being published and the
+            // other CTAs are still arriving.
+            if constexpr (GEMV) {
+                if (ti.un.phase != cur_phase) {
+                    cur_phase = ti.un.phase;
+                    enter_phase(cur_phase);
+                }
+                const int xslot = ti.j - phase_j0;
+                const float* xs = xslot < kXSlots ? reinterpret_cast<const float*>(sm + L::off_xs) + xslot * kTN : nullptr;
+                gemv_x_fragment(mp.gv[cur_phase], xs, ti.un.col0, warp, lane, x_inv, xb0, xb1);
+                if (tl_probe) tl_stamp(mp.timeline, 32);
+            }
         }
         new_unit = ti.next(p);
 
         if (GEMV && tl_probe) tl_stamp(mp.timeline, 29);
-        mbar_wait(&full[stage], ph);
+        mbar_wait_timed(&full[stage], ph, GEMV && mp.timeline, cons_waited);
         if (GEMV && tl_probe) tl_stamp(mp.timeline, 30);
         const uint32_t w_stage = w_base + stage * kWStageBytes + wbox * kBoxBytes + w_off;
         const uint32_t up_stage = up_base + stage * L::up_stage_bytes;
@@ -932,7 +968,11 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         }
     }
     if constexpr (GEMV) {
-        if (tid == 0) tl_stamp(mp.timeline, 7);
+        if (tid == 0) {
+            tl_stamp(mp.timeline, 7);
+            tl_put(mp.timeline, 36, cons_waited);
+            tl_put(mp.timeline, 41, clock64() - cons_t0);
+        }
     }
 }
 

@@ -461,7 +461,8 @@ class LlamaEngine:
         d, eps = cfg.hidden, cfg.rms_eps
         xa, xb = self.x
         prev = self.prev if (with_prev and cfg.switch_mode == "inplace") else None
-        kw = dict(max_k=cfg.top_k, mode=cfg.switch_mode)
+        kw = dict(max_k=cfg.top_k, mode=cfg.switch_mode, plan_prebuilt=True)
+        self.table.build_plan(prev, self.cur, max_k=cfg.top_k, mode=cfg.switch_mode)
         self.acc_arena.zero_()
         self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
         for li in range(cfg.layers):

@@ -25,7 +25,7 @@ forced = np.random.Generator(np.random.PCG64(1)).integers(0, cfg.vocab, 64)
 eng.reset(forced=forced)
 for _ in range(4):
     eng.decode_step()
-SLOTS = 36
+SLOTS = 42
 n_launch = (cfg.layers + 1) if not args.no_chain else 4 * cfg.layers
 grid = _capi.device_info()["sm_count"]
 buf = torch.zeros(n_launch * grid * SLOTS, dtype=torch.int64, device="cuda")
@@ -85,10 +85,17 @@ if not args.no_chain:
         for k, lb in enumerate(labels):
             v = d[:, :, k][has]
             print(f"unit change: {lb:22s} med {np.nanmedian(v):6.2f}  max {np.nanmax(v):6.2f} us  (n={v.size})")
-        fine = tl[1:-1, :, [28, 32, 33, 34, 35, 29]]
+        fine = tl[1:-1, :, [28, 33, 34, 35, 32, 29]]
         df = (fine[:, :, 1:] - fine[:, :, :-1]) / 1e3
-        for k, lb in enumerate(["x fragment", "B fragments (ldmatrix)", "A offsets", "peek + prefetch issue", "ti.next"]):
+        for k, lb in enumerate(["B fragments (ldmatrix)", "A offsets", "peek + prefetch issue", "x fragment", "ti.next"]):
             v = df[:, :, k][has]
             print(f"   setup: {lb:24s} med {np.nanmedian(v):6.2f}  max {np.nanmax(v):6.2f} us")
+# cycles each role spent blocked, as a share of the consumers' lifetime (mean over CTAs and launches)
+life = np.nan_to_num(tl[:, :, 41])
+ok = life > 0
+for slot, nm in ((36, "consumer warp 0 waiting for full[stage] (data)"), (37, "W producer waiting for empty[stage] (ring full)"),
+                 (38, "storer waiting for computed[stage]"), (39, "storer waiting for its stores to drain smem")):
+    v = np.nan_to_num(tl[:, :, slot])[ok] / life[ok]
+    print(f"blocked: {nm:52s} mean {100 * v.mean():5.1f} %  max {100 * v.max():5.1f} %")
 t_last = np.nanmax(tl[-1, :, 6])
 print(f"first entry -> last storer done: {(t_last - t_first) / 1e3:.1f} us; sum of launch spans {total_span:.1f} us")
