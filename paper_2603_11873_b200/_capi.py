@@ -12,7 +12,8 @@ import os
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libadafuse_b200.so")
+# AF_LIB_PATH: an alternative build of the same library (kernel-variant A/B runs on one box)
+LIB_PATH = os.environ.get("AF_LIB_PATH") or os.path.join(HERE, "libadafuse_b200.so")
 
 AF_ABI_VERSION = 2
 AF_OK, AF_EVALUE, AF_EDIM, AF_EPRECISION, AF_EALIAS, AF_EINPUT, AF_ESTATE, AF_EINDEX, AF_ECUDA = range(9)

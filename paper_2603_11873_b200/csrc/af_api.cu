@@ -118,6 +118,7 @@ struct af_table {
     Plan* d_plan = nullptr;         // af_plan_build target
     bool fast_fma = false, fast_mma = false, has_pristine = false;
     bool rank16 = true;  // every segment's rank is a multiple of 16
+    bool mixed_rank = false;
     int max_rank = 0, min_experts = 0;
     long long target_elems = 0;
     int sm_count = 0;
@@ -265,6 +266,7 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         // ranks fetched through the swizzled UP map need the bank packed as one [N * d_out][rank] matrix
         if (up_swizzled(s.rank) && s.up_expert_stride != (long long)s.d_out * s.rank) mma_ok = false;
         if (s.rank % 16 != 0) t->rank16 = false;
+        if (s.rank != segments[0].rank) t->mixed_rank = true;
     }
     t->fast_fma = fma_ok;
     t->fast_mma = mma_ok;
@@ -366,12 +368,12 @@ int af_table_status(af_table* t, void* stream) {
 
 namespace af {
 
-template <int KS, bool BA, bool GEMV = false>
+template <int KS, bool BA, bool GEMV = false, bool TL = false>
 static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     using L = MmaLayout<KS, BA, GEMV>;
     static bool configured = false;
     if (!configured) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS, BA, GEMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS, BA, GEMV, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured = true;
     }
     MmaParams mp2 = mp;
@@ -396,9 +398,9 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = mp2.pdl ? 1 : 0;
-        AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_mma_kernel<KS, BA, GEMV>, mp2));
+        AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_mma_kernel<KS, BA, GEMV, TL>, mp2));
     } else {
-        switch_mma_kernel<KS, BA, GEMV><<<grid, kMmaThreads, L::total, st>>>(mp2);
+        switch_mma_kernel<KS, BA, GEMV, TL><<<grid, kMmaThreads, L::total, st>>>(mp2);
     }
     AF_LAUNCH_CHECK("switch_mma_kernel");
     return AF_OK;
@@ -497,6 +499,7 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
         mp.tmaps_ld = t->d_maps + (size_t)(p.from_pristine ? 3 : 2) * S;
         mp.tmaps_st = t->d_maps + (size_t)2 * S;
         mp.tmaps_up = t->d_maps + (size_t)4 * S;
+        mp.mixed_rank = t->mixed_rank ? 1 : 0;
         const int grid = std::min(t->n_units, t->sm_count);
         const int ks = std::max(1, (s_bound + 15) / 16);
         // block-accumulate form when every block is a whole number of rank-16 steps and the hi/lo
@@ -828,12 +831,14 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     mp.n_phases = n_phases;
     mp.phase_done = phase_done_dev;
     mp.seg_yoff = g->d_seg_yoff;
+    mp.mixed_rank = t->mixed_rank ? 1 : 0;
     mp.n_chain_segs = (int)g->segs.size();
     for (size_t i = 0; i < g->segs.size(); ++i) mp.chain_segs[i] = g->segs[i];
     mp.pdl = (pdl && g_pdl.load()) ? 1 : 0;
     static const int env_dbg = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
     mp.dbg = env_dbg ^ 24;
-    if (g_timeline && g_timeline_left > 0) {
+    const int ks_tl = std::max(1, (s_bound + 15) / 16);
+    if (g_timeline && g_timeline_left > 0 && ks_tl == 2) {  // the probe is compiled into the KS = 2 hi/lo variant only
         mp.timeline = g_timeline;
         g_timeline += g_timeline_stride;
         --g_timeline_left;
@@ -844,6 +849,7 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     if (env_dbg & 4) {  // experiment: the plain switch kernel on this group's schedule (no GEMV at all)
         if (ks == 2) return launch_mma<2, false, false>(mp, g->grid, st);
     }
+    if (mp.timeline && ks == 2) return launch_mma<2, false, true, true>(mp, g->grid, st);
     switch (ks) {
         case 1: return launch_mma<1, false, true>(mp, g->grid, st);
         case 2: return launch_mma<2, false, true>(mp, g->grid, st);

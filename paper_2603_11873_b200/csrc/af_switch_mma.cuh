@@ -30,6 +30,9 @@ namespace af {
 #ifndef AF_WPROD
 #define AF_WPROD 1      /* threads (one per warp) issuing the W box loads */
 #endif
+#ifndef AF_W_EARLY
+#define AF_W_EARLY 0    /* W fragments of a tile are loaded before its MMAs (1) or after them (0) */
+#endif
 #ifndef AF_STORERS
 #define AF_STORERS 1    /* threads (one per warp) issuing the W box stores */
 #endif
@@ -100,11 +103,33 @@ __device__ __forceinline__ void stmatrix_x4(uint32_t addr, const uint32_t (&r)[4
                  "r"(r[2]), "r"(r[3])
                  : "memory");
 }
+// (not volatile: a pure register operation the compiler may interleave with its neighbours)
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// mbarrier / shared-store forms that take the 32-bit shared address directly (computed once per
+// unit of work instead of being re-derived from a generic pointer at every use)
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 // 1-D bulk copy global -> smem, completes on bar (bytes % 16 == 0, both sides 16-byte aligned).
 __device__ __forceinline__ void bulk_load_1d(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -188,6 +213,7 @@ struct MmaParams {
     int pdl;                       // launched with programmatic stream serialization
     // optional timeline probe (af_set_timeline): [gridDim.x][kTlSlots] globaltimer stamps of this launch
     unsigned long long* timeline;
+    int mixed_rank;                // the table's segments do not all have the same rank
     int dbg;                       // experiments (env AF_DBG): 4 = plain switch kernel on the group schedule
     const CUtensorMap* tmaps_ld;   // per segment: 32 x 64 swizzled box on the source (live or pristine)
     const CUtensorMap* tmaps_st;   // per segment: the same box shape on the live matrix
@@ -408,7 +434,8 @@ __device__ __forceinline__ void gemv_x_fragment(const GemvParams& g, const float
     xb1 = n == 0 ? pack_bf16x2(h2, h3) : (n == 1 ? pack_bf16x2(l2, l3) : 0u);
 }
 
-template <int KS, bool BA, bool GEMV>
+// TL: timeline probe compiled in (af_set_timeline); the production instantiations carry none of it.
+template <int KS, bool BA, bool GEMV, bool TL = false>
 __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switch_mma_kernel(const __grid_constant__ MmaParams mp) {
     using L = MmaLayout<KS, BA, GEMV>;
     constexpr int kSt = L::stages < kMmaDefaultStages ? L::stages : kMmaDefaultStages;
@@ -432,12 +459,15 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
     if constexpr (GEMV) {
         if (tid >= 64 && tid < 64 + mp.n_chain_segs) seg_cache[tid - 64] = p.segs[mp.chain_segs[tid - 64]];
     }
+    // the UP ring starts as zeros (see need_mask)
+    for (int i = tid * 16; i < kSt * L::up_stage_bytes; i += (int)blockDim.x * 16)
+        *reinterpret_cast<uint4*>(sm + L::off_up + i) = make_uint4(0u, 0u, 0u, 0u);
     // descriptor of a unit's segment
     auto seg_of = [&](const UnitDev& un) -> SegDev { return GEMV ? seg_cache[un.slot] : p.segs[un.seg]; };
 
     if (tid == 0) {
         if constexpr (GEMV) {
-            tl_stamp(mp.timeline, 0);
+            if constexpr (TL) tl_stamp(mp.timeline, 0);
             if (mp.timeline) {
                 unsigned smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -457,7 +487,7 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 plan = p.host_plan;
             if (!plan_usable(p, plan, p.prev_dev, p.cur_dev)) plan.n_blocks = -1;
         }
-        if constexpr (GEMV) tl_stamp(mp.timeline, 1);
+        if constexpr (GEMV) if constexpr (TL) tl_stamp(mp.timeline, 1);
     }
     if (p.plan_dev) {  // prebuilt by af_plan_build: one global round trip, concurrent with the barrier setup
         constexpr int kWords = (int)(sizeof(Plan) / 4);
@@ -491,13 +521,13 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             for (int it = 0; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
-                mbar_wait_timed(&empty[stage], ph ^ 1, GEMV && mp.timeline, waited);
+                mbar_wait_timed(&empty[stage], ph ^ 1, TL && mp.timeline, waited);
                 int mine = 0;
 #pragma unroll
                 for (int j = 0; j < kMine; ++j) mine += (who + j * kWProd < kBoxes) ? 1 : 0;
                 mbar_expect_tx(&full[stage], mine * kBoxBytes);
                 if constexpr (GEMV) {
-                    if (who == 0 && it == 0) tl_stamp(mp.timeline, 4);
+                    if (who == 0 && it == 0) if constexpr (TL) tl_stamp(mp.timeline, 4);
                 }
                 const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
 #pragma unroll
@@ -516,8 +546,8 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             }
             if constexpr (GEMV) {
                 if (who == 0) {
-                    tl_stamp(mp.timeline, 5);
-                    tl_put(mp.timeline, 37, waited);
+                    if constexpr (TL) tl_stamp(mp.timeline, 5);
+                    if constexpr (TL) tl_put(mp.timeline, 37, waited);
                 }
             }
         }
@@ -574,7 +604,7 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             for (; ti.valid(p); ++it) {
                 const int stage = it % kSt;
                 const uint32_t ph = (it / kSt) & 1;
-                mbar_wait_timed(&computed[stage], ph, GEMV && mp.timeline, waited);
+                mbar_wait_timed(&computed[stage], ph, TL && mp.timeline, waited);
                 if (store_w) {
                     const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
 #pragma unroll
@@ -592,20 +622,20 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 }
                 // the stores of tile it - depth have drained their stage: hand it back
                 const int depth = mp.store_depth;
-                const long long tr0 = (GEMV && mp.timeline) ? clock64() : 0;
+                const long long tr0 = (TL && mp.timeline) ? clock64() : 0;
                 if (depth <= 0) bulk_wait_read<0>();
                 else if (depth == 1) bulk_wait_read<1>();
                 else if (depth == 2) bulk_wait_read<2>();
                 else bulk_wait_read<3>();
-                if (GEMV && mp.timeline) waited_read += clock64() - tr0;
+                if (TL && mp.timeline) waited_read += clock64() - tr0;
                 if (it >= depth) mbar_arrive(&empty[(it - depth) % kSt]);
                 ti.next(p);
             }
             bulk_wait_all<0>();  // global writes complete before the CTA retires
             if constexpr (GEMV) {
-                tl_stamp(mp.timeline, 6);
-                tl_put(mp.timeline, 38, waited);
-                tl_put(mp.timeline, 39, waited_read);
+                if constexpr (TL) tl_stamp(mp.timeline, 6);
+                if constexpr (TL) tl_put(mp.timeline, 38, waited);
+                if constexpr (TL) tl_put(mp.timeline, 39, waited_read);
             }
         }
         return;
@@ -684,22 +714,22 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
     int cur_phase = -1, phase_j0 = 0;
     bool tl_first_tile = false, tl_probe = false, tl_probe_done = false;
     long long cons_waited = 0;
-    const long long cons_t0 = clock64();
+    const long long cons_t0 = TL ? clock64() : 0;
     if constexpr (GEMV) {
-        if (tid == 0) tl_stamp(mp.timeline, 2);
+        if (tid == 0) if constexpr (TL) tl_stamp(mp.timeline, 2);
         if (mp.pdl) {
             pdl_wait();
             // the dependent may start (its own pre-wait part reads nothing this chain writes later
             // than one kernel back); triggered after the wait so the chain stays one kernel deep
             if (tid == 0) pdl_launch_dependents();
         }
-        if (tid == 0) tl_stamp(mp.timeline, 3);
+        if (tid == 0) if constexpr (TL) tl_stamp(mp.timeline, 3);
     }
     // Entering phase ph of the chain: wait until every CTA has published its partial sums of phase
     // ph - 1, then the prologue over the whole input vector (RMSNorm scale, residual stream out).
     auto enter_phase = [&](int ph) {
         const GemvParams& g = mp.gv[ph];
-        if (tid == 0) tl_stamp(mp.timeline, 8 + 4 * ph);
+        if (tid == 0) if constexpr (TL) tl_stamp(mp.timeline, 8 + 4 * ph);
         if (ph > 0) {
             if (tid == 0) {
                 const int target = (int)gridDim.x;
@@ -717,7 +747,7 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             }
             named_bar_sync(1, kMmaConsumers);
         }
-        if (tid == 0) tl_stamp(mp.timeline, 9 + 4 * ph);
+        if (tid == 0) if constexpr (TL) tl_stamp(mp.timeline, 9 + 4 * ph);
         x_inv = 1.0f;
         // Input-vector strips of this CTA's units of the phase (at most kXSlots of them) are staged in
         // shared memory now: their loads go out together with the whole-vector pass below -- ONE
@@ -796,11 +826,12 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             }
             named_bar_sync(1, kMmaConsumers);  // strips visible to every consumer warp
         }
-        if (tid == 0) tl_stamp(mp.timeline, 10 + 4 * ph);
+        if (tid == 0) if constexpr (TL) tl_stamp(mp.timeline, 10 + 4 * ph);
         tl_first_tile = true;
     };
     bool new_unit = true;
     constexpr int kHalves = BA ? 1 : 2;
+    constexpr int kMT = kMR / 16;
     uint32_t bfr[kHalves][KS][4];
     float gate[KS];  // BA: signed gate of the block each rank-16 step belongs to (0 past the stacked rank)
 #pragma unroll
@@ -810,14 +841,18 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
     const int lrow = (mi & 1) * 8 + rr;                               // row inside an m16 tile this lane addresses
     const uint32_t w_off = lrow * 128 + ((wchunk ^ rr) << 4);         // (row & 7) == rr for every m16 tile
     uint32_t a_off[KS];                                               // A-fragment byte offset inside the UP stage
-    uint32_t a_keep_lo[KS], a_keep_hi[KS];                            // 0 / ~0: zero the fragment halves past S
+    uint32_t a_keep_lo[KS], a_keep_hi[KS];                            // (switch-only loop) 0 / ~0: zero the fragment halves past S
     uint32_t a_mt_stride = 0;
-    SegDev sg_next = sg;
-    int S_next = 0;
+    bool need_mask = false;       // the stacked rank does not fill the last rank-16 step: zero the A fragments past it
+    int rank_next = sg.rank, S_next = 0;
     bool have_next = false;
-    for (int it = 0; ti.valid(p); ++it) {
-        const int stage = it % kSt;
-        const uint32_t ph = (it / kSt) & 1;
+    // shared addresses of the ring, advanced with the stage instead of being rebuilt per tile
+    const uint32_t w_lane_base = w_base + wbox * kBoxBytes + w_off;
+    const uint32_t full_u32 = smem_u32(full), computed_u32 = smem_u32(computed);
+    const uint32_t part_lane = smem_u32(sm + L::off_part) + (warp * kMR + (lane >> 2)) * 4;
+    int stage = 0;
+    uint32_t ph = 0;
+    for (; ti.valid(p);) {
         if (new_unit) {
             // B fragments of this unit's slab -> registers (kept for every tile of the unit)
 #pragma unroll
@@ -831,8 +866,12 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
 #pragma unroll
                 for (int j = 0; j < KS; ++j) gate[j] = (16 * j < S) ? plan.weight[(16 * j) / sg.rank] : 0.f;
             }
-            if (GEMV && tl_probe) tl_stamp(mp.timeline, 33);
+            if (TL && tl_probe) tl_stamp(mp.timeline, 33);
             a_mt_stride = 16 * sg.rank * 2;
+            // With one rank for the whole table a block's slot in the UP ring never moves, so the slots
+            // past the stacked rank keep the zeros the ring was initialised with; only tables that mix
+            // ranks can leave another segment's rows there.
+            need_mask = mp.mixed_rank && S != KS * 16;
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
                 const int k0 = 16 * j + (mi >> 1) * 8;  // first rank of the 8x8 matrix this lane addresses
@@ -847,16 +886,17 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 a_keep_lo[j] = (16 * j < S) ? 0xffffffffu : 0u;
                 a_keep_hi[j] = (16 * j + 8 < S) ? 0xffffffffu : 0u;
             }
-            if (GEMV && tl_probe) tl_stamp(mp.timeline, 34);
+            if (TL && tl_probe) tl_stamp(mp.timeline, 34);
             // start fetching the NEXT unit's DOWN rows; they are committed to the slab at its start
             const UnitDev nu = ti.peek(p);
             have_next = nu.rows > 0;
             if (have_next) {
-                sg_next = seg_of(nu);
-                S_next = n_blocks * sg_next.rank;
-                down_prefetch<KS>(dn_regs, sg_next, plan, S_next, nu.col0, tid);
+                const SegDev sn = seg_of(nu);
+                rank_next = sn.rank;
+                S_next = n_blocks * sn.rank;
+                down_prefetch<KS>(dn_regs, sn, plan, S_next, nu.col0, tid);
             }
-            if (GEMV && tl_probe) tl_stamp(mp.timeline, 35);
+            if (TL && tl_probe) tl_stamp(mp.timeline, 35);
             // The input vector comes LAST: everything above is independent of it, so at a phase
             // boundary it runs while this CTA's own partial sums are still being published and the
             // other CTAs are still arriving.
@@ -868,79 +908,168 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                 const int xslot = ti.j - phase_j0;
                 const float* xs = xslot < kXSlots ? reinterpret_cast<const float*>(sm + L::off_xs) + xslot * kTN : nullptr;
                 gemv_x_fragment(mp.gv[cur_phase], xs, ti.un.col0, warp, lane, x_inv, xb0, xb1);
-                if (tl_probe) tl_stamp(mp.timeline, 32);
+                if (TL && tl_probe) tl_stamp(mp.timeline, 32);
             }
         }
         new_unit = ti.next(p);
 
-        if (GEMV && tl_probe) tl_stamp(mp.timeline, 29);
-        mbar_wait_timed(&full[stage], ph, GEMV && mp.timeline, cons_waited);
-        if (GEMV && tl_probe) tl_stamp(mp.timeline, 30);
-        const uint32_t w_stage = w_base + stage * kWStageBytes + wbox * kBoxBytes + w_off;
+        if (TL && tl_probe) tl_stamp(mp.timeline, 29);
+        if constexpr (TL) {
+            mbar_wait_timed(&full[stage], ph, mp.timeline != nullptr, cons_waited);
+        } else {
+            mbar_wait_u32(full_u32 + stage * 8, ph);
+        }
+        if (TL && tl_probe) tl_stamp(mp.timeline, 30);
+        const uint32_t w_stage = w_lane_base + stage * kWStageBytes;
         const uint32_t up_stage = up_base + stage * L::up_stage_bytes;
+        if constexpr (!GEMV) {
+            // Switch only: one m16 half at a time, W fragment first.  (Measured on one box against
+            // the interleaved form below: 4.68 vs 4.83 ms on the Llama-2-7B table -- without the
+            // GEMV's extra work the shorter live ranges win; with it the four-chain form does.)
 #pragma unroll
-        for (int mt = 0; mt < kMR / 16; ++mt) {
-            const uint32_t waddr = w_stage + mt * (16 * 128);
-            uint32_t wv[4];
-            ldmatrix_x4(wv, waddr);
-            // A fragments (UP rows); ranks past S are padding and read as 0 (the slab rows are 0 too)
-            uint32_t afrag[KS][4];
-#pragma unroll
-            for (int j = 0; j < KS; ++j) {
-                ldmatrix_x4(afrag[j], up_stage + a_off[j] + mt * a_mt_stride);
-                afrag[j][0] &= a_keep_lo[j];
-                afrag[j][1] &= a_keep_lo[j];
-                afrag[j][2] &= a_keep_hi[j];
-                afrag[j][3] &= a_keep_hi[j];
-            }
-            float acc[2][4];
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-            if constexpr (BA) {
+            for (int mt = 0; mt < kMT; ++mt) {
+                const uint32_t waddr = w_stage + mt * (16 * 128);
+                uint32_t wv[4];
+                ldmatrix_x4(wv, waddr);
+                // A fragments (UP rows); ranks past S are padding and read as 0 (the slab rows are 0 too)
+                uint32_t afrag[KS][4];
 #pragma unroll
                 for (int j = 0; j < KS; ++j) {
-                    float pr[2][4] = {};
-                    mma_bf16_16816(pr[0], afrag[j], bfr[0][j][0], bfr[0][j][1]);
-                    mma_bf16_16816(pr[1], afrag[j], bfr[0][j][2], bfr[0][j][3]);
-#pragma unroll
-                    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) acc[nt][e] = fmaf(gate[j], pr[nt][e], acc[nt][e]);
+                    ldmatrix_x4(afrag[j], up_stage + a_off[j] + mt * a_mt_stride);
+                    afrag[j][0] &= a_keep_lo[j];
+                    afrag[j][1] &= a_keep_lo[j];
+                    afrag[j][2] &= a_keep_hi[j];
+                    afrag[j][3] &= a_keep_hi[j];
                 }
-            } else {
+                float acc[2][4];
 #pragma unroll
-                for (int half = 0; half < 2; ++half)
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+                if constexpr (BA) {
 #pragma unroll
                     for (int j = 0; j < KS; ++j) {
-                        mma_bf16_16816(acc[0], afrag[j], bfr[half][j][0], bfr[half][j][1]);
-                        mma_bf16_16816(acc[1], afrag[j], bfr[half][j][2], bfr[half][j][3]);
+                        float pr[2][4] = {};
+                        mma_bf16_16816(pr[0], afrag[j], bfr[0][j][0], bfr[0][j][1]);
+                        mma_bf16_16816(pr[1], afrag[j], bfr[0][j][2], bfr[0][j][3]);
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) acc[nt][e] = fmaf(gate[j], pr[nt][e], acc[nt][e]);
                     }
+                } else {
+#pragma unroll
+                    for (int half = 0; half < 2; ++half)
+#pragma unroll
+                        for (int j = 0; j < KS; ++j) {
+                            mma_bf16_16816(acc[0], afrag[j], bfr[half][j][0], bfr[half][j][1]);
+                            mma_bf16_16816(acc[1], afrag[j], bfr[half][j][2], bfr[half][j][3]);
+                        }
+                }
+                // W + D, rounded RNE to bf16, written back in place (swizzled smem)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const uint32_t a = wv[nt * 2], b2 = wv[nt * 2 + 1];
+                    wv[nt * 2] = pack_bf16x2(bf16lo_to_f32(a) + acc[nt][0], bf16hi_to_f32(a) + acc[nt][1]);
+                    wv[nt * 2 + 1] = pack_bf16x2(bf16lo_to_f32(b2) + acc[nt][2], bf16hi_to_f32(b2) + acc[nt][3]);
+                }
+                stmatrix_x4(waddr, wv);
+            }
+        } else {
+            // Both m16 halves of the tile advance together: four independent accumulator chains
+            // (2 halves x 2 n8 tiles) instead of two, so a dependent HMMA never waits alone.
+            uint32_t wv[kMT][4];
+    #if AF_W_EARLY
+    #pragma unroll
+            for (int mt = 0; mt < kMT; ++mt) ldmatrix_x4(wv[mt], w_stage + mt * (16 * 128));   // in flight under the MMAs
+    #endif
+            float acc[kMT][2][4];
+    #pragma unroll
+            for (int mt = 0; mt < kMT; ++mt)
+    #pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+    #pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+    #pragma unroll
+            for (int j = 0; j < KS; ++j) {
+                // A fragments (UP rows) of rank step j for both halves
+                uint32_t afrag[kMT][4];
+    #pragma unroll
+                for (int mt = 0; mt < kMT; ++mt) ldmatrix_x4(afrag[mt], up_stage + a_off[j] + mt * a_mt_stride);
+                if (need_mask) {  // ranks past S are padding: the ring may hold stale data there, read it as 0
+                    asm volatile("" ::: "memory");  // keep this a branch: the common case must not pay for the selects
+                    const uint32_t keep_lo = (16 * j < S) ? 0xffffffffu : 0u, keep_hi = (16 * j + 8 < S) ? 0xffffffffu : 0u;
+    #pragma unroll
+                    for (int mt = 0; mt < kMT; ++mt) {
+                        afrag[mt][0] &= keep_lo;
+                        afrag[mt][1] &= keep_lo;
+                        afrag[mt][2] &= keep_hi;
+                        afrag[mt][3] &= keep_hi;
+                    }
+                }
+                if constexpr (BA) {
+    #pragma unroll
+                    for (int mt = 0; mt < kMT; ++mt) {
+                        float pr[2][4] = {};
+                        mma_bf16_16816(pr[0], afrag[mt], bfr[0][j][0], bfr[0][j][1]);
+                        mma_bf16_16816(pr[1], afrag[mt], bfr[0][j][2], bfr[0][j][3]);
+    #pragma unroll
+                        for (int nt = 0; nt < 2; ++nt)
+    #pragma unroll
+                            for (int e = 0; e < 4; ++e) acc[mt][nt][e] = fmaf(gate[j], pr[nt][e], acc[mt][nt][e]);
+                    }
+                } else {
+    #pragma unroll
+                    for (int half = 0; half < 2; ++half)
+    #pragma unroll
+                        for (int mt = 0; mt < kMT; ++mt) {
+                            mma_bf16_16816(acc[mt][0], afrag[mt], bfr[half][j][0], bfr[half][j][1]);
+                            mma_bf16_16816(acc[mt][1], afrag[mt], bfr[half][j][2], bfr[half][j][3]);
+                        }
+                }
             }
             // W + D, rounded RNE to bf16, written back in place (swizzled smem)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const uint32_t a = wv[nt * 2], b2 = wv[nt * 2 + 1];
-                wv[nt * 2] = pack_bf16x2(bf16lo_to_f32(a) + acc[nt][0], bf16hi_to_f32(a) + acc[nt][1]);
-                wv[nt * 2 + 1] = pack_bf16x2(bf16lo_to_f32(b2) + acc[nt][2], bf16hi_to_f32(b2) + acc[nt][3]);
+    #if !AF_W_EARLY
+    #pragma unroll
+            for (int mt = 0; mt < kMT; ++mt) ldmatrix_x4(wv[mt], w_stage + mt * (16 * 128));
+    #endif
+    #pragma unroll
+            for (int mt = 0; mt < kMT; ++mt) {
+    #pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const uint32_t a = wv[mt][nt * 2], b2 = wv[mt][nt * 2 + 1];
+                    wv[mt][nt * 2] = pack_bf16x2(bf16lo_to_f32(a) + acc[mt][nt][0], bf16hi_to_f32(a) + acc[mt][nt][1]);
+                    wv[mt][nt * 2 + 1] = pack_bf16x2(bf16lo_to_f32(b2) + acc[mt][nt][2], bf16hi_to_f32(b2) + acc[mt][nt][3]);
+                }
+                stmatrix_x4(w_stage + mt * (16 * 128), wv[mt]);
             }
-            stmatrix_x4(waddr, wv);
             if constexpr (GEMV) {
                 // the rounded tile is an A fragment as it stands: y[16 rows] = Wnew[16 x 16] . x[16]
-                float yv[4] = {0.f, 0.f, 0.f, 0.f};
-                mma_bf16_16816(yv, wv, xb0, xb1);
+                float yv[kMT][4];
+    #pragma unroll
+                for (int mt = 0; mt < kMT; ++mt) {
+    #pragma unroll
+                    for (int e = 0; e < 4; ++e) yv[mt][e] = 0.f;
+                    mma_bf16_16816(yv[mt], wv[mt], xb0, xb1);
+                }
                 if ((lane & 3) == 0) {  // columns n = 0 (hi) and n = 1 (lo) of rows lane/4 and lane/4 + 8
-                    float* part = reinterpret_cast<float*>(sm + L::off_part + stage * L::part_stage_bytes) + warp * kMR + mt * 16;
-                    part[lane >> 2] = yv[0] + yv[1];
-                    part[(lane >> 2) + 8] = yv[2] + yv[3];
+                    const uint32_t pa = part_lane + stage * L::part_stage_bytes;
+    #pragma unroll
+                    for (int mt = 0; mt < kMT; ++mt) {
+                        st_shared_f32(pa + mt * 64, yv[mt][0] + yv[mt][1]);
+                        st_shared_f32(pa + mt * 64 + 32, yv[mt][2] + yv[mt][3]);
+                    }
                 }
             }
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA store
         __syncwarp();
-        if (lane == 0) mbar_arrive(&computed[stage]);
-        if constexpr (GEMV) {
+        if (lane == 0) mbar_arrive_u32(computed_u32 + stage * 8);
+        if (++stage == kSt) {
+            stage = 0;
+            ph ^= 1;
+        }
+        if constexpr (TL) {
             if (tl_probe) {
                 tl_stamp(mp.timeline, 31);
                 tl_probe = false;
@@ -952,11 +1081,11 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
         }
 
         if (new_unit && have_next) {
-            const bool probe = GEMV && tid == 0 && cur_phase == 1 && ti.valid(p) && ti.un.phase == 1 && !tl_probe_done;
+            const bool probe = TL && tid == 0 && cur_phase == 1 && ti.valid(p) && ti.un.phase == 1 && !tl_probe_done;
             if (probe) tl_stamp(mp.timeline, 26);
             named_bar_sync(1, kMmaConsumers);  // every warp holds its B fragments: the slab may be rewritten
             if (probe) tl_stamp(mp.timeline, 27);
-            sg = sg_next;
+            sg.rank = rank_next;
             S = S_next;
             down_commit<KS, BA>(down_smem, dn_regs, sg.rank, plan, S, tid);
             named_bar_sync(1, kMmaConsumers);  // next slab visible
@@ -967,7 +1096,7 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
             }
         }
     }
-    if constexpr (GEMV) {
+    if constexpr (TL) {
         if (tid == 0) {
             tl_stamp(mp.timeline, 7);
             tl_put(mp.timeline, 36, cons_waited);
