@@ -215,6 +215,25 @@ int af_embed(const void* table, int32_t dtype, int32_t d, const int32_t* token_d
 int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const float* x, float* out,
                   int32_t prologue, const float* norm_w, float eps, int32_t epilogue, const float* res,
                   void* stream);
+/* af_gemv_chain : up to four af_gemv_fused calls whose inputs depend on each other's outputs
+ *    (o -> gate|up -> down -> next layer's q|k|v, or -> lm_head) as ONE persistent launch.  The
+ *    weights of every phase stream through one shared-memory ring without stopping at a phase
+ *    boundary; only the consumers wait there (phase_done_dev: n_phases - 1 int32 counters, zeroed by
+ *    the caller).  Same arithmetic contract as af_gemv_fused per phase; a row is summed by one warp
+ *    in a fixed order.  The launch is one CTA per SM, all co-resident. */
+typedef struct af_gv_phase {
+    const void* w;       /* rows x cols bf16, row pitch ld                                  */
+    int32_t rows, cols;
+    int64_t ld;
+    const float* x;      /* cols entries (2 * cols for AF_PRO_SILU_MUL)                      */
+    float* out;          /* rows entries                                                     */
+    const float* res;    /* epilogue residual or NULL                                        */
+    const float* norm_w; /* RMSNorm weight or NULL                                           */
+    float eps;
+    int32_t prologue, epilogue;
+} af_gv_phase;
+int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t pdl,
+                  void* stream);
 int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table,
                    const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
                    int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,

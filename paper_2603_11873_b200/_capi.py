@@ -83,6 +83,24 @@ class GemvPhase(ctypes.Structure):
     ]
 
 
+class GvPhase(ctypes.Structure):
+    """`af_gv_phase`: one projection of a chained plain-GEMV launch."""
+
+    _fields_ = [
+        ("w", ctypes.c_void_p),
+        ("rows", ctypes.c_int32),
+        ("cols", ctypes.c_int32),
+        ("ld", ctypes.c_int64),
+        ("x", ctypes.c_void_p),
+        ("out", ctypes.c_void_p),
+        ("res", ctypes.c_void_p),
+        ("norm_w", ctypes.c_void_p),
+        ("eps", ctypes.c_float),
+        ("prologue", ctypes.c_int32),
+        ("epilogue", ctypes.c_int32),
+    ]
+
+
 assert ctypes.sizeof(Decision) == 128
 
 _vp = ctypes.c_void_p
@@ -123,6 +141,7 @@ SIGNATURES = {
     "af_group_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
     "af_switch_gemv_chain": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, ctypes.POINTER(GemvPhase), _i32, _vp, _i32, _vp]),
     "af_switch_gemv": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _i32, _vp]),
+    "af_gemv_chain": (ctypes.c_int, [ctypes.POINTER(GvPhase), _i32, _vp, _i32, _vp]),
     "af_plan_build": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp]),
     "af_set_timeline": (ctypes.c_int, [_vp, _i32, _i64]),
     "af_accum_to_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp]),

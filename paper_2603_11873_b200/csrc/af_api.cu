@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "af_decode.cuh"
+#include "af_gemv_chain.cuh"
 #include "af_llama.cuh"
 #include "af_switch_mma.cuh"
 
@@ -1060,6 +1061,73 @@ static int attn_decode_impl(const float* qkv, const long long* qkv_fix, void* k_
                             const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
                             int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace, int32_t* tickets, float* out,
                             void* stream);
+
+int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t pdl, void* stream) {
+    if (!phases || n_phases < 1 || n_phases > kGcMaxPhases) return fail(AF_EVALUE, "a GEMV chain has 1..4 phases");
+    if (n_phases > 1 && !phase_done_dev) return fail(AF_EVALUE, "a chain of several phases needs its phase_done counters");
+    const DeviceInfo& di = device_info();
+    if (!di.ok) return fail(AF_ECUDA, "no CUDA device");
+    GcParams gp{};
+    int max_cols = 0;
+    long long max_rows = 0;
+    for (int i = 0; i < n_phases; ++i) {
+        const af_gv_phase& f = phases[i];
+        if (f.rows < 1 || f.cols < 1 || f.ld < f.cols) return fail(AF_EDIM, "bad GEMV shape");
+        if (f.cols % 8 != 0 || f.ld % 8 != 0 || (reinterpret_cast<uintptr_t>(f.w) & 15) != 0)
+            return fail(AF_EDIM, "chained GEMV needs 16-byte aligned bf16 rows (cols % 8 == 0)");
+        if (f.prologue < AF_PRO_NONE || f.prologue > AF_PRO_SILU_MUL) return fail(AF_EVALUE, "unknown prologue");
+        if (f.prologue == AF_PRO_RMSNORM && !f.norm_w) return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
+        if (f.epilogue < AF_EPI_NONE || f.epilogue > AF_EPI_RESIDUAL) return fail(AF_EVALUE, "unknown epilogue");
+        if (f.epilogue != AF_EPI_NONE && !f.res) return fail(AF_EVALUE, "epilogue needs a residual vector");
+        if (!f.w || !f.x || !f.out) return fail(AF_EVALUE, "NULL argument");
+        if (f.out == f.x) return fail(AF_EALIAS, "GEMV output aliases its input");
+        if ((reinterpret_cast<uintptr_t>(f.x) & 15) != 0 || (f.norm_w && (reinterpret_cast<uintptr_t>(f.norm_w) & 15) != 0))
+            return fail(AF_EDIM, "chained GEMV needs 16-byte aligned f32 vectors");
+        GcPhase& g = gp.ph[i];
+        g.w = reinterpret_cast<const __nv_bfloat16*>(f.w);
+        g.rows = f.rows;
+        g.cols = f.cols;
+        g.ld = f.ld;
+        g.x = f.x;
+        g.out = f.out;
+        g.res = f.res;
+        g.norm_w = f.norm_w;
+        g.eps = f.eps;
+        g.prologue = f.prologue;
+        g.epilogue = f.epilogue;
+        max_cols = std::max(max_cols, (int)f.cols);
+        max_rows = std::max<long long>(max_rows, f.rows);
+    }
+    const int xs_bytes = max_cols * 4;
+    int n_stages = (di.max_smem_optin - 1024 - xs_bytes) / kGcStage;
+    n_stages = std::min(n_stages, kGcMaxStages);
+    if (n_stages < 2) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory next to the weight ring");
+    const int smem = n_stages * kGcStage + xs_bytes;
+    static int configured = 0;
+    if (smem > configured) {
+        AF_CUDA_TRY(cudaFuncSetAttribute(gemv_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured = smem;
+    }
+    gp.n_phases = n_phases;
+    gp.phase_done = phase_done_dev;
+    gp.n_stages = n_stages;
+    gp.pdl = (pdl && g_pdl.load()) ? 1 : 0;
+    gp.err_flag = nullptr;
+    cudaLaunchConfig_t cfg{};
+    // every CTA takes part in the phase barriers: the grid is one CTA per SM, all co-resident
+    cfg.gridDim = dim3(di.sm_count);
+    cfg.blockDim = dim3(kGcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = gp.pdl ? 1 : 0;
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_chain_kernel, gp));
+    AF_LAUNCH_CHECK("gemv_chain_kernel");
+    return AF_OK;
+}
 
 int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table, const float* sin_table,
                    const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t max_seq,

@@ -958,10 +958,12 @@ __global__ void __launch_bounds__(GEMV ? kMmaThreadsGemv : kMmaThreads, 1) switc
                             for (int e = 0; e < 4; ++e) acc[nt][e] = fmaf(gate[j], pr[nt][e], acc[nt][e]);
                     }
                 } else {
+                    // same accumulation order as the fused GEMV loop (rank step outer, hi then lo):
+                    // both kernels leave bit-identical weights
 #pragma unroll
-                    for (int half = 0; half < 2; ++half)
+                    for (int j = 0; j < KS; ++j)
 #pragma unroll
-                        for (int j = 0; j < KS; ++j) {
+                        for (int half = 0; half < 2; ++half) {
                             mma_bf16_16816(acc[0], afrag[j], bfr[half][j][0], bfr[half][j][1]);
                             mma_bf16_16816(acc[1], afrag[j], bfr[half][j][2], bfr[half][j][3]);
                         }

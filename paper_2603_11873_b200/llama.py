@@ -64,6 +64,7 @@ class LlamaConfig:
     # "auto": chase when it applies (adapters, single rank, tensor path)
     forward_mode: str = "auto"
     chain: bool = True               # chase: o -> gate|up -> down -> next q|k|v as ONE launch with in-kernel phase barriers
+    gemv_chain: bool = True          # plain forward (separate / adapter-free): the same four projections as one persistent GEMV launch
 
     def validate(self) -> None:
         for name in ("layers", "hidden", "ffn", "n_heads", "n_kv_heads", "vocab", "experts", "rank", "top_k", "max_seq", "tp_size"):
@@ -352,6 +353,9 @@ class LlamaEngine:
         self.attn_tickets = torch.zeros(self.heads_local, dtype=torch.int32, device=dev)
         self.forced_dev = None
         self._graphs = {}
+        # phase counters of the chained plain-GEMV launches (4 per layer), zeroed once per forward
+        self.use_gemv_chain = cfg.gemv_chain and cfg.tp_size == 1
+        self.gc_done = torch.zeros(4 * cfg.layers, dtype=torch.int32, device=dev)
         # ---- fused switch + GEMV ("chase") ----
         want = cfg.forward_mode
         can = cfg.adapters and cfg.tp_size == 1 and self.table is not None and self.table.info()["tensor_path"] \
@@ -422,8 +426,47 @@ class LlamaEngine:
         else:
             self.fused_switch(self.prev if with_prev else None, self.cur)
 
+    def _gv_phase(self, w, rows, cols, x, out, prologue=0, norm_w=None, eps=0.0, epilogue=0, res=None):
+        return _capi.GvPhase(w=_ptr(w), rows=rows, cols=cols, ld=cols, x=_ptr(x), out=_ptr(out), res=_ptr(res) if res is not None else None,
+                             norm_w=_ptr(norm_w) if norm_w is not None else None, eps=float(eps), prologue=prologue, epilogue=epilogue)
+
+    def forward_chained(self) -> None:
+        """The same forward as `forward`, with o -> gate|up -> down -> next q|k|v (-> lm_head for
+        the last layer) as ONE persistent launch per layer (af_gemv_chain): the weights of the four
+        projections stream back to back while the consumers hop over the phase boundaries."""
+        cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
+        d, eps = cfg.hidden, cfg.rms_eps
+        xa, xb = self.x
+        n_qkv, n_gu = self.q_rows + 2 * self.kv_rows, 2 * self.ffn_local
+        self.gc_done.zero_()
+        self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
+        self._check(L.af_gemv_fused(_ptr(self.wqkv[0]), n_qkv, d, d, _ptr(xa), _ptr(self.qkv_buf), _capi.AF_PRO_RMSNORM,
+                                    _ptr(self.attn_norm[0]), eps, _capi.AF_EPI_NONE, None, st))
+        for li in range(cfg.layers):
+            self._check(L.af_attn_decode(_ptr(self.qkv_buf), _ptr(self.k_cache[li]), _ptr(self.v_cache[li]), _ptr(self.cos),
+                                         _ptr(self.sin), _ptr(self.pos_dev), self.heads_local, self.kv_local, cfg.head_dim,
+                                         cfg.max_seq, self.attn_splits, _ptr(self.attn_ws), _ptr(self.attn_tickets),
+                                         _ptr(self.attn_buf), st))
+            phases = [
+                self._gv_phase(self.wo[li], d, self.q_rows, self.attn_buf, xb, epilogue=_capi.AF_EPI_RESIDUAL, res=xa),
+                self._gv_phase(self.wgu[li], n_gu, d, xb, self.gu_buf, prologue=_capi.AF_PRO_RMSNORM, norm_w=self.ffn_norm[li], eps=eps),
+                self._gv_phase(self.wdown[li], d, self.ffn_local, self.gu_buf, xa, prologue=_capi.AF_PRO_SILU_MUL,
+                               epilogue=_capi.AF_EPI_RESIDUAL, res=xb),
+            ]
+            if li + 1 < cfg.layers:
+                phases.append(self._gv_phase(self.wqkv[li + 1], n_qkv, d, xa, self.qkv_buf, prologue=_capi.AF_PRO_RMSNORM,
+                                             norm_w=self.attn_norm[li + 1], eps=eps))
+            else:
+                phases.append(self._gv_phase(self.lm_head.data, self.vocab_local, d, xa, self.logits, prologue=_capi.AF_PRO_RMSNORM,
+                                             norm_w=self.final_norm, eps=eps))
+            arr = (_capi.GvPhase * len(phases))(*phases)
+            self._check(L.af_gemv_chain(arr, len(phases), _ptr(self.gc_done[4 * li: 4 * li + 4]), 1, st))
+        self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
+
     def forward(self) -> None:
         """Merged-path forward of one token (model.py:367-371 on the Llama block)."""
+        if self.use_gemv_chain:
+            return self.forward_chained()
         cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
         d, eps = cfg.hidden, cfg.rms_eps
         tp = cfg.tp_size

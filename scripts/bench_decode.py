@@ -12,7 +12,8 @@ from paper_2603_11873_b200 import _capi, llama  # noqa: E402
 
 def main():
     workload = sys.argv[1] if len(sys.argv) > 1 else "llama2-7b"
-    cfg = llama.preset(workload, max_seq=256, adapters=False)
+    chain = os.environ.get("AF_GEMV_CHAIN", "1") != "0"   # one persistent launch per layer (af_gemv_chain) vs one launch per projection
+    cfg = llama.preset(workload, max_seq=256, adapters=False, gemv_chain=chain)
     eng = llama.LlamaEngine(cfg, init="device")
     L = _capi.lib()
     combos = ((0, 0), (1, 0), (2, 0), (3, 0), (4, 0), (2, 1), (4, 1), (3, 1))
@@ -45,7 +46,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / n
-            print(json.dumps({"variant": variant, "full_sm": full_sm, "pdl": pdl, "ms_per_token": round(ms, 4),
+            print(json.dumps({"chain": chain, "variant": variant, "full_sm": full_sm, "pdl": pdl, "ms_per_token": round(ms, 4),
                               "tok_s": round(1e3 / ms, 1), "GBps": round(cfg.decode_bytes() / ms / 1e6, 1)}), flush=True)
 
 

@@ -115,17 +115,40 @@ def full(tag, name, rep):
     return first
 
 
+def to_bytes(first, key):
+    v, u = first[key]
+    v = float(v.replace(",", ""))
+    return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}.get(u, 1.0)
+
+
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    chase = "--chase" in sys.argv   # artifacts of scripts/gpu_round4.sh (the one-pass schedule)
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
+    if chase:
+        first = full(tag, "chase", "prof_chase.ncu-rep")
+        if first:
+            rd, wr = to_bytes(first, "dram__bytes_read.sum"), to_bytes(first, "dram__bytes_write.sum")
+            layers = 32
+            json.dump({"workload": "llama2-7b", "kernel": "switch_mma_kernel<2, GEMV> (one chained launch: o -> gate|up -> down -> next q|k|v)",
+                       "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+                       "dram_bytes_per_token": (rd + wr) * layers,
+                       "note": "a chained launch covers one layer's seven matrices; per token = per launch x 32 layers "
+                               "(writes still in L2 at kernel end are not counted by dram__bytes_write)",
+                       "source": f"profiles/{tag}_chase_full.txt (one ncu --set full capture inside bench.py's e2e region)"},
+                      open(os.path.join(PROF, "chase_traffic.json"), "w"), indent=1)
+            print("chase traffic per launch", (rd + wr) / 1e6, "MB")
+        for name, dst in (("chase_timeline.txt", "chase_timeline.txt"), ("bench.json", "bench.json"), ("bench_separate.json", "bench_separate.json"),
+                          ("chase_kernel.txt", "chase_kernel.txt"), ("ab.txt", "consumer_loop_ab.txt")):
+            pth = os.path.join(OUT, name)
+            if os.path.exists(pth):
+                with open(pth) as f, open(os.path.join(PROF, f"{tag}_{dst}"), "w") as g:
+                    g.write(f.read())
+        return
     first = full(tag, "switch", "prof_switch.ncu-rep")
     if first:
-        def gb(key):
-            v, u = first[key]
-            v = float(v.replace(",", ""))
-            return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}.get(u, 1.0)
-        rd, wr = gb("dram__bytes_read.sum"), gb("dram__bytes_write.sum")
+        rd, wr = to_bytes(first, "dram__bytes_read.sum"), to_bytes(first, "dram__bytes_write.sum")
         json.dump({"workload": "llama2-7b", "kernel": "switch_mma_kernel<2>", "dram_bytes_read": rd, "dram_bytes_write": wr,
                    "dram_bytes_per_launch": rd + wr, "source": f"profiles/{tag}_switch_full.txt (one ncu --set full capture, steady switch s=2kr)"},
                   open(os.path.join(PROF, "switch_traffic.json"), "w"), indent=1)

@@ -132,6 +132,25 @@ def test_split_attention_and_pdl_do_not_change_results(llama, forward_mode):
     assert np.array_equal(outs[2][1], outs[0][1])
 
 
+def test_chained_plain_forward_equals_per_projection_launches(llama):
+    """af_gemv_chain (one persistent launch per layer) against one af_gemv_fused launch per projection:
+    same tokens, logits equal to f32 summation-order round-off; adapter-free and separate schedules."""
+    forced = np.random.Generator(np.random.PCG64(31)).integers(0, 512, 16)
+    for kw in (dict(adapters=False), dict(forward_mode="separate")):
+        outs = []
+        for chain in (True, False):
+            eng = llama.LlamaEngine(llama.preset("tiny", max_seq=24, gemv_chain=chain, **kw), init="host")
+            assert eng.use_gemv_chain == chain
+            eng.reset(forced=forced)
+            lg = []
+            for _ in range(16):
+                eng.decode_step()
+                lg.append(eng.logits.cpu().numpy().copy())
+            outs.append((eng.tokens(), np.stack(lg)))
+        np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=0, atol=1e-4 * np.max(np.abs(outs[1][1])))
+        assert outs[0][0] == outs[1][0]
+
+
 def test_generate_and_base_engine(llama):
     cfg = llama.preset("tiny", max_seq=64)
     eng = llama.LlamaEngine(cfg, init="host")
