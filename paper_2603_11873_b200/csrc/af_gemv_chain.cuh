@@ -130,7 +130,6 @@ __global__ void __launch_bounds__(kGcThreads, 1) gemv_chain_kernel(const __grid_
                 do {
                     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(gp.phase_done + p - 1) : "memory");
                     if (seen >= G) break;
-                    __nanosleep(32);
                     if (clock64() - t0 > (1ll << 32)) {  // ~2 s: never hang the device on a lost CTA
                         if (gp.err_flag) atomicExch(gp.err_flag, AF_ECUDA);
                         break;
