@@ -36,8 +36,9 @@ def main():
     ap.add_argument("workload", nargs="?", default="llama3-8b")
     ap.add_argument("--steps", type=int, default=48)
     ap.add_argument("--switch-mode", default="inplace")
+    ap.add_argument("--forward-mode", default="auto", choices=["auto", "chase", "separate"])
     args = ap.parse_args()
-    cfg = llama.preset(args.workload, max_seq=8 * args.steps + 64, switch_mode=args.switch_mode)
+    cfg = llama.preset(args.workload, max_seq=8 * args.steps + 64, switch_mode=args.switch_mode, forward_mode=args.forward_mode)
     eng = llama.LlamaEngine(cfg, init="device")
     forced = np.random.Generator(np.random.PCG64(7)).integers(0, cfg.vocab, 4096)
     eng.reset(forced=forced)
@@ -55,7 +56,12 @@ def main():
         peak = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"])
     except OSError:
         pass
-    print(json.dumps({"workload": args.workload, "switch_mode": args.switch_mode, "segments": eng.table.info()["n_segments"],
+    lm_head_bytes = 2 * (cfg.vocab // cfg.tp_size) * cfg.hidden
+    # a switching step moves the switch bytes and, in the separate schedule, the forward's bytes on top;
+    # in the chase schedule the forward rides on the switch's pass (only lm_head is extra)
+    switch_step_bytes = cfg.switch_bytes() + (lm_head_bytes if eng.chase else cfg.decode_bytes())
+    print(json.dumps({"workload": args.workload, "switch_mode": args.switch_mode, "forward_mode": "chase" if eng.chase else "separate",
+                      "segments": eng.table.info()["n_segments"],
                       "switch_bytes": cfg.switch_bytes(), "decode_bytes": cfg.decode_bytes()}), flush=True)
     for period in (1, 2, 4, 8, 16, 0):
         eng.pos_dev.fill_(4)
@@ -74,7 +80,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
-        bytes_per_tok = cfg.decode_bytes() + cfg.switch_bytes() * n_sw / args.steps
+        bytes_per_tok = (switch_step_bytes * n_sw + cfg.decode_bytes() * (args.steps - n_sw)) / args.steps
         print(json.dumps({"switch_period": period if period else "inf", "switches": n_sw, "ms_per_token": round(ms, 4),
                           "tok_s": round(1e3 / ms, 1), "hbm_GBps": round(bytes_per_tok / ms / 1e6, 1),
                           "frac_of_measured_peak": round(bytes_per_tok / ms / 1e6 / peak, 4)}), flush=True)
