@@ -10,6 +10,7 @@
 #include "af_gemv_chain.cuh"
 #include "af_llama.cuh"
 #include "af_switch_mma.cuh"
+#include "af_switch_umma.cuh"
 
 namespace af {
 
@@ -43,6 +44,11 @@ static std::atomic<int> g_gemv_full_sm{[] {
 static unsigned long long* g_timeline = nullptr;
 static int g_timeline_left = 0;
 static long long g_timeline_stride = 0;
+// tcgen05 / TMEM kernels for eligible tables (af_set_umma; env AF_UMMA=0 turns them off): 1 = tcgen05, 0 = mma.sync
+static std::atomic<int> g_umma{[] {
+    const char* e = getenv("AF_UMMA");
+    return e ? atoi(e) : 1;
+}()};
 static const bool g_force_hilo = [] { const char* e = getenv("AF_FORCE_HILO"); return e && e[0] == '1'; }();
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline size_t esize(int dtype) { return dtype == AF_BF16 ? 2 : 4; }
@@ -114,12 +120,15 @@ struct af_table {
     SegDev* d_segs = nullptr;
     UnitDev* d_units = nullptr;
     int n_units = 0;
+    UnitDev* d_units_umma = nullptr;   // whole-table schedule in 128 x 128 tiles (tcgen05 kernel)
+    int n_units_umma = 0;
     CUtensorMap* d_maps = nullptr;  // [5][n_segments]: fma live, fma pristine, mma live, mma pristine, UP bank (swizzled)
     int* d_err = nullptr;
     Plan* d_plan = nullptr;         // af_plan_build target
     bool fast_fma = false, fast_mma = false, has_pristine = false;
     bool rank16 = true;  // every segment's rank is a multiple of 16
     bool mixed_rank = false;
+    bool umma_ok = false;   // tcgen05 path: rank 8 everywhere, every matrix a multiple of 128 x 128
     int max_rank = 0, min_experts = 0;
     long long target_elems = 0;
     int sm_count = 0;
@@ -132,6 +141,8 @@ struct af_group {
     std::vector<int> segs;
     UnitDev* d_units = nullptr;
     int n_units = 0, grid = 0;
+    UnitDev* d_units_umma = nullptr;   // the same phases cut into 128 x 128 tiles (tcgen05 path), when the table allows it
+    int n_units_umma = 0, grid_umma = 0;
     int* d_seg_yoff = nullptr;
     int n_phases = 1;
     int x_len[kMaxPhases] = {0, 0, 0, 0}, y_rows[kMaxPhases] = {0, 0, 0, 0};
@@ -160,6 +171,11 @@ int af_set_pdl(int32_t enable) {
     return AF_OK;
 }
 
+int af_set_umma(int32_t enable) {
+    g_umma.store(enable ? 1 : 0);
+    return AF_OK;
+}
+
 int af_set_gemv_variant(int32_t variant, int32_t full_sm) {
     if (variant < 0 || variant > 4) return fail(AF_EVALUE, "GEMV variant must be 0..4");
     g_gemv_variant.store(variant);
@@ -173,6 +189,7 @@ int af_table_destroy(af_table* t) {
     if (!t) return AF_OK;
     if (t->d_segs) cudaFree(t->d_segs);
     if (t->d_units) cudaFree(t->d_units);
+    if (t->d_units_umma) cudaFree(t->d_units_umma);
     if (t->d_maps) cudaFree(t->d_maps);
     if (t->d_err) cudaFree(t->d_err);
     if (t->d_plan) cudaFree(t->d_plan);
@@ -271,6 +288,9 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
     }
     t->fast_fma = fma_ok;
     t->fast_mma = mma_ok;
+    t->umma_ok = mma_ok;
+    for (int i = 0; i < n_segments; ++i)
+        if (segments[i].rank != 8 || segments[i].d_out % kUM != 0 || segments[i].d_in % kUN != 0) t->umma_ok = false;
 
     // ---- work units: column strips of kTN columns cut into runs of row tiles ----
     // Static round-robin schedule over the persistent grid: aim for ~32 units per SM so the
@@ -295,12 +315,31 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         return wa > wb;
     });
     t->n_units = (int)units.size();
+    // the same walk in 128 x 128 tiles for the tcgen05 kernel
+    std::vector<UnitDev> units_u;
+    if (t->umma_ok) {
+        long long tiles_u = 0;
+        for (int i = 0; i < n_segments; ++i) tiles_u += (long long)(segments[i].d_out / kUM) * (segments[i].d_in / kUN);
+        long long per_u = std::max(1LL, std::min(32LL, tiles_u / ((long long)std::max(1, t->sm_count) * 32)));
+        for (int i = 0; i < n_segments; ++i) {
+            const af_segment_desc& s = segments[i];
+            const int rows_per_unit = (int)per_u * kUM;
+            for (int c0 = 0; c0 < s.d_in; c0 += kUN)
+                for (int r0 = 0; r0 < s.d_out; r0 += rows_per_unit)
+                    units_u.push_back({i, r0, std::min(rows_per_unit, s.d_out - r0), c0, 0, 0});
+        }
+        std::stable_sort(units_u.begin(), units_u.end(), [&](const UnitDev& a, const UnitDev& b) { return a.rows > b.rows; });
+        t->n_units_umma = (int)units_u.size();
+    }
 
     cudaError_t e = cudaMalloc(&t->d_segs, sizeof(SegDev) * n_segments);
     if (e == cudaSuccess) e = cudaMemcpy(t->d_segs, hs.data(), sizeof(SegDev) * n_segments, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && t->n_units) e = cudaMalloc(&t->d_units, sizeof(UnitDev) * units.size());
     if (e == cudaSuccess && t->n_units)
         e = cudaMemcpy(t->d_units, units.data(), sizeof(UnitDev) * units.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && t->n_units_umma) e = cudaMalloc(&t->d_units_umma, sizeof(UnitDev) * units_u.size());
+    if (e == cudaSuccess && t->n_units_umma)
+        e = cudaMemcpy(t->d_units_umma, units_u.data(), sizeof(UnitDev) * units_u.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&t->d_err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(t->d_err, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&t->d_plan, sizeof(Plan));
@@ -310,7 +349,7 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         return fail(AF_ECUDA, std::string("table upload: ") + cudaGetErrorString(e));
     }
     if (t->fast_fma) {
-        std::vector<CUtensorMap> maps((size_t)5 * n_segments);
+        std::vector<CUtensorMap> maps((size_t)7 * n_segments);   // [5], [6]: 128 x 64 boxes of the tcgen05 path (live, pristine)
         std::memset(maps.data(), 0, sizeof(CUtensorMap) * maps.size());
         for (int i = 0; i < n_segments; ++i) {
             const af_segment_desc& s = segments[i];
@@ -324,6 +363,10 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
                 const CUtensorMapSwizzle sw = s.rank == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
                                               : s.rank == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
                 rc = make_map(&maps[4 * n_segments + i], s.up, s.n_experts * s.d_out, s.rank, s.rank, s.rank, kMR, sw);
+            }
+            if (!rc && t->umma_ok) {
+                rc = make_map(&maps[5 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kUBoxCols, kUM, CU_TENSOR_MAP_SWIZZLE_128B);
+                if (!rc) rc = make_map(&maps[6 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kUBoxCols, kUM, CU_TENSOR_MAP_SWIZZLE_128B);
             }
             if (rc) {
                 af_table_destroy(t);
@@ -404,6 +447,30 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
         switch_mma_kernel<KS, BA, GEMV, TL><<<grid, kMmaThreads, L::total, st>>>(mp2);
     }
     AF_LAUNCH_CHECK("switch_mma_kernel");
+    return AF_OK;
+}
+
+// tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = block slots (even).
+template <int NB, bool GEMV>
+static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
+    using L = UmmaLayout<NB, GEMV>;
+    static bool configured = false;
+    if (!configured) {
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kUThreads);
+    cfg.dynamicSmemBytes = L::total;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = mp.pdl ? 1 : 0;
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV>, mp));
+    AF_LAUNCH_CHECK("switch_umma_kernel");
     return AF_OK;
 }
 
@@ -494,6 +561,20 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
         return fail(AF_EVALUE, "tensor path needs bf16 targets and factors, rank % 8 == 0, 16-byte aligned rows and "
                                "at most 64 stacked ranks");
     const int S = t->n_segments;
+    if (want_mma && mma_fits && g_umma.load() && t->umma_ok && t->n_units_umma && n_blocks_bound <= 8 && !host_plan_override) {
+        MmaParams mp{};
+        mp.base = p;
+        mp.base.units = t->d_units_umma;
+        mp.base.n_units = t->n_units_umma;
+        mp.tmaps_ld = t->d_maps + (size_t)(p.from_pristine ? 6 : 5) * S;
+        mp.tmaps_st = t->d_maps + (size_t)5 * S;
+        mp.n_chain_segs = 0;
+        mp.n_phases = 1;
+        const int grid = std::min(t->n_units_umma, t->sm_count);
+        const int nb = std::max(2, (n_blocks_bound + 1) & ~1);
+        if (nb <= 4) return launch_umma<4, false>(mp, grid, st);
+        return launch_umma<8, false>(mp, grid, st);
+    }
     if (want_mma && mma_fits) {
         MmaParams mp{};
         mp.base = p;
@@ -601,6 +682,7 @@ int af_max_deviation(af_table* t, float* out_dev, void* stream) {
 int af_group_destroy(af_group* g) {
     if (!g) return AF_OK;
     if (g->d_units) cudaFree(g->d_units);
+    if (g->d_units_umma) cudaFree(g->d_units_umma);
     if (g->d_seg_yoff) cudaFree(g->d_seg_yoff);
     delete g;
     return AF_OK;
@@ -650,74 +732,87 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
     // ---- schedule: per phase, the tiles in (segment, column strip, row tile) order cut into one
     //      contiguous span per CTA -- every SM streams the same number of tiles (+-1) and restages
     //      the DOWN slab only when its span crosses into another strip.  A CTA's spans of all phases
-    //      are concatenated into its unit list. ----
+    //      are concatenated into its unit list.  Built for a tile geometry: 32 x 256 (mma.sync kernel)
+    //      and, when the table allows it, 128 x 128 (tcgen05 kernel). ----
     const int G = std::max(1, t->sm_count);
-    std::vector<std::vector<UnitDev>> per_cta(G);
-    int used = 0, first = 0;
-    for (int ph = 0; ph < n_phases; ++ph) {
-        const int strips = (g->x_len[ph] + kTN - 1) / kTN;
-        long long total = 0;
-        for (int i = 0; i < phase_len[ph]; ++i) total += (long long)strips * ((t->segs[seg_ids[first + i]].d_out + kMR - 1) / kMR);
-        g->tiles += total;
-        const int Gp = (int)std::min<long long>(total, G);   // CTA 0 always owns tiles of every phase (it writes h_out)
-        used = std::max(used, Gp);
-        // Cost model of a span: its tiles + `penalty` tile-times for every strip boundary inside it
-        // (a unit change restages the gated DOWN slab and refills the per-unit registers: ~4 us
-        // against ~0.85 us per tile, profiles/r01_chase_timeline.txt).  All CTAs meet at the phase
-        // barrier, so spans are cut to equal COST, not equal tile count: the smallest per-CTA
-        // budget that needs at most Gp spans, found by bisection.
-        static const int penalty = [] { const char* e = getenv("AF_UNIT_PENALTY"); return e ? atoi(e) : 4; }();
-        struct Strip { int sidx, slot, sp, rt, d_out; };
-        std::vector<Strip> strips_v;
-        for (int i = 0; i < phase_len[ph]; ++i) {
-            const int sidx = seg_ids[first + i];
-            const int d_out = t->segs[sidx].d_out;
-            for (int sp = 0; sp < strips; ++sp) strips_v.push_back({sidx, first + i, sp, (d_out + kMR - 1) / kMR, d_out});
-        }
-        auto cut = [&](long long budget, std::vector<std::vector<UnitDev>>* out) -> int {
-            int cta = 0;
-            long long cost = 0;   // cost already in the current span
-            for (const Strip& st : strips_v) {
-                int r = 0;
-                while (r < st.rt) {
-                    long long room = budget - cost - (cost > 0 ? penalty : 0);   // entering a strip mid-span costs the penalty
-                    if (cost > 0 && room < std::max(1, penalty)) {   // not worth a unit change: close the span, start a new one here
-                        ++cta;
-                        cost = 0;
-                        continue;
-                    }
-                    if (room < 1) room = 1;
-                    const int take = (int)std::min<long long>(st.rt - r, room);
-                    if (out) {
-                        const int row0 = r * kMR;
-                        (*out)[std::min(cta, Gp - 1)].push_back({st.sidx, row0, std::min(take * kMR, st.d_out - row0), st.sp * kTN, ph, st.slot});
-                    }
-                    cost += take + (cost > 0 ? penalty : 0);
-                    r += take;
-                }
+    static const int env_penalty = [] { const char* e = getenv("AF_UNIT_PENALTY"); return e ? atoi(e) : 4; }();
+    auto build = [&](int tile_rows, int tile_cols, int penalty, std::vector<UnitDev>& units, int& grid, long long* tiles_out) {
+        std::vector<std::vector<UnitDev>> per_cta(G);
+        int used = 0, first = 0;
+        for (int ph = 0; ph < n_phases; ++ph) {
+            const int strips = (g->x_len[ph] + tile_cols - 1) / tile_cols;
+            long long total = 0;
+            for (int i = 0; i < phase_len[ph]; ++i)
+                total += (long long)strips * ((t->segs[seg_ids[first + i]].d_out + tile_rows - 1) / tile_rows);
+            if (tiles_out) *tiles_out += total;
+            const int Gp = (int)std::min<long long>(total, G);   // CTA 0 always owns tiles of every phase (it writes h_out)
+            used = std::max(used, Gp);
+            // Cost model of a span: its tiles + `penalty` tile-times for every strip boundary inside it
+            // (a unit change restages the gated DOWN slab and refills the per-unit registers: ~4 us
+            // against ~0.85 us per tile, profiles/r01c_chase_timeline.txt).  All CTAs meet at the phase
+            // barrier, so spans are cut to equal COST, not equal tile count: the smallest per-CTA
+            // budget that needs at most Gp spans, found by bisection.
+            struct Strip { int sidx, slot, sp, rt, d_out; };
+            std::vector<Strip> strips_v;
+            for (int i = 0; i < phase_len[ph]; ++i) {
+                const int sidx = seg_ids[first + i];
+                const int d_out = t->segs[sidx].d_out;
+                for (int sp = 0; sp < strips; ++sp) strips_v.push_back({sidx, first + i, sp, (d_out + tile_rows - 1) / tile_rows, d_out});
             }
-            return cta + 1;
-        };
-        long long lo = (total + Gp - 1) / Gp, hi = lo + (long long)penalty * 4 + 8;
-        while (cut(hi, nullptr) > Gp) hi *= 2;
-        while (lo < hi) {
-            const long long mid = (lo + hi) / 2;
-            if (cut(mid, nullptr) <= Gp) hi = mid;
-            else lo = mid + 1;
+            auto cut = [&](long long budget, std::vector<std::vector<UnitDev>>* out) -> int {
+                int cta = 0;
+                long long cost = 0;   // cost already in the current span
+                for (const Strip& st : strips_v) {
+                    int r = 0;
+                    while (r < st.rt) {
+                        long long room = budget - cost - (cost > 0 ? penalty : 0);   // entering a strip mid-span costs the penalty
+                        if (cost > 0 && room < std::max(1, penalty)) {   // not worth a unit change: close the span, start a new one here
+                            ++cta;
+                            cost = 0;
+                            continue;
+                        }
+                        if (room < 1) room = 1;
+                        const int take = (int)std::min<long long>(st.rt - r, room);
+                        if (out) {
+                            const int row0 = r * tile_rows;
+                            (*out)[std::min(cta, Gp - 1)].push_back({st.sidx, row0, std::min(take * tile_rows, st.d_out - row0), st.sp * tile_cols, ph, st.slot});
+                        }
+                        cost += take + (cost > 0 ? penalty : 0);
+                        r += take;
+                    }
+                }
+                return cta + 1;
+            };
+            long long lo = (total + Gp - 1) / Gp, hi = lo + (long long)penalty * 4 + 8;
+            while (cut(hi, nullptr) > Gp) hi *= 2;
+            while (lo < hi) {
+                const long long mid = (lo + hi) / 2;
+                if (cut(mid, nullptr) <= Gp) hi = mid;
+                else lo = mid + 1;
+            }
+            cut(lo, &per_cta);
+            first += phase_len[ph];
         }
-        cut(lo, &per_cta);
-        first += phase_len[ph];
-    }
-    const int grid = used;
-    size_t depth = 0;
-    for (auto& v : per_cta) depth = std::max(depth, v.size());
-    std::vector<UnitDev> units(depth * grid, UnitDev{0, 0, 0, 0, 0, 0});
-    for (int c = 0; c < grid; ++c)
-        for (size_t j = 0; j < per_cta[c].size(); ++j) units[j * grid + c] = per_cta[c][j];
-    g->grid = grid;
+        grid = used;
+        size_t depth = 0;
+        for (auto& v : per_cta) depth = std::max(depth, v.size());
+        units.assign(depth * grid, UnitDev{0, 0, 0, 0, 0, 0});
+        for (int c = 0; c < grid; ++c)
+            for (size_t j = 0; j < per_cta[c].size(); ++j) units[j * grid + c] = per_cta[c][j];
+    };
+    std::vector<UnitDev> units, units_umma;
+    build(kMR, kTN, env_penalty, units, g->grid, &g->tiles);
     g->n_units = (int)units.size();
+    bool umma = t->umma_ok;
+    if (umma) {
+        build(kUM, kUN, 1, units_umma, g->grid_umma, nullptr);   // a 128 x 128 tile is 4x the bytes: a unit change weighs about one tile
+        g->n_units_umma = (int)units_umma.size();
+    }
     cudaError_t e = cudaMalloc(&g->d_units, sizeof(UnitDev) * units.size());
     if (e == cudaSuccess) e = cudaMemcpy(g->d_units, units.data(), sizeof(UnitDev) * units.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && umma) e = cudaMalloc(&g->d_units_umma, sizeof(UnitDev) * units_umma.size());
+    if (e == cudaSuccess && umma)
+        e = cudaMemcpy(g->d_units_umma, units_umma.data(), sizeof(UnitDev) * units_umma.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_seg_yoff, sizeof(int) * yoff.size());
     if (e == cudaSuccess) e = cudaMemcpy(g->d_seg_yoff, yoff.data(), sizeof(int) * yoff.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -849,6 +944,16 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     cudaStream_t st = as_stream(stream);
     if (env_dbg & 4) {  // experiment: the plain switch kernel on this group's schedule (no GEMV at all)
         if (ks == 2) return launch_mma<2, false, false>(mp, g->grid, st);
+    }
+    // tcgen05 path (env AF_UMMA=1 while it is being validated): rank-8 tables of 128-multiples
+    if (g_umma.load() && t->umma_ok && g->d_units_umma && !mp.timeline && n_blocks_bound <= 8) {
+        p.units = g->d_units_umma;
+        p.n_units = g->n_units_umma;
+        mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 6 : 5) * S;
+        mp.tmaps_st = t->d_maps + (size_t)5 * S;
+        const int nb = std::max(2, (n_blocks_bound + 1) & ~1);
+        if (nb <= 4) return launch_umma<4, true>(mp, g->grid_umma, st);
+        return launch_umma<8, true>(mp, g->grid_umma, st);
     }
     if (mp.timeline && ks == 2) return launch_mma<2, false, true, true>(mp, g->grid, st);
     switch (ks) {

@@ -1,0 +1,599 @@
+// af_switch_umma.cuh -- the fused switch (+ GEMV) with the rank-s product on the 5th-generation
+// tensor cores: tcgen05.mma issued by ONE thread, accumulators in tensor memory (TMEM).
+//
+// Why: the mma.sync tile loop of af_switch_mma.cuh is consumer-bound (profiles/README.md): 16 warps
+// spend ~130 instructions per warp and 16 KB tile feeding the tensor pipe (ldmatrix of UP, B
+// fragments in registers, 16 HMMA, fragment bookkeeping) -- 0.8 us per tile against 0.72 us of HBM
+// time.  Here the product  D[128 x 128] = U[128 x 8 n_blocks] . (hi + lo)(g A)[8 n_blocks x 128]  is
+// 2 * ceil(n_blocks / 2) tcgen05.mma instructions from one thread, straight from shared memory:
+//   A = the UP ring as it is loaded -- one expert block (128 rows x 8 ranks) is a contiguous
+//       [128][16 B] slab = one K-chunk of the K-major no-swizzle canonical layout (LBO = slab
+//       stride, SBO = 128 B);
+//   B = the gated DOWN slab written in the MN-major no-swizzle canonical layout (8 k x 8 n core
+//       matrices; n-groups 128 B apart, k-groups = blocks 2 KB apart), hi blocks then lo blocks;
+//   D = f32 in TMEM, two 128-column accumulators so the MMAs of tile t+1 run under the epilogue of t.
+// The epilogue warps own one row each (TMEM lane = row): tcgen05.ld 32 columns, add the W row
+// from the swizzled TMA tile, round to bf16, store back, and -- fused GEMV -- dot the rounded row
+// with the staged input strip; the row's partial sum goes straight to the fixed-point accumulator
+// (no cross-warp reduction: a thread holds the whole 128-column row strip).
+//
+// Scope: rank == 8 tables whose matrices are multiples of 128 in both directions (every Llama
+// shape of BASELINE.json); anything else keeps the mma.sync kernel.  (scripts/micro/umma_test.cu
+// pins the descriptor encodings in isolation.)
+#pragma once
+
+#include "af_switch_mma.cuh"
+
+namespace af {
+
+constexpr int kUM = 128;                           // tile rows  (UMMA M)
+constexpr int kUN = 128;                           // tile cols  (UMMA N) = strip width
+constexpr int kUBoxCols = 64;                      // TMA box: 128 rows x 64 cols, 128-byte swizzle
+constexpr int kUBoxes = kUN / kUBoxCols;           // 2
+constexpr int kUBoxBytes = kUM * kUBoxCols * 2;    // 16 KB
+constexpr int kUWStage = kUM * kUN * 2;            // 32 KB
+constexpr int kUBlockBytes = kUM * 8 * 2;          // one expert block of the UP stage: 128 rows x 8 ranks = 2 KB
+constexpr int kUSlabBlock = 8 * kUN * 2;           // one k-group (8 ranks) of the slab: 2 KB
+constexpr int kUEpiWarps = 8;                      // two groups of 4: TMEM lane quarter = warp % 4
+constexpr int kUEpi = kUEpiWarps * 32;
+constexpr int kUThreads = kUEpi + 4 * 32;          // + W producer, UP producer, MMA issuer, storer
+constexpr int kUXSlots = 4;
+#ifndef AF_UMMA_PF
+#define AF_UMMA_PF 0   /* measured: prefetching W into L2 beyond the ring costs 20 % (profiles/README.md) */
+#endif
+constexpr int kUPrefetch = AF_UMMA_PF;             // W tiles prefetched into L2 beyond the shared-memory ring (0 = off)
+
+template <int NB, bool GEMV>   // NB = block slots (2 * top_k, even)
+struct UmmaLayout {
+    static constexpr int up_stage = NB * kUBlockBytes;
+    static constexpr int slab_bytes = 2 * NB * kUSlabBlock;            // hi + lo
+    static constexpr int xs_bytes = GEMV ? kUXSlots * kUN * 4 : 0;
+    static constexpr int misc = 512 /*barriers*/ + (int)sizeof(Plan) + 256 + kUnitCache * (int)sizeof(UnitDev) + kSegCache * (int)sizeof(SegDev);
+    static constexpr int fixed = slab_bytes + xs_bytes + misc + 2048;
+    static constexpr int by_smem = (227 * 1024 - fixed) / (kUWStage + up_stage);
+    static constexpr int stages = by_smem < 6 ? by_smem : 6;
+    static constexpr int off_w = 0;
+    static constexpr int off_up = off_w + stages * kUWStage;
+    static constexpr int off_slab = off_up + stages * up_stage;        // 1024-aligned (multiples of 2 KB)
+    static constexpr int off_xs = off_slab + slab_bytes;
+    static constexpr int off_bar = off_xs + xs_bytes;
+    static constexpr int off_plan = off_bar + 512;
+    static constexpr int off_red = (off_plan + (int)sizeof(Plan) + 15) & ~15;
+    static constexpr int off_units = off_red + 256;
+    static constexpr int off_segs = off_units + kUnitCache * (int)sizeof(UnitDev);
+    static constexpr int total = off_segs + kSegCache * (int)sizeof(SegDev) + 1024;
+    static_assert(stages >= 3 && total <= 227 * 1024, "shared memory budget");
+};
+
+// ---- tcgen05 wrappers ----
+__device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3fff);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3fff) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3fff) << 32;
+    d |= (uint64_t)1 << 46;   // descriptor version of sm_100
+    return d;                 // layout type 0: no swizzle
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// TMA prefetch of one box into L2 (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_l2_2d(const void* tmap, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tmap), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,"
+        "%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+          "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// tile walk with 128-row tiles (units are cut at multiples of kUM)
+struct UmmaIter {
+    int j, u, m0, row_end;
+    UnitDev un;
+    const UnitDev* cache;
+    __device__ __forceinline__ bool valid(const SwitchParams& p) const { return u < p.n_units; }
+    __device__ __forceinline__ UnitDev fetch(const SwitchParams& p, int jj, int uu) const { return jj < kUnitCache ? cache[jj] : p.units[uu]; }
+    __device__ __forceinline__ void load_unit(const SwitchParams& p) {
+        if (u < p.n_units) {
+            un = fetch(p, j, u);
+            m0 = un.row0;
+            row_end = un.row0 + un.rows;
+            if (un.rows <= 0) u = p.n_units;
+        }
+    }
+    __device__ __forceinline__ void init(const SwitchParams& p, const UnitDev* c) {
+        cache = c;
+        j = 0;
+        u = blockIdx.x;
+        load_unit(p);
+    }
+    __device__ __forceinline__ bool next(const SwitchParams& p) {
+        m0 += kUM;
+        if (m0 < row_end) return false;
+        u += gridDim.x;
+        ++j;
+        load_unit(p);
+        return true;
+    }
+    __device__ __forceinline__ UnitDev peek(const SwitchParams& p) const {
+        const int un2 = u + gridDim.x;
+        if (un2 >= p.n_units) return UnitDev{0, 0, 0, 0, 0, 0};
+        return fetch(p, j + 1, un2);
+    }
+};
+
+// Gated DOWN slab of one unit in the MN-major canonical layout: element (rank row q, column n) at
+//   (q / 8) * 2 KB + (n / 8) * 128 B + (q % 8) * 16 B + (n % 8) * 2 B ;  lo blocks NB k-groups after the hi blocks.
+template <int NB>
+__device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const SegDev& sg, const Plan& plan, int S, int col0, int tid) {
+    constexpr int chunks = kUN / 8;                 // 16-byte chunks per rank row
+    const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(sg.down);
+    for (int i = tid; i < NB * 8 * chunks; i += kUEpi) {
+        const int q = i / chunks, c = (i % chunks) * 8;
+        uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
+        if (q < S && col0 + c < sg.d_in) {
+            const int b = q >> 3, qr = q & 7;       // rank == 8
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (long long)plan.expert[b] * sg.down_estride +
+                                                                   (long long)qr * sg.ld_down + col0 + c));
+            const float w = plan.weight[b];
+            const uint32_t in[4] = {v.x, v.y, v.z, v.w};
+            uint32_t oh[4], ol[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float f0 = __fmul_rn(w, bf16lo_to_f32(in[e]));
+                const float f1 = __fmul_rn(w, bf16hi_to_f32(in[e]));
+                const uint32_t h = pack_bf16x2(f0, f1);
+                oh[e] = h;
+                ol[e] = pack_bf16x2(f0 - bf16lo_to_f32(h), f1 - bf16hi_to_f32(h));
+            }
+            hi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+            lo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+        }
+        const int off = (q >> 3) * kUSlabBlock + (c >> 3) * 128 + (q & 7) * 16;
+        *reinterpret_cast<uint4*>(slab + off) = hi;
+        *reinterpret_cast<uint4*>(slab + NB * kUSlabBlock + off) = lo;
+    }
+}
+
+template <int NB, bool GEMV>
+__global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_constant__ MmaParams mp) {
+    using L = UmmaLayout<NB, GEMV>;
+    constexpr int kSt = L::stages;
+    extern __shared__ unsigned char smem_dyn[];
+    const SwitchParams& p = mp.base;
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::off_bar);   // [8]
+    uint64_t* computed = full + 8;                                    // [8]
+    uint64_t* empty = full + 16;                                      // [8]
+    uint64_t* acc_full = full + 24;                                   // [2]
+    uint64_t* acc_empty = full + 26;                                  // [2]
+    uint64_t* slab_bar = full + 28;                                   // [1]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 30);
+    Plan& plan = *reinterpret_cast<Plan*>(sm + L::off_plan);
+    UnitDev* unit_cache = reinterpret_cast<UnitDev*>(sm + L::off_units);
+    SegDev* seg_cache = reinterpret_cast<SegDev*>(sm + L::off_segs);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid >= 32 && tid < 32 + kUnitCache) {
+        const int jj = tid - 32;
+        const long long uu = (long long)blockIdx.x + (long long)jj * gridDim.x;
+        unit_cache[jj] = uu < p.n_units ? p.units[uu] : UnitDev{0, 0, 0, 0, 0, 0};
+    }
+    if (tid >= 64 && tid < 64 + mp.n_chain_segs) seg_cache[tid - 64] = p.segs[mp.chain_segs[tid - 64]];
+    for (int i = tid * 16; i < kSt * L::up_stage; i += kUThreads * 16)   // block slots past n_blocks must read as zeros
+        *reinterpret_cast<uint4*>(sm + L::off_up + i) = make_uint4(0u, 0u, 0u, 0u);
+    if (tid == 0) {
+        for (int s = 0; s < kSt; ++s) {
+            mbar_init(&full[s], 2);
+            mbar_init(&computed[s], 4);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        mbar_init(slab_bar, kUEpiWarps);
+        *reinterpret_cast<volatile int*>(full + 31) = 0;
+        fence_mbar_init();
+        if (!p.plan_dev) {
+            if (p.use_dev)
+                build_plan(plan, p.from_pristine ? nullptr : p.prev_dev, p.cur_dev, p.scale, false, p.n_experts_limit);
+            else
+                plan = p.host_plan;
+            if (!plan_usable(p, plan, p.prev_dev, p.cur_dev)) plan.n_blocks = -1;
+        }
+    }
+    if (p.plan_dev) {
+        constexpr int kWords = (int)(sizeof(Plan) / 4);
+        if (tid >= 128 && tid < 128 + kWords) reinterpret_cast<int*>(&plan)[tid - 128] = reinterpret_cast<const int*>(p.plan_dev)[tid - 128];
+    }
+    if (warp == kUEpiWarps + 2) {   // the MMA warp owns the tensor memory: two 128-column accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_proxy_async_smem();       // zero-filled UP ring -> visible to the tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int n_blocks = plan.n_blocks;
+    const bool store_w = n_blocks > 0 || p.from_pristine;
+    const bool bail = n_blocks < 0 || (!GEMV && !store_w);
+    const uint32_t w_base = smem_u32(sm + L::off_w), up_base = smem_u32(sm + L::off_up), slab_base = smem_u32(sm + L::off_slab);
+    // chains cache their few segment descriptors in shared memory; a whole-table launch reads them from global
+    auto seg_of = [&](const UnitDev& un) -> SegDev { return mp.n_chain_segs > 0 ? seg_cache[un.slot] : p.segs[un.seg]; };
+
+    if (!bail) {
+        if (warp == kUEpiWarps) {
+            // ============ W producer: two 128 x 64 swizzled boxes per tile ============
+            // Lane 1 runs ahead of it and prefetches the next kUPrefetch tiles into L2.  The ring alone holds
+            // ~3 us of HBM time; a phase boundary stalls the consumers for ~5 us, during which the ring fills
+            // up and HBM would go idle.  With the prefetcher the reads keep streaming (into L2), and after the
+            // boundary the epilogue -- 4x faster than HBM -- catches up on tiles that now come from L2.
+            if (lane == 1 && kUPrefetch > 0) {
+                volatile int* prod_it = reinterpret_cast<volatile int*>(full + 31);
+                UmmaIter ti;
+                ti.init(p, unit_cache);
+                for (int it = 0; ti.valid(p); ++it) {
+                    while (it >= *prod_it + kUPrefetch) __nanosleep(64);   // at most kUPrefetch tiles beyond the loader
+                    if (it >= kSt) {   // the first ring fill is loaded directly
+                        const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
+#pragma unroll
+                        for (int b = 0; b < kUBoxes; ++b) tma_prefetch_l2_2d(tm, ti.un.col0 + b * kUBoxCols, ti.m0);
+                    }
+                    ti.next(p);
+                }
+            }
+            if (lane == 0) {
+                const uint64_t pol = l2_evict_first_policy();
+                UmmaIter ti;
+                ti.init(p, unit_cache);
+                for (int it = 0; ti.valid(p); ++it) {
+                    const int stage = it % kSt;
+                    const uint32_t ph = (it / kSt) & 1;
+                    *reinterpret_cast<volatile int*>(full + 31) = it + kSt;   // tiles up to it + kSt are the ring's business
+                    mbar_wait(&empty[stage], ph ^ 1);
+                    mbar_expect_tx(&full[stage], kUWStage);
+                    const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
+#pragma unroll
+                    for (int b = 0; b < kUBoxes; ++b)
+                        tma_load_2d_hint(w_base + stage * kUWStage + b * kUBoxBytes, tm, ti.un.col0 + b * kUBoxCols, ti.m0, &full[stage], pol);
+                    ti.next(p);
+                }
+            }
+        } else if (warp == kUEpiWarps + 1) {
+            // ============ UP producer: one 2 KB bulk copy per selected expert block ============
+            if (lane == 0) {
+                UmmaIter ti;
+                ti.init(p, unit_cache);
+                SegDev sg;
+                int cur_seg = -1;
+                for (int it = 0; ti.valid(p); ++it) {
+                    const int stage = it % kSt;
+                    const uint32_t ph = (it / kSt) & 1;
+                    if (ti.un.seg != cur_seg) {
+                        cur_seg = ti.un.seg;
+                        sg = seg_of(ti.un);
+                    }
+                    mbar_wait(&empty[stage], ph ^ 1);
+                    mbar_expect_tx(&full[stage], n_blocks * kUBlockBytes);
+                    const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
+                    for (int b = 0; b < n_blocks; ++b)
+                        bulk_load_1d(up_base + stage * L::up_stage + b * kUBlockBytes,
+                                     upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &full[stage]);
+                    ti.next(p);
+                }
+            }
+        } else if (warp == kUEpiWarps + 2) {
+            // ============ MMA issuer: D[buf] = U . hi + U . lo, one thread ============
+            if (lane == 0) {
+                // D f32, A / B bf16, A K-major, B MN-major, N = 128, M = 128
+                constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(kUN >> 3) << 17) | ((uint32_t)(kUM >> 4) << 24);
+                const int ksteps = (n_blocks + 1) >> 1;   // rank-16 steps = pairs of blocks
+                UmmaIter ti;
+                ti.init(p, unit_cache);
+                int unit_j = -1;
+                for (int it = 0; ti.valid(p); ++it) {
+                    const int stage = it % kSt, buf = it & 1;
+                    const uint32_t ph = (it / kSt) & 1, aph = (it >> 1) & 1;
+                    if (ti.j != unit_j) {   // the unit's slab has been written (and made visible to the tensor core)
+                        unit_j = ti.j;
+                        mbar_wait(slab_bar, (uint32_t)unit_j & 1);
+                    }
+                    mbar_wait(&full[stage], ph);
+                    mbar_wait(&acc_empty[buf], aph ^ 1);
+                    tc_fence_after();
+                    const uint32_t a0 = up_base + stage * L::up_stage;
+                    uint32_t accumulate = 0;
+                    for (int half = 0; half < 2; ++half)
+                        for (int ks = 0; ks < ksteps; ++ks) {
+                            const uint64_t da = umma_desc(a0 + ks * 2 * kUBlockBytes, kUBlockBytes, 128);
+                            const uint64_t db = umma_desc(slab_base + (half * NB + ks * 2) * kUSlabBlock, kUSlabBlock, 128);
+                            umma_bf16(tmem + buf * kUN, da, db, idesc, accumulate);
+                            accumulate = 1;
+                        }
+                    if (ksteps == 0) {   // nothing selected (plain GEMV): D = 0 through a K = 16 product with the zeroed slot
+                        const uint64_t da = umma_desc(a0, kUBlockBytes, 128);
+                        const uint64_t db = umma_desc(slab_base, kUSlabBlock, 128);
+                        umma_bf16(tmem + buf * kUN, da, db, idesc, 0);
+                    }
+                    umma_commit(smem_u32(&acc_full[buf]));
+                    ti.next(p);
+                }
+            }
+        } else if (warp == kUEpiWarps + 3) {
+            // ============ storer ============
+            if (lane == 0) {
+                const uint64_t pol = l2_evict_first_policy();
+                UmmaIter ti;
+                ti.init(p, unit_cache);
+                for (int it = 0; ti.valid(p); ++it) {
+                    const int stage = it % kSt;
+                    const uint32_t ph = (it / kSt) & 1;
+                    mbar_wait(&computed[stage], ph);
+                    if (store_w) {
+                        const CUtensorMap* tm = mp.tmaps_st + ti.un.seg;
+#pragma unroll
+                        for (int b = 0; b < kUBoxes; ++b)
+                            tma_store_2d_hint(tm, ti.un.col0 + b * kUBoxCols, ti.m0, w_base + stage * kUWStage + b * kUBoxBytes, pol);
+                        bulk_commit();
+                    }
+                    bulk_wait_read<0>();
+                    mbar_arrive(&empty[stage]);
+                    ti.next(p);
+                }
+                bulk_wait_all<0>();
+            }
+        } else {
+            // ============ epilogue warps: group g = warp / 4 takes the tiles with it % 2 == g ============
+            const int group = warp >> 2, quarter = warp & 3;
+            const int row_in_tile = quarter * 32 + lane;
+            unsigned char* slab = sm + L::off_slab;
+            float* xs_all = reinterpret_cast<float*>(sm + L::off_xs);
+            UmmaIter ti;
+            ti.init(p, unit_cache);
+            if (ti.valid(p)) {
+                if constexpr (GEMV) {
+                    if (mp.pdl) {
+                        pdl_wait();
+                        if (tid == 0) pdl_launch_dependents();
+                    }
+                }
+                float x_inv = 1.0f;
+                int cur_phase = -1, phase_j0 = 0, published = 0;
+                // entering a phase: previous phase published by every CTA, then the input vector
+                auto enter_phase = [&](int ph) {
+                    const GemvParams& g = mp.gv[ph];
+                    if (ph > 0) {
+                        if (tid == 0) {
+                            const int target = (int)gridDim.x;
+                            const long long t0 = clock64();
+                            int seen;
+                            do {
+                                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(mp.phase_done + ph - 1) : "memory");
+                                if (seen >= target) break;
+                                if (clock64() - t0 > (1ll << 32)) {
+                                    if (p.err_flag) atomicExch(p.err_flag, AF_ECUDA);
+                                    break;
+                                }
+                            } while (true);
+                        }
+                        named_bar_sync(1, kUEpi);
+                    }
+                    x_inv = 1.0f;
+                    phase_j0 = ti.j;
+                    // strips of this CTA's units of the phase: thread t -> column t % 128 of slots t / 128 and t / 128 + 2
+                    float xr_h[2], xr_w[2];
+#pragma unroll
+                    for (int k2 = 0; k2 < 2; ++k2) {
+                        const int slot = (tid >> 7) + 2 * k2;
+                        xr_h[k2] = 0.f;
+                        xr_w[k2] = 1.f;
+                        const long long uu = (long long)ti.u + (long long)slot * gridDim.x;
+                        if (uu < p.n_units) {
+                            const UnitDev un2 = ti.fetch(p, ti.j + slot, (int)uu);
+                            const int c = un2.col0 + (tid & 127);
+                            if (un2.rows > 0 && un2.phase == ph && c < g.x_len) {
+                                if (g.prologue == AF_PRO_SILU_MUL) {
+                                    xr_h[k2] = gemv_x(g, c, 1.0f);
+                                } else {
+                                    xr_h[k2] = gemv_h(g, c);
+                                    if (g.prologue == AF_PRO_RMSNORM) xr_w[k2] = g.norm_w[c];
+                                }
+                            }
+                        }
+                    }
+                    if (g.prologue == AF_PRO_RMSNORM || (g.h_out && blockIdx.x == 0)) {
+                        float ss = 0.f;
+                        const bool write_h = g.h_out && blockIdx.x == 0;
+                        constexpr int kStep = 2 * kUEpi;
+                        for (int base = 2 * tid; base < g.x_len; base += 4 * kStep) {
+                            float2 hv[4];
+#pragma unroll
+                            for (int u4 = 0; u4 < 4; ++u4) {
+                                const int c = base + u4 * kStep;
+                                hv[u4] = make_float2(0.f, 0.f);
+                                if (c < g.x_len) {
+                                    if (g.acc_in) {
+                                        const longlong2 q = __ldcg(reinterpret_cast<const longlong2*>(g.acc_in + c));
+                                        hv[u4] = make_float2(fix_to_f32(q.x), fix_to_f32(q.y));
+                                    } else {
+                                        hv[u4] = __ldcg(reinterpret_cast<const float2*>(g.xin + c));
+                                    }
+                                    if (g.res) {
+                                        const float2 r = __ldcg(reinterpret_cast<const float2*>(g.res + c));
+                                        hv[u4].x += r.x;
+                                        hv[u4].y += r.y;
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int u4 = 0; u4 < 4; ++u4) {
+                                const int c = base + u4 * kStep;
+                                ss = fmaf(hv[u4].x, hv[u4].x, fmaf(hv[u4].y, hv[u4].y, ss));
+                                if (write_h && c < g.x_len) *reinterpret_cast<float2*>(g.h_out + c) = hv[u4];
+                            }
+                        }
+                        float* red = reinterpret_cast<float*>(sm + L::off_red);
+                        ss = warp_sum(ss);
+                        named_bar_sync(1, kUEpi);
+                        if (lane == 0) red[warp] = ss;
+                        named_bar_sync(1, kUEpi);
+                        float tot = 0.f;
+#pragma unroll
+                        for (int i = 0; i < kUEpiWarps; ++i) tot += red[i];
+                        x_inv = rsqrtf(tot / (float)g.x_len + g.eps);
+                    }
+#pragma unroll
+                    for (int k2 = 0; k2 < 2; ++k2) {
+                        float v = xr_h[k2];
+                        if (g.prologue == AF_PRO_RMSNORM) v *= x_inv * xr_w[k2];
+                        xs_all[((tid >> 7) + 2 * k2) * kUN + (tid & 127)] = v;
+                    }
+                    named_bar_sync(1, kUEpi);
+                };
+
+                SegDev sg = seg_of(ti.un);
+                int S = n_blocks * 8;
+                bool new_unit = true;
+                int yoff = 0;
+                unsigned long long* acc_out = nullptr;
+                const float* xs = nullptr;
+                for (int it = 0; ti.valid(p); ++it) {
+                    const int stage = it % kSt, buf = it & 1;
+                    const uint32_t ph = (it / kSt) & 1, aph = (it >> 1) & 1;
+                    if (new_unit) {
+                        // every MMA of the previous unit has completed (its last accumulators were read below) and
+                        // both groups are here: the slab may be rewritten for this unit
+                        named_bar_sync(1, kUEpi);
+                        if constexpr (GEMV) {
+                            // the phases this CTA has finished (or has no tiles in) are complete on its side: every
+                            // epilogue warp issued its atomics before the barrier above -- publish before anything else
+                            if (ti.un.phase != cur_phase) {
+                                if (tid == 0 && published < ti.un.phase) {
+                                    __threadfence();
+                                    for (int ph2 = published; ph2 < ti.un.phase && ph2 < mp.n_phases - 1; ++ph2) atomicAdd(mp.phase_done + ph2, 1);
+                                }
+                                published = ti.un.phase;
+                            }
+                        }
+                        sg = seg_of(ti.un);
+                        S = n_blocks * 8;
+                        umma_slab_commit<NB>(slab, sg, plan, S, ti.un.col0, tid);
+                        fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(slab_bar);
+                        if constexpr (GEMV) {
+                            if (ti.un.phase != cur_phase) {
+                                cur_phase = ti.un.phase;
+                                enter_phase(cur_phase);
+                                acc_out = mp.gv[cur_phase].acc_out;
+                            }
+                            yoff = mp.seg_yoff[ti.un.seg];
+                            const int xslot = ti.j - phase_j0;
+                            xs = xslot < kUXSlots ? xs_all + xslot * kUN : nullptr;
+                        }
+                    }
+                    const int m0 = ti.m0, row_end = ti.row_end, col0 = ti.un.col0;
+                    new_unit = ti.next(p);
+                    if ((it & 1) == group) {
+                        mbar_wait(&full[stage], ph);        // the W tile (TMA) is in shared memory
+                        mbar_wait(&acc_full[buf], aph);     // the MMAs of this tile have completed
+                        tc_fence_after();
+                        const uint32_t wrow = w_base + stage * kUWStage + row_in_tile * 128;
+                        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * kUN;
+                        float y = 0.f;
+#pragma unroll 1
+                        for (int c4 = 0; c4 < kUN / 32; ++c4) {
+                            uint32_t d[32];
+                            tmem_ld32(taddr + c4 * 32, d);
+                            const uint32_t wbox = wrow + (c4 >> 1) * kUBoxBytes;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const uint32_t addr = wbox + (((uint32_t)((c4 & 1) * 4 + i) ^ (uint32_t)(row_in_tile & 7)) << 4);
+                                uint4 w = lds128(addr);
+                                uint32_t in[4] = {w.x, w.y, w.z, w.w}, out[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    out[e] = pack_bf16x2(bf16lo_to_f32(in[e]) + __uint_as_float(d[i * 8 + 2 * e]),
+                                                         bf16hi_to_f32(in[e]) + __uint_as_float(d[i * 8 + 2 * e + 1]));
+                                sts128(addr, make_uint4(out[0], out[1], out[2], out[3]));
+                                if constexpr (GEMV) {
+                                    const int c = c4 * 32 + i * 8;
+                                    float4 xa, xb;
+                                    if (xs) {
+                                        xa = *reinterpret_cast<const float4*>(xs + c);
+                                        xb = *reinterpret_cast<const float4*>(xs + c + 4);
+                                    } else {
+                                        const GemvParams& g = mp.gv[cur_phase];
+                                        float t[8];
+#pragma unroll
+                                        for (int e = 0; e < 8; ++e) t[e] = (col0 + c + e < g.x_len) ? gemv_x(g, col0 + c + e, x_inv) : 0.f;
+                                        xa = make_float4(t[0], t[1], t[2], t[3]);
+                                        xb = make_float4(t[4], t[5], t[6], t[7]);
+                                    }
+                                    // the ROUNDED weights, as a decode after the switch would read them
+                                    y = fmaf(bf16lo_to_f32(out[0]), xa.x, y); y = fmaf(bf16hi_to_f32(out[0]), xa.y, y);
+                                    y = fmaf(bf16lo_to_f32(out[1]), xa.z, y); y = fmaf(bf16hi_to_f32(out[1]), xa.w, y);
+                                    y = fmaf(bf16lo_to_f32(out[2]), xb.x, y); y = fmaf(bf16hi_to_f32(out[2]), xb.y, y);
+                                    y = fmaf(bf16lo_to_f32(out[3]), xb.z, y); y = fmaf(bf16hi_to_f32(out[3]), xb.w, y);
+                                }
+                            }
+                        }
+                        tc_fence_before();
+                        fence_proxy_async_smem();   // tile written back -> visible to the TMA store
+                        __syncwarp();
+                        if (lane == 0) {
+                            mbar_arrive(&acc_empty[buf]);
+                            mbar_arrive(&computed[stage]);
+                        }
+                        if constexpr (GEMV) {
+                            if (m0 + row_in_tile < row_end)
+                                atomicAdd(acc_out + yoff + m0 + row_in_tile, (unsigned long long)f32_to_fix(y));
+                        }
+                    }
+                }
+                if constexpr (GEMV) {   // the remaining phases of the chain
+                    named_bar_sync(1, kUEpi);
+                    if (tid == 0 && published < mp.n_phases - 1) {
+                        __threadfence();
+                        for (int ph2 = published; ph2 < mp.n_phases - 1; ++ph2) atomicAdd(mp.phase_done + ph2, 1);
+                    }
+                }
+            } else if constexpr (GEMV) {
+                // a CTA without work still takes part in the phase barriers
+                if (tid == 0)
+                    for (int ph = 0; ph < mp.n_phases - 1; ++ph) atomicAdd(mp.phase_done + ph, 1);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kUEpiWarps + 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
+}
+
+}  // namespace af
