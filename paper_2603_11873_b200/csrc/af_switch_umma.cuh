@@ -99,8 +99,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
           "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
           "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
@@ -148,19 +148,47 @@ struct UmmaIter {
 
 // Gated DOWN slab of one unit in the MN-major canonical layout: element (rank row q, column n) at
 //   (q / 8) * 2 KB + (n / 8) * 128 B + (q % 8) * 16 B + (n % 8) * 2 B ;  lo blocks NB k-groups after the hi blocks.
+// Staged in two steps like the mma.sync kernel's: umma_slab_prefetch() issues this thread's 16-byte
+// loads of the NEXT unit's DOWN rows (predicated asm: nothing consumes them yet, so nothing waits),
+// umma_slab_commit() folds the gate, splits into bf16 hi + lo and writes the slab.
 template <int NB>
-__device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const SegDev& sg, const Plan& plan, int S, int col0, int tid) {
+__device__ __forceinline__ void umma_slab_prefetch(uint4 (&regs)[NB * 8 * (kUN / 8) / kUEpi], const SegDev& sg, const Plan& plan, int S,
+                                                   int col0, int tid) {
     constexpr int chunks = kUN / 8;                 // 16-byte chunks per rank row
     const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(sg.down);
-    for (int i = tid; i < NB * 8 * chunks; i += kUEpi) {
+#pragma unroll
+    for (int j = 0; j < NB * 8 * chunks / kUEpi; ++j) {
+        const int i = tid + j * kUEpi;
+        const int q = i / chunks, c = (i % chunks) * 8;
+        const bool ok = q < S && col0 + c < sg.d_in;
+        const int qq = ok ? q : 0;
+        const __nv_bfloat16* src = base + (long long)plan.expert[qq >> 3] * sg.down_estride + (long long)(qq & 7) * sg.ld_down + col0 + c;
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %5, 0;\n"
+            "mov.b32 %0, 0;\n"
+            "mov.b32 %1, 0;\n"
+            "mov.b32 %2, 0;\n"
+            "mov.b32 %3, 0;\n"
+            "@p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+            "}\n"
+            : "=r"(regs[j].x), "=r"(regs[j].y), "=r"(regs[j].z), "=r"(regs[j].w)
+            : "l"(ok ? src : base), "r"((int)ok));
+    }
+}
+template <int NB>
+__device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const uint4 (&regs)[NB * 8 * (kUN / 8) / kUEpi], const Plan& plan, int S,
+                                                 int tid) {
+    constexpr int chunks = kUN / 8;
+#pragma unroll
+    for (int j = 0; j < NB * 8 * chunks / kUEpi; ++j) {
+        const int i = tid + j * kUEpi;
         const int q = i / chunks, c = (i % chunks) * 8;
         uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
-        if (q < S && col0 + c < sg.d_in) {
-            const int b = q >> 3, qr = q & 7;       // rank == 8
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (long long)plan.expert[b] * sg.down_estride +
-                                                                   (long long)qr * sg.ld_down + col0 + c));
-            const float w = plan.weight[b];
-            const uint32_t in[4] = {v.x, v.y, v.z, v.w};
+        if (q < S) {
+            const float w = plan.weight[q >> 3];    // rank == 8
+            const uint32_t in[4] = {regs[j].x, regs[j].y, regs[j].z, regs[j].w};
             uint32_t oh[4], ol[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -477,8 +505,9 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     named_bar_sync(1, kUEpi);
                 };
 
-                SegDev sg = seg_of(ti.un);
-                int S = n_blocks * 8;
+                const int S = n_blocks * 8;
+                uint4 dn_regs[NB * 8 * (kUN / 8) / kUEpi];
+                umma_slab_prefetch<NB>(dn_regs, seg_of(ti.un), plan, S, ti.un.col0, tid);
                 bool new_unit = true;
                 int yoff = 0;
                 unsigned long long* acc_out = nullptr;
@@ -501,12 +530,14 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                 published = ti.un.phase;
                             }
                         }
-                        sg = seg_of(ti.un);
-                        S = n_blocks * 8;
-                        umma_slab_commit<NB>(slab, sg, plan, S, ti.un.col0, tid);
+                        umma_slab_commit<NB>(slab, dn_regs, plan, S, tid);
                         fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
                         __syncwarp();
                         if (lane == 0) mbar_arrive(slab_bar);
+                        {   // start fetching the NEXT unit's DOWN rows; they are committed at its start
+                            const UnitDev nu = ti.peek(p);
+                            if (nu.rows > 0) umma_slab_prefetch<NB>(dn_regs, seg_of(nu), plan, S, nu.col0, tid);
+                        }
                         if constexpr (GEMV) {
                             if (ti.un.phase != cur_phase) {
                                 cur_phase = ti.un.phase;
@@ -527,10 +558,8 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         const uint32_t wrow = w_base + stage * kUWStage + row_in_tile * 128;
                         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * kUN;
                         float y = 0.f;
-#pragma unroll 1
-                        for (int c4 = 0; c4 < kUN / 32; ++c4) {
-                            uint32_t d[32];
-                            tmem_ld32(taddr + c4 * 32, d);
+                        // one 32-column chunk of this thread's row: W + D, round, store back, dot with x
+                        auto chunk = [&](const uint32_t (&d)[32], int c4) {
                             const uint32_t wbox = wrow + (c4 >> 1) * kUBoxBytes;
 #pragma unroll
                             for (int i = 0; i < 4; ++i) {
@@ -563,6 +592,13 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                     y = fmaf(bf16lo_to_f32(out[3]), xb.z, y); y = fmaf(bf16hi_to_f32(out[3]), xb.w, y);
                                 }
                             }
+                        };
+#pragma unroll 1
+                        for (int c4 = 0; c4 < kUN / 32; ++c4) {
+                            uint32_t da[32];
+                            tmem_ld32(taddr + c4 * 32, da);
+                            tmem_ld_wait();
+                            chunk(da, c4);
                         }
                         tc_fence_before();
                         fence_proxy_async_smem();   // tile written back -> visible to the TMA store
