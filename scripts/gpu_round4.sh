@@ -16,7 +16,7 @@ timeout 300 python scripts/timeline_chase.py --show 0,1,17,32 > gpurun_out/chase
 if [ "$1" != "noncu" ]; then
 AF_NCU=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off -c 300 --csv --log-file gpurun_out/launches.csv \
    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
-AF_NCU=1 timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:switch_mma -s 17 -c 1 -o gpurun_out/prof_chase -f \
+AF_NCU=1 timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:switch_u?mma -s 17 -c 1 -o gpurun_out/prof_chase -f \
    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_chase.log 2>&1
 fi
 grep -E "passed|failed|exit" gpurun_out/tests.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err; cat gpurun_out/bench_separate.json

@@ -131,7 +131,7 @@ def main():
         if first:
             rd, wr = to_bytes(first, "dram__bytes_read.sum"), to_bytes(first, "dram__bytes_write.sum")
             layers = 32
-            json.dump({"workload": "llama2-7b", "kernel": "switch_mma_kernel<2, GEMV> (one chained launch: o -> gate|up -> down -> next q|k|v)",
+            json.dump({"workload": "llama2-7b", "kernel": "switch_umma_kernel<4, GEMV> (one chained launch: o -> gate|up -> down -> next q|k|v)",
                        "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
                        "dram_bytes_per_token": (rd + wr) * layers,
                        "note": "a chained launch covers one layer's seven matrices; per token = per launch x 32 layers "
@@ -139,7 +139,8 @@ def main():
                        "source": f"profiles/{tag}_chase_full.txt (one ncu --set full capture inside bench.py's e2e region)"},
                       open(os.path.join(PROF, "chase_traffic.json"), "w"), indent=1)
             print("chase traffic per launch", (rd + wr) / 1e6, "MB")
-        for name, dst in (("chase_timeline.txt", "chase_timeline.txt"), ("bench.json", "bench.json"), ("bench_separate.json", "bench_separate.json"),
+        full(tag, "switch_umma", "prof_switch_umma.ncu-rep")
+        for name, dst in (("chase_timeline.txt", "chase_timeline.txt"), ("umma_ab.txt", "umma_ab.txt"), ("umma_switch_ab.txt", "umma_switch_ab.txt"), ("bench.json", "bench.json"), ("bench_separate.json", "bench_separate.json"),
                           ("chase_kernel.txt", "chase_kernel.txt"), ("ab.txt", "consumer_loop_ab.txt")):
             pth = os.path.join(OUT, name)
             if os.path.exists(pth):
