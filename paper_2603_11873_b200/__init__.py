@@ -46,11 +46,14 @@ from .adapters import (
     ConcatAdapter,
     ExpertBank,
     LoraExpert,
+    SegmentGroup,
     SwitchTable,
     build_switch,
     concat_gated,
     expert_apply,
+    load_bank,
     merge_all,
+    save_bank,
 )
 from .model import (
     DecodeState,
@@ -63,9 +66,11 @@ from .model import (
     forward_layer,
     fused_switch,
     generate,
+    load_checkpoint,
     max_backbone_deviation,
     merge,
     prefill,
+    save_checkpoint,
     unmerge,
     weights_digest,
 )

@@ -23,6 +23,8 @@ import torch
 from . import _capi
 from .errors import DeviceError, DimensionError, PrecisionError
 from .linalg import (
+    PRECISION_DTYPES,
+    default_device,
     DEFAULT_TILE,
     DeviceTable,
     DispatchRecorder,
@@ -340,6 +342,82 @@ class SwitchTable:
             self._dev_scalar = torch.zeros(1, dtype=torch.float32, device="cuda")
         _capi.check(_capi.lib().af_max_deviation(self.device_table.handle, _ptr(self._dev_scalar), _capi.stream_ptr()))
         return float(self._dev_scalar.item())
+
+
+# ---------------------------------------------------------------------------
+# Serialization (adapters.py:265-306): the reference's npz container, read and written
+# ---------------------------------------------------------------------------
+
+_BANK_FORMAT = "lorafuse-bank-v1"
+
+
+def _load_precision(stored: str, wanted: str | None) -> str:
+    """Device precision for arrays stored under the reference's tag: "single"/"double" files load as
+    "single" unless the caller asks for "bf16" (values on the bf16 grid survive exactly)."""
+    if wanted is not None:
+        if wanted not in ("bf16", "single"):
+            raise PrecisionError(f"unknown precision tag {wanted!r}")
+        return wanted
+    return stored if stored in ("bf16", "single") else "single"
+
+
+def save_bank(bank: ExpertBank, path) -> None:
+    """adapters.py:268-284: header + `layer{l}/expert{e}/{down,up}` arrays.  Arrays are written as
+    f32 (a bf16 factor upcasts exactly), so the reference's own `load_bank` reads the file; the
+    header keeps the device precision tag."""
+    import json
+
+    import numpy as np
+
+    bank.validate()
+    prec = bank.layers[0][0].down.precision
+    header = {"format": _BANK_FORMAT, "n_layers": bank.n_layers, "n_experts": bank.n_experts, "rank": bank.rank,
+              "precision": "single" if prec == "bf16" else prec, "device_precision": prec}
+    arrays = {"header": np.frombuffer(json.dumps(header).encode("utf-8"), dtype=np.uint8)}
+    for li, layer in enumerate(bank.layers):
+        for ei, expert in enumerate(layer):
+            arrays[f"layer{li}/expert{ei}/down"] = expert.down.numpy().astype(np.float32)
+            arrays[f"layer{li}/expert{ei}/up"] = expert.up.numpy().astype(np.float32)
+    with open(path, "wb") as fh:
+        np.savez(fh, **arrays)
+
+
+def pack_bank_arrays(archive, n_layers: int, n_experts: int, precision: str, device=None):
+    """`layer{l}/expert{e}/{down,up}` arrays -> the packed device layout the switch kernels read:
+    per layer one contiguous [N][r][d_in] tensor and one [N][d_out][r] tensor, with an `ExpertBank`
+    whose experts are VIEWS into them (no second copy)."""
+    import numpy as np
+
+    dtype = PRECISION_DTYPES[precision]
+    dev = device if device is not None else default_device()
+    bank_down, bank_up, layers = [], [], []
+    for li in range(n_layers):
+        dn = np.stack([np.asarray(archive[f"layer{li}/expert{ei}/down"], dtype=np.float32) for ei in range(n_experts)])
+        up = np.stack([np.asarray(archive[f"layer{li}/expert{ei}/up"], dtype=np.float32) for ei in range(n_experts)])
+        dn_t = torch.from_numpy(dn).to(device=dev, dtype=dtype).contiguous()
+        up_t = torch.from_numpy(up).to(device=dev, dtype=dtype).contiguous()
+        bank_down.append(dn_t)
+        bank_up.append(up_t)
+        layers.append(tuple(LoraExpert(down=Matrix(dn_t[e], precision), up=Matrix(up_t[e], precision)) for e in range(n_experts)))
+    bank = ExpertBank(layers=tuple(layers))
+    bank.validate()
+    return bank, bank_down, bank_up
+
+
+def load_bank(path, precision: str | None = None, device=None, packed: bool = False):
+    """adapters.py:287-306.  Reads files written by the reference or by `save_bank`.  With
+    ``packed=True`` also returns the per-layer packed tensors (`SwitchTable(targets, downs, ups)`)."""
+    import json
+
+    import numpy as np
+
+    with np.load(path) as archive:
+        header = json.loads(bytes(archive["header"]).decode("utf-8"))
+        if header.get("format") != _BANK_FORMAT:
+            raise ValueError(f"not a {_BANK_FORMAT} container: {path}")
+        prec = _load_precision(header.get("device_precision", header["precision"]), precision)
+        bank, downs, ups = pack_bank_arrays(archive, header["n_layers"], header["n_experts"], prec, device)
+    return (bank, downs, ups) if packed else bank
 
 
 class SegmentGroup:

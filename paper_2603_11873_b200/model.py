@@ -25,7 +25,7 @@ import torch
 
 from . import _capi
 from .adapters import ConcatAdapter, ExpertBank, LoraExpert, SwitchTable, expert_apply  # noqa: F401
-from .errors import DeviceError, InputError, StateError
+from .errors import DeviceError, DimensionError, InputError, StateError
 from .linalg import PRECISION_DTYPES, _AF_DTYPE, DispatchEvent, DispatchRecorder, Matrix, _ptr, gemm
 from .routing import DeviceDecision, GateDecision, RouterParams, pregate_device, pregate_token_device
 
@@ -460,3 +460,73 @@ def unmerge(model: DecoderModel, decision, recorder: DispatchRecorder | None = N
 
 __all__ = [n for n in dir() if not n.startswith("_")] + ["_merged_pass", "_embed_token", "_unembed"]
 _ = (DispatchEvent, DeviceError, pregate_token_device)
+
+
+# ---------------------------------------------------------------------------
+# Checkpoints (model.py:481-541): the reference's npz container, read and written
+# ---------------------------------------------------------------------------
+
+_CHECKPOINT_FORMAT = "lorafuse-checkpoint-v1"
+_REFERENCE_CONFIG_KEYS = ("layers", "hidden", "vocab", "experts", "rank", "top_k", "precision", "seed", "strategy", "refresh_every")
+
+
+def save_checkpoint(model: DecoderModel, path) -> None:
+    """model.py:484-505: config + all weights; the PRISTINE backbone is what gets saved, so a
+    checkpoint captures the unmerged model even while a token's delta is fused in.  Arrays are
+    written as f32 and the header's config carries only the reference's keys with a reference
+    precision tag, so the reference's own `load_checkpoint` reads the file; the device-side extras
+    travel under "device"."""
+    import json
+
+    cfg = model.config.to_dict()
+    ref_cfg = {k: cfg[k] for k in _REFERENCE_CONFIG_KEYS}
+    ref_cfg["precision"] = "single" if cfg["precision"] == "bf16" else cfg["precision"]
+    header = {"format": _CHECKPOINT_FORMAT, "config": ref_cfg,
+              "device": {"precision": cfg["precision"], "compute": cfg["compute"], "switch_mode": cfg["switch_mode"]}}
+    f32 = lambda m: m.numpy().astype(np.float32)  # noqa: E731
+    arrays = {"header": np.frombuffer(json.dumps(header).encode("utf-8"), dtype=np.uint8), "embed": f32(model.embed),
+              "router": f32(model.router.weight), "unembed": f32(model.unembed)}
+    for li in range(model.config.layers):
+        arrays[f"backbone{li}"] = f32(model.pristine_backbone[li])
+        for ei, expert in enumerate(model.bank.layers[li]):
+            arrays[f"layer{li}/expert{ei}/down"] = f32(expert.down)
+            arrays[f"layer{li}/expert{ei}/up"] = f32(expert.up)
+    with open(path, "wb") as fh:
+        np.savez(fh, **arrays)
+
+
+def load_checkpoint(path, precision: str | None = None, device=None) -> DecoderModel:
+    """model.py:508-541.  Reads checkpoints written by the reference or by `save_checkpoint`, uploads
+    the weights, packs the expert bank into the per-layer [N][r][d] / [N][d][r] device layout and
+    builds the descriptor table -- the model is ready to decode."""
+    import json
+
+    from .adapters import _load_precision, pack_bank_arrays
+
+    torch_ = _capi.require_cuda()
+    dev = torch_.device(device) if device is not None else torch_.device("cuda", torch_.cuda.current_device())
+    with np.load(path) as archive:
+        header = json.loads(bytes(archive["header"]).decode("utf-8"))
+        if header.get("format") != _CHECKPOINT_FORMAT:
+            raise ValueError(f"not a {_CHECKPOINT_FORMAT} container: {path}")
+        raw = dict(header["config"])
+        extra = header.get("device", {})
+        prec = _load_precision(extra.get("precision", raw.get("precision", "single")), precision)
+        raw["precision"] = prec
+        for key in ("compute", "switch_mode"):
+            if key in extra:
+                raw[key] = extra[key]
+        config = ModelConfig.from_dict(raw)
+
+        def up(name):
+            return Matrix(torch_.from_numpy(np.asarray(archive[name], dtype=np.float32)), prec, device=dev)
+
+        embed, router, unembed = up("embed"), RouterParams(weight=up("router")), up("unembed")
+        backbone = [up(f"backbone{li}") for li in range(config.layers)]
+        bank, bank_down, bank_up = pack_bank_arrays(archive, config.layers, config.experts, prec, dev)
+    if embed.rows != config.vocab or embed.cols != config.hidden:
+        raise DimensionError("checkpoint embed shape disagrees with its config")
+    pristine = [m.copy() for m in backbone]
+    table = SwitchTable(backbone, bank_down, bank_up, pristine=pristine)
+    return DecoderModel(config, embed, backbone, bank, router, unembed, pristine, bank_down, bank_up, table)
+

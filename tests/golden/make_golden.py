@@ -213,7 +213,24 @@ def golden_generate():
     np.savez_compressed(os.path.join(HERE, "generate.npz"), **out)
 
 
+def golden_io():
+    """Containers written by the reference's OWN save_bank / save_checkpoint (adapters.py:265-306,
+    model.py:481-541) for a small bf16-shimmed model, plus what the reference decodes from it: the
+    loaders of the B200 package must read these files and reproduce the tokens."""
+    kw = dict(layers=2, hidden=32, vocab=48, experts=4, rank=8, top_k=2, seed=7)
+    model = lf.build_model(lf.ModelConfig(precision="single", strategy=lf.Strategy.PRE_GATED_FUSED, **kw))
+    shim_model_to_bf16(model)
+    lfa.save_bank(model.bank, os.path.join(HERE, "ref_bank.npz"))
+    lfm.save_checkpoint(model, os.path.join(HERE, "ref_checkpoint.npz"))
+    rec = lf.DispatchRecorder()
+    toks, _ = lf.generate(model, [3, 11, 40], 10, rec)
+    np.savez(os.path.join(HERE, "ref_io_expected.npz"), tokens=np.array(toks, np.int32), digest=np.frombuffer(
+        lf.weights_digest(model).encode(), dtype=np.uint8), config=np.array([kw[k] for k in ("layers", "hidden", "vocab", "experts", "rank", "top_k", "seed")]))
+    print("io fixtures: tokens", toks)
+
+
 if __name__ == "__main__":
+    golden_io()
     golden_router()
     golden_sgmm()
     golden_switch()
