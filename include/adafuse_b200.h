@@ -124,7 +124,8 @@ int af_set_umma(int32_t enable);
 int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t target_dtype,
                     int32_t factor_dtype, af_table** out);
 int af_table_destroy(af_table* table);
-/* n_units: persistent-kernel work units; fast_path: 1 if the TMA kernel applies. */
+/* n_units: persistent-kernel work units; fast_path bits: 1 = TMA kernels apply, 2 = tensor path
+ * (mma.sync) applies, 4 = the tcgen05 / TMEM kernels apply and are enabled (af_set_umma). */
 int af_table_info(const af_table* table, int32_t* n_segments, int64_t* target_elems,
                   int32_t* n_units, int32_t* fast_path);
 /* Device-side validation result of the launches issued on `stream` so far (SYNCHRONISES the

@@ -389,7 +389,7 @@ int af_table_info(const af_table* t, int32_t* n_segments, int64_t* target_elems,
     if (n_segments) *n_segments = t->n_segments;
     if (target_elems) *target_elems = t->target_elems;
     if (n_units) *n_units = t->n_units;
-    if (fast_path) *fast_path = (t->fast_fma ? 1 : 0) | (t->fast_mma ? 2 : 0);
+    if (fast_path) *fast_path = (t->fast_fma ? 1 : 0) | (t->fast_mma ? 2 : 0) | ((t->umma_ok && g_umma.load()) ? 4 : 0);
     return AF_OK;
 }
 

@@ -284,6 +284,7 @@ class DeviceTable:
             "n_units": units.value,
             "tma_path": bool(fast.value & 1),
             "tensor_path": bool(fast.value & 2),
+            "umma_path": bool(fast.value & 4),
         }
 
     def status(self) -> None:
