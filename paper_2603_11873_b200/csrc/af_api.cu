@@ -2,6 +2,7 @@
 // kernel selection and launches.  No torch types anywhere; every device buffer belongs to the
 // caller.  Citations are relative to /root/reference/pkg/src/lorafuse/.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -759,38 +760,46 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
                 const int d_out = t->segs[sidx].d_out;
                 for (int sp = 0; sp < strips; ++sp) strips_v.push_back({sidx, first + i, sp, (d_out + tile_rows - 1) / tile_rows, d_out});
             }
-            auto cut = [&](long long budget, std::vector<std::vector<UnitDev>>* out) -> int {
-                int cta = 0;
-                long long cost = 0;   // cost already in the current span
+            // Spans end at multiples of a fractional per-CTA budget (total cost / Gp), so every CTA gets
+            // its share to within one tile; the total cost depends on how many spans cross a strip
+            // boundary, which depends on the cut -- three fixed-point rounds settle it.
+            auto cut = [&](double budget, std::vector<std::vector<UnitDev>>* out) -> int {
+                int cta = 0, crossings = 0;
+                double cost = 0.0;   // cumulative cost of everything emitted so far
                 for (const Strip& st : strips_v) {
                     int r = 0;
+                    bool entered = false;
                     while (r < st.rt) {
-                        long long room = budget - cost - (cost > 0 ? penalty : 0);   // entering a strip mid-span costs the penalty
-                        if (cost > 0 && room < std::max(1, penalty)) {   // not worth a unit change: close the span, start a new one here
-                            ++cta;
-                            cost = 0;
-                            continue;
+                        const double span_start = cta * budget, span_end = (cta + 1) * budget;
+                        if (!entered) {
+                            entered = true;
+                            if (cost > span_start + 0.5) {   // the span continues into this strip: a unit change
+                                cost += penalty;
+                                ++crossings;
+                            }
                         }
-                        if (room < 1) room = 1;
+                        long long room = (long long)std::floor(span_end - cost + 1e-6);
+                        if (room < 1) {
+                            if (cta < Gp - 1) {
+                                ++cta;
+                                continue;
+                            }
+                            room = st.rt - r;   // the last CTA takes what is left
+                        }
                         const int take = (int)std::min<long long>(st.rt - r, room);
                         if (out) {
                             const int row0 = r * tile_rows;
-                            (*out)[std::min(cta, Gp - 1)].push_back({st.sidx, row0, std::min(take * tile_rows, st.d_out - row0), st.sp * tile_cols, ph, st.slot});
+                            (*out)[cta].push_back({st.sidx, row0, std::min(take * tile_rows, st.d_out - row0), st.sp * tile_cols, ph, st.slot});
                         }
-                        cost += take + (cost > 0 ? penalty : 0);
+                        cost += take;
                         r += take;
                     }
                 }
-                return cta + 1;
+                return crossings;
             };
-            long long lo = (total + Gp - 1) / Gp, hi = lo + (long long)penalty * 4 + 8;
-            while (cut(hi, nullptr) > Gp) hi *= 2;
-            while (lo < hi) {
-                const long long mid = (lo + hi) / 2;
-                if (cut(mid, nullptr) <= Gp) hi = mid;
-                else lo = mid + 1;
-            }
-            cut(lo, &per_cta);
+            int crossings = 0;
+            for (int round = 0; round < 3; ++round) crossings = cut((double)(total + (long long)penalty * crossings) / Gp, nullptr);
+            cut((double)(total + (long long)penalty * crossings) / Gp, &per_cta);
             first += phase_len[ph];
         }
         grid = used;
@@ -934,7 +943,8 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     static const int env_dbg = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
     mp.dbg = env_dbg ^ 24;
     const int ks_tl = std::max(1, (s_bound + 15) / 16);
-    if (g_timeline && g_timeline_left > 0 && ks_tl == 2) {  // the probe is compiled into the KS = 2 hi/lo variant only
+    const bool umma_launch = g_umma.load() && t->umma_ok && g->d_units_umma && n_blocks_bound <= 8;
+    if (g_timeline && g_timeline_left > 0 && (ks_tl == 2 || umma_launch)) {  // mma.sync: the probe is compiled into the KS = 2 hi/lo variant only
         mp.timeline = g_timeline;
         g_timeline += g_timeline_stride;
         --g_timeline_left;
@@ -946,7 +956,7 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         if (ks == 2) return launch_mma<2, false, false>(mp, g->grid, st);
     }
     // tcgen05 path (env AF_UMMA=1 while it is being validated): rank-8 tables of 128-multiples
-    if (g_umma.load() && t->umma_ok && g->d_units_umma && !mp.timeline && n_blocks_bound <= 8) {
+    if (umma_launch) {
         p.units = g->d_units_umma;
         p.n_units = g->n_units_umma;
         mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 6 : 5) * S;

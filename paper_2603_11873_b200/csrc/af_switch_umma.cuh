@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
     SegDev* seg_cache = reinterpret_cast<SegDev*>(sm + L::off_segs);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
+    unsigned long long* const tl = GEMV ? mp.timeline : nullptr;   // probe: a few stamps per phase, none per tile
+    if (tid == 0) tl_stamp(tl, 0);
     if (tid >= 32 && tid < 32 + kUnitCache) {
         const int jj = tid - 32;
         const long long uu = (long long)blockIdx.x + (long long)jj * gridDim.x;
@@ -395,9 +397,12 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     ti.next(p);
                 }
                 bulk_wait_all<0>();
+                tl_stamp(tl, 6);
             }
         } else {
-            // ============ epilogue warps: group g = warp / 4 takes the tiles with it % 2 == g ============
+            // ============ epilogue warps: group g = warp / 4 takes the tiles with it % 2 == g (TMEM lane quarter =
+            // warp % 4).  Sharing every tile between the groups (64 columns each) halves a tile's latency at the
+            // phase boundaries but slows the steady state by 5 % (twice the atomics): measured, not kept. ============
             const int group = warp >> 2, quarter = warp & 3;
             const int row_in_tile = quarter * 32 + lane;
             unsigned char* slab = sm + L::off_slab;
@@ -410,12 +415,15 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         pdl_wait();
                         if (tid == 0) pdl_launch_dependents();
                     }
+                    if (tid == 0) tl_stamp(tl, 3);
                 }
                 float x_inv = 1.0f;
+                bool tl_first = false;
                 int cur_phase = -1, phase_j0 = 0, published = 0;
                 // entering a phase: previous phase published by every CTA, then the input vector
                 auto enter_phase = [&](int ph) {
                     const GemvParams& g = mp.gv[ph];
+                    if (tid == 0) tl_stamp(tl, 8 + 4 * ph);
                     if (ph > 0) {
                         if (tid == 0) {
                             const int target = (int)gridDim.x;
@@ -432,6 +440,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         }
                         named_bar_sync(1, kUEpi);
                     }
+                    if (tid == 0) tl_stamp(tl, 9 + 4 * ph);
                     x_inv = 1.0f;
                     phase_j0 = ti.j;
                     // strips of this CTA's units of the phase: thread t -> column t % 128 of slots t / 128 and t / 128 + 2
@@ -459,10 +468,11 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         float ss = 0.f;
                         const bool write_h = g.h_out && blockIdx.x == 0;
                         constexpr int kStep = 2 * kUEpi;
-                        for (int base = 2 * tid; base < g.x_len; base += 4 * kStep) {
-                            float2 hv[4];
+                        constexpr int kFly = 8;   // steps of loads in flight: 4096 entries are ONE L2 round trip
+                        for (int base = 2 * tid; base < g.x_len; base += kFly * kStep) {
+                            float2 hv[kFly];
 #pragma unroll
-                            for (int u4 = 0; u4 < 4; ++u4) {
+                            for (int u4 = 0; u4 < kFly; ++u4) {
                                 const int c = base + u4 * kStep;
                                 hv[u4] = make_float2(0.f, 0.f);
                                 if (c < g.x_len) {
@@ -480,7 +490,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                 }
                             }
 #pragma unroll
-                            for (int u4 = 0; u4 < 4; ++u4) {
+                            for (int u4 = 0; u4 < kFly; ++u4) {
                                 const int c = base + u4 * kStep;
                                 ss = fmaf(hv[u4].x, hv[u4].x, fmaf(hv[u4].y, hv[u4].y, ss));
                                 if (write_h && c < g.x_len) *reinterpret_cast<float2*>(g.h_out + c) = hv[u4];
@@ -503,6 +513,8 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         xs_all[((tid >> 7) + 2 * k2) * kUN + (tid & 127)] = v;
                     }
                     named_bar_sync(1, kUEpi);
+                    if (tid == 0) tl_stamp(tl, 10 + 4 * ph);
+                    tl_first = true;
                 };
 
                 const int S = n_blocks * 8;
@@ -610,9 +622,12 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         if constexpr (GEMV) {
                             if (m0 + row_in_tile < row_end)
                                 atomicAdd(acc_out + yoff + m0 + row_in_tile, (unsigned long long)f32_to_fix(y));
+                            if (tl_first && tid == (it & 1) * 128) tl_stamp(tl, 11 + 4 * cur_phase);
                         }
                     }
+                    tl_first = false;
                 }
+                if (tid == 0) tl_stamp(tl, 7);
                 if constexpr (GEMV) {   // the remaining phases of the chain
                     named_bar_sync(1, kUEpi);
                     if (tid == 0 && published < mp.n_phases - 1) {

@@ -79,7 +79,7 @@ if not args.no_chain:
     # first unit change inside phase 1 (CTAs whose span crosses a strip boundary)
     uc = tl[1:-1, :, 26:32]
     has = ~np.isnan(uc[:, :, 0])
-    if has.any():
+    if has.any():   # (the tcgen05 kernel carries no per-unit stamps)
         d = (uc[:, :, 1:] - uc[:, :, :-1]) / 1e3
         labels = ["wait for all warps", "commit slab + barrier", "new-unit setup", "wait full[stage]", "first tile compute"]
         for k, lb in enumerate(labels):
@@ -93,7 +93,7 @@ if not args.no_chain:
 # cycles each role spent blocked, as a share of the consumers' lifetime (mean over CTAs and launches)
 life = np.nan_to_num(tl[:, :, 41])
 ok = life > 0
-for slot, nm in ((36, "consumer warp 0 waiting for full[stage] (data)"), (37, "W producer waiting for empty[stage] (ring full)"),
+for slot, nm in () if not ok.any() else ((36, "consumer warp 0 waiting for full[stage] (data)"), (37, "W producer waiting for empty[stage] (ring full)"),
                  (38, "storer waiting for computed[stage]"), (39, "storer waiting for its stores to drain smem")):
     v = np.nan_to_num(tl[:, :, slot])[ok] / life[ok]
     print(f"blocked: {nm:52s} mean {100 * v.mean():5.1f} %  max {100 * v.max():5.1f} %")
