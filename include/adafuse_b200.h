@@ -219,6 +219,9 @@ int af_embed(const void* table, int32_t dtype, int32_t d, const int32_t* token_d
 #define AF_PRO_NONE 0
 #define AF_PRO_RMSNORM 1
 #define AF_PRO_SILU_MUL 2
+#define AF_PRO_RMSNORM_DEFERRED 3 /* af_switch_gemv_chain on the tcgen05 path only: x' = x * norm_w; the scale
+                                     rsqrt(mean(x^2) + eps) is written to inv_out by one CTA and applied by the
+                                     consumer of the phase's outputs (inv_in / qkv_scale_dev) */
 int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const float* x, float* out,
                   int32_t prologue, const float* norm_w, float eps, int32_t epilogue, const float* res,
                   void* stream);
@@ -275,7 +278,8 @@ int af_step_advance(af_decision* prev_dev, const af_decision* cur_dev, int32_t* 
  *    while the previous kernel of the stream drains; the previous kernel must be one of this
  *    library's decode kernels (they all execute griddepcontrol.wait).
  * af_accum_to_f32 : out = (res ? res : 0) + fix^-1(acc)   (hand-over to af_gemv_fused / lm_head).
- * af_attn_decode_fix : af_attn_decode reading q|k|v from fixed-point accumulators.
+ * af_attn_decode_fix : af_attn_decode reading q|k|v from fixed-point accumulators, times
+ *    *qkv_scale_dev when given (the deferred RMSNorm scale of the launch that produced them).
  *
  * Chains: up to 4 projections whose inputs depend on each other's outputs (o -> gate|up -> down ->
  * next layer's q|k|v) run in ONE launch (af_chain_create / af_switch_gemv_chain).  The weight
@@ -296,6 +300,8 @@ typedef struct af_gemv_phase {
     int64_t* acc_out;       /* y_rows accumulators of this phase, zeroed by the caller             */
     float eps;
     int32_t prologue;
+    float* inv_out;         /* AF_PRO_RMSNORM_DEFERRED: receives the scale of this phase's input   */
+    const float* inv_in;    /* scale of this phase's input accumulators (deferred by their producer) */
 } af_gemv_phase;
 int af_group_create(af_table* table, const int32_t* seg_ids, int32_t n, af_group** out);
 /* seg_ids: the phases' segment lists back to back; phase_len[p] segments belong to phase p. */
@@ -330,9 +336,9 @@ int af_switch_gemv(af_group* group, const af_decision* prev_dev, const af_decisi
 #define AF_TIMELINE_SLOTS 42
 int af_set_timeline(uint64_t* buffer_dev, int32_t n_launches, int64_t stride_elems);
 int af_accum_to_f32(const int64_t* acc, const float* res, float* out, int32_t n, void* stream);
-int af_attn_decode_fix(const int64_t* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,
-                       const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
-                       int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,
+int af_attn_decode_fix(const int64_t* qkv_fix, const float* qkv_scale_dev, void* k_cache, void* v_cache,
+                       const float* cos_table, const float* sin_table, const int32_t* pos_dev, int32_t n_heads,
+                       int32_t n_kv_heads, int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,
                        int32_t* tickets, float* out, void* stream);
 
 #ifdef __cplusplus

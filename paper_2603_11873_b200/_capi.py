@@ -80,6 +80,8 @@ class GemvPhase(ctypes.Structure):
         ("acc_out", ctypes.c_void_p),
         ("eps", ctypes.c_float),
         ("prologue", ctypes.c_int32),
+        ("inv_out", ctypes.c_void_p),
+        ("inv_in", ctypes.c_void_p),
     ]
 
 
@@ -146,11 +148,11 @@ SIGNATURES = {
     "af_plan_build": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp]),
     "af_set_timeline": (ctypes.c_int, [_vp, _i32, _i64]),
     "af_accum_to_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp]),
-    "af_attn_decode_fix": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "af_attn_decode_fix": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 AF_FIX_SHIFT = 40
 AF_CHAIN_PDL, AF_CHAIN_PLAN_PREBUILT = 1, 2
-AF_PRO_NONE, AF_PRO_RMSNORM, AF_PRO_SILU_MUL = 0, 1, 2
+AF_PRO_NONE, AF_PRO_RMSNORM, AF_PRO_SILU_MUL, AF_PRO_RMSNORM_DEFERRED = 0, 1, 2, 3
 
 _lib = None
 

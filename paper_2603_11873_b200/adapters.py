@@ -429,7 +429,8 @@ class SegmentGroup:
     `seg_ids` may also be a list of lists: a CHAIN of up to four such groups whose inputs depend
     on each other's outputs, run as one launch (`switch_gemv_chain`)."""
 
-    PROLOGUES = {"none": _capi.AF_PRO_NONE, "rmsnorm": _capi.AF_PRO_RMSNORM, "silu_mul": _capi.AF_PRO_SILU_MUL}
+    PROLOGUES = {"none": _capi.AF_PRO_NONE, "rmsnorm": _capi.AF_PRO_RMSNORM, "silu_mul": _capi.AF_PRO_SILU_MUL,
+                 "rmsnorm_deferred": _capi.AF_PRO_RMSNORM_DEFERRED}
 
     def __init__(self, table: SwitchTable, seg_ids):
         import ctypes
@@ -452,14 +453,15 @@ class SegmentGroup:
         self.x_len, self.y_rows = self.x_lens[0], self.y_rows_all[0]
         self.n_units, self.grid, self.tiles = n_units.value, grid.value, tiles.value
 
-    def _phase_struct(self, ph: int, acc_out, xin=None, acc_in=None, res=None, h_out=None, prologue="none", norm_w=None, eps: float = 0.0):
+    def _phase_struct(self, ph: int, acc_out, xin=None, acc_in=None, res=None, h_out=None, prologue="none", norm_w=None, eps: float = 0.0,
+                      inv_out=None, inv_in=None):
         if prologue not in self.PROLOGUES:
             raise ValueError(f"unknown prologue {prologue!r}")
         x_len, y_rows = self.x_lens[ph], self.y_rows_all[ph]
         need = x_len * (2 if prologue == "silu_mul" else 1)
         for name, t, dt, n in (("xin", xin, torch.float32, need), ("acc_in", acc_in, torch.int64, need), ("res", res, torch.float32, x_len),
                                ("h_out", h_out, torch.float32, x_len), ("norm_w", norm_w, torch.float32, x_len),
-                               ("acc_out", acc_out, torch.int64, y_rows)):
+                               ("acc_out", acc_out, torch.int64, y_rows), ("inv_out", inv_out, torch.float32, 1), ("inv_in", inv_in, torch.float32, 1)):
             if t is None:
                 continue
             if not t.is_cuda:
@@ -468,7 +470,7 @@ class SegmentGroup:
                 raise DimensionError(f"{name} must be a contiguous {dt} vector of at least {n} entries")
         p = lambda t: _ptr(t) if t is not None else None  # noqa: E731
         return _capi.GemvPhase(xin=p(xin), acc_in=p(acc_in), res=p(res), h_out=p(h_out), norm_w=p(norm_w), acc_out=p(acc_out),
-                               eps=float(eps), prologue=self.PROLOGUES[prologue])
+                               eps=float(eps), prologue=self.PROLOGUES[prologue], inv_out=p(inv_out), inv_in=p(inv_in))
 
     def switch_gemv_chain(self, prev, cur, phases, phase_done=None, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0,
                           mode: str = "inplace", pdl: bool = False, plan_prebuilt: bool = False) -> None:

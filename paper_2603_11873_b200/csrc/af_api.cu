@@ -737,7 +737,10 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
     //      and, when the table allows it, 128 x 128 (tcgen05 kernel). ----
     const int G = std::max(1, t->sm_count);
     static const int env_penalty = [] { const char* e = getenv("AF_UNIT_PENALTY"); return e ? atoi(e) : 4; }();
-    auto build = [&](int tile_rows, int tile_cols, int penalty, std::vector<UnitDev>& units, int& grid, long long* tiles_out) {
+    // cta0_extra: CTA 0 also materialises the residual stream and, with deferred RMSNorm scales, reads the
+    // whole input vector alone -- its spans are shorter by that many tile-times
+    auto build = [&](int tile_rows, int tile_cols, int penalty, int cta0_extra, std::vector<UnitDev>& units, int& grid,
+                     long long* tiles_out) {
         std::vector<std::vector<UnitDev>> per_cta(G);
         int used = 0, first = 0;
         for (int ph = 0; ph < n_phases; ++ph) {
@@ -765,15 +768,18 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
             // boundary, which depends on the cut -- three fixed-point rounds settle it.
             auto cut = [&](double budget, std::vector<std::vector<UnitDev>>* out) -> int {
                 int cta = 0, crossings = 0;
-                double cost = 0.0;   // cumulative cost of everything emitted so far
+                // cumulative cost of everything emitted so far; CTA 0 starts with its extra duties on the books,
+                // but always keeps at least one tile (it is the one that writes h_out / the deferred scale)
+                double cost = Gp > 1 ? std::min<double>(cta0_extra, std::max(0.0, std::floor(budget) - 1.0)) : 0.0;
+                long long in_span = 0;                             // tiles the current span already holds
                 for (const Strip& st : strips_v) {
                     int r = 0;
                     bool entered = false;
                     while (r < st.rt) {
-                        const double span_start = cta * budget, span_end = (cta + 1) * budget;
+                        const double span_end = (cta + 1) * budget;
                         if (!entered) {
                             entered = true;
-                            if (cost > span_start + 0.5) {   // the span continues into this strip: a unit change
+                            if (in_span > 0) {   // the span continues into this strip: a unit change
                                 cost += penalty;
                                 ++crossings;
                             }
@@ -782,6 +788,7 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
                         if (room < 1) {
                             if (cta < Gp - 1) {
                                 ++cta;
+                                in_span = 0;
                                 continue;
                             }
                             room = st.rt - r;   // the last CTA takes what is left
@@ -792,14 +799,16 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
                             (*out)[cta].push_back({st.sidx, row0, std::min(take * tile_rows, st.d_out - row0), st.sp * tile_cols, ph, st.slot});
                         }
                         cost += take;
+                        in_span += take;
                         r += take;
                     }
                 }
                 return crossings;
             };
             int crossings = 0;
-            for (int round = 0; round < 3; ++round) crossings = cut((double)(total + (long long)penalty * crossings) / Gp, nullptr);
-            cut((double)(total + (long long)penalty * crossings) / Gp, &per_cta);
+            const long long extra = Gp > 1 ? cta0_extra : 0;
+            for (int round = 0; round < 3; ++round) crossings = cut((double)(total + extra + (long long)penalty * crossings) / Gp, nullptr);
+            cut((double)(total + extra + (long long)penalty * crossings) / Gp, &per_cta);
             first += phase_len[ph];
         }
         grid = used;
@@ -810,11 +819,11 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
             for (size_t j = 0; j < per_cta[c].size(); ++j) units[j * grid + c] = per_cta[c][j];
     };
     std::vector<UnitDev> units, units_umma;
-    build(kMR, kTN, env_penalty, units, g->grid, &g->tiles);
+    build(kMR, kTN, env_penalty, 2, units, g->grid, &g->tiles);
     g->n_units = (int)units.size();
     bool umma = t->umma_ok;
     if (umma) {
-        build(kUM, kUN, 1, units_umma, g->grid_umma, nullptr);   // a 128 x 128 tile is 4x the bytes: a unit change weighs about one tile
+        build(kUM, kUN, 1, 2, units_umma, g->grid_umma, nullptr);   // a 128 x 128 tile is 4x the bytes: a unit change weighs about one tile
         g->n_units_umma = (int)units_umma.size();
     }
     cudaError_t e = cudaMalloc(&g->d_units, sizeof(UnitDev) * units.size());
@@ -883,8 +892,10 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     if (n_phases > 1 && !phase_done_dev) return fail(AF_EVALUE, "a chain of several phases needs its phase_done counters");
     for (int ph = 0; ph < n_phases; ++ph) {
         const af_gemv_phase& f = phases[ph];
-        if (f.prologue < AF_PRO_NONE || f.prologue > AF_PRO_SILU_MUL) return fail(AF_EVALUE, "unknown prologue");
-        if (f.prologue == AF_PRO_RMSNORM && !f.norm_w) return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
+        if (f.prologue < AF_PRO_NONE || f.prologue > AF_PRO_RMSNORM_DEFERRED) return fail(AF_EVALUE, "unknown prologue");
+        if ((f.prologue == AF_PRO_RMSNORM || f.prologue == AF_PRO_RMSNORM_DEFERRED) && !f.norm_w)
+            return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
+        if (f.prologue == AF_PRO_RMSNORM_DEFERRED && !f.inv_out) return fail(AF_EVALUE, "deferred RMSNorm needs inv_out");
         if ((f.xin == nullptr) == (f.acc_in == nullptr)) return fail(AF_EVALUE, "exactly one of xin / acc_in must be given");
         if (!f.acc_out) return fail(AF_EVALUE, "acc_out is NULL");
         if (reinterpret_cast<uintptr_t>(f.acc_out) % 8 != 0 || reinterpret_cast<uintptr_t>(f.acc_in) % 16 != 0)
@@ -932,6 +943,8 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         gv.prologue = f.prologue;
         gv.x_len = g->x_len[ph];
         gv.acc_out = reinterpret_cast<unsigned long long*>(f.acc_out);
+        gv.inv_out = f.inv_out;
+        gv.inv_in = f.inv_in;
     }
     mp.n_phases = n_phases;
     mp.phase_done = phase_done_dev;
@@ -956,6 +969,9 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         if (ks == 2) return launch_mma<2, false, false>(mp, g->grid, st);
     }
     // tcgen05 path (env AF_UMMA=1 while it is being validated): rank-8 tables of 128-multiples
+    for (int ph = 0; ph < n_phases; ++ph)
+        if ((phases[ph].prologue == AF_PRO_RMSNORM_DEFERRED || phases[ph].inv_in) && !umma_launch)
+            return fail(AF_ESTATE, "deferred RMSNorm scales are implemented by the tcgen05 kernel only (table info: umma_path)");
     if (umma_launch) {
         p.units = g->d_units_umma;
         p.n_units = g->n_units_umma;
@@ -986,6 +1002,8 @@ int af_switch_gemv(af_group* g, const af_decision* prev_dev, const af_decision* 
     f.acc_out = acc_out;
     f.eps = eps;
     f.prologue = prologue;
+    f.inv_out = nullptr;
+    f.inv_in = nullptr;
     return af_switch_gemv_chain(g, prev_dev, cur_dev, max_k, scale, mode, &f, 1, nullptr, pdl, stream);
 }
 
@@ -1172,10 +1190,10 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
     return AF_OK;
 }
 
-static int attn_decode_impl(const float* qkv, const long long* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,
-                            const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
-                            int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace, int32_t* tickets, float* out,
-                            void* stream);
+static int attn_decode_impl(const float* qkv, const long long* qkv_fix, const float* qkv_scale, void* k_cache, void* v_cache,
+                            const float* cos_table, const float* sin_table, const int32_t* pos_dev, int32_t n_heads,
+                            int32_t n_kv_heads, int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,
+                            int32_t* tickets, float* out, void* stream);
 
 int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t pdl, void* stream) {
     if (!phases || n_phases < 1 || n_phases > kGcMaxPhases) return fail(AF_EVALUE, "a GEMV chain has 1..4 phases");
@@ -1248,22 +1266,22 @@ int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* 
                    const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t max_seq,
                    int32_t n_split, float* workspace, int32_t* tickets, float* out, void* stream) {
     if (!qkv) return fail(AF_EVALUE, "NULL argument");
-    return attn_decode_impl(qkv, nullptr, k_cache, v_cache, cos_table, sin_table, pos_dev, n_heads, n_kv_heads, head_dim, max_seq,
+    return attn_decode_impl(qkv, nullptr, nullptr, k_cache, v_cache, cos_table, sin_table, pos_dev, n_heads, n_kv_heads, head_dim, max_seq,
                             n_split, workspace, tickets, out, stream);
 }
 
-int af_attn_decode_fix(const int64_t* qkv_fix, void* k_cache, void* v_cache, const float* cos_table, const float* sin_table,
-                       const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t max_seq,
-                       int32_t n_split, float* workspace, int32_t* tickets, float* out, void* stream) {
+int af_attn_decode_fix(const int64_t* qkv_fix, const float* qkv_scale_dev, void* k_cache, void* v_cache, const float* cos_table,
+                       const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                       int32_t max_seq, int32_t n_split, float* workspace, int32_t* tickets, float* out, void* stream) {
     if (!qkv_fix) return fail(AF_EVALUE, "NULL argument");
-    return attn_decode_impl(nullptr, reinterpret_cast<const long long*>(qkv_fix), k_cache, v_cache, cos_table, sin_table, pos_dev,
+    return attn_decode_impl(nullptr, reinterpret_cast<const long long*>(qkv_fix), qkv_scale_dev, k_cache, v_cache, cos_table, sin_table, pos_dev,
                             n_heads, n_kv_heads, head_dim, max_seq, n_split, workspace, tickets, out, stream);
 }
 
-static int attn_decode_impl(const float* qkv, const long long* qkv_fix, void* k_cache, void* v_cache, const float* cos_table,
-                            const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
-                            int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace, int32_t* tickets, float* out,
-                            void* stream) {
+static int attn_decode_impl(const float* qkv, const long long* qkv_fix, const float* qkv_scale, void* k_cache, void* v_cache,
+                            const float* cos_table, const float* sin_table, const int32_t* pos_dev, int32_t n_heads,
+                            int32_t n_kv_heads, int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,
+                            int32_t* tickets, float* out, void* stream) {
     if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads != 0) return fail(AF_EDIM, "heads must be a multiple of kv heads");
     if (head_dim < 2 || head_dim % 2 != 0 || head_dim > kAttnMaxHd) return fail(AF_EDIM, "head_dim must be even and <= 256");
     if (max_seq < 1) return fail(AF_EDIM, "max_seq must be positive");
@@ -1285,7 +1303,7 @@ static int attn_decode_impl(const float* qkv, const long long* qkv_fix, void* k_
     __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
     const bool aligned = (reinterpret_cast<uintptr_t>(k_cache) % 16 == 0) && (reinterpret_cast<uintptr_t>(v_cache) % 16 == 0);
 #define AF_ATTN(EL)                                                                                                       \
-    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode_kernel<EL>, qkv, qkv_fix, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,  \
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode_kernel<EL>, qkv, qkv_fix, qkv_scale, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,  \
                                    (int)n_kv_heads, (int)head_dim, (int)max_seq, scale, (int)n_split, workspace,           \
                                    reinterpret_cast<int*>(tickets), out))
     if (aligned && head_dim == 64) AF_ATTN(2);

@@ -376,6 +376,7 @@ __device__ __forceinline__ void load_bf16_vec(const __nv_bfloat16* p, float (&f)
 template <int EL>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* __restrict__ qkv,
                                                                    const long long* __restrict__ qkv_fix,
+                                                                   const float* __restrict__ qkv_scale,
                                                                    __nv_bfloat16* __restrict__ k_cache,
                                                                    __nv_bfloat16* __restrict__ v_cache,
                                                                    const float* __restrict__ cos_t,
@@ -403,7 +404,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
     // q/k/v of this head: f32, or the fixed-point accumulators of a fused switch + GEMV launch
     const long long oq = (long long)h * hd, ok = (long long)n_heads * hd + (long long)kvh * hd,
                     ov = (long long)(n_heads + n_kv) * hd + (long long)kvh * hd;
-    auto ld = [&](long long i) { return qkv_fix ? __ll2float_rn(qkv_fix[i]) * (1.0f / (float)(1ll << AF_FIX_SHIFT)) : qkv[i]; };
+    // (a launch with a deferred RMSNorm leaves q|k|v unscaled: qkv_scale holds the factor)
+    const float fix_scale = (qkv_scale ? *qkv_scale : 1.0f) * (1.0f / (float)(1ll << AF_FIX_SHIFT));
+    auto ld = [&](long long i) { return qkv_fix ? __ll2float_rn(qkv_fix[i]) * fix_scale : qkv[i]; };
     // RoPE (rotate-half): x'[i] = x[i] c - x[i+half] s ; x'[i+half] = x[i+half] c + x[i] s
     for (int i = tid; i < half; i += kAttnThreads) {
         const float c = cos_t[(long long)pos * half + i], s = sin_t[(long long)pos * half + i];

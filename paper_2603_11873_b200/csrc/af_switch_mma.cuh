@@ -193,6 +193,12 @@ struct GemvParams {
     int prologue;
     int x_len;                     // d_in of the group
     unsigned long long* acc_out;
+    // Deferred RMSNorm (AF_PRO_RMSNORM_DEFERRED, tcgen05 kernel): the scale rsqrt(mean(h^2) + eps) factors out of
+    // the GEMV, so only CTA 0 reads the whole vector (and writes the scale to inv_out); everyone else starts on
+    // x' = h * norm_w at once.  The launch's outputs are then unscaled: their consumer multiplies by the scale
+    // (inv_in of the SiLU phase that follows, `scale` of af_attn_decode_fix).
+    float* inv_out;
+    const float* inv_in;           // scale of THIS phase's input accumulators (NULL = 1)
 };
 
 // A launch may chain up to kMaxPhases projections whose inputs depend on each other's outputs
@@ -400,14 +406,16 @@ __device__ __forceinline__ float gemv_h(const GemvParams& g, int c) {
     return h;
 }
 // One element of the projection's input vector x; inv = rsqrt(mean(h^2) + eps) for RMSNORM.
-__device__ __forceinline__ float gemv_x(const GemvParams& g, int c, float inv) {
+// in_scale: the deferred RMSNorm scale of the launch that produced acc_in (1 when there is none).
+__device__ __forceinline__ float gemv_x(const GemvParams& g, int c, float inv, float in_scale = 1.0f) {
     if (g.prologue == AF_PRO_SILU_MUL) {
-        const float a = g.acc_in ? fix_to_f32(__ldcg(g.acc_in + c)) : __ldcg(g.xin + c);
-        const float b = g.acc_in ? fix_to_f32(__ldcg(g.acc_in + g.x_len + c)) : __ldcg(g.xin + g.x_len + c);
+        const float a = in_scale * (g.acc_in ? fix_to_f32(__ldcg(g.acc_in + c)) : __ldcg(g.xin + c));
+        const float b = in_scale * (g.acc_in ? fix_to_f32(__ldcg(g.acc_in + g.x_len + c)) : __ldcg(g.xin + g.x_len + c));
         return a / (1.0f + expf(-a)) * b;
     }
     float h = gemv_h(g, c);
     if (g.prologue == AF_PRO_RMSNORM) h *= inv * g.norm_w[c];
+    else if (g.prologue == AF_PRO_RMSNORM_DEFERRED) h *= g.norm_w[c];
     return h;
 }
 // B fragment (k16 x n8, col-major) of the input vector for this warp's 16 columns: column n = 0

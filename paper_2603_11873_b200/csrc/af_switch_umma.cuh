@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     }
                     if (tid == 0) tl_stamp(tl, 3);
                 }
-                float x_inv = 1.0f;
+                float x_inv = 1.0f, in_scale = 1.0f;
                 bool tl_first = false;
                 int cur_phase = -1, phase_j0 = 0, published = 0;
                 // entering a phase: previous phase published by every CTA, then the input vector
@@ -442,6 +442,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     }
                     if (tid == 0) tl_stamp(tl, 9 + 4 * ph);
                     x_inv = 1.0f;
+                    in_scale = g.inv_in ? __ldcg(g.inv_in) : 1.0f;
                     phase_j0 = ti.j;
                     // strips of this CTA's units of the phase: thread t -> column t % 128 of slots t / 128 and t / 128 + 2
                     float xr_h[2], xr_w[2];
@@ -456,15 +457,17 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                             const int c = un2.col0 + (tid & 127);
                             if (un2.rows > 0 && un2.phase == ph && c < g.x_len) {
                                 if (g.prologue == AF_PRO_SILU_MUL) {
-                                    xr_h[k2] = gemv_x(g, c, 1.0f);
+                                    xr_h[k2] = gemv_x(g, c, 1.0f, in_scale);
                                 } else {
                                     xr_h[k2] = gemv_h(g, c);
-                                    if (g.prologue == AF_PRO_RMSNORM) xr_w[k2] = g.norm_w[c];
+                                    if (g.prologue == AF_PRO_RMSNORM || g.prologue == AF_PRO_RMSNORM_DEFERRED) xr_w[k2] = g.norm_w[c];
                                 }
                             }
                         }
                     }
-                    if (g.prologue == AF_PRO_RMSNORM || (g.h_out && blockIdx.x == 0)) {
+                    // the whole-vector pass: every CTA for a plain RMSNorm; CTA 0 alone when the scale is deferred
+                    // (or when it only has to materialise h)
+                    if (g.prologue == AF_PRO_RMSNORM || ((g.h_out || g.prologue == AF_PRO_RMSNORM_DEFERRED) && blockIdx.x == 0)) {
                         float ss = 0.f;
                         const bool write_h = g.h_out && blockIdx.x == 0;
                         constexpr int kStep = 2 * kUEpi;
@@ -505,11 +508,16 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
 #pragma unroll
                         for (int i = 0; i < kUEpiWarps; ++i) tot += red[i];
                         x_inv = rsqrtf(tot / (float)g.x_len + g.eps);
+                        if (g.prologue == AF_PRO_RMSNORM_DEFERRED) {
+                            if (tid == 0 && g.inv_out) *g.inv_out = x_inv;   // read by the consumer of this launch's outputs
+                            x_inv = 1.0f;
+                        }
                     }
 #pragma unroll
                     for (int k2 = 0; k2 < 2; ++k2) {
                         float v = xr_h[k2];
                         if (g.prologue == AF_PRO_RMSNORM) v *= x_inv * xr_w[k2];
+                        else if (g.prologue == AF_PRO_RMSNORM_DEFERRED) v *= xr_w[k2];
                         xs_all[((tid >> 7) + 2 * k2) * kUN + (tid & 127)] = v;
                     }
                     named_bar_sync(1, kUEpi);
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                         const GemvParams& g = mp.gv[cur_phase];
                                         float t[8];
 #pragma unroll
-                                        for (int e = 0; e < 8; ++e) t[e] = (col0 + c + e < g.x_len) ? gemv_x(g, col0 + c + e, x_inv) : 0.f;
+                                        for (int e = 0; e < 8; ++e) t[e] = (col0 + c + e < g.x_len) ? gemv_x(g, col0 + c + e, x_inv, in_scale) : 0.f;
                                         xa = make_float4(t[0], t[1], t[2], t[3]);
                                         xb = make_float4(t[4], t[5], t[6], t[7]);
                                     }

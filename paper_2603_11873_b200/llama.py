@@ -64,6 +64,7 @@ class LlamaConfig:
     # "auto": chase when it applies (adapters, single rank, tensor path)
     forward_mode: str = "auto"
     chain: bool = True               # chase: o -> gate|up -> down -> next q|k|v as ONE launch with in-kernel phase barriers
+    defer_norm: bool = True          # chase on the tcgen05 path: RMSNorm scales computed by one CTA, applied by the consumers
     gemv_chain: bool = True          # plain forward (separate / adapter-free): the same four projections as one persistent GEMV launch
 
     def validate(self) -> None:
@@ -384,6 +385,11 @@ class LlamaEngine:
             self.acc_arena = torch.zeros(cfg.layers * (per_layer + 2), dtype=torch.int64, device=dev)
             self.acc = []
             self.phase_done = []
+            # tcgen05 path: RMSNorm scales are deferred -- one CTA computes them, the consumers of q|k|v
+            # (attention) and gate|up (the SiLU prologue of the down projection) apply them
+            self.defer_norm = bool(self.table.info().get("umma_path")) and cfg.defer_norm
+            self.inv_qkv = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
+            self.inv_gu = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
             counters = self.acc_arena[cfg.layers * per_layer:].view(torch.int32)   # 4 int32 per layer
             for li in range(cfg.layers):
                 o = li * per_layer
@@ -508,27 +514,31 @@ class LlamaEngine:
         self.table.build_plan(prev, self.cur, max_k=cfg.top_k, mode=cfg.switch_mode)
         self.acc_arena.zero_()
         self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
+        norm = "rmsnorm_deferred" if self.defer_norm else "rmsnorm"
         for li in range(cfg.layers):
             g, a = self.groups[li], self.acc[li]
             last = li + 1 == cfg.layers
-            qkv_first = dict(acc_out=a["qkv"], xin=xa, prologue="rmsnorm", norm_w=self.attn_norm[li], eps=eps)
+            iq = self.inv_qkv[li: li + 1] if self.defer_norm else None
+            ig = self.inv_gu[li: li + 1] if self.defer_norm else None
+            qkv_first = dict(acc_out=a["qkv"], xin=xa, prologue=norm, norm_w=self.attn_norm[li], eps=eps, inv_out=iq)
             if li == 0:
                 g["qkv"].switch_gemv(prev, self.cur, pdl=False, **qkv_first, **kw)
             elif not self.chase_chained:
-                g["qkv"].switch_gemv(prev, self.cur, a["qkv"], acc_in=self.acc[li - 1]["down"], res=xb, h_out=xa, prologue="rmsnorm",
-                                     norm_w=self.attn_norm[li], eps=eps, pdl=True, **kw)
-            self._check(L.af_attn_decode_fix(_ptr(a["qkv"]), _ptr(self.k_cache[li]), _ptr(self.v_cache[li]), _ptr(self.cos),
-                                             _ptr(self.sin), _ptr(self.pos_dev), self.heads_local, self.kv_local, cfg.head_dim,
-                                             cfg.max_seq, self.attn_splits, _ptr(self.attn_ws), _ptr(self.attn_tickets),
-                                             _ptr(self.attn_buf), st))
+                g["qkv"].switch_gemv(prev, self.cur, a["qkv"], acc_in=self.acc[li - 1]["down"], res=xb, h_out=xa, prologue=norm,
+                                     norm_w=self.attn_norm[li], eps=eps, inv_out=iq, pdl=True, **kw)
+            self._check(L.af_attn_decode_fix(_ptr(a["qkv"]), _ptr(iq) if iq is not None else None, _ptr(self.k_cache[li]),
+                                             _ptr(self.v_cache[li]), _ptr(self.cos), _ptr(self.sin), _ptr(self.pos_dev),
+                                             self.heads_local, self.kv_local, cfg.head_dim, cfg.max_seq, self.attn_splits,
+                                             _ptr(self.attn_ws), _ptr(self.attn_tickets), _ptr(self.attn_buf), st))
             ph_o = dict(acc_out=a["o"], xin=self.attn_buf)
-            ph_gu = dict(acc_out=a["gu"], acc_in=a["o"], res=xa, h_out=xb, prologue="rmsnorm", norm_w=self.ffn_norm[li], eps=eps)
-            ph_down = dict(acc_out=a["down"], acc_in=a["gu"], prologue="silu_mul")
+            ph_gu = dict(acc_out=a["gu"], acc_in=a["o"], res=xa, h_out=xb, prologue=norm, norm_w=self.ffn_norm[li], eps=eps, inv_out=ig)
+            ph_down = dict(acc_out=a["down"], acc_in=a["gu"], prologue="silu_mul", inv_in=ig)
             if self.chase_chained:
                 phases = [ph_o, ph_gu, ph_down]
                 if not last:
-                    phases.append(dict(acc_out=self.acc[li + 1]["qkv"], acc_in=a["down"], res=xb, h_out=xa, prologue="rmsnorm",
-                                       norm_w=self.attn_norm[li + 1], eps=eps))
+                    phases.append(dict(acc_out=self.acc[li + 1]["qkv"], acc_in=a["down"], res=xb, h_out=xa, prologue=norm,
+                                       norm_w=self.attn_norm[li + 1], eps=eps,
+                                       inv_out=self.inv_qkv[li + 1: li + 2] if self.defer_norm else None))
                 g["mid"].switch_gemv_chain(prev, self.cur, phases, self.phase_done[li], pdl=True, **kw)
             else:
                 g["o"].switch_gemv(prev, self.cur, pdl=True, **ph_o, **kw)

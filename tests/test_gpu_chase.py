@@ -217,3 +217,43 @@ def test_chase_engine_equals_separate_engine(af):
     assert np.array_equal(la, lc)            # chaining is a schedule change only: bit-identical logits
     a.finalize()
     assert a.max_backbone_deviation() < 0.02
+
+
+def test_deferred_rmsnorm_scale(af):
+    """AF_PRO_RMSNORM_DEFERRED (tcgen05 path): the launch multiplies by x * norm_w only; the scale
+    rsqrt(mean(x^2) + eps) lands in inv_out and the consumer applies it -- inv_out * outputs equals the
+    plain RMSNorm launch, and a SiLU phase given inv_in equals one fed pre-scaled accumulators."""
+    from paper_2603_11873_b200.adapters import SegmentGroup
+
+    d_in, rows = 512, (256, 128)
+    tg, tab = _mk_table(af, [(r, d_in) for r in rows], seed=11)
+    if not tab.info()["umma_path"]:
+        pytest.skip("tcgen05 path not enabled")
+    grp = SegmentGroup(tab, [0, 1])
+    cur = _decision(af, (0, 3), (0.6, 0.4))
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.empty(d_in, device="cuda").uniform_(-3, 3, generator=g)
+    nw = 1.0 + 0.1 * torch.empty(d_in, device="cuda").uniform_(-1, 1, generator=g)
+    acc_plain = torch.zeros(grp.y_rows, dtype=torch.int64, device="cuda")
+    acc_def = torch.zeros_like(acc_plain)
+    inv = torch.zeros(1, device="cuda")
+    grp.switch_gemv(None, cur, acc_plain, xin=x, prologue="rmsnorm", norm_w=nw, eps=1e-5, max_k=2)
+    grp.switch_gemv(cur, cur, acc_def, xin=x, prologue="rmsnorm_deferred", norm_w=nw, eps=1e-5, inv_out=inv, max_k=2)
+    tab.status()
+    want_inv = float(1.0 / np.sqrt(np.mean(x.cpu().numpy().astype(np.float64) ** 2) + 1e-5))
+    assert abs(float(inv.item()) - want_inv) <= 1e-6 * want_inv
+    a = acc_plain.cpu().numpy().astype(np.float64) * FIX
+    b = acc_def.cpu().numpy().astype(np.float64) * FIX * float(inv.item())
+    np.testing.assert_allclose(b, a, rtol=0, atol=3e-5 * np.max(np.abs(a)))
+    # consumer side: SiLU(gate) * up over accumulators that still lack the scale
+    tg2, tab2 = _mk_table(af, [(128, 256)], seed=12)
+    grp2 = SegmentGroup(tab2, [0])
+    raw = (torch.empty(512, device="cuda").uniform_(-2, 2, generator=g) / FIX).to(torch.int64)
+    scale = torch.full((1,), 0.37, device="cuda")
+    scaled = (raw.to(torch.float64) * 0.37).round().to(torch.int64)
+    o1 = torch.zeros(128, dtype=torch.int64, device="cuda")
+    o2 = torch.zeros_like(o1)
+    grp2.switch_gemv(None, None, o1, acc_in=raw, prologue="silu_mul", inv_in=scale)
+    grp2.switch_gemv(None, None, o2, acc_in=scaled, prologue="silu_mul")
+    v1, v2 = o1.cpu().numpy() * FIX, o2.cpu().numpy() * FIX
+    np.testing.assert_allclose(v1, v2, rtol=0, atol=2e-5 * np.max(np.abs(v2)))
