@@ -220,7 +220,8 @@ struct MmaParams {
     // optional timeline probe (af_set_timeline): [gridDim.x][kTlSlots] globaltimer stamps of this launch
     unsigned long long* timeline;
     int mixed_rank;                // the table's segments do not all have the same rank
-    int dbg;                       // experiments (env AF_DBG): 4 = plain switch kernel on the group schedule
+    int dbg;                       // bit 8 / 16: L2 evict-first hint on the W loads / stores (on by default; the env
+                                   // AF_DBG flips bits for A/B runs; AF_DBG=4: plain switch kernel on a group's schedule)
     const CUtensorMap* tmaps_ld;   // per segment: 32 x 64 swizzled box on the source (live or pristine)
     const CUtensorMap* tmaps_st;   // per segment: the same box shape on the live matrix
     const CUtensorMap* tmaps_up;   // per segment: UP bank as [N * d_out][rank], box 32 rows x rank, swizzle = row bytes

@@ -2,7 +2,8 @@
 decode chain around it: `n` layers of a workload's shapes, the same group of every layer launched
 back to back (no dependencies between them), CUDA events around the whole sequence.
     python scripts/bench_chase_kernel.py [workload] [--layers 8] [--group gu|qkv|o|down]
-Env AF_DBG: 1 storer skips the reduce, 2 consumers skip the GEMV mma, 4 plain switch kernel on the group schedule."""
+Env: AF_UMMA=0 selects the mma.sync kernel; AF_DBG=4 runs the plain switch kernel on the group's schedule
+(mma.sync path), AF_DBG=8 / 16 / 24 switch the L2 evict-first hints of the W loads / stores off."""
 import argparse
 import os
 import sys
