@@ -108,8 +108,8 @@ int af_set_pdl(int32_t enable);
  * 4 KB x1, 4 KB x2); full_sm != 0 lets the ring take the whole SM instead of half of it.
  * Results are identical up to f32 summation order.  Env: AF_GEMV, AF_GEMV_FULL_SM. */
 int af_set_gemv_variant(int32_t variant, int32_t full_sm);
-/* Tensor path of the fused switch (+ GEMV) on eligible tables (rank 8 everywhere, every matrix a
- * multiple of 128 x 128): 1 = tcgen05.mma with the accumulators in tensor memory
+/* Tensor path of the fused switch (+ GEMV) on eligible tables (one rank in {8, 16, 32, 64} everywhere,
+ * every matrix a multiple of 128 x 128; launches of at most 32 stacked ranks): 1 = tcgen05.mma with the accumulators in tensor memory
  * (csrc/af_switch_umma.cuh; default), 0 = mma.sync kernels (what every other table uses).  Both are
  * within 1 bf16 ulp of the f32 merge; they round differently in the last bit, so do not mix them
  * inside one comparison.  Env: AF_UMMA=0 turns the tcgen05 path off at load. */

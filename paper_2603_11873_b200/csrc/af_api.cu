@@ -290,8 +290,11 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
     t->fast_fma = fma_ok;
     t->fast_mma = mma_ok;
     t->umma_ok = mma_ok;
-    for (int i = 0; i < n_segments; ++i)
-        if (segments[i].rank != 8 || segments[i].d_out % kUM != 0 || segments[i].d_in % kUN != 0) t->umma_ok = false;
+    for (int i = 0; i < n_segments; ++i) {
+        const af_segment_desc& s = segments[i];
+        const bool rank_ok = s.rank == segments[0].rank && (s.rank == 8 || s.rank == 16 || s.rank == 32 || s.rank == 64);
+        if (!rank_ok || s.d_out % kUM != 0 || s.d_in % kUN != 0) t->umma_ok = false;
+    }
 
     // ---- work units: column strips of kTN columns cut into runs of row tiles ----
     // Static round-robin schedule over the persistent grid: aim for ~32 units per SM so the
@@ -350,7 +353,8 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         return fail(AF_ECUDA, std::string("table upload: ") + cudaGetErrorString(e));
     }
     if (t->fast_fma) {
-        std::vector<CUtensorMap> maps((size_t)7 * n_segments);   // [5], [6]: 128 x 64 boxes of the tcgen05 path (live, pristine)
+        // [5], [6]: 128 x 64 boxes of the tcgen05 path (live, pristine); [7]: its UP blocks (128 rows x rank, swizzled)
+        std::vector<CUtensorMap> maps((size_t)8 * n_segments);
         std::memset(maps.data(), 0, sizeof(CUtensorMap) * maps.size());
         for (int i = 0; i < n_segments; ++i) {
             const af_segment_desc& s = segments[i];
@@ -368,6 +372,11 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
             if (!rc && t->umma_ok) {
                 rc = make_map(&maps[5 * n_segments + i], s.target, s.d_out, s.d_in, s.ld_target, kUBoxCols, kUM, CU_TENSOR_MAP_SWIZZLE_128B);
                 if (!rc) rc = make_map(&maps[6 * n_segments + i], pr, s.d_out, s.d_in, s.ld_target, kUBoxCols, kUM, CU_TENSOR_MAP_SWIZZLE_128B);
+                if (!rc && s.rank > 8) {
+                    const CUtensorMapSwizzle sw = s.rank == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                  : s.rank == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+                    rc = make_map(&maps[7 * n_segments + i], s.up, s.n_experts * s.d_out, s.rank, s.rank, s.rank, kUM, sw);
+                }
             }
             if (rc) {
                 af_table_destroy(t);
@@ -451,7 +460,8 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     return AF_OK;
 }
 
-// tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = block slots (even).
+constexpr int kUmmaMaxRanks = 32;   // stacked ranks (2 k r in the steady switch) the tcgen05 kernel is used for
+// tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = k-groups of 8 stacked ranks per half.
 template <int NB, bool GEMV>
 static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
     using L = UmmaLayout<NB, GEMV>;
@@ -562,19 +572,18 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
         return fail(AF_EVALUE, "tensor path needs bf16 targets and factors, rank % 8 == 0, 16-byte aligned rows and "
                                "at most 64 stacked ranks");
     const int S = t->n_segments;
-    if (want_mma && mma_fits && g_umma.load() && t->umma_ok && t->n_units_umma && n_blocks_bound <= 8 && !host_plan_override) {
+    if (want_mma && mma_fits && g_umma.load() && t->umma_ok && t->n_units_umma && s_bound <= kUmmaMaxRanks && !host_plan_override) {
         MmaParams mp{};
         mp.base = p;
         mp.base.units = t->d_units_umma;
         mp.base.n_units = t->n_units_umma;
         mp.tmaps_ld = t->d_maps + (size_t)(p.from_pristine ? 6 : 5) * S;
         mp.tmaps_st = t->d_maps + (size_t)5 * S;
+        mp.tmaps_up = t->d_maps + (size_t)7 * S;
         mp.n_chain_segs = 0;
         mp.n_phases = 1;
         const int grid = std::min(t->n_units_umma, t->sm_count);
-        const int nb = std::max(2, (n_blocks_bound + 1) & ~1);
-        if (nb <= 4) return launch_umma<4, false>(mp, grid, st);
-        return launch_umma<8, false>(mp, grid, st);
+        return launch_umma<4, false>(mp, grid, st);
     }
     if (want_mma && mma_fits) {
         MmaParams mp{};
@@ -956,7 +965,9 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     static const int env_dbg = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
     mp.dbg = env_dbg ^ 24;
     const int ks_tl = std::max(1, (s_bound + 15) / 16);
-    const bool umma_launch = g_umma.load() && t->umma_ok && g->d_units_umma && n_blocks_bound <= 8;
+    // At most 32 stacked ranks: with 64 the hi + lo slab (32 KB) and the UP stage (16 KB) leave the tcgen05
+    // kernel three ring stages and it loses to the mma.sync kernel (Llama-3-8B shapes, r = 16: 7.93 vs 7.04 ms)
+    const bool umma_launch = g_umma.load() && t->umma_ok && g->d_units_umma && s_bound <= kUmmaMaxRanks;
     if (g_timeline && g_timeline_left > 0 && (ks_tl == 2 || umma_launch)) {  // mma.sync: the probe is compiled into the KS = 2 hi/lo variant only
         mp.timeline = g_timeline;
         g_timeline += g_timeline_stride;
@@ -977,9 +988,8 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         p.n_units = g->n_units_umma;
         mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 6 : 5) * S;
         mp.tmaps_st = t->d_maps + (size_t)5 * S;
-        const int nb = std::max(2, (n_blocks_bound + 1) & ~1);
-        if (nb <= 4) return launch_umma<4, true>(mp, g->grid_umma, st);
-        return launch_umma<8, true>(mp, g->grid_umma, st);
+        mp.tmaps_up = t->d_maps + (size_t)7 * S;
+        return launch_umma<4, true>(mp, g->grid_umma, st);   // 4 k-groups of 8 stacked ranks per half
     }
     if (mp.timeline && ks == 2) return launch_mma<2, false, true, true>(mp, g->grid, st);
     switch (ks) {

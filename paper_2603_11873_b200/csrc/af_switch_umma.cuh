@@ -17,8 +17,9 @@
 // with the staged input strip; the row's partial sum goes straight to the fixed-point accumulator
 // (no cross-warp reduction: a thread holds the whole 128-column row strip).
 //
-// Scope: rank == 8 tables whose matrices are multiples of 128 in both directions (every Llama
-// shape of BASELINE.json); anything else keeps the mma.sync kernel.  (scripts/micro/umma_test.cu
+// Scope: tables of ONE rank in {8, 16, 32, 64}, matrices multiples of 128 in both directions (every
+// Llama shape of BASELINE.json), launches of at most 32 stacked ranks (with 64 the slab and the UP
+// stage leave three ring stages and the mma.sync kernel wins); anything else keeps the mma.sync kernel.  (scripts/micro/umma_test.cu
 // pins the descriptor encodings in isolation.)
 #pragma once
 
@@ -66,13 +67,25 @@ struct UmmaLayout {
 };
 
 // ---- tcgen05 wrappers ----
-__device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// layout: 0 = no swizzle, 6 / 4 / 2 = 32- / 64- / 128-byte swizzle (UMMA::LayoutType)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout = 0) {
     uint64_t d = 0;
     d |= (uint64_t)((smem_addr >> 4) & 0x3fff);
     d |= (uint64_t)((lbo_bytes >> 4) & 0x3fff) << 16;
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3fff) << 32;
     d |= (uint64_t)1 << 46;   // descriptor version of sm_100
-    return d;                 // layout type 0: no swizzle
+    d |= (uint64_t)(layout & 7) << 61;
+    return d;
+}
+// A operand (UP stage) of the rank-16 step ks.  rank 8: an expert block is a [128][16 B] slab, two blocks make a
+// step (no swizzle, LBO = block stride).  rank 16 / 32 / 64: the block came through a tensor map whose swizzle
+// span is the row (32 / 64 / 128 bytes), which IS the K-major swizzled canonical layout; a step is 32 bytes
+// further along the row, blocks follow each other.
+__device__ __forceinline__ uint64_t umma_a_desc(uint32_t up_stage, int rank, int ks) {
+    if (rank == 8) return umma_desc(up_stage + ks * 2 * kUBlockBytes, kUBlockBytes, 128);
+    const int k0 = 16 * ks, b = k0 / rank, ko = k0 % rank;
+    const uint32_t layout = rank == 16 ? 6u : (rank == 32 ? 4u : 2u);
+    return umma_desc(up_stage + b * (kUM * rank * 2) + ko * 2, 16, 8 * rank * 2, layout);
 }
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
     asm volatile(
@@ -162,7 +175,9 @@ __device__ __forceinline__ void umma_slab_prefetch(uint4 (&regs)[NB * 8 * (kUN /
         const int q = i / chunks, c = (i % chunks) * 8;
         const bool ok = q < S && col0 + c < sg.d_in;
         const int qq = ok ? q : 0;
-        const __nv_bfloat16* src = base + (long long)plan.expert[qq >> 3] * sg.down_estride + (long long)(qq & 7) * sg.ld_down + col0 + c;
+        int qb, qr;
+        rank_divmod(qq, sg.rank, qb, qr);
+        const __nv_bfloat16* src = base + (long long)plan.expert[qb] * sg.down_estride + (long long)qr * sg.ld_down + col0 + c;
         asm volatile(
             "{\n"
             ".reg .pred p;\n"
@@ -179,7 +194,7 @@ __device__ __forceinline__ void umma_slab_prefetch(uint4 (&regs)[NB * 8 * (kUN /
 }
 template <int NB>
 __device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const uint4 (&regs)[NB * 8 * (kUN / 8) / kUEpi], const Plan& plan, int S,
-                                                 int tid) {
+                                                 int rank, int tid) {
     constexpr int chunks = kUN / 8;
 #pragma unroll
     for (int j = 0; j < NB * 8 * chunks / kUEpi; ++j) {
@@ -187,7 +202,9 @@ __device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const uint
         const int q = i / chunks, c = (i % chunks) * 8;
         uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
         if (q < S) {
-            const float w = plan.weight[q >> 3];    // rank == 8
+            int wb, wr;
+            rank_divmod(q, rank, wb, wr);
+            const float w = plan.weight[wb];
             const uint32_t in[4] = {regs[j].x, regs[j].y, regs[j].z, regs[j].w};
             uint32_t oh[4], ol[4];
 #pragma unroll
@@ -330,11 +347,19 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         sg = seg_of(ti.un);
                     }
                     mbar_wait(&empty[stage], ph ^ 1);
-                    mbar_expect_tx(&full[stage], n_blocks * kUBlockBytes);
-                    const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
-                    for (int b = 0; b < n_blocks; ++b)
-                        bulk_load_1d(up_base + stage * L::up_stage + b * kUBlockBytes,
-                                     upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &full[stage]);
+                    const uint32_t blk_bytes = (uint32_t)kUM * sg.rank * 2;
+                    mbar_expect_tx(&full[stage], n_blocks * blk_bytes);
+                    if (sg.rank == 8) {   // an expert block is 128 contiguous 16-byte rows: one bulk copy
+                        const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
+                        for (int b = 0; b < n_blocks; ++b)
+                            bulk_load_1d(up_base + stage * L::up_stage + b * kUBlockBytes,
+                                         upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &full[stage]);
+                    } else {              // 128 rows x rank through the tensor map whose swizzle span is the row
+                        const CUtensorMap* tm = mp.tmaps_up + ti.un.seg;
+                        for (int b = 0; b < n_blocks; ++b)
+                            tma_load_2d_addr(up_base + stage * L::up_stage + b * blk_bytes, tm, 0, plan.expert[b] * sg.d_out + ti.m0,
+                                             &full[stage]);
+                    }
                     ti.next(p);
                 }
             }
@@ -343,9 +368,10 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
             if (lane == 0) {
                 // D f32, A / B bf16, A K-major, B MN-major, N = 128, M = 128
                 constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(kUN >> 3) << 17) | ((uint32_t)(kUM >> 4) << 24);
-                const int ksteps = (n_blocks + 1) >> 1;   // rank-16 steps = pairs of blocks
                 UmmaIter ti;
                 ti.init(p, unit_cache);
+                const int rank = ti.valid(p) ? seg_of(ti.un).rank : 8;   // one rank for the whole table (eligibility)
+                const int ksteps = (n_blocks * rank + 15) >> 4;          // rank-16 steps over the stacked ranks
                 int unit_j = -1;
                 for (int it = 0; ti.valid(p); ++it) {
                     const int stage = it % kSt, buf = it & 1;
@@ -361,13 +387,13 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     uint32_t accumulate = 0;
                     for (int half = 0; half < 2; ++half)
                         for (int ks = 0; ks < ksteps; ++ks) {
-                            const uint64_t da = umma_desc(a0 + ks * 2 * kUBlockBytes, kUBlockBytes, 128);
+                            const uint64_t da = umma_a_desc(a0, rank, ks);
                             const uint64_t db = umma_desc(slab_base + (half * NB + ks * 2) * kUSlabBlock, kUSlabBlock, 128);
                             umma_bf16(tmem + buf * kUN, da, db, idesc, accumulate);
                             accumulate = 1;
                         }
                     if (ksteps == 0) {   // nothing selected (plain GEMV): D = 0 through a K = 16 product with the zeroed slot
-                        const uint64_t da = umma_desc(a0, kUBlockBytes, 128);
+                        const uint64_t da = umma_a_desc(a0, rank, 0);
                         const uint64_t db = umma_desc(slab_base, kUSlabBlock, 128);
                         umma_bf16(tmem + buf * kUN, da, db, idesc, 0);
                     }
@@ -525,7 +551,8 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     tl_first = true;
                 };
 
-                const int S = n_blocks * 8;
+                const int rank = seg_of(ti.un).rank;
+                const int S = n_blocks * rank;
                 uint4 dn_regs[NB * 8 * (kUN / 8) / kUEpi];
                 umma_slab_prefetch<NB>(dn_regs, seg_of(ti.un), plan, S, ti.un.col0, tid);
                 bool new_unit = true;
@@ -550,7 +577,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                 published = ti.un.phase;
                             }
                         }
-                        umma_slab_commit<NB>(slab, dn_regs, plan, S, tid);
+                        umma_slab_commit<NB>(slab, dn_regs, plan, S, rank, tid);
                         fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
                         __syncwarp();
                         if (lane == 0) mbar_arrive(slab_bar);

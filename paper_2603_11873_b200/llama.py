@@ -387,7 +387,8 @@ class LlamaEngine:
             self.phase_done = []
             # tcgen05 path: RMSNorm scales are deferred -- one CTA computes them, the consumers of q|k|v
             # (attention) and gate|up (the SiLU prologue of the down projection) apply them
-            self.defer_norm = bool(self.table.info().get("umma_path")) and cfg.defer_norm
+            stacked = (1 if cfg.switch_mode == "from_pristine" else 2) * cfg.top_k * cfg.rank   # ranks of a steady switch
+            self.defer_norm = bool(self.table.info().get("umma_path")) and cfg.defer_norm and stacked <= 32
             self.inv_qkv = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
             self.inv_gu = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
             counters = self.acc_arena[cfg.layers * per_layer:].view(torch.int32)   # 4 int32 per layer

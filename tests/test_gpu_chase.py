@@ -87,7 +87,13 @@ def test_switch_gemv_weights_and_outputs(af, d_in, rows, rank):
     assert torch.equal(acc, acc2)
     acc3 = torch.zeros_like(acc)
     grp.switch_gemv(None, None, acc3, xin=x)              # no decision at all: plain GEMV
-    assert torch.equal(acc, acc3)
+    # (a launch without a decision may run on the other tensor path -- the tcgen05 kernel takes launches of up
+    #  to 32 stacked ranks -- which sums a row in a different order: equal to f32 round-off, bitwise only when
+    #  both launches are on one path)
+    got3 = acc3.cpu().numpy().astype(np.float64) * FIX
+    assert np.max(np.abs(got3 - got) / (scale + 1e-30)) < 2e-5
+    if 4 * rank <= 32 or not tab_a.info()["umma_path"]:
+        assert torch.equal(acc, acc3)
 
 
 def test_switch_gemv_prologues(af):

@@ -39,10 +39,13 @@ def _oracle_for(eng, llama):
                           rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps, max_seq=cfg.max_seq)
 
 
+@pytest.mark.parametrize("shape", ["r8", "r16-gqa"])
 @pytest.mark.parametrize("forward_mode", ["chase", "separate"])
 @pytest.mark.parametrize("switch_mode", ["inplace", "from_pristine"])
-def test_decode_steps_against_oracle(llama, switch_mode, forward_mode):
-    cfg = llama.preset("tiny", switch_mode=switch_mode, max_seq=32, forward_mode=forward_mode)
+def test_decode_steps_against_oracle(llama, switch_mode, forward_mode, shape):
+    # "r16-gqa": BASELINE configs[2]-like -- 16 experts of rank 16, 4 query heads on 1 kv head
+    extra = dict(experts=16, rank=16, n_heads=4, n_kv_heads=1) if shape == "r16-gqa" else {}
+    cfg = llama.preset("tiny", switch_mode=switch_mode, max_seq=32, forward_mode=forward_mode, **extra)
     eng = llama.LlamaEngine(cfg, init="host")
     assert eng.table.info()["tensor_path"]
     assert eng.chase == (forward_mode == "chase")
