@@ -229,7 +229,58 @@ def golden_io():
     print("io fixtures: tokens", toks)
 
 
+def golden_harness():
+    """Reports written by the reference's OWN harness (cli.py) on a small single-precision config:
+    the bench report + CSV, the profile document and the seeded workload; plus known answers of
+    perf.estimate / breakdown / calibrate on a hand-made trace.  The B200 harness must reproduce
+    every field that is a function of the dispatch trace (counts, flops, estimated ms)."""
+    import json
+
+    from lorafuse import cli as lfc
+    from lorafuse import perf as lfp
+    from lorafuse.linalg import DispatchEvent
+
+    os.environ["SOURCE_DATE_EPOCH"] = "0"
+    cfg_text = ("layers: 3\nhidden: 64\nvocab: 128\nexperts: 4\nrank: 4\ntop_k: 2\nprecision: single\nseed: 5\n"
+                "launch_seconds: 1.0e-5\nflops_throughput: 1.0e+10\nbytes_bandwidth: 2.0e+9\n"
+                "n_new: 6\nsynthetic_prompts: 3\nsynthetic_len_min: 2\nsynthetic_len_max: 5\n")
+    cfg_path = os.path.join(HERE, "ref_harness_config.yaml")
+    with open(cfg_path, "w", encoding="utf-8") as fh:
+        fh.write(cfg_text)
+    cfg = lfc.load_config(cfg_path)
+    workload = lfc.synthetic_workload(cfg)
+    lfc.write_workload(workload.prompts, os.path.join(HERE, "ref_harness_workload.jsonl"))
+    report = lfc.run_bench(cfg, workload)
+    lfc._write_json(report, os.path.join(HERE, "ref_harness_bench.json"))
+    lfc.write_bench_csv(report, os.path.join(HERE, "ref_harness_bench.csv"))
+    lfc._write_json(lfc.run_profile(cfg), os.path.join(HERE, "ref_harness_profile.json"))
+    code, lines = lfc.run_verify(cfg)
+    # perf known answers
+    trace = [DispatchEvent("gemm", 2_000_000, 48_000, "backbone"), DispatchEvent("sgmm", 9_000_000, 800_000, "switch"),
+             DispatchEvent("gemm", 4_096, 2_048, "router"), DispatchEvent("elementwise", 64, 512, "backbone"),
+             DispatchEvent("reduce", 128, 512, "other"), DispatchEvent("gemm", 512, 256, "adapter")]
+    cm = lfp.CostModel(2e-6, 5e9, 1e9)
+    est = lfp.estimate(trace, cm, n_tokens=3)
+    rows = [[r.label, r.kind, r.count, r.flops] for r in lfp.breakdown(trace)]
+    samples = [(trace[:2], 0.00231), (trace[:4], 0.00236), (trace, 0.00240), (trace[2:], 0.00009)]
+    fit = lfp.calibrate(samples)
+    with open(os.path.join(HERE, "ref_perf_expected.json"), "w", encoding="utf-8") as fh:
+        json.dump({"trace": [[e.kind, e.flops, e.bytes_touched, e.label] for e in trace],
+                   "cost_model": [2e-6, 5e9, 1e9], "n_tokens": 3,
+                   "total_ms_per_token": est.total_ms_per_token, "per_component_ms": est.per_component_ms,
+                   "dispatch_counts": est.dispatch_counts, "breakdown": rows,
+                   "max_compute_fraction": lfp.max_compute_fraction(trace, cm),
+                   "calibration_samples": [[len(t), s] for t, s in samples],
+                   "calibration_slices": [[0, 2], [0, 4], [0, 6], [2, 6]],
+                   "fit_launch_seconds": fit.cost_model.launch_seconds,
+                   "fit_flops_throughput": fit.cost_model.flops_throughput,
+                   "fit_residuals": [float(r) for r in fit.residuals],
+                   "verify_exit_code": code, "verify_lines": lines}, fh, indent=1, sort_keys=True)
+    print("harness golden written; reference verify:", code, lines[-1])
+
+
 if __name__ == "__main__":
+    golden_harness()
     golden_io()
     golden_router()
     golden_sgmm()
