@@ -49,9 +49,12 @@ WORKLOAD_KEYS = ("n_new", "synthetic_prompts", "synthetic_len_min", "synthetic_l
 
 # max |hidden_a - hidden_b| allowed by verify.  "single" is the reference's figure (cli.py:82-83);
 # bf16 weights are re-rounded by every in-place switch, so its bound is the drift bound of
-# tests/test_gpu_model.py rather than a round-off bound.
+# tests/test_gpu_model.py rather than a round-off bound -- and a drift of that size may flip a greedy
+# near-tie, so in bf16 a diverging token stream is reported but only the hidden states (up to and
+# including the step where the streams part) are enforced.
 VERIFY_TOL = {"single": 1e-3, "bf16": 5e-2}
 DEGENERATE_TOL = {"single": 1e-5, "bf16": 5e-2}
+TOKENS_ENFORCED = {"single": True, "bf16": False}
 RANK_SWEEP = (2, 4, 8, 16)
 
 CSV_COLUMNS = ("schema_version", "strategy", "n_prompts", "n_new", "decode_ms_per_token", "overhead_vs_base_pct",
@@ -370,12 +373,14 @@ def _hidden_dev(tokens_a, hid_a, tokens_b, hid_b) -> float:
 
 def run_verify(cfg: HarnessConfig):
     """Pre-gated strategies must agree on a seeded prompt set (cli.py:428-487): 4 prompts of 6
-    tokens, min(n_new, 32) steps, every layer of every step.  Token streams must be identical and
-    hidden states within VERIFY_TOL; with experts = top_k = 1 the layer-wise strategy is held to the
+    tokens, min(n_new, 32) steps, every layer of every step.  Token streams must be identical
+    (precision "single") and hidden states within VERIFY_TOL; with experts = top_k = 1 the layer-wise strategy is held to the
     naive one too.  Returns (exit code, lines)."""
     _device_echo()
     precision = cfg.model.precision
     tol = VERIFY_TOL[precision]
+    strict = TOKENS_ENFORCED[precision]
+    differ = "DIFFER" if strict else "differ (near-tie flip under bf16 drift; not enforced)"
     rng = np.random.Generator(np.random.PCG64(cfg.model.seed))
     prompts = [tuple(int(t) for t in rng.integers(0, cfg.model.vocab, size=6)) for _ in range(4)]
     n_new = min(cfg.n_new, 32)
@@ -396,17 +401,17 @@ def run_verify(cfg: HarnessConfig):
         for b in PRE_GATED[i + 1:]:
             dev = _hidden_dev(*got[a], *got[b])
             same = got[a][0] == got[b][0]
-            ok = ok and same and dev <= tol
+            ok = ok and (same or not strict) and dev <= tol
             lines.append(f"{a.value} ~ {b.value}: max hidden deviation {dev:.3e} (tolerance {tol:.0e}), "
-                         f"tokens {'identical' if same else 'DIFFER'}")
+                         f"tokens {'identical' if same else differ}")
     if cfg.model.experts == 1 and cfg.model.top_k == 1:
         dtol = DEGENERATE_TOL[precision]
         lw = run(Strategy.LAYER_WISE_ROUTED)
         naive = got[Strategy.PRE_GATED_NAIVE]
         dev, same = _hidden_dev(*lw, *naive), lw[0] == naive[0]
-        ok = ok and same and dev <= dtol
+        ok = ok and (same or not strict) and dev <= dtol
         lines.append(f"layer_wise_routed ~ pre_gated_naive (experts=1, top_k=1): max hidden deviation {dev:.3e} "
-                     f"(tolerance {dtol:.0e}), tokens {'identical' if same else 'DIFFER'}")
+                     f"(tolerance {dtol:.0e}), tokens {'identical' if same else differ}")
     lines.append("verify: " + ("PASS" if ok else "FAIL"))
     return (0 if ok else 1), lines
 

@@ -286,9 +286,8 @@ def test_verify_and_profile_match_reference(tmp_path, monkeypatch, capsys):
     # bf16, the production precision: strategies agree within the drift bound
     b16 = tmp_path / "b16.yaml"
     b16.write_text("layers: 3\nhidden: 64\nvocab: 128\nexperts: 4\nrank: 4\ntop_k: 2\nprecision: bf16\nseed: 5\nn_new: 8\n")
-    code = harness.main(["verify", "--config", str(b16)])
-    print(capsys.readouterr().out)
-    assert code in (0, 1)   # bf16 streams may legitimately part ways; the exit code reports it
+    assert harness.main(["verify", "--config", str(b16)]) == 0   # hidden states enforced, near-tie token flips reported
+    assert "verify: PASS" in capsys.readouterr().out
 
 
 @pytest.mark.gpu
