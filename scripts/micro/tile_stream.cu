@@ -163,6 +163,9 @@ int main() {
         run(32, 64, 4, 10, 3, order, true, 1);
         run(32, 64, 4, 6, 2, order, true, 1);
         run(128, 64, 2, 5, 1, order, true, 1);   // the tcgen05 kernel's tile: 128 rows x 128 cols, 5 stages of 32 KB
+        run(128, 64, 2, 4, 1, order, true, 1);   // ... with the ring depths a 64-rank launch could afford
+        run(128, 64, 2, 3, 1, order, true, 1);
+        run(128, 64, 2, 6, 1, order, true, 1);
         run(16, 64, 8, 10, 2, order, true, 1);   // 16 rows x 512 cols
         run(8, 64, 16, 10, 2, order, true, 1);   // 8 rows x 1024 cols
         run(32, 256, 1, 10, 2, order, true, 0);  // unswizzled 512-byte box rows, one box per tile
