@@ -635,9 +635,98 @@ class LlamaEngine:
         n = self.steps_done() if n is None else n
         return [int(v) for v in self.history[:n].cpu().numpy()]
 
-    def generate(self, prompt, n_new: int, use_graph: bool = True) -> list:
-        """Greedy generation: the prompt is consumed token by token along the same merged path
-        (token-level pre-gating makes merged == unmerged, PAPER Eq. 2-4), then n_new tokens."""
+    def prefill(self, prompt) -> int:
+        """Batched UNMERGED prefill of a whole prompt (model.py:408-425; PAPER Eq. 2): all T tokens go
+        through every layer at once, token t with its own pre-gated decision,
+
+            Y = X W^T + ((X A_all^T) * G) B_all^T        G[t, e*r .. e*r+r) = gate weight of expert e for token t
+
+        i.e. three dense GEMMs per projection (grouped over the experts by stacking them), causal
+        attention over the prompt, and the backbone is never written -- the reference's prefill
+        never runs an sgmm either.  The GEMMs and the attention are library calls (cuBLAS f32 on the
+        upcast bf16 weights, torch SDPA): this path is outside the decode metric and, as in the
+        paper, not tuned; the router decisions come from the same `pregate_kernel` the decode uses.
+        Fills the KV cache for positions 0 .. T-1 (bf16, rotated, as the decode kernel stores
+        them), leaves the engine at position T with pristine weights, and returns the token
+        emitted after the prompt.  Single rank."""
+        cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
+        prompt = [int(t) for t in prompt]
+        if not prompt:
+            raise InputError("prompt must contain at least one token")
+        if any(not 0 <= t < cfg.vocab for t in prompt):
+            raise InputError(f"prompt leaves the vocabulary of {cfg.vocab}")
+        if len(prompt) > cfg.max_seq:
+            raise InputError("prompt exceeds max_seq")
+        if cfg.tp_size != 1:
+            raise StateError("batched prefill is single-rank; TP engines consume the prompt step by step")
+        self.reset(prompt[0])
+        T, d, hd, f32 = len(prompt), cfg.hidden, cfg.head_dim, torch.float32
+        nh, nkv = self.heads_local, self.kv_local
+        tok = torch.tensor(prompt, dtype=torch.int32, device=self.dev)
+        gates = None
+        if cfg.adapters:
+            decs = torch.zeros((T, DECISION_BYTES), dtype=torch.uint8, device=self.dev)
+            for t in range(T):   # the decode's own router kernel, one launch per prompt token (routing.py:81-89)
+                self._check(L.af_pregate(_ptr(self.router.data), _capi.AF_BF16, cfg.experts, d, _ptr(self.embed.data), _capi.AF_BF16,
+                                         _ptr(tok[t: t + 1]), cfg.top_k, _ptr(decs[t]), None, st))
+            ids = decs.view(torch.int32)[:, 1: 1 + cfg.top_k].long()
+            wts = decs.view(f32)[:, 1 + _capi.AF_MAX_K: 1 + _capi.AF_MAX_K + cfg.top_k]
+            gates = torch.zeros((T, cfg.experts), dtype=f32, device=self.dev).scatter_add_(1, ids, wts)
+            gates = gates.repeat_interleave(cfg.rank, dim=1)                       # [T, N r]
+
+        def linear(x, li, j, w):
+            y = x @ w.float().t()
+            if gates is not None:
+                a = self.bank_down[7 * li + j].float().reshape(cfg.experts * cfg.rank, -1)              # [N r, d_in]
+                b = self.bank_up[7 * li + j].float().permute(1, 0, 2).reshape(w.shape[0], -1)           # [d_out, N r]
+                y = y + ((x @ a.t()) * gates) @ b.t()
+            return y
+
+        def rmsnorm(x, w):
+            return x * torch.rsqrt(x.pow(2).mean(dim=-1, keepdim=True) + cfg.rms_eps) * w
+
+        def rope(v):   # [T, heads, hd], rotate-half
+            half = hd // 2
+            c, s_ = self.cos[:T, None, :], self.sin[:T, None, :]
+            a, b = v[..., :half], v[..., half:]
+            return torch.cat([a * c - b * s_, b * c + a * s_], dim=-1)
+
+        x = self.embed.data[tok.long()].float()
+        for li in range(cfg.layers):
+            xn = rmsnorm(x, self.attn_norm[li])
+            wq, wk, wv = self.wqkv[li][: self.q_rows], self.wqkv[li][self.q_rows: self.q_rows + self.kv_rows], self.wqkv[li][self.q_rows + self.kv_rows:]
+            q = rope(linear(xn, li, 0, wq).view(T, nh, hd))
+            k = rope(linear(xn, li, 1, wk).view(T, nkv, hd)).to(torch.bfloat16)    # the cache holds bf16; attention reads it back
+            v = linear(xn, li, 2, wv).view(T, nkv, hd).to(torch.bfloat16)
+            self.k_cache[li][:, :T] = k.permute(1, 0, 2)
+            self.v_cache[li][:, :T] = v.permute(1, 0, 2)
+            rep = nh // nkv
+            kk = k.float().permute(1, 0, 2).repeat_interleave(rep, dim=0)          # [nh, T, hd]
+            vv = v.float().permute(1, 0, 2).repeat_interleave(rep, dim=0)
+            att = torch.nn.functional.scaled_dot_product_attention(q.permute(1, 0, 2)[None], kk[None], vv[None], is_causal=True)[0]
+            x = x + linear(att.permute(1, 0, 2).reshape(T, nh * hd), li, 3, self.wo[li])
+            xn = rmsnorm(x, self.ffn_norm[li])
+            g = linear(xn, li, 4, self.wgu[li][: self.ffn_local])
+            u = linear(xn, li, 5, self.wgu[li][self.ffn_local:])
+            x = x + linear(torch.nn.functional.silu(g) * u, li, 6, self.wdown[li])
+        # the emitted token: the decode's own lm_head + argmax kernels on the last position
+        self.x[0].copy_(x[T - 1])
+        self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(self.x[0]), _ptr(self.logits),
+                                    _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), cfg.rms_eps, _capi.AF_EPI_NONE, None, st))
+        self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
+        nxt = int(self.next_dev.item())
+        self.pos_dev.fill_(T)
+        self.step_dev.fill_(T)
+        self.history[T - 1] = nxt
+        self.token_dev.fill_(nxt)
+        self.last_prefill_hidden = x[T - 1]
+        return nxt
+
+    def generate(self, prompt, n_new: int, use_graph: bool = True, prefill: str = "auto") -> list:
+        """Greedy generation.  prefill="batched" (default on one rank): the whole prompt in one
+        unmerged batched pass (`prefill`), as the reference prefills (model.py:408-425);
+        "stepwise": the prompt token by token along the merged path (token-level pre-gating makes
+        merged == unmerged, PAPER Eq. 2-4).  Then n_new tokens, the steady steps as a CUDA graph."""
         prompt = [int(t) for t in prompt]
         if not prompt:
             raise InputError("prompt must contain at least one token")
@@ -645,19 +734,28 @@ class LlamaEngine:
             raise InputError(f"n_new must be >= 1, got {n_new}")
         if len(prompt) + n_new > self.cfg.max_seq:
             raise InputError("prompt + n_new exceeds max_seq")
-        self.reset(prompt[0])
-        out = []
-        nxt = None
-        for t in prompt:
-            nxt = self.decode_step(t)
-        out.append(nxt)
+        if prefill not in ("auto", "batched", "stepwise"):
+            raise ValueError(f"unknown prefill mode {prefill!r}")
+        if prefill == "auto":
+            prefill = "batched" if self.cfg.tp_size == 1 else "stepwise"
+        if prefill == "batched":
+            out = [self.prefill(prompt)]
+        else:
+            self.reset(prompt[0])
+            nxt = None
+            for t in prompt:
+                nxt = self.decode_step(t)
+            out = [nxt]
         remaining = n_new - 1
+        if remaining and not self.have_prev and self.cfg.adapters and self.cfg.switch_mode == "inplace":
+            out.append(self.decode_step())     # the first merge has no previous decision: eager, then the steady graph
+            remaining -= 1
         if remaining and use_graph and self.cfg.tp_size == 1:
             self.capture()
             for _ in range(remaining):
                 self.replay()
             torch.cuda.synchronize()
-            out = out + self.tokens()[len(prompt):]
+            out = out + self.tokens()[len(prompt) + len(out) - 1:]
         else:
             for _ in range(remaining):
                 out.append(self.decode_step())

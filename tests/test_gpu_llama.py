@@ -196,3 +196,59 @@ def test_tp_shards_are_slices_of_the_full_switch(llama):
                     n = shp[name][1]
                     want = fw[:, rank * n:(rank + 1) * n]
                 assert torch.equal(one.targets[i].data, want), f"rank {rank} layer {li} {name}"
+
+
+@pytest.mark.parametrize("shape", ["r8", "r16-gqa", "base"])
+def test_batched_unmerged_prefill(llama, shape):
+    """SURVEY.md 8f-4 (model.py:408-425, PAPER Eq. 2): the whole prompt in one unmerged batched pass
+    == the per-token merged path of the oracle (each token with its own pre-gated decision switched
+    into the weights), up to the bf16 rounding of the merged weights; the backbone is not touched;
+    KV cache, position and the emitted token are those of the step-by-step path."""
+    extra = {"r8": {}, "r16-gqa": dict(experts=16, rank=16, n_heads=4, n_kv_heads=1), "base": dict(adapters=False)}[shape]
+    cfg = llama.preset("tiny", max_seq=48, **extra)
+    eng = llama.LlamaEngine(cfg, init="host")
+    prompt = [int(t) for t in np.random.Generator(np.random.PCG64(21)).integers(0, cfg.vocab, 13)]
+    w_before = [_bits(t.data) for t in eng.targets]
+    nxt = eng.prefill(prompt)
+    assert int(eng.pos_dev.item()) == len(prompt) and eng.steps_done() == len(prompt) and not eng.have_prev
+    for before, t in zip(w_before, eng.targets):
+        np.testing.assert_array_equal(before, _bits(t.data))            # unmerged: never an sgmm
+    got_hidden = eng.last_prefill_hidden.cpu().numpy()
+    got_logits = eng.logits.cpu().numpy()
+    got_k = [c[:, : len(prompt)].float().cpu().numpy() for c in eng.k_cache]
+    got_v = [c[:, : len(prompt)].float().cpu().numpy() for c in eng.v_cache]
+    # oracle: merged path, token by token, from pristine weights each time (no drift on its side)
+    ora = _oracle_for(eng, llama)
+    pristine = [{n: ora.w["layers"][li][n]["bits"].copy() for n in llama.SEGMENT_NAMES} for li in range(cfg.layers)]
+    for tkn in prompt:
+        if cfg.adapters:
+            ora.switch(ora.route(tkn), from_pristine=True, pristine=pristine)
+        o_next, o_logits, o_hidden = ora.forward(tkn)
+    scale = np.max(np.abs(o_hidden))
+    assert np.max(np.abs(got_hidden - o_hidden)) <= 2e-2 * scale
+    assert np.max(np.abs(got_logits - o_logits)) <= 2e-2 * np.max(np.abs(o_logits))
+    for li in range(cfg.layers):
+        np.testing.assert_allclose(got_k[li], ora.kc[li][:, : len(prompt)], atol=3e-2 * max(1.0, np.abs(ora.kc[li]).max()))
+        np.testing.assert_allclose(got_v[li], ora.vc[li][:, : len(prompt)], atol=3e-2 * max(1.0, np.abs(ora.vc[li]).max()))
+    top2 = np.sort(o_logits)[-2:]
+    if top2[1] - top2[0] > 4e-2 * np.max(np.abs(o_logits)):
+        assert nxt == o_next
+    # the engine's own step-by-step prompt path agrees, and decoding continues from the prefilled cache
+    step = llama.LlamaEngine(cfg, init="host")
+    step.reset(prompt[0])
+    for t in prompt:
+        s_nxt = step.decode_step(t)
+    np.testing.assert_allclose(step.logits.cpu().numpy(), got_logits, atol=2e-2 * np.max(np.abs(got_logits)))
+    a = eng.generate(prompt, 6, prefill="batched")
+    b = eng.generate(prompt, 6, prefill="stepwise")
+    c = eng.generate(prompt, 6, prefill="batched", use_graph=False)
+    assert len(a) == len(b) == 6 and a == c                                # graph == eager after a batched prefill
+    assert a[0] == nxt and (a[0] == b[0] or top2[1] - top2[0] <= 4e-2 * np.max(np.abs(o_logits)))
+    if cfg.adapters:
+        assert eng.max_backbone_deviation() < 0.02
+    with pytest.raises(Exception):
+        eng.prefill([])
+    with pytest.raises(Exception):
+        eng.prefill([cfg.vocab])
+    with pytest.raises(Exception):
+        eng.prefill(list(range(cfg.max_seq + 1)))
