@@ -252,3 +252,102 @@ def test_batched_unmerged_prefill(llama, shape):
         eng.prefill([cfg.vocab])
     with pytest.raises(Exception):
         eng.prefill(list(range(cfg.max_seq + 1)))
+
+
+class _Lockstep:
+    """Exchange layer of `tp` shard engines driven by `tp` threads on ONE GPU: the collectives of
+    llama.Collectives, done through shared slots and a barrier (all work is on one stream, so
+    enqueue order is execution order).  Exercises the TP forward path without a second device."""
+
+    def __init__(self, tp):
+        import threading
+
+        self.tp = tp
+        self.slots = [None] * tp
+        self.barrier = threading.Barrier(tp, timeout=120)
+
+    def comm(self, llama, rank):
+        shared = self
+
+        class Comm(llama.Collectives):
+            def __init__(self):
+                self.group, self.tp_size = None, shared.tp
+
+            def all_reduce_sum(self, t):
+                shared.slots[rank] = t
+                shared.barrier.wait()
+                total = torch.stack(list(shared.slots)).sum(dim=0)
+                shared.barrier.wait()          # every rank has read the originals
+                t.copy_(total)
+                shared.barrier.wait()
+
+            def broadcast_decision(self, buf):
+                shared.slots[rank] = buf
+                shared.barrier.wait()
+                if rank != 0:
+                    buf.copy_(shared.slots[0])
+                shared.barrier.wait()
+
+            def argmax_pairs(self, val, idx, out_idx):
+                shared.slots[rank] = (val.clone(), idx.clone())
+                shared.barrier.wait()
+                vals = torch.cat([v.view(1) for v, _ in shared.slots])
+                idxs = torch.cat([i.view(1) for _, i in shared.slots])
+                best = vals.max()
+                winner = torch.where(vals == best, idxs, torch.full_like(idxs, 2 ** 30)).min()
+                shared.barrier.wait()
+                out_idx.copy_(winner.to(torch.int32).view(1))
+                shared.barrier.wait()
+
+        return Comm()
+
+
+def _run_lockstep(llama, tp, make_cfg, forced, n_steps):
+    import threading
+
+    shared = _Lockstep(tp)
+    engines = [llama.LlamaEngine(make_cfg(rank), init="host", comm=shared.comm(llama, rank)) for rank in range(tp)]
+    tokens, logits, errors = [[] for _ in range(tp)], [[] for _ in range(tp)], []
+
+    def drive(rank):
+        try:
+            eng = engines[rank]
+            eng.reset(forced=forced)
+            for _ in range(n_steps):
+                tokens[rank].append(eng.decode_step())
+                logits[rank].append(eng.logits.clone())
+            eng.finalize()
+        except BaseException as exc:  # noqa: BLE001 - reported by the main thread
+            errors.append((rank, repr(exc)))
+            shared.barrier.abort()
+
+    threads = [threading.Thread(target=drive, args=(rank,)) for rank in range(tp)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=300)
+    assert not errors, errors
+    return engines, tokens, logits
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_forward_in_lockstep_equals_the_full_model(llama, tp):
+    """tp shard engines (column-parallel q/k/v/gate/up, row-parallel o/down, vocab-parallel
+    lm_head; decision broadcast, two all-reduces per layer, argmax over (value, index) pairs) decode
+    the tokens of the unsharded engine, with the same logits up to the summation order."""
+    forced = np.random.Generator(np.random.PCG64(31)).integers(0, 512, 8)
+    base = dict(max_seq=16, n_heads=4, n_kv_heads=4)
+    full = llama.LlamaEngine(llama.preset("tiny", forward_mode="separate", **base), init="host")
+    full.reset(forced=forced)
+    want_tokens, want_logits = [], []
+    for _ in range(len(forced)):
+        want_tokens.append(full.decode_step())
+        want_logits.append(full.logits.clone())
+    engines, tokens, logits = _run_lockstep(llama, tp, lambda r: llama.preset("tiny", tp_size=tp, tp_rank=r, **base), forced, len(forced))
+    for rank in range(tp):
+        assert tokens[rank] == want_tokens, f"rank {rank}"
+        assert engines[rank].max_backbone_deviation() < 0.02
+    for step in range(len(forced)):
+        got = torch.cat([logits[r][step] for r in range(tp)])
+        scale = want_logits[step].abs().max().item()
+        assert (got - want_logits[step]).abs().max().item() <= 2e-3 * scale, f"step {step}"
