@@ -94,8 +94,8 @@ class LlamaConfig:
             raise ValueError("from_pristine needs keep_pristine")
         if self.forward_mode not in ("auto", "chase", "separate"):
             raise ValueError(f"unknown forward mode {self.forward_mode!r}")
-        if self.forward_mode == "chase" and (not self.adapters or self.tp_size > 1):
-            raise ValueError("forward_mode='chase' needs adapters and tp_size == 1")
+        if self.forward_mode == "chase" and not self.adapters:
+            raise ValueError("forward_mode='chase' needs adapters")
 
     @property
     def head_dim(self) -> int:
@@ -359,14 +359,16 @@ class LlamaEngine:
         self.gc_done = torch.zeros(4 * cfg.layers, dtype=torch.int32, device=dev)
         # ---- fused switch + GEMV ("chase") ----
         want = cfg.forward_mode
-        can = cfg.adapters and cfg.tp_size == 1 and self.table is not None and self.table.info()["tensor_path"] \
+        can = cfg.adapters and self.table is not None and self.table.info()["tensor_path"] \
             and 2 * cfg.top_k * cfg.rank <= 64 and cfg.compute in ("auto", "mma")
         if want == "chase" and not can:
             raise ConfigError("forward_mode='chase' needs the tensor path (bf16, rank % 8 == 0) and 2*top_k*rank <= 64")
         self.chase = can and want in ("auto", "chase")
         if self.chase:
             # launches of one token: [qkv(0)] attn [o gu down qkv(1)] attn ... [o gu down (L-1)]
-            self.chase_chained = cfg.chain
+            # TP: the row-parallel projections (o, down) end in an all-reduce of their fixed-point accumulators
+            # (exact: integer sums), so the phases cannot share one launch -- one launch per projection
+            self.chase_chained = cfg.chain and cfg.tp_size == 1
             seg = lambda li: {"qkv": [7 * li, 7 * li + 1, 7 * li + 2], "o": [7 * li + 3], "gu": [7 * li + 4, 7 * li + 5],  # noqa: E731
                               "down": [7 * li + 6]}                                 # SEGMENT_NAMES order: q k v o gate up down
             self.groups = []
@@ -543,12 +545,16 @@ class LlamaEngine:
                 g["mid"].switch_gemv_chain(prev, self.cur, phases, self.phase_done[li], pdl=True, **kw)
             else:
                 g["o"].switch_gemv(prev, self.cur, pdl=True, **ph_o, **kw)
+                self.comm.all_reduce_sum(a["o"])          # TP: partial sums of the row-parallel o, as int64 (no-op on one rank)
                 g["gu"].switch_gemv(prev, self.cur, pdl=True, **ph_gu, **kw)
                 g["down"].switch_gemv(prev, self.cur, pdl=True, **ph_down, **kw)
+                self.comm.all_reduce_sum(a["down"])
         self._check(L.af_accum_to_f32(_ptr(self.acc[-1]["down"]), _ptr(xb), _ptr(xa), d, st))
         self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),
                                     _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))
-        self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
+        self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, cfg.tp_rank * self.vocab_local, _ptr(self.next_dev),
+                                    _ptr(self.next_val), st))
+        self.comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
 
     def _advance(self) -> None:
         L, st = _capi.lib(), _capi.stream_ptr()
