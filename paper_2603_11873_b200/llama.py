@@ -649,8 +649,8 @@ class LlamaEngine:
 
         i.e. three dense GEMMs per projection (grouped over the experts by stacking them), causal
         attention over the prompt, and the backbone is never written -- the reference's prefill
-        never runs an sgmm either.  The GEMMs and the attention are library calls (cuBLAS f32 on the
-        upcast bf16 weights, torch SDPA): this path is outside the decode metric and, as in the
+        never runs an sgmm either.  The GEMMs and the attention are library calls (cuBLAS bf16 with f32
+        accumulation and output, the f32 activations split hi + lo; torch SDPA): this path is outside the decode metric and, as in the
         paper, not tuned; the router decisions come from the same `pregate_kernel` the decode uses.
         Fills the KV cache for positions 0 .. T-1 (bf16, rotated, as the decode kernel stores
         them), leaves the engine at position T with pristine weights, and returns the token
@@ -680,12 +680,19 @@ class LlamaEngine:
             gates = torch.zeros((T, cfg.experts), dtype=f32, device=self.dev).scatter_add_(1, ids, wts)
             gates = gates.repeat_interleave(cfg.rank, dim=1)                       # [T, N r]
 
+        def mm(x, wt):
+            """f32 [T, K] x bf16 [N, K]^T -> f32 [T, N] on the tensor cores: x = hi + lo in bf16 (residual
+            2^-17, the split the fused decode launches use), f32 accumulation and f32 output."""
+            hi = x.to(torch.bfloat16)
+            lo = (x - hi.float()).to(torch.bfloat16)
+            return torch.mm(hi, wt.t(), out_dtype=f32) + torch.mm(lo, wt.t(), out_dtype=f32)
+
         def linear(x, li, j, w):
-            y = x @ w.float().t()
+            y = mm(x, w)
             if gates is not None:
-                a = self.bank_down[7 * li + j].float().reshape(cfg.experts * cfg.rank, -1)              # [N r, d_in]
-                b = self.bank_up[7 * li + j].float().permute(1, 0, 2).reshape(w.shape[0], -1)           # [d_out, N r]
-                y = y + ((x @ a.t()) * gates) @ b.t()
+                a = self.bank_down[7 * li + j].reshape(cfg.experts * cfg.rank, -1)                       # [N r, d_in]
+                b = self.bank_up[7 * li + j].permute(1, 0, 2).reshape(w.shape[0], -1).contiguous()       # [d_out, N r]
+                y = y + mm(mm(x, a) * gates, b)
             return y
 
         def rmsnorm(x, w):

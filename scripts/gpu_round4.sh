@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 rm -f gpurun_out/tests.log
 nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-for f in tests/test_gpu_*.py; do
+for f in tests/test_gpu_*.py tests/test_harness.py tests/test_io.py; do
   echo "=== $f" >> gpurun_out/tests.log
   timeout 600 python -m pytest $f -q -m gpu --timeout 300 --timeout-method=thread >> gpurun_out/tests.log 2>&1
   echo "exit $?" >> gpurun_out/tests.log
