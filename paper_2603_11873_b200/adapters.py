@@ -314,6 +314,55 @@ class SwitchTable:
             )
         )
 
+    TENSOR_PATH_RANKS = 64   # stacked ranks one tensor-path launch holds (include/adafuse_b200.h, af_fused_switch)
+
+    def switch_in_passes(self, prev, cur, *, rank: int, max_k: int, scale: float = 1.0, mode: str = "inplace",
+                         compute: str = "auto") -> int:
+        """The switch of `switch`, for decisions whose stacked rank (blocks x rank) exceeds what one
+        tensor-path launch holds (Llama-2-70B: r = 32, k = 4 -> 256): the experts are taken
+        `TENSOR_PATH_RANKS // rank` at a time -- first the previous decision's (unmerged), then the
+        current one's (merged; the first of them from pristine in that mode) -- each pass one
+        tensor-path launch over all segments.  The sub-decisions are cut on the device (no host
+        round trip, capturable).  Costs one pass over W per launch and rounds W to bf16 once per
+        pass instead of once (still fewer roundings than the reference's accumulate-into-target
+        order, linalg.py:338-343); the CUDA-core kernel that takes any stacked rank in ONE pass is
+        FMA-bound and 5x slower at 256.  Decisions must be DeviceDecisions of exactly max_k experts.
+        Returns the number of launches."""
+        for dec in (prev, cur):
+            if dec is not None and not isinstance(dec, DeviceDecision):
+                raise TypeError("switch_in_passes takes device-resident decisions (DeviceDecision) or None")
+        per = max(1, self.TENSOR_PATH_RANKS // int(rank))
+        chunks = [(start, min(per, max_k - start)) for start in range(0, max_k, per)]
+        if not hasattr(self, "_sub_decisions"):
+            self._sub_decisions = {}
+        passes = []
+        if mode == "inplace" and prev is not None:
+            passes += [("prev", c) for c in chunks]
+        if cur is not None:
+            passes += [("cur", c) for c in chunks]
+        launches = 0
+        first_cur = True
+        for which, (start, count) in passes:
+            src = prev if which == "prev" else cur
+            key = (which, start)
+            sub = self._sub_decisions.get(key)
+            if sub is None or sub.buf.device != src.buf.device:
+                sub = self._sub_decisions[key] = DeviceDecision(src.buf.device)
+            si, di = src.buf.view(torch.int32), sub.buf.view(torch.int32)
+            di[0:1].fill_(count)
+            di[1: 1 + count].copy_(si[1 + start: 1 + start + count])                                           # expert ids
+            di[1 + _capi.AF_MAX_K: 1 + _capi.AF_MAX_K + count].copy_(si[1 + _capi.AF_MAX_K + start: 1 + _capi.AF_MAX_K + start + count])  # weights (raw bits)
+            if which == "prev":
+                self.switch(sub, None, max_k=count, scale=scale, compute=compute)
+            else:
+                self.switch(None, sub, max_k=count, scale=scale, compute=compute,
+                            mode=mode if (mode == "from_pristine" and first_cur) else "inplace")
+                first_cur = False
+            launches += 1
+        if mode == "from_pristine" and cur is None:
+            self.refresh()
+        return launches
+
     def build_plan(self, prev, cur, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace") -> None:
         """Once per token: the block list of (prev, cur) for the switch + GEMV launches that pass
         plan_prebuilt=True (adapters.py:188-233 bookkeeping, on the device)."""

@@ -64,6 +64,7 @@ class LlamaConfig:
     # "auto": chase when it applies (adapters, single rank, tensor path)
     forward_mode: str = "auto"
     chain: bool = True               # chase: o -> gate|up -> down -> next q|k|v as ONE launch with in-kernel phase barriers
+    split_switch: bool = True        # > 64 stacked ranks: several tensor-path passes instead of one CUDA-core pass
     defer_norm: bool = True          # chase on the tcgen05 path: RMSNorm scales computed by one CTA, applied by the consumers
     gemv_chain: bool = True          # plain forward (separate / adapter-free): the same four projections as one persistent GEMV launch
 
@@ -327,6 +328,8 @@ class LlamaEngine:
         self.targets, self.bank_down, self.bank_up = targets, downs, ups
         self.pristine = [t.copy() for t in targets] if (cfg.adapters and cfg.keep_pristine) else None
         self.table = SwitchTable(targets, downs, ups, pristine=self.pristine) if cfg.adapters else None
+        self.split_switch = bool(self.table is not None and cfg.split_switch and self.table.info()["tensor_path"]
+                                 and cfg.rank <= SwitchTable.TENSOR_PATH_RANKS)
         cos, sin = rope_tables(cfg)
         self.cos, self.sin = put(cos, torch.float32), put(sin, torch.float32)
         self.k_cache = [torch.zeros((self.kv_local, cfg.max_seq, hd), dtype=bf, device=dev) for _ in range(cfg.layers)]
@@ -421,6 +424,15 @@ class LlamaEngine:
             raise StateError("this engine was built without adapters")
         kw.setdefault("max_k", self.cfg.top_k)
         kw.setdefault("compute", self.cfg.compute)
+        cfg = self.cfg
+        blocks = (cfg.top_k if (prev is not None and kw.get("mode", "inplace") == "inplace") else 0) + (cfg.top_k if cur is not None else 0)
+        if self.split_switch and blocks * cfg.rank > SwitchTable.TENSOR_PATH_RANKS and kw["compute"] in ("auto", "mma") \
+                and all(isinstance(dec, DeviceDecision) for dec in (prev, cur) if dec is not None):
+            # more stacked ranks than one tensor-path launch holds (Llama-2-70B): a few tensor-path passes
+            # instead of one FMA-bound CUDA-core pass
+            self.table.switch_in_passes(prev, cur, rank=cfg.rank, max_k=cfg.top_k, mode=kw.get("mode", "inplace"),
+                                        compute=kw["compute"], scale=kw.get("scale", 1.0))
+            return
         self.table.switch(prev, cur, **kw)
 
     def merge(self, dec, **kw) -> None:

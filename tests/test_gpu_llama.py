@@ -360,3 +360,45 @@ def test_tp_forward_in_lockstep_equals_the_full_model(llama, tp, forward_mode):
         top2 = torch.topk(want_logits[step], 2).values
         if (top2[0] - top2[1]).item() > 4 * tol * scale:
             assert tokens[0][step] == want_tokens[step], f"step {step}"
+
+
+@pytest.mark.parametrize("switch_mode", ["inplace", "from_pristine"])
+def test_switch_in_passes_for_more_than_64_stacked_ranks(llama, switch_mode):
+    """BASELINE configs[4]-like (rank 32, top-4: 256 stacked ranks in a steady switch): the engine cuts the
+    switch into tensor-path passes of 64 stacked ranks.  Against the single CUDA-core pass over all ranks
+    the weights differ by at most one bf16 rounding per pass, the logits agree, the backbone is restored."""
+    from paper_2603_11873_b200 import _capi
+
+    base = dict(max_seq=16, experts=8, rank=32, top_k=4, switch_mode=switch_mode, forward_mode="separate")
+    forced = np.random.Generator(np.random.PCG64(41)).integers(0, 512, 6)
+    one = llama.LlamaEngine(llama.preset("tiny", split_switch=False, **base), init="host")
+    many = llama.LlamaEngine(llama.preset("tiny", **base), init="host")
+    assert many.split_switch and not one.split_switch and not many.chase
+    one.reset(forced=forced)
+    many.reset(forced=forced)
+    n_pass = 8 if switch_mode == "inplace" else 2
+    for step in range(len(forced)):
+        before = _capi.launch_count()
+        a = one.decode_step()
+        single = _capi.launch_count() - before
+        before = _capi.launch_count()
+        b = many.decode_step()
+        launches = _capi.launch_count() - before
+        assert many.decision() == one.decision()
+        want_passes = (2 if switch_mode == "from_pristine" else (4 if step else 2))    # 2 experts of rank 32 per pass
+        assert launches - single == want_passes - 1, f"step {step}: {launches} launches against {single}"
+        for i, (ta, tb) in enumerate(zip(one.targets, many.targets)):
+            # every pass rounds at the magnitude the element has at that moment: bound the difference by
+            # half a bf16 ulp of the matrix's largest element per pass (+ the single pass's own rounding)
+            fa, fb = ta.data.float(), tb.data.float()
+            ulp = 2.0 ** (np.floor(np.log2(max(fa.abs().max().item(), fb.abs().max().item()))) - 7)
+            worst = (fa - fb).abs().max().item() / ulp
+            # in place, both engines carry their own roundings from token to token (the drift refresh_every bounds)
+            tokens_of_drift = step + 1 if switch_mode == "inplace" else 1
+            assert worst <= 0.5 * (n_pass + 1) * tokens_of_drift, f"step {step} segment {i}: {worst} ulp of the largest element"
+        scale = one.logits.abs().max().item()
+        assert (one.logits - many.logits).abs().max().item() <= 2e-2 * scale
+    one.finalize()
+    many.finalize()
+    assert many.max_backbone_deviation() < 0.05 and one.max_backbone_deviation() < 0.05
+
