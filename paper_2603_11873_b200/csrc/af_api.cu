@@ -460,7 +460,11 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     return AF_OK;
 }
 
-constexpr int kUmmaMaxRanks = 32;   // stacked ranks (2 k r in the steady switch) the tcgen05 kernel is used for
+// Stacked ranks (2 k r in the steady switch) up to which the tcgen05 kernel is used.  The plain switch gains
+// 2-3 % over mma.sync at 64 (four W stages, three UP stages); the fused switch + GEMV loses 4 % there (measured on
+// Llama-3-8B, profiles/README.md), so chains stay on mma.sync above 32.  AF_UMMA_MAX_RANKS[_CHAIN] override (A/B runs).
+static const int kUmmaMaxRanks = [] { const char* e = getenv("AF_UMMA_MAX_RANKS"); return e ? atoi(e) : 64; }();
+static const int kUmmaMaxRanksChain = [] { const char* e = getenv("AF_UMMA_MAX_RANKS_CHAIN"); return e ? atoi(e) : 32; }();
 // tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = k-groups of 8 stacked ranks per half.
 template <int NB, bool GEMV>
 static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
@@ -583,7 +587,7 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
         mp.n_chain_segs = 0;
         mp.n_phases = 1;
         const int grid = std::min(t->n_units_umma, t->sm_count);
-        return launch_umma<4, false>(mp, grid, st);
+        return s_bound <= 32 ? launch_umma<4, false>(mp, grid, st) : launch_umma<8, false>(mp, grid, st);
     }
     if (want_mma && mma_fits) {
         MmaParams mp{};
@@ -967,7 +971,7 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     const int ks_tl = std::max(1, (s_bound + 15) / 16);
     // At most 32 stacked ranks: with 64 the hi + lo slab (32 KB) and the UP stage (16 KB) leave the tcgen05
     // kernel three ring stages and it loses to the mma.sync kernel (Llama-3-8B shapes, r = 16: 7.93 vs 7.04 ms)
-    const bool umma_launch = g_umma.load() && t->umma_ok && g->d_units_umma && s_bound <= kUmmaMaxRanks;
+    const bool umma_launch = g_umma.load() && t->umma_ok && g->d_units_umma && s_bound <= kUmmaMaxRanksChain;
     if (g_timeline && g_timeline_left > 0 && (ks_tl == 2 || umma_launch)) {  // mma.sync: the probe is compiled into the KS = 2 hi/lo variant only
         mp.timeline = g_timeline;
         g_timeline += g_timeline_stride;
@@ -989,7 +993,8 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 6 : 5) * S;
         mp.tmaps_st = t->d_maps + (size_t)5 * S;
         mp.tmaps_up = t->d_maps + (size_t)7 * S;
-        return launch_umma<4, true>(mp, g->grid_umma, st);   // 4 k-groups of 8 stacked ranks per half
+        // 4 (8) k-groups of 8 stacked ranks per half
+        return s_bound <= 32 ? launch_umma<4, true>(mp, g->grid_umma, st) : launch_umma<8, true>(mp, g->grid_umma, st);
     }
     if (mp.timeline && ks == 2) return launch_mma<2, false, true, true>(mp, g->grid, st);
     switch (ks) {

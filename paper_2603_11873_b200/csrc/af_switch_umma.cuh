@@ -18,9 +18,9 @@
 // (no cross-warp reduction: a thread holds the whole 128-column row strip).
 //
 // Scope: tables of ONE rank in {8, 16, 32, 64}, matrices multiples of 128 in both directions (every
-// Llama shape of BASELINE.json), launches of at most 32 stacked ranks (with 64 the slab and the UP
-// stage leave three ring stages and the mma.sync kernel wins); anything else keeps the mma.sync kernel.  (scripts/micro/umma_test.cu
-// pins the descriptor encodings in isolation.)
+// Llama shape of BASELINE.json), launches of at most 64 stacked ranks (plain switch) / 32 (fused switch +
+// GEMV, where mma.sync still wins at 64: af_api.cu kUmmaMaxRanks[Chain]); anything else keeps the mma.sync
+// kernel.  (scripts/micro/umma_test.cu pins the descriptor encodings in isolation.)
 #pragma once
 
 #include "af_switch_mma.cuh"
@@ -49,21 +49,27 @@ struct UmmaLayout {
     static constexpr int up_stage = NB * kUBlockBytes;
     static constexpr int slab_bytes = 2 * NB * kUSlabBlock;            // hi + lo
     static constexpr int xs_bytes = GEMV ? kUXSlots * kUN * 4 : 0;
-    static constexpr int misc = 512 /*barriers*/ + (int)sizeof(Plan) + 256 + kUnitCache * (int)sizeof(UnitDev) + kSegCache * (int)sizeof(SegDev);
+    static constexpr int misc = 1024 /*barriers*/ + (int)sizeof(Plan) + 256 + kUnitCache * (int)sizeof(UnitDev) + kSegCache * (int)sizeof(SegDev);
     static constexpr int fixed = slab_bytes + xs_bytes + misc + 2048;
-    static constexpr int by_smem = (227 * 1024 - fixed) / (kUWStage + up_stage);
-    static constexpr int stages = by_smem < 6 ? by_smem : 6;
+    // Two rings.  W tiles (32 KB, from HBM) live from their load until their store has read them; UP stages
+    // (from L2) only until the tile's MMAs have completed, two tiles ahead of the epilogue at most -- three UP
+    // stages are enough, which leaves a 64-rank launch (16 KB UP stages, 32 KB slab) four W stages instead of three.
+    static constexpr int up_stages_wanted = NB > 4 ? 3 : 6;
+    static constexpr int by_smem = (227 * 1024 - fixed) / (kUWStage + up_stage);          // equal depths
+    static constexpr int by_smem_w = (227 * 1024 - fixed - up_stages_wanted * up_stage) / kUWStage;
+    static constexpr int stages = NB > 4 ? (by_smem_w < 6 ? by_smem_w : 6) : (by_smem < 6 ? by_smem : 6);
+    static constexpr int up_stages = NB > 4 ? up_stages_wanted : stages;
     static constexpr int off_w = 0;
     static constexpr int off_up = off_w + stages * kUWStage;
-    static constexpr int off_slab = off_up + stages * up_stage;        // 1024-aligned (multiples of 2 KB)
+    static constexpr int off_slab = off_up + up_stages * up_stage;     // 1024-aligned (multiples of 2 KB)
     static constexpr int off_xs = off_slab + slab_bytes;
     static constexpr int off_bar = off_xs + xs_bytes;
-    static constexpr int off_plan = off_bar + 512;
+    static constexpr int off_plan = off_bar + 1024;
     static constexpr int off_red = (off_plan + (int)sizeof(Plan) + 15) & ~15;
     static constexpr int off_units = off_red + 256;
     static constexpr int off_segs = off_units + kUnitCache * (int)sizeof(UnitDev);
     static constexpr int total = off_segs + kSegCache * (int)sizeof(SegDev) + 1024;
-    static_assert(stages >= 3 && total <= 227 * 1024, "shared memory budget");
+    static_assert(stages >= 3 && up_stages >= 3 && up_stages <= 8 && total <= 227 * 1024, "shared memory budget");
 };
 
 // ---- tcgen05 wrappers ----
@@ -227,7 +233,7 @@ __device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const uint
 template <int NB, bool GEMV>
 __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_constant__ MmaParams mp) {
     using L = UmmaLayout<NB, GEMV>;
-    constexpr int kSt = L::stages;
+    constexpr int kSt = L::stages, kUpSt = L::up_stages;
     extern __shared__ unsigned char smem_dyn[];
     const SwitchParams& p = mp.base;
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
@@ -238,6 +244,8 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
     uint64_t* acc_empty = full + 26;                                  // [2]
     uint64_t* slab_bar = full + 28;                                   // [1]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 30);
+    uint64_t* up_full = full + 32;                                    // [8]  UP ring: loaded by the UP producer ...
+    uint64_t* up_empty = full + 40;                                   // [8]  ... released when the tile's MMAs have completed
     Plan& plan = *reinterpret_cast<Plan*>(sm + L::off_plan);
     UnitDev* unit_cache = reinterpret_cast<UnitDev*>(sm + L::off_units);
     SegDev* seg_cache = reinterpret_cast<SegDev*>(sm + L::off_segs);
@@ -251,13 +259,17 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
         unit_cache[jj] = uu < p.n_units ? p.units[uu] : UnitDev{0, 0, 0, 0, 0, 0};
     }
     if (tid >= 64 && tid < 64 + mp.n_chain_segs) seg_cache[tid - 64] = p.segs[mp.chain_segs[tid - 64]];
-    for (int i = tid * 16; i < kSt * L::up_stage; i += kUThreads * 16)   // block slots past n_blocks must read as zeros
+    for (int i = tid * 16; i < kUpSt * L::up_stage; i += kUThreads * 16)   // block slots past n_blocks must read as zeros
         *reinterpret_cast<uint4*>(sm + L::off_up + i) = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) {
         for (int s = 0; s < kSt; ++s) {
-            mbar_init(&full[s], 2);
+            mbar_init(&full[s], 1);
             mbar_init(&computed[s], 4);
             mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < kUpSt; ++s) {
+            mbar_init(&up_full[s], 1);
+            mbar_init(&up_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
@@ -340,25 +352,25 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 SegDev sg;
                 int cur_seg = -1;
                 for (int it = 0; ti.valid(p); ++it) {
-                    const int stage = it % kSt;
-                    const uint32_t ph = (it / kSt) & 1;
+                    const int stage = it % kUpSt;
+                    const uint32_t ph = (it / kUpSt) & 1;
                     if (ti.un.seg != cur_seg) {
                         cur_seg = ti.un.seg;
                         sg = seg_of(ti.un);
                     }
-                    mbar_wait(&empty[stage], ph ^ 1);
+                    mbar_wait(&up_empty[stage], ph ^ 1);
                     const uint32_t blk_bytes = (uint32_t)kUM * sg.rank * 2;
-                    mbar_expect_tx(&full[stage], n_blocks * blk_bytes);
+                    mbar_expect_tx(&up_full[stage], n_blocks * blk_bytes);
                     if (sg.rank == 8) {   // an expert block is 128 contiguous 16-byte rows: one bulk copy
                         const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
                         for (int b = 0; b < n_blocks; ++b)
                             bulk_load_1d(up_base + stage * L::up_stage + b * kUBlockBytes,
-                                         upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &full[stage]);
+                                         upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &up_full[stage]);
                     } else {              // 128 rows x rank through the tensor map whose swizzle span is the row
                         const CUtensorMap* tm = mp.tmaps_up + ti.un.seg;
                         for (int b = 0; b < n_blocks; ++b)
                             tma_load_2d_addr(up_base + stage * L::up_stage + b * blk_bytes, tm, 0, plan.expert[b] * sg.d_out + ti.m0,
-                                             &full[stage]);
+                                             &up_full[stage]);
                     }
                     ti.next(p);
                 }
@@ -374,13 +386,13 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 const int ksteps = (n_blocks * rank + 15) >> 4;          // rank-16 steps over the stacked ranks
                 int unit_j = -1;
                 for (int it = 0; ti.valid(p); ++it) {
-                    const int stage = it % kSt, buf = it & 1;
-                    const uint32_t ph = (it / kSt) & 1, aph = (it >> 1) & 1;
+                    const int stage = it % kUpSt, buf = it & 1;
+                    const uint32_t ph = (it / kUpSt) & 1, aph = (it >> 1) & 1;
                     if (ti.j != unit_j) {   // the unit's slab has been written (and made visible to the tensor core)
                         unit_j = ti.j;
                         mbar_wait(slab_bar, (uint32_t)unit_j & 1);
                     }
-                    mbar_wait(&full[stage], ph);
+                    mbar_wait(&up_full[stage], ph);
                     mbar_wait(&acc_empty[buf], aph ^ 1);
                     tc_fence_after();
                     const uint32_t a0 = up_base + stage * L::up_stage;
@@ -398,6 +410,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         umma_bf16(tmem + buf * kUN, da, db, idesc, 0);
                     }
                     umma_commit(smem_u32(&acc_full[buf]));
+                    umma_commit(smem_u32(&up_empty[stage]));   // the UP stage is free once these MMAs have read it
                     ti.next(p);
                 }
             }

@@ -393,7 +393,10 @@ class LlamaEngine:
             # tcgen05 path: RMSNorm scales are deferred -- one CTA computes them, the consumers of q|k|v
             # (attention) and gate|up (the SiLU prologue of the down projection) apply them
             stacked = (1 if cfg.switch_mode == "from_pristine" else 2) * cfg.top_k * cfg.rank   # ranks of a steady switch
-            self.defer_norm = bool(self.table.info().get("umma_path")) and cfg.defer_norm and stacked <= 32
+            import os
+
+            umma_ranks = int(os.environ.get("AF_UMMA_MAX_RANKS_CHAIN", "32"))   # af_api.cu: stacked ranks the tcgen05 chain kernel takes
+            self.defer_norm = bool(self.table.info().get("umma_path")) and cfg.defer_norm and stacked <= umma_ranks
             self.inv_qkv = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
             self.inv_gu = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
             counters = self.acc_arena[cfg.layers * per_layer:].view(torch.int32)   # 4 int32 per layer

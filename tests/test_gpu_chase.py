@@ -71,8 +71,18 @@ def test_switch_gemv_weights_and_outputs(af, d_in, rows, rank):
     grp.switch_gemv(prev, cur, acc, xin=x, max_k=2)
     tab_b.switch(prev, cur, max_k=2)
     tab_a.status()
+    # Same kernel family on both sides -> the same bits.  Between 33 and 64 stacked ranks the plain switch runs on
+    # tcgen05 and the fused launch on mma.sync (af_api.cu kUmmaMaxRanks / kUmmaMaxRanksChain): the f32 sums differ in
+    # order, so a rounding may tip on a rare element -- never more than one bf16 step.
+    same_path = 4 * rank <= 32 or not tab_a.info()["umma_path"]
     for a, b in zip(tg_a, tg_b):
-        assert torch.equal(a.data, b.data), "fused switch + GEMV must leave the same weights as the plain switch"
+        if same_path:
+            assert torch.equal(a.data, b.data), "fused switch + GEMV must leave the same weights as the plain switch"
+        else:
+            fa, fb = a.data.float(), b.data.float()
+            mag = torch.maximum(torch.maximum(fa.abs(), fb.abs()), fa.abs().mean())     # cancellation: judge at the operands' size
+            step = torch.exp2(torch.floor(torch.log2(mag)) - 7)
+            assert ((fa - fb).abs() <= step).all() and (fa != fb).float().mean().item() < 1e-3
     w_new = np.concatenate([_bf16_to_f64(t.data) for t in tg_a], axis=0)
     want = w_new @ x.cpu().numpy().astype(np.float64)
     got = acc.cpu().numpy().astype(np.float64) * FIX
@@ -81,9 +91,10 @@ def test_switch_gemv_weights_and_outputs(af, d_in, rows, rank):
     assert np.max(np.abs(got - want) / (scale + 1e-30)) < 2e-5
     # arrival-order independence: repeat from the same state, bit-identical accumulators
     acc2 = torch.zeros_like(acc)
+    w_before = [a.data.clone() for a in tg_a]
     grp.switch_gemv(cur, cur, acc2, xin=x, max_k=2)       # unchanged decision: pure GEMV, nothing stored
-    for a, b in zip(tg_a, tg_b):
-        assert torch.equal(a.data, b.data)
+    for a, b in zip(tg_a, w_before):
+        assert torch.equal(a.data, b)
     assert torch.equal(acc, acc2)
     acc3 = torch.zeros_like(acc)
     grp.switch_gemv(None, None, acc3, xin=x)              # no decision at all: plain GEMV
