@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--forward-mode", default="auto", choices=["auto", "chase", "separate"])
     ap.add_argument("--no-chain", action="store_true", help="chase: one launch per projection instead of chained phases")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--attn-splits", type=int, default=0, help="KV splits of the decode attention (0 = the engine's choice)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -203,7 +204,8 @@ def main():
     max_seq = 2 * (args.steps + args.warmup) + 16
     max_seq += 16  # roofline pass of the chase schedule
     cfg = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
-                       compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain)
+                       compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain,
+                       attn_splits=args.attn_splits)
     eng = llama.LlamaEngine(cfg, init="device")
     info = eng.table.info()
     forced = np.random.Generator(np.random.PCG64(cfg.seed + 1)).integers(0, cfg.vocab, 4096)

@@ -352,6 +352,10 @@ constexpr int kAttnThreads = 256;
 constexpr int kAttnWarps = kAttnThreads / 32;
 constexpr int kAttnMaxHd = 256;
 constexpr int kAttnUnroll = 8;
+#ifndef AF_ATTN_POS_PER_SPLIT
+#define AF_ATTN_POS_PER_SPLIT 32
+#endif
+constexpr int kAttnPosPerSplit = AF_ATTN_POS_PER_SPLIT;   // positions below which a further KV split does not pay
 
 template <int EL>
 __device__ __forceinline__ void load_bf16_vec(const __nv_bfloat16* p, float (&f)[EL]) {
@@ -398,6 +402,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
     pdl_launch_dependents();  // after the wait: a dependent's pre-wait part then never runs ahead of qkv's producer
     const int pos = *pos_dev;
     const int n_pos = pos + 1;
+    // the grid is sized for the longest context; a short one uses fewer splits (a split below ~32 positions costs
+    // more in the combine than it saves), the other CTAs of the head leave here
+    n_split = min(n_split, max(1, (n_pos + kAttnPosPerSplit - 1) / kAttnPosPerSplit));
+    if (sp >= n_split) return;
     const int per = (n_pos + n_split - 1) / n_split;
     const int t0 = sp * per, t1 = min(n_pos, t0 + per);
     const int half = hd >> 1;
