@@ -109,10 +109,12 @@ int af_set_pdl(int32_t enable);
  * Results are identical up to f32 summation order.  Env: AF_GEMV, AF_GEMV_FULL_SM. */
 int af_set_gemv_variant(int32_t variant, int32_t full_sm);
 /* Tensor path of the fused switch (+ GEMV) on eligible tables (one rank in {8, 16, 32, 64} everywhere,
- * every matrix a multiple of 128 x 128; launches of at most 32 stacked ranks): 1 = tcgen05.mma with the accumulators in tensor memory
- * (csrc/af_switch_umma.cuh; default), 0 = mma.sync kernels (what every other table uses).  Both are
- * within 1 bf16 ulp of the f32 merge; they round differently in the last bit, so do not mix them
- * inside one comparison.  Env: AF_UMMA=0 turns the tcgen05 path off at load. */
+ * every matrix a multiple of 128 x 128; launches of at most 64 stacked ranks for af_fused_switch, 32 for
+ * af_switch_gemv[_chain]): 1 = tcgen05.mma with the accumulators in tensor memory
+ * (csrc/af_switch_umma.cuh; default), 0 = mma.sync kernels (what every other table and launch uses).
+ * Both are within 1 bf16 ulp of the f32 merge; they round differently in the last bit, so do not mix
+ * them inside one comparison.  Env: AF_UMMA=0 turns the tcgen05 path off at load;
+ * AF_UMMA_MAX_RANKS / AF_UMMA_MAX_RANKS_CHAIN move the two limits (A/B runs). */
 int af_set_umma(int32_t enable);
 
 /* ---- segment table: built once at model load -------------------------------------
