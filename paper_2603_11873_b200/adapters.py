@@ -317,7 +317,7 @@ class SwitchTable:
     TENSOR_PATH_RANKS = 64   # stacked ranks one tensor-path launch holds (include/adafuse_b200.h, af_fused_switch)
 
     def switch_in_passes(self, prev, cur, *, rank: int, max_k: int, scale: float = 1.0, mode: str = "inplace",
-                         compute: str = "auto") -> int:
+                         compute: str = "auto", hold_last: bool = False):
         """The switch of `switch`, for decisions whose stacked rank (blocks x rank) exceeds what one
         tensor-path launch holds (Llama-2-70B: r = 32, k = 4 -> 256): the experts are taken
         `TENSOR_PATH_RANKS // rank` at a time -- first the previous decision's (unmerged), then the
@@ -327,7 +327,9 @@ class SwitchTable:
         pass instead of once (still fewer roundings than the reference's accumulate-into-target
         order, linalg.py:338-343); the CUDA-core kernel that takes any stacked rank in ONE pass is
         FMA-bound and 5x slower at 256.  Decisions must be DeviceDecisions of exactly max_k experts.
-        Returns the number of launches."""
+        Returns the number of launches -- or, with hold_last, leaves the last merge pass to the caller
+        (who fuses it with the forward, `SegmentGroup.switch_gemv`) and returns its
+        (sub-decision, expert count, mode)."""
         for dec in (prev, cur):
             if dec is not None and not isinstance(dec, DeviceDecision):
                 raise TypeError("switch_in_passes takes device-resident decisions (DeviceDecision) or None")
@@ -342,7 +344,8 @@ class SwitchTable:
             passes += [("cur", c) for c in chunks]
         launches = 0
         first_cur = True
-        for which, (start, count) in passes:
+        held = None
+        for idx, (which, (start, count)) in enumerate(passes):
             src = prev if which == "prev" else cur
             key = (which, start)
             sub = self._sub_decisions.get(key)
@@ -355,13 +358,16 @@ class SwitchTable:
             if which == "prev":
                 self.switch(sub, None, max_k=count, scale=scale, compute=compute)
             else:
-                self.switch(None, sub, max_k=count, scale=scale, compute=compute,
-                            mode=mode if (mode == "from_pristine" and first_cur) else "inplace")
+                pass_mode = mode if (mode == "from_pristine" and first_cur) else "inplace"
                 first_cur = False
+                if hold_last and idx == len(passes) - 1:
+                    held = (sub, count, pass_mode)
+                    break
+                self.switch(None, sub, max_k=count, scale=scale, compute=compute, mode=pass_mode)
             launches += 1
         if mode == "from_pristine" and cur is None:
             self.refresh()
-        return launches
+        return held if hold_last else launches
 
     def build_plan(self, prev, cur, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace") -> None:
         """Once per token: the block list of (prev, cur) for the switch + GEMV launches that pass

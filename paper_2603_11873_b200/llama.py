@@ -364,8 +364,10 @@ class LlamaEngine:
         self.gc_done = torch.zeros(4 * cfg.layers, dtype=torch.int32, device=dev)
         # ---- fused switch + GEMV ("chase") ----
         want = cfg.forward_mode
+        # more than 64 stacked ranks: the switch runs in tensor-path passes and the LAST pass carries the GEMVs
+        self.chase_split = bool(self.split_switch and 2 * cfg.top_k * cfg.rank > SwitchTable.TENSOR_PATH_RANKS)
         can = cfg.adapters and self.table is not None and self.table.info()["tensor_path"] \
-            and 2 * cfg.top_k * cfg.rank <= 64 and cfg.compute in ("auto", "mma")
+            and (2 * cfg.top_k * cfg.rank <= 64 or self.chase_split) and cfg.compute in ("auto", "mma")
         if want == "chase" and not can:
             raise ConfigError("forward_mode='chase' needs the tensor path (bf16, rank % 8 == 0) and 2*top_k*rank <= 64")
         self.chase = can and want in ("auto", "chase")
@@ -530,8 +532,14 @@ class LlamaEngine:
         d, eps = cfg.hidden, cfg.rms_eps
         xa, xb = self.x
         prev = self.prev if (with_prev and cfg.switch_mode == "inplace") else None
-        kw = dict(max_k=cfg.top_k, mode=cfg.switch_mode, plan_prebuilt=True)
-        self.table.build_plan(prev, self.cur, max_k=cfg.top_k, mode=cfg.switch_mode)
+        cur, max_k, mode = self.cur, cfg.top_k, cfg.switch_mode
+        if self.chase_split:
+            # all passes but the last as plain switch launches; the last merge pass is the one fused with the forward
+            cur, max_k, mode = self.table.switch_in_passes(prev, self.cur, rank=cfg.rank, max_k=cfg.top_k, mode=cfg.switch_mode,
+                                                           compute=cfg.compute, hold_last=True)
+            prev = None
+        kw = dict(max_k=max_k, mode=mode, plan_prebuilt=True)
+        self.table.build_plan(prev, cur, max_k=max_k, mode=mode)
         self.acc_arena.zero_()
         self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
         norm = "rmsnorm_deferred" if self.defer_norm else "rmsnorm"
@@ -542,9 +550,9 @@ class LlamaEngine:
             ig = self.inv_gu[li: li + 1] if self.defer_norm else None
             qkv_first = dict(acc_out=a["qkv"], xin=xa, prologue=norm, norm_w=self.attn_norm[li], eps=eps, inv_out=iq)
             if li == 0:
-                g["qkv"].switch_gemv(prev, self.cur, pdl=False, **qkv_first, **kw)
+                g["qkv"].switch_gemv(prev, cur, pdl=False, **qkv_first, **kw)
             elif not self.chase_chained:
-                g["qkv"].switch_gemv(prev, self.cur, a["qkv"], acc_in=self.acc[li - 1]["down"], res=xb, h_out=xa, prologue=norm,
+                g["qkv"].switch_gemv(prev, cur, a["qkv"], acc_in=self.acc[li - 1]["down"], res=xb, h_out=xa, prologue=norm,
                                      norm_w=self.attn_norm[li], eps=eps, inv_out=iq, pdl=True, **kw)
             self._check(L.af_attn_decode_fix(_ptr(a["qkv"]), _ptr(iq) if iq is not None else None, _ptr(self.k_cache[li]),
                                              _ptr(self.v_cache[li]), _ptr(self.cos), _ptr(self.sin), _ptr(self.pos_dev),
@@ -559,12 +567,12 @@ class LlamaEngine:
                     phases.append(dict(acc_out=self.acc[li + 1]["qkv"], acc_in=a["down"], res=xb, h_out=xa, prologue=norm,
                                        norm_w=self.attn_norm[li + 1], eps=eps,
                                        inv_out=self.inv_qkv[li + 1: li + 2] if self.defer_norm else None))
-                g["mid"].switch_gemv_chain(prev, self.cur, phases, self.phase_done[li], pdl=True, **kw)
+                g["mid"].switch_gemv_chain(prev, cur, phases, self.phase_done[li], pdl=True, **kw)
             else:
-                g["o"].switch_gemv(prev, self.cur, pdl=True, **ph_o, **kw)
+                g["o"].switch_gemv(prev, cur, pdl=True, **ph_o, **kw)
                 self.comm.all_reduce_sum(a["o"])          # TP: partial sums of the row-parallel o, as int64 (no-op on one rank)
-                g["gu"].switch_gemv(prev, self.cur, pdl=True, **ph_gu, **kw)
-                g["down"].switch_gemv(prev, self.cur, pdl=True, **ph_down, **kw)
+                g["gu"].switch_gemv(prev, cur, pdl=True, **ph_gu, **kw)
+                g["down"].switch_gemv(prev, cur, pdl=True, **ph_down, **kw)
                 self.comm.all_reduce_sum(a["down"])
         self._check(L.af_accum_to_f32(_ptr(self.acc[-1]["down"]), _ptr(xb), _ptr(xa), d, st))
         self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),
