@@ -449,19 +449,23 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
             UmmaIter ti;
             ti.init(p, unit_cache);
             if (ti.valid(p)) {
-                if constexpr (GEMV) {
-                    if (mp.pdl) {
-                        pdl_wait();
-                        if (tid == 0) pdl_launch_dependents();
-                    }
-                    if (tid == 0) tl_stamp(tl, 3);
-                }
+                // (programmatic dependent launch: the wait for the previous kernel sits in the first enter_phase, after
+                //  this CTA's first slab has been staged and its first MMAs issued -- they only need the factors)
+                bool pdl_pending = GEMV && mp.pdl;
                 float x_inv = 1.0f, in_scale = 1.0f;
                 bool tl_first = false;
                 int cur_phase = -1, phase_j0 = 0, published = 0;
                 // entering a phase: previous phase published by every CTA, then the input vector
                 auto enter_phase = [&](int ph) {
                     const GemvParams& g = mp.gv[ph];
+                    if (pdl_pending) {
+                        pdl_pending = false;
+                        pdl_wait();
+                        if (tid == 0) {
+                            pdl_launch_dependents();
+                            tl_stamp(tl, 3);
+                        }
+                    }
                     if (tid == 0) tl_stamp(tl, 8 + 4 * ph);
                     if (ph > 0) {
                         if (tid == 0) {
