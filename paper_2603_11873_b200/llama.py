@@ -21,6 +21,7 @@ vocab-parallel lm_head.
 from __future__ import annotations
 
 import math
+import os
 import zlib
 from dataclasses import dataclass, replace
 
@@ -397,8 +398,6 @@ class LlamaEngine:
             # tcgen05 path: RMSNorm scales are deferred -- one CTA computes them, the consumers of q|k|v
             # (attention) and gate|up (the SiLU prologue of the down projection) apply them
             stacked = (1 if cfg.switch_mode == "from_pristine" else 2) * cfg.top_k * cfg.rank   # ranks of a steady switch
-            import os
-
             umma_ranks = int(os.environ.get("AF_UMMA_MAX_RANKS_CHAIN", "32"))   # af_api.cu: stacked ranks the tcgen05 chain kernel takes
             self.defer_norm = bool(self.table.info().get("umma_path")) and cfg.defer_norm and stacked <= umma_ranks
             self.inv_qkv = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
