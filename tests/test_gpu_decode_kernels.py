@@ -110,10 +110,14 @@ def test_argmax_lowest_index_on_ties(capi):
     assert int(out.item()) == 1123 and float(val.item()) == 7.5
 
 
-@pytest.mark.parametrize("hd,n_heads,n_kv,splits", [(64, 4, 2, 1), (128, 8, 2, 1), (128, 8, 8, 3), (256, 2, 1, 2), (80, 4, 4, 1), (128, 32, 8, 5)])
+@pytest.mark.parametrize("hd,n_heads,n_kv,splits", [(64, 4, 2, 1), (128, 8, 2, 1), (128, 8, 8, 3), (256, 2, 1, 2), (80, 4, 4, 1), (128, 32, 8, 5),
+                                                    (128, 4, 2, 8)])
 def test_attention_decode_against_numpy(capi, hd, n_heads, n_kv, splits):
+    """The grid carries `splits` CTAs per head; the kernel uses ceil(positions / 32) of them, so the run crosses
+    every change of the effective split count (the 8-split case runs to 170 positions: 1 -> 6 splits)."""
     L = capi.lib()
-    max_seq, theta = 96, 10000.0
+    steps = 170 if splits == 8 else 70
+    max_seq, theta = (192 if splits == 8 else 96), 10000.0
     rng = np.random.Generator(np.random.PCG64(hd + n_heads))
     cos, sin = lo.rope_tables(hd, max_seq, theta)
     kc = torch.zeros((n_kv, max_seq, hd), dtype=torch.bfloat16, device="cuda")
@@ -127,7 +131,7 @@ def test_attention_decode_against_numpy(capi, hd, n_heads, n_kv, splits):
     group = n_heads // n_kv
     cosd, sind = _dev(cos), _dev(sin)
     qkvd = torch.zeros((n_heads + 2 * n_kv) * hd, dtype=torch.float32, device="cuda")
-    for t in range(70):
+    for t in range(steps):
         qkv = rng.normal(size=(n_heads + 2 * n_kv) * hd).astype(np.float32)
         pos.fill_(t)
         qkvd.copy_(torch.from_numpy(qkv))
@@ -144,14 +148,14 @@ def test_attention_decode_against_numpy(capi, hd, n_heads, n_kv, splits):
             sc = (kc_ref[h // group, : t + 1].astype(np.float64) @ q[h].astype(np.float64)) / np.sqrt(hd)
             p = np.exp(sc - sc.max())
             want[h] = (p / p.sum()) @ vc_ref[h // group, : t + 1].astype(np.float64)
-        if t in (0, 1, 7, 8, 31, 32, 33, 63, 64, 69):
+        if t in (0, 1, 7, 8, 31, 32, 33, 63, 64, 69, 95, 96, 127, 128, 159, 160, 169):
             np.testing.assert_allclose(out.cpu().numpy().reshape(n_heads, hd), want, rtol=2e-4, atol=2e-5)
     # the cache holds the bf16-rounded rotated keys (the GPU contracts x*c - y*s into an FMA, so a value
     # on a rounding boundary may land on the neighbouring bf16: at most 1 ulp, a handful of elements)
-    got_bits = kc[:, :70].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
-    worst, ndiff = orc.max_ulp_diff_bf16(got_bits, orc.to_bf16_bits(kc_ref[:, :70]))
+    got_bits = kc[:, :steps].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    worst, ndiff = orc.max_ulp_diff_bf16(got_bits, orc.to_bf16_bits(kc_ref[:, :steps]))
     assert worst <= 1 and ndiff <= got_bits.size // 1000 + 1
-    np.testing.assert_array_equal(vc.float().cpu().numpy()[:, :70], vc_ref[:, :70])
+    np.testing.assert_array_equal(vc.float().cpu().numpy()[:, :steps], vc_ref[:, :steps])
     assert int(tickets.sum().item()) == 0                                              # tickets reset for graph replay
 
 

@@ -114,12 +114,14 @@ def test_split_attention_and_pdl_do_not_change_results(llama, forward_mode):
 
     forced = np.random.Generator(np.random.PCG64(13)).integers(0, 512, 24)
     outs = []
+    # 80 positions: the kernel uses up to ceil(80 / 32) = 3 of the grid's splits, so the split runs really split
+    forced = np.random.Generator(np.random.PCG64(13)).integers(0, 512, 80)
     for splits, pdl in ((1, 1), (3, 1), (1, 0), (5, 0)):
         _capi.check(_capi.lib().af_set_pdl(pdl))
-        eng = llama.LlamaEngine(llama.preset("tiny", max_seq=40, attn_splits=splits, forward_mode=forward_mode), init="host")
+        eng = llama.LlamaEngine(llama.preset("tiny", max_seq=96, attn_splits=splits, forward_mode=forward_mode), init="host")
         eng.reset(forced=forced)
         logits = []
-        for _ in range(24):
+        for _ in range(80):
             eng.decode_step()
             logits.append(eng.logits.cpu().numpy().copy())
         outs.append((eng.tokens(), np.stack(logits)))
