@@ -89,6 +89,12 @@ def cpu_sample(cfg_kw: dict, budget_s: float = 15.0, max_layers: int | None = No
     return t_total / done * L, done, orc.num_threads()
 
 
+def workload_name(args, cfg_kw) -> str:
+    """config.workload — the same string on both arms, so the driver compares like with like."""
+    return (f"{args.workload}: Llama-shaped bf16, {cfg_kw['experts']} experts rank {cfg_kw['rank']} top-{cfg_kw['top_k']} "
+            f"on q/k/v/o/gate/up/down, bs=1 decode, teacher-forced tokens, switch every token ({args.switch_mode})")
+
+
 def run_reference_arm(args, cfg_kw):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -106,7 +112,7 @@ def run_reference_arm(args, cfg_kw):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16 storage, f32 accumulate", "data": "synthetic",
-        "config": {"workload": args.workload, "note": "CPU port of the reference algorithm (oracle/liboracle.so, OpenMP); "
+        "config": {"workload": workload_name(args, cfg_kw), "parallelism": f"tp{args.gpus}", "note": "CPU port of the reference algorithm (oracle/liboracle.so, OpenMP); "
                    "the reference package itself is pure Python and is not present on the GPU box"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -400,8 +406,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16 storage, f32 accumulate", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: Llama-shaped bf16, {cfg.experts} experts rank {cfg.rank} top-{cfg.top_k} on q/k/v/o/gate/up/down, "
-                               f"bs=1 decode, teacher-forced tokens, switch every token ({cfg.switch_mode})",
+        "config": {"workload": workload_name(args, cfg_kw),
                    "parallelism": f"tp{world}", "l2": "inputs larger than L2 (weights 13 GB >> 126 MB), no flush needed",
                    "segments": info["n_segments"], "work_units": info["n_units"], "compute": args.compute,
                    "forward_mode": "chase (GEMV fused into the switch: W read and written once per token)" if chase
