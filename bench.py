@@ -62,6 +62,7 @@ def cpu_sample(cfg_kw: dict, budget_s: float = 15.0, max_layers: int | None = No
     backbone GEMVs.  Returns (seconds per token extrapolated to all layers, layers timed, threads)."""
     from oracle import oracle as orc
 
+    orc.set_num_threads(len(os.sched_getaffinity(0)))   # all host cores, also under torchrun (OMP_NUM_THREADS=1 there)
     d, ffn, L = cfg_kw["hidden"], cfg_kw["ffn"], cfg_kw["layers"]
     hd = d // cfg_kw["n_heads"]
     kv = cfg_kw["n_kv_heads"] * hd
@@ -198,9 +199,17 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # AF_DIST_BACKEND=gloo with AF_SHARE_DEVICE=1 is the one-GPU rehearsal of the N > 1 path (every rank on cuda:0,
+    # collectives staged through the host): it checks the plumbing, its timings mean nothing.
+    backend = os.environ.get("AF_DIST_BACKEND", "nccl")
+    if os.environ.get("AF_SHARE_DEVICE") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -433,7 +442,10 @@ def main():
                     out["roofline"]["traffic_per_token"] = tr.get("dram_bytes_per_token")
         except (OSError, ValueError):
             pass
-    if not args.no_cpu_baseline:
+    if world > 1:
+        out["roofline"]["traffic"] = None   # the ncu capture is of the one-GPU launch, not of a shard's
+        out["roofline"].pop("traffic_per_token", None)
+    if not args.no_cpu_baseline and world == 1:
         sec_per_token, layers_timed, threads = cpu_sample(cfg_kw, budget_s=15.0)
         out["cpu_baseline"] = {
             "value": 1.0 / sec_per_token, "unit": UNIT, "cores": threads, "kind": "port",

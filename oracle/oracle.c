@@ -77,6 +77,15 @@ int orc_num_threads(void) {
 #endif
 }
 
+/* torchrun exports OMP_NUM_THREADS=1 to its workers; the timed baseline asks for the host's cores explicitly. */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* --------------------------------------------------------------- router --- */
 
 /* routing.py:49-78 `route` (== `pre_gate`, routing.py:81-89).

@@ -7,6 +7,7 @@ Two anchors:
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -217,3 +218,19 @@ class TestBf16Helpers:
         b[0] += 1
         b[3] -= 2
         assert orc.max_ulp_diff_bf16(a, b) == (2, 2)
+
+
+def test_oracle_thread_override_under_torchrun_env():
+    """torchrun exports OMP_NUM_THREADS=1; the timed baseline (bench.py cpu_sample) must still get
+    the host's cores by asking for them explicitly."""
+    import subprocess
+    import sys
+
+    code = ("from oracle import oracle as o\n"
+            "assert o.num_threads() == 1, o.num_threads()\n"
+            "o.set_num_threads(4)\n"
+            "assert o.num_threads() == 4, o.num_threads()\n")
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
