@@ -407,3 +407,43 @@ def test_switch_in_passes_for_more_than_64_stacked_ranks(llama, switch_mode, for
     many.finalize()
     assert many.max_backbone_deviation() < 0.05 and one.max_backbone_deviation() < 0.05
 
+
+
+@pytest.mark.parametrize("forward_mode", ["separate", "chase"])
+def test_tp_two_processes_over_torch_distributed(llama, forward_mode, tmp_path):
+    """The lockstep test above with real processes and the engine's own exchange layer: two ranks launched
+    by torch.distributed.run, `llama.Collectives` over a gloo group (both ranks on cuda:0 — one GPU here;
+    NCCL carries the same calls on a multi-GPU box), decode the unsharded engine's tokens."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    tp = 2
+    forced = np.random.Generator(np.random.PCG64(31)).integers(0, 512, 8)
+    full = llama.LlamaEngine(llama.preset("tiny", forward_mode="separate", max_seq=16, n_heads=4, n_kv_heads=4), init="host")
+    full.reset(forced=forced)
+    want_tokens, want_logits = [], []
+    for _ in range(len(forced)):
+        want_tokens.append(int(full.decode_step()))
+        want_logits.append(full.logits.float().cpu().numpy().copy())
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_tp_worker.py")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={tp}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), worker, str(tmp_path), forward_mode],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-4000:]
+    ranks = [np.load(tmp_path / f"rank{k}.npz") for k in range(tp)]
+    tol = 2e-3 if forward_mode == "separate" else 4e-3
+    for k in range(tp):
+        assert ranks[k]["tokens"].tolist() == ranks[0]["tokens"].tolist(), f"rank {k}"
+        assert float(ranks[k]["deviation"]) < 0.02
+    for step in range(len(forced)):
+        got = np.concatenate([ranks[k]["logits"][step] for k in range(tp)])
+        scale = np.abs(want_logits[step]).max()
+        assert np.abs(got - want_logits[step]).max() <= tol * scale, f"step {step}"
+        top2 = np.sort(want_logits[step])[-2:]
+        if top2[1] - top2[0] > 4 * tol * scale:
+            assert int(ranks[0]["tokens"][step]) == want_tokens[step], f"step {step}"
