@@ -571,9 +571,21 @@ __global__ void __launch_bounds__(1024) argmax_val_kernel(const float* __restric
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     float best = -INFINITY;
     int best_i = 0x7fffffff;
-    for (int i = tid; i < n; i += blockDim.x) {
-        const float x = v[i];
-        if (best_i == 0x7fffffff || x > best) { best = x; best_i = i; }
+    // 8 loads in flight per thread (one load per iteration is a chain of L2 round trips: 32 of them at 32000 entries);
+    // a thread's indices ascend, so the strict > keeps the lowest index among equal values
+    constexpr int kFly = 8;
+    for (int base = tid; base < n; base += kFly * blockDim.x) {
+        float x[kFly];
+#pragma unroll
+        for (int u = 0; u < kFly; ++u) {
+            const int i = base + u * blockDim.x;
+            x[u] = i < n ? v[i] : -INFINITY;
+        }
+#pragma unroll
+        for (int u = 0; u < kFly; ++u) {
+            const int i = base + u * blockDim.x;
+            if (i < n && (best_i == 0x7fffffff || x[u] > best)) { best = x[u]; best_i = i; }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
