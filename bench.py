@@ -309,7 +309,7 @@ def main():
         fused_ms = [sum(per_launch[i * n_per_step:(i + 1) * n_per_step]) for i in range(n_roof)]   # per token
 
     # ---------------- (2) value: inputs resident, the step replayed as one CUDA graph ----
-    graph_ok = world == 1
+    graph_ok = world == 1 or os.environ.get("AF_TP_GRAPH") == "1"   # TP capture is opt-in (llama.LlamaEngine.capture)
     if graph_ok:
         eng.capture()
         for _ in range(args.warmup):

@@ -240,7 +240,7 @@ class Collectives:
         if self.tp_size == 1:
             return
         pair = torch.stack([val.view(1), idx.view(1).to(torch.float32)], dim=1)  # idx < 2^24 is exact in f32
-        gathered = [torch.empty_like(pair) for _ in range(self.tp_size)]
+        gathered = [torch.empty_like(pair) for _ in range(self.dist.get_world_size(self.group))]
         self.dist.all_gather(gathered, pair, group=self.group)
         allp = torch.cat(gathered, dim=0)
         best = torch.max(allp[:, 0])
@@ -643,8 +643,11 @@ class LlamaEngine:
         """Capture the steady-state step (switch with a previous decision) as a CUDA graph."""
         if not self.have_prev and self.cfg.adapters and self.cfg.switch_mode == "inplace":
             raise StateError("run one eager decode_step first: the steady graph unmerges a previous decision")
-        if self.cfg.tp_size > 1:
-            raise StateError("graph capture is single-rank; TP steps run eagerly")
+        if self.cfg.tp_size > 1 and os.environ.get("AF_TP_GRAPH") != "1":
+            # torch's NCCL collectives can be captured (each rank captures its own graph after eager warm-up steps
+            # have created the communicator); verified here only on a one-rank NCCL group
+            # (tests/test_gpu_llama.py::test_tp_step_with_nccl_collectives_captures), hence opt-in
+            raise StateError("TP steps run eagerly unless AF_TP_GRAPH=1")
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()

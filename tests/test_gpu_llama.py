@@ -447,3 +447,21 @@ def test_tp_two_processes_over_torch_distributed(llama, forward_mode, tmp_path):
         top2 = np.sort(want_logits[step])[-2:]
         if top2[1] - top2[0] > 4 * tol * scale:
             assert int(ranks[0]["tokens"][step]) == want_tokens[step], f"step {step}"
+
+
+@pytest.mark.parametrize("forward_mode", ["separate", "chase"])
+def test_tp_step_with_nccl_collectives_captures(forward_mode):
+    """A TP shard's step — the engine's collectives on torch's NCCL process group — captured as a CUDA graph
+    (opt-in, AF_TP_GRAPH=1) replays to the eager step's tokens and weights.  One-rank NCCL group (one GPU
+    here): the capture mechanics, not the exchange, are what this covers."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_tp_graph_worker.py")
+    r = subprocess.run([sys.executable, worker, forward_mode, str(port)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "TP_GRAPH_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
