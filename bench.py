@@ -12,9 +12,10 @@ over the KV cache), lm_head and argmax.  Two schedules of the same arithmetic:
 
   value        tokens/s with every per-step input already in HBM (forced token stream on the
                device, the step replayed as one CUDA graph), max over ranks.
-  e2e          the same metric through the public API `LlamaEngine.decode_step(token)`: the
-               consumed token comes from pinned host memory every step (4 B H2D) and the next
-               token is read back (4 B D2H).
+  e2e          the same metric through the public API, verbatim: `eng.decode_step(token)` per step --
+               the consumed token goes up from pinned host memory (4 B H2D), the next token and the
+               step's status word come back (8 B D2H).
+  context      both are timed with `--context` (default 1024) positions already in the KV cache.
   roofline     the fused-switch kernel (chase: its 4 x L launches per token, switch + GEMV):
                algorithmic bytes / launch duration by CUDA events on the launching
                stream -- separate: inside the e2e timed region; chase: in extra e2e steps right
@@ -24,7 +25,9 @@ over the KV cache), lm_head and argmax.  Two schedules of the same arithmetic:
                box's host cores on a bounded sample (whole layers), scaled to tokens/s.
 
 `--impl reference` times that CPU port alone (the reference itself is pure Python and does not
-exist on the GPU box).
+exist on the GPU box): every step is one whole token -- all layers -- when K + W such
+steps fit in ~4 minutes, otherwise a bounded sample of layers, and `ms_per_step` is what a step
+really took (`value` is then scaled to all layers; `cpu_baseline.sample` says so).
 """
 
 from __future__ import annotations
@@ -56,6 +59,9 @@ def load_peaks():
 # ------------------------------------------------------------------ CPU arm ----
 
 
+_CPU_SEGS: dict = {}
+
+
 def cpu_sample(cfg_kw: dict, budget_s: float = 15.0, max_layers: int | None = None):
     """Time the oracle port (reference algorithm, f32 arithmetic on bf16 weights) on whole
     layers of the workload: per layer the steady switch of its 7 matrices (s = 2kr) and the 7
@@ -68,18 +74,22 @@ def cpu_sample(cfg_kw: dict, budget_s: float = 15.0, max_layers: int | None = No
     kv = cfg_kw["n_kv_heads"] * hd
     n, r, k = cfg_kw["experts"], cfg_kw["rank"], cfg_kw["top_k"]
     shapes = [(d, d), (kv, d), (kv, d), (d, d), (ffn, d), (ffn, d), (d, ffn)]
-    rng = np.random.Generator(np.random.PCG64(0))
-    segs = []
-    for d_out, d_in in shapes:
-        w = orc.to_bf16_bits((rng.random((d_out, d_in), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(d_in)))
-        dn = orc.to_bf16_bits((rng.random((n, r, d_in), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(d_in)))
-        up = orc.to_bf16_bits((rng.random((n, d_out, r), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(r)))
-        segs.append((w, dn, up, rng.random(d_in, dtype=np.float32)))
+    key = (d, ffn, kv, n, r)
+    if _CPU_SEGS.get("key") != key:          # one layer's worth of synthetic matrices, built once (not inside any timed step)
+        rng = np.random.Generator(np.random.PCG64(0))
+        segs = []
+        for d_out, d_in in shapes:
+            w = orc.to_bf16_bits((rng.random((d_out, d_in), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(d_in)))
+            dn = orc.to_bf16_bits((rng.random((n, r, d_in), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(d_in)))
+            up = orc.to_bf16_bits((rng.random((n, d_out, r), dtype=np.float32) - 0.5) * (2.0 / np.sqrt(r)))
+            segs.append((w, dn, up, rng.random(d_in, dtype=np.float32)))
+        _CPU_SEGS.update(key=key, segs=segs)
+    segs = _CPU_SEGS["segs"]
     prev = (tuple(range(k)), tuple([1.0 / k] * k))
     cur = (tuple(range(k, 2 * k)), tuple([1.0 / k] * k))
     done, t_total = 0, 0.0
     cap = max_layers or L
-    while done < cap and (done == 0 or t_total + t_total / done <= budget_s):
+    while done < cap and (done == 0 or t_total + t_total / done <= budget_s):   # at least one layer, then as the budget allows
         t0 = time.perf_counter()
         for w, dn, up, x in segs:
             orc.switch_segment_bf16(w, dn, up, prev, cur)
@@ -96,25 +106,45 @@ def workload_name(args, cfg_kw) -> str:
             f"on q/k/v/o/gate/up/down, bs=1 decode, teacher-forced tokens, switch every token ({args.switch_mode})")
 
 
+def workload_config(args, cfg_kw, world) -> dict:
+    """The `config` object: what is computed, identical on both arms (how it is computed goes to `impl_config`)."""
+    return {"workload": workload_name(args, cfg_kw), "parallelism": f"tp{world}", "context_positions": args.context,
+            "switch_mode": args.switch_mode, "refresh_every": args.refresh_every,
+            "l2": "inputs larger than L2 (weights >= 13 GB >> 126 MB), no flush needed"}
+
+
 def run_reference_arm(args, cfg_kw):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    per_step_budget = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
-    vals, layers_timed, threads = [], 0, 1
-    for i in range(args.warmup + args.steps):
-        sec_per_token, layers_timed, threads = cpu_sample(cfg_kw, budget_s=per_step_budget, max_layers=4)
+    L = cfg_kw["layers"]
+    # one probe layer sizes the steps: whole tokens when W + K of them fit in ~4 minutes, else a bounded sample of layers
+    probe, _, threads = cpu_sample(cfg_kw, budget_s=0.0, max_layers=1)
+    n = args.warmup + args.steps
+    per_layer = probe / L
+    layers_per_step = int(max(1, min(L, 240.0 / max(1, n) / max(per_layer, 1e-9))))
+    vals, walls = [], []
+    for i in range(n):
+        t0 = time.perf_counter()
+        sec_per_token, layers_timed, threads = cpu_sample(cfg_kw, budget_s=1e9, max_layers=layers_per_step)
+        wall = time.perf_counter() - t0
         if i >= args.warmup:
             vals.append(sec_per_token)
+            walls.append(wall)
     sec = statistics.mean(vals)
     v = 1.0 / sec
-    sample = f"{layers_timed} of {cfg_kw['layers']} layers per step (steady switch s=2kr + 7 GEMVs each), scaled to all layers"
+    whole = layers_per_step == L
+    sample = (f"every step is one whole token: all {L} layers (steady switch s=2kr + 7 GEMVs each; attention and lm_head not included)"
+              if whole else
+              f"{layers_per_step} of {L} layers per step (steady switch s=2kr + 7 GEMVs each), value scaled to all layers; "
+              f"ms_per_step is the time of the sampled layers")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16 storage, f32 accumulate", "data": "synthetic",
-        "config": {"workload": workload_name(args, cfg_kw), "parallelism": f"tp{args.gpus}", "note": "CPU port of the reference algorithm (oracle/liboracle.so, OpenMP); "
-                   "the reference package itself is pure Python and is not present on the GPU box"},
+        "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3, "ms_per_token": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16 storage, f32 accumulate", "data": "synthetic",
+        "config": workload_config(args, cfg_kw, args.gpus),
+        "impl_config": {"note": "CPU port of the reference algorithm (oracle/liboracle.so, OpenMP, all host cores); "
+                                "the reference package itself is pure Python and is not present on the GPU box"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -179,6 +209,10 @@ def main():
     ap.add_argument("--no-chain", action="store_true", help="chase: one launch per projection instead of chained phases")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--attn-splits", type=int, default=0, help="KV splits of the decode attention (0 = the engine's choice)")
+    ap.add_argument("--context", type=int, default=1024, help="positions already in the KV cache when the timed regions start")
+    ap.add_argument("--refresh-every", type=int, default=16,
+                    help="in-place mode: rebuild W from the pristine copy every N tokens (reference model.py:344-349; folded into "
+                         "that token's switch launch, 0 = never)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -216,11 +250,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    max_seq = 2 * (args.steps + args.warmup) + 16
-    max_seq += 16  # roofline pass of the chase schedule
+    max_seq = args.context + 3 * (args.steps + args.warmup) + 64
     cfg = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
                        compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain,
-                       attn_splits=args.attn_splits)
+                       attn_splits=args.attn_splits, refresh_every=args.refresh_every)
     eng = llama.LlamaEngine(cfg, init="device")
     info = eng.table.info()
     forced = np.random.Generator(np.random.PCG64(cfg.seed + 1)).integers(0, cfg.vocab, 4096)
@@ -242,16 +275,16 @@ def main():
             ms = float(t.item())
         return ms
 
-    # ---------------- (1) e2e: public API, host token in / next token out, eager launches ----
+    # ---------------- (1) e2e: the public API verbatim -- eng.decode_step(token): host token in, next token + status out ----
     eng.reset(forced=forced)
-    pinned = torch.from_numpy(forced.astype(np.int32)).pin_memory()
+    host_tokens = [int(t) for t in forced]
     switch_events = []
     orig_switch = eng._switch_for_step
 
-    def instrumented_switch(with_prev):
+    def instrumented_switch(with_prev, refresh=False):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        orig_switch(with_prev)
+        orig_switch(with_prev, refresh)
         b.record()
         switch_events.append((a, b))
 
@@ -259,16 +292,20 @@ def main():
 
     def api_step():
         i = step_i[0]
-        eng.token_dev.copy_(pinned[i:i + 1], non_blocking=True)      # H2D of the step's input
-        eng._step_body(eng.have_prev)
-        eng.have_prev = True
-        _ = int(eng.next_dev.item())                                   # D2H of the step's result
+        eng.decode_step(host_tokens[i % len(host_tokens)])            # 4 B H2D, the whole step, 8 B D2H (token + status word)
         step_i[0] = i + 1
 
+    api_step()                                                         # first merge (no previous decision yet)
+    eng.set_position(args.context)                                     # the timed steps attend over >= `context` cached positions
     for _ in range(args.warmup):
         api_step()
-    eng._switch_for_step = instrumented_switch
+    if not eng.chase:
+        eng.auto_graph = False          # separate schedule: the timed steps carry events around the switch launch
+        eng._switch_for_step = instrumented_switch
+    # kernels launched per step, counted on one eagerly launched step (the timed steps replay exactly these as a graph)
     launches0 = _capi.launch_count()
+    eng.decode_step(host_tokens[0], graph=False)
+    step_launches = _capi.launch_count() - launches0
     sampler = ClockSampler(local_rank)
     profiling = bool(os.environ.get("AF_NCU"))   # `ncu --profile-from-start off`: profile the timed region only
     if profiling:
@@ -276,7 +313,6 @@ def main():
     e2e_ms = timed(api_step, args.steps)
     if profiling:
         torch.cuda.profiler.stop()
-    launches_e2e = _capi.launch_count() - launches0
     eng._switch_for_step = orig_switch
     e2e_value = args.steps / (e2e_ms / 1e3)
     chase = eng.chase
@@ -299,33 +335,39 @@ def main():
             fused_events.append((e0, e1))
 
         SegmentGroup.switch_gemv_chain = instrumented_sg
+        eng.auto_graph = False          # eager launches: events around every fused launch
         n_roof = 4
         for _ in range(n_roof):
             api_step()
         torch.cuda.synchronize()
+        eng.auto_graph = True
         SegmentGroup.switch_gemv_chain = orig_sg
         per_launch = [a.elapsed_time(b) for a, b in fused_events]
         n_per_step = len(per_launch) // n_roof
         fused_ms = [sum(per_launch[i * n_per_step:(i + 1) * n_per_step]) for i in range(n_roof)]   # per token
 
+    kernel_name = _capi.lib().af_last_switch_kernel().decode()
     # ---------------- (2) value: inputs resident, the step replayed as one CUDA graph ----
     graph_ok = world == 1 or os.environ.get("AF_TP_GRAPH") == "1"   # TP capture is opt-in (llama.LlamaEngine.capture)
+    eng.set_position(args.context)
     if graph_ok:
         eng.capture()
         for _ in range(args.warmup):
             eng.replay()
         dev_ms = timed(eng.replay, args.steps)
-        launches_per_step = launches_e2e // args.steps
+        launches_per_step = step_launches
     else:
         def dev_step():
-            eng._step_body(True)
+            refresh = eng._refresh_due()
+            eng._step_body(not refresh, refresh)
+            eng._stepped()
         for _ in range(args.warmup):
             dev_step()
         dev_ms = timed(dev_step, args.steps)
-        launches_per_step = launches_e2e // args.steps
+        launches_per_step = step_launches
     clocks = sampler.stop()
     value = args.steps / (dev_ms / 1e3)
-    eng.table.status()
+    eng.check()
 
     # ---------------- (3) the adapter-free backbone with the same kernels (decode only) ----
     def decode_only():
@@ -340,14 +382,14 @@ def main():
             with torch.cuda.graph(g, stream=side):
                 decode_only()
         torch.cuda.current_stream().wait_stream(side)
-        eng.pos_dev.fill_(8)
+        eng.set_position(args.context)
         for _ in range(3):
             g.replay()
-        eng.pos_dev.fill_(8)
+        eng.set_position(args.context)
         dec_ms = timed(g.replay, min(args.steps, 30))
         dec_n = min(args.steps, 30)
     else:
-        eng.pos_dev.fill_(8)
+        eng.set_position(args.context)
         dec_n = min(args.steps, 30)
         dec_ms = timed(decode_only, dec_n)
     decode_only_tok_s = dec_n / (dec_ms / 1e3)
@@ -402,26 +444,29 @@ def main():
         n_launch = n_per_step
         roof_ms = statistics.mean(fused_ms)
         roof_achieved = sw_bytes / (roof_ms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "switch_mma_kernel<GEMV> (fused switch + GEMV; " + ("chained: o -> gate|up -> down -> next q|k|v per launch)" if eng.chase_chained else "one launch per projection)"),
+        roofline = {"bound": "hbm", "kernel": kernel_name + " -- fused switch + GEMV; " + ("chained: o -> gate|up -> down -> next q|k|v per launch" if eng.chase_chained else "one launch per projection"),
                     "achieved": roof_achieved, "peak": peak, "unit": "GB/s", "frac": roof_achieved / peak,
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)", "launches_per_token": n_launch,
                     "bytes_per_launch": sw_bytes / n_launch, "avg_launch_ms": roof_ms / n_launch,
                     "bytes_per_token": sw_bytes, "ms_per_token": roof_ms, "min_ms_per_token": min(fused_ms), "traffic": None}
     else:
-        roofline = {"bound": "hbm", "kernel": "switch_mma_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        roofline = {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                     "bytes_per_launch": sw_bytes, "avg_launch_ms": switch_ms, "min_launch_ms": min(sw_ms), "traffic": None}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16 storage, f32 accumulate", "data": "synthetic",
-        "config": {"workload": workload_name(args, cfg_kw),
-                   "parallelism": f"tp{world}", "l2": "inputs larger than L2 (weights 13 GB >> 126 MB), no flush needed",
-                   "segments": info["n_segments"], "work_units": info["n_units"], "compute": args.compute,
-                   "forward_mode": "chase (GEMV fused into the switch: W read and written once per token)" if chase
-                   else "separate (one switch launch, then plain GEMVs)"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4,
-                "ms_per_step": e2e_ms / args.steps},
+        "config": workload_config(args, cfg_kw, world),
+        "impl_config": {"segments": info["n_segments"], "work_units": info["n_units"], "compute": args.compute,
+                        "forward_mode": "chase (GEMV fused into the switch: W read and written once per token)" if chase
+                        else "separate (one switch launch, then plain GEMVs)",
+                        "refresh": "every %d-th token switches from the pristine copy (same bytes, same launch)" % eng.refresh_every
+                        if eng.refresh_every else "none"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 8,
+                "ms_per_step": e2e_ms / args.steps,
+                "api": "LlamaEngine.decode_step(token): pinned H2D of the token, the step (a CUDA graph replay from the second token on), "
+                       "one pinned D2H of next token + status word"},
         "gpu_launches": int(launches_per_step * args.steps),
         "launches_per_step": int(launches_per_step),
         "clocks": clocks,
@@ -429,6 +474,14 @@ def main():
         "switch_hbm_gbs": achieved,
         "decode_only_tok_s": decode_only_tok_s,
         "decode_only_hbm_gbs": cfg.decode_bytes() * decode_only_tok_s / 1e9,
+        "decode_only": {"bound": "hbm", "kernel": "gemv_chain_kernel (adapter-free backbone, same attention / lm_head kernels)",
+                        "achieved": cfg.decode_bytes() * decode_only_tok_s / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": cfg.decode_bytes() * decode_only_tok_s / 1e9 / peak, "bytes_per_token": cfg.decode_bytes(),
+                        "value_over_decode_only": value / decode_only_tok_s,
+                        "bound_note": "a token that switches moves every weight twice (read + write back, 2W) where the adapter-free "
+                                      "forward reads it once (1W): switch-every-token decode is bounded at %.3f of decode_only by bytes alone; "
+                                      "north_star's 'within 10 %% of the adapter-free backbone' is reachable only for steps that keep the "
+                                      "previous selection (no bytes written)" % (cfg.decode_bytes() / cfg.switch_bytes(steady=True))},
         "box_hbm_copy_gbs": box_copy,
         "roofline": roofline,
     }

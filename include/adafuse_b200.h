@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define AF_ABI_VERSION 2
+#define AF_ABI_VERSION 3
 
 /* ---- status codes: one per reference exception class (errors.py:8-33) ---- */
 #define AF_OK 0
@@ -99,6 +99,9 @@ const char* af_last_error(void);
 int af_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_bytes);
 /* Number of kernel launches issued by this library since load (bench `gpu_launches`). */
 int64_t af_launch_count(void);
+/* Name (template arguments included) of the switch kernel the calling thread's last af_fused_switch /
+ * af_merge / af_unmerge / af_sgmm / af_switch_gemv[_chain] call launched -- what a benchmark reports. */
+const char* af_last_switch_kernel(void);
 /* Programmatic dependent launch of the decode GEMV / attention chain (default on; the
  * environment variable AF_PDL=0 turns it off at load).  With it, a GEMV prefetches its first
  * weight tiles while the previous kernel of the stream is still draining. */
@@ -135,6 +138,15 @@ int af_table_info(const af_table* table, int32_t* n_segments, int64_t* target_el
  * expert outside the bank (adapters.py:199-200) or carried more than max_k experts; the
  * offending launch touched nothing.  Reading clears the flag. */
 int af_table_status(af_table* table, void* stream);
+/* Asynchronous form of the same check, for callers that already read something back every step
+ * (model.py:396: the next token): the table's kernels raise into `word_dev` -- a caller-owned,
+ * zero-initialised int32 in device memory (NULL: back to the table's own word) -- so that ONE
+ * device-to-host copy returns the step's result and its status together.  The word is sticky
+ * until the caller clears it; af_flag_message names a raised code.  Codes: AF_EINDEX / AF_EVALUE
+ * (unusable device decision, adapters.py:199-200), AF_ECUDA (a chained launch gave up at a phase
+ * barrier), AF_ESTATE (KV cache full). */
+int af_table_set_error_word(af_table* table, int32_t* word_dev);
+const char* af_flag_message(int32_t flag);
 
 /* ---- pre-gating router --------------------------------------------------------------
  * Replaces: routing.py:49-78 `route` / routing.py:81-89 `pre_gate`, fused with the row
@@ -232,7 +244,9 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
  *    weights of every phase stream through one shared-memory ring without stopping at a phase
  *    boundary; only the consumers wait there (phase_done_dev: n_phases - 1 int32 counters, zeroed by
  *    the caller).  Same arithmetic contract as af_gemv_fused per phase; a row is summed by one warp
- *    in a fixed order.  The launch is one CTA per SM, all co-resident. */
+ *    in a fixed order.  The launch is one CTA per SM, all co-resident; a CTA that waits ~2 s at a
+ *    phase barrier raises AF_ECUDA in *err_flag_dev (may be NULL) and every CTA stops waiting, so a
+ *    lost CTA ends the launch with an error instead of a hang or silently wrong outputs. */
 typedef struct af_gv_phase {
     const void* w;       /* rows x cols bf16, row pitch ld                                  */
     int32_t rows, cols;
@@ -244,8 +258,8 @@ typedef struct af_gv_phase {
     float eps;
     int32_t prologue, epilogue;
 } af_gv_phase;
-int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t pdl,
-                  void* stream);
+int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev,
+                  int32_t* err_flag_dev, int32_t pdl, void* stream);
 int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table,
                    const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
                    int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # AF_LIB_PATH: an alternative build of the same library (kernel-variant A/B runs on one box)
 LIB_PATH = os.environ.get("AF_LIB_PATH") or os.path.join(HERE, "libadafuse_b200.so")
 
-AF_ABI_VERSION = 2
+AF_ABI_VERSION = 3
 AF_OK, AF_EVALUE, AF_EDIM, AF_EPRECISION, AF_EALIAS, AF_EINPUT, AF_ESTATE, AF_EINDEX, AF_ECUDA = range(9)
 AF_BF16, AF_F32 = 0, 1
 AF_SWITCH_INPLACE, AF_SWITCH_FROM_PRISTINE = 0, 1
@@ -116,6 +116,7 @@ SIGNATURES = {
     "af_last_error": (ctypes.c_char_p, []),
     "af_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 3 + [ctypes.POINTER(_i64)]),
     "af_launch_count": (_i64, []),
+    "af_last_switch_kernel": (ctypes.c_char_p, []),
     "af_set_pdl": (ctypes.c_int, [_i32]),
     "af_set_gemv_variant": (ctypes.c_int, [_i32, _i32]),
     "af_set_umma": (ctypes.c_int, [_i32]),
@@ -123,6 +124,8 @@ SIGNATURES = {
     "af_table_destroy": (ctypes.c_int, [_vp]),
     "af_table_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "af_table_status": (ctypes.c_int, [_vp, _vp]),
+    "af_table_set_error_word": (ctypes.c_int, [_vp, _vp]),
+    "af_flag_message": (ctypes.c_char_p, [_i32]),
     "af_pregate": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp, _vp]),
     "af_fused_switch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.POINTER(Decision), ctypes.POINTER(Decision), _i32, _f32, _i32, _i32, _vp]),
     "af_merge": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(Decision), _i32, _f32, _i32, _vp]),
@@ -144,7 +147,7 @@ SIGNATURES = {
     "af_group_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
     "af_switch_gemv_chain": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, ctypes.POINTER(GemvPhase), _i32, _vp, _i32, _vp]),
     "af_switch_gemv": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _i32, _vp]),
-    "af_gemv_chain": (ctypes.c_int, [ctypes.POINTER(GvPhase), _i32, _vp, _i32, _vp]),
+    "af_gemv_chain": (ctypes.c_int, [ctypes.POINTER(GvPhase), _i32, _vp, _vp, _i32, _vp]),
     "af_plan_build": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp]),
     "af_set_timeline": (ctypes.c_int, [_vp, _i32, _i64]),
     "af_accum_to_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp]),
@@ -183,6 +186,15 @@ def check(status: int) -> None:
         return
     msg = lib().af_last_error().decode("utf-8", "replace")
     raise _STATUS_TO_EXC.get(status, errors.DeviceError)(msg)
+
+
+def raise_for_flag(flag: int) -> None:
+    """Raise the reference's exception class for a status word a kernel raised on the device
+    (the asynchronous form of `af_table_status`; include/adafuse_b200.h af_table_set_error_word)."""
+    if flag == AF_OK:
+        return
+    msg = lib().af_flag_message(int(flag)).decode("utf-8", "replace")
+    raise _STATUS_TO_EXC.get(int(flag), errors.DeviceError)(msg)
 
 
 def require_cuda():

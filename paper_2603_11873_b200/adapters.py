@@ -273,6 +273,7 @@ class SwitchTable:
         self.factor_itemsize = downs[0].element_size()
         self.device_table = DeviceTable(descs, tprec, fprec, keepalive=(targets, downs, ups, pristine))
         self.n_segments = len(targets)
+        self.device = targets[0].data.device
         self._dev_scalar = None
 
     # -- accounting (identical formulas to linalg.py:293-303) --
@@ -300,7 +301,14 @@ class SwitchTable:
         raise TypeError(f"decision must be a GateDecision, a DeviceDecision or None, got {type(dec).__name__}")
 
     def switch(self, prev, cur, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace", compute: str = "auto") -> None:
-        """W <- W + delta(cur) - delta(prev) on every segment, one launch (model.py:350-357)."""
+        """W <- W + delta(cur) - delta(prev) on every segment, one launch (model.py:350-357).
+
+        Host decisions (`GateDecision`) are validated before anything moves and raise here
+        (IndexError for an expert outside the bank, adapters.py:199-200).  Device decisions
+        (`DeviceDecision`) cannot be read without a synchronisation, so the launch is asynchronous:
+        the kernel validates, touches nothing when the decision is unusable, and raises into the
+        table's status word -- call `status()` (synchronises) at the next point where the host
+        waits anyway; `decode_step` / `generate` / `LlamaEngine.decode_step` do."""
         if mode not in _MODES:
             raise ValueError(f"unknown switch mode {mode!r}")
         if compute not in _capi.COMPUTE_MODES:
@@ -394,7 +402,7 @@ class SwitchTable:
     def max_deviation(self) -> float:
         """model.py:231-236 `max_backbone_deviation` (synchronises)."""
         if self._dev_scalar is None:
-            self._dev_scalar = torch.zeros(1, dtype=torch.float32, device="cuda")
+            self._dev_scalar = torch.zeros(1, dtype=torch.float32, device=self.device)
         _capi.check(_capi.lib().af_max_deviation(self.device_table.handle, _ptr(self._dev_scalar), _capi.stream_ptr()))
         return float(self._dev_scalar.item())
 

@@ -3,6 +3,7 @@
 // caller.  Citations are relative to /root/reference/pkg/src/lorafuse/.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -24,6 +25,12 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 std::atomic<long long> g_launches{0};
+// name of the switch kernel the last switch / switch + GEMV call launched (af_last_switch_kernel: bench.py reports it)
+static thread_local char g_last_switch_kernel[96] = "none";
+static void note_kernel(const char* fmt, int a, int b, int c = -1) {
+    if (c >= 0) snprintf(g_last_switch_kernel, sizeof(g_last_switch_kernel), fmt, a, b, c);
+    else snprintf(g_last_switch_kernel, sizeof(g_last_switch_kernel), fmt, a, b);
+}
 // Programmatic dependent launch for the decode GEMV chain (af_set_pdl; env AF_PDL=0 disables).
 static std::atomic<int> g_pdl{[] {
     const char* e = getenv("AF_PDL");
@@ -51,6 +58,16 @@ static std::atomic<int> g_umma{[] {
     return e ? atoi(e) : 1;
 }()};
 static const bool g_force_hilo = [] { const char* e = getenv("AF_FORCE_HILO"); return e && e[0] == '1'; }();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and occupancy are per DEVICE: what has been configured is
+// remembered per device id, so a second GPU in the same process gets its own attribute call.
+struct PerDevice {
+    int v[64] = {};
+    int& cur() {
+        int d = 0;
+        cudaGetDevice(&d);
+        return v[d & 63];
+    }
+};
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline size_t esize(int dtype) { return dtype == AF_BF16 ? 2 : 4; }
 
@@ -125,6 +142,7 @@ struct af_table {
     int n_units_umma = 0;
     CUtensorMap* d_maps = nullptr;  // [5][n_segments]: fma live, fma pristine, mma live, mma pristine, UP bank (swizzled)
     int* d_err = nullptr;
+    int* err_word = nullptr;        // where the kernels raise: d_err, or a caller-owned word (af_table_set_error_word)
     Plan* d_plan = nullptr;         // af_plan_build target
     bool fast_fma = false, fast_mma = false, has_pristine = false;
     bool rank16 = true;  // every segment's rank is a multiple of 16
@@ -166,6 +184,7 @@ int af_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_byte
 }
 
 int64_t af_launch_count(void) { return g_launches.load(); }
+const char* af_last_switch_kernel(void) { return g_last_switch_kernel; }
 
 int af_set_pdl(int32_t enable) {
     g_pdl.store(enable ? 1 : 0);
@@ -346,6 +365,7 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
         e = cudaMemcpy(t->d_units_umma, units_u.data(), sizeof(UnitDev) * units_u.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&t->d_err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(t->d_err, 0, sizeof(int));
+    t->err_word = t->d_err;
     if (e == cudaSuccess) e = cudaMalloc(&t->d_plan, sizeof(Plan));
     if (e == cudaSuccess) e = cudaMemset(t->d_plan, 0, sizeof(Plan));
     if (e != cudaSuccess) {
@@ -403,15 +423,31 @@ int af_table_info(const af_table* t, int32_t* n_segments, int64_t* target_elems,
     return AF_OK;
 }
 
+const char* af_flag_message(int32_t flag) {
+    switch (flag) {
+        case AF_OK: return "ok";
+        case AF_EINDEX: return "a device decision names an expert outside the bank";
+        case AF_EVALUE: return "a device decision carries more experts than max_k";
+        case AF_ESTATE: return "the KV cache is full (position >= max_seq)";
+        case AF_ECUDA: return "a chained launch timed out at a phase barrier (a CTA of the launch was not co-resident)";
+        default: return "a kernel raised an unknown status";
+    }
+}
+
+int af_table_set_error_word(af_table* t, int32_t* word_dev) {
+    if (!t) return fail(AF_EVALUE, "table is NULL");
+    t->err_word = word_dev ? word_dev : t->d_err;
+    return AF_OK;
+}
+
 int af_table_status(af_table* t, void* stream) {
     if (!t) return fail(AF_EVALUE, "table is NULL");
     int flag = 0;
-    AF_CUDA_TRY(cudaMemcpyAsync(&flag, t->d_err, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream)));
+    AF_CUDA_TRY(cudaMemcpyAsync(&flag, t->err_word, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream)));
     AF_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
     if (flag) {
-        AF_CUDA_TRY(cudaMemsetAsync(t->d_err, 0, sizeof(int), as_stream(stream)));
-        return fail(flag, flag == AF_EINDEX ? "a device decision names an expert outside the bank"
-                                            : "a device decision carries more experts than max_k");
+        AF_CUDA_TRY(cudaMemsetAsync(t->err_word, 0, sizeof(int), as_stream(stream)));
+        return fail(flag, af_flag_message(flag));
     }
     return AF_OK;
 }
@@ -425,10 +461,10 @@ namespace af {
 template <int KS, bool BA, bool GEMV = false, bool TL = false>
 static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     using L = MmaLayout<KS, BA, GEMV>;
-    static bool configured = false;
-    if (!configured) {
+    static PerDevice configured;
+    if (!configured.cur()) {
         AF_CUDA_TRY(cudaFuncSetAttribute(switch_mma_kernel<KS, BA, GEMV, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
-        configured = true;
+        configured.cur() = 1;
     }
     MmaParams mp2 = mp;
     static const int env_stages = [] { const char* e = getenv("AF_MMA_STAGES"); return e ? atoi(e) : 0; }();
@@ -457,6 +493,7 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
         switch_mma_kernel<KS, BA, GEMV, TL><<<grid, kMmaThreads, L::total, st>>>(mp2);
     }
     AF_LAUNCH_CHECK("switch_mma_kernel");
+    note_kernel("switch_mma_kernel<KS=%d,BA=%d,GEMV=%d> (mma.sync)", KS, (int)BA, (int)GEMV);
     return AF_OK;
 }
 
@@ -469,10 +506,10 @@ static const int kUmmaMaxRanksChain = [] { const char* e = getenv("AF_UMMA_MAX_R
 template <int NB, bool GEMV>
 static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
     using L = UmmaLayout<NB, GEMV>;
-    static bool configured = false;
-    if (!configured) {
+    static PerDevice configured;
+    if (!configured.cur()) {
         AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
-        configured = true;
+        configured.cur() = 1;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -486,19 +523,21 @@ static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
     cfg.numAttrs = mp.pdl ? 1 : 0;
     AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV>, mp));
     AF_LAUNCH_CHECK("switch_umma_kernel");
+    note_kernel("switch_umma_kernel<NB=%d,GEMV=%d> (tcgen05 + TMEM)", NB, (int)GEMV);
     return AF_OK;
 }
 
 template <typename FT, bool EXACT, bool F2>
 static int launch_tma(const SwitchParams& p, int grid, cudaStream_t st) {
-    static bool configured = false;
+    static PerDevice configured;
     const int smem = (int)sizeof(SwitchSmem) + 128;
-    if (!configured) {
+    if (!configured.cur()) {
         AF_CUDA_TRY(cudaFuncSetAttribute(switch_tma_kernel<FT, EXACT, F2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured = true;
+        configured.cur() = 1;
     }
     switch_tma_kernel<FT, EXACT, F2><<<grid, kConsumers + 32, smem, st>>>(p);
     AF_LAUNCH_CHECK("switch_tma_kernel");
+    note_kernel("switch_tma_kernel<EXACT=%d,F2=%d> (CUDA cores)", (int)EXACT, (int)F2);
     return AF_OK;
 }
 
@@ -551,7 +590,7 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
     p.use_dev = use_dev ? 1 : 0;
     p.scale = scale;
     p.n_experts_limit = t->min_experts;
-    p.err_flag = t->d_err;
+    p.err_flag = t->err_word;
     int n_blocks_bound;
     if (host_plan_override) {
         p.host_plan = *host_plan_override;
@@ -884,7 +923,7 @@ int af_plan_build(af_table* t, const af_decision* prev_dev, const af_decision* c
     p.use_dev = 1;
     p.scale = scale;
     p.n_experts_limit = t->min_experts;
-    p.err_flag = t->d_err;
+    p.err_flag = t->err_word;
     const int bound = (p.from_pristine || !prev_dev ? 0 : max_k) + (cur_dev ? max_k : 0);
     p.max_blocks = std::min(bound, kMaxBlocks);
     plan_build_kernel<<<1, 32, 0, as_stream(stream)>>>(p, t->d_plan);
@@ -933,7 +972,7 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     p.use_dev = use_dev ? 1 : 0;
     p.scale = scale;
     p.n_experts_limit = t->min_experts;
-    p.err_flag = t->d_err;
+    p.err_flag = t->err_word;
     p.host_plan.n_blocks = 0;  // no decision at all: a plain GEMV over the live weights
     p.plan_dev = (use_dev && (flags & AF_CHAIN_PLAN_PREBUILT)) ? t->d_plan : nullptr;
     const int n_blocks_bound = use_dev ? ((from_pristine || !prev_dev ? 0 : max_k) + (cur_dev ? max_k : 0)) : 0;
@@ -1154,15 +1193,17 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
     if (variant == 0) {
         // register-streamed kernel: even split of the rows over SMs x resident CTAs
         if (xs_bytes + 1024 > di.max_smem_optin) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory");
-        static int configured = 48 * 1024;
-        if (xs_bytes > configured) {
+        static PerDevice configured;
+        if (xs_bytes > std::max(48 * 1024, configured.cur())) {
             AF_CUDA_TRY(cudaFuncSetAttribute(gemv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, xs_bytes));
-            configured = xs_bytes;
+            configured.cur() = xs_bytes;
         }
-        static int occ_smem = -1, occ = 0;
-        if (occ_smem != xs_bytes) {
+        static PerDevice occ_smem_d, occ_d;
+        int& occ_smem = occ_smem_d.cur();
+        int& occ = occ_d.cur();
+        if (occ_smem != xs_bytes + 1) {
             AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_fused_kernel, kGemvFThreads, xs_bytes));
-            occ_smem = xs_bytes;
+            occ_smem = xs_bytes + 1;
         }
         cfg.gridDim = dim3(std::max(1, std::min(rows, di.sm_count * std::max(1, std::min(occ, 8)))));
         cfg.blockDim = dim3(kGemvFThreads);
@@ -1186,10 +1227,10 @@ int af_gemv_fused(const void* w, int32_t rows, int32_t cols, int64_t ld, const f
         cfg.dynamicSmemBytes = smem;
 #define AF_GV_LAUNCH(CH, NP)                                                                                              \
     do {                                                                                                                  \
-        static int configured = 0;                                                                                        \
-        if (smem > configured) {                                                                                          \
+        static PerDevice configured;                                                                                      \
+        if (smem > configured.cur()) {                                                                                    \
             AF_CUDA_TRY(cudaFuncSetAttribute(gemv_tma_kernel<CH, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
-            configured = smem;                                                                                            \
+            configured.cur() = smem;                                                                                      \
         }                                                                                                                 \
         cfg.blockDim = dim3(kGvWarps * 32 + 32 * NP);                                                                     \
         AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_tma_kernel<CH, NP>, wp, (int)rows, (int)cols, (long long)ld, x, out,     \
@@ -1210,7 +1251,8 @@ static int attn_decode_impl(const float* qkv, const long long* qkv_fix, const fl
                             int32_t n_kv_heads, int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,
                             int32_t* tickets, float* out, void* stream);
 
-int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t pdl, void* stream) {
+int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev, int32_t* err_flag_dev, int32_t pdl,
+                  void* stream) {
     if (!phases || n_phases < 1 || n_phases > kGcMaxPhases) return fail(AF_EVALUE, "a GEMV chain has 1..4 phases");
     if (n_phases > 1 && !phase_done_dev) return fail(AF_EVALUE, "a chain of several phases needs its phase_done counters");
     const DeviceInfo& di = device_info();
@@ -1251,16 +1293,16 @@ int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_do
     n_stages = std::min(n_stages, kGcMaxStages);
     if (n_stages < 2) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory next to the weight ring");
     const int smem = n_stages * kGcStage + xs_bytes;
-    static int configured = 0;
-    if (smem > configured) {
+    static PerDevice configured;
+    if (smem > configured.cur()) {
         AF_CUDA_TRY(cudaFuncSetAttribute(gemv_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured = smem;
+        configured.cur() = smem;
     }
     gp.n_phases = n_phases;
     gp.phase_done = phase_done_dev;
     gp.n_stages = n_stages;
     gp.pdl = (pdl && g_pdl.load()) ? 1 : 0;
-    gp.err_flag = nullptr;
+    gp.err_flag = err_flag_dev;
     cudaLaunchConfig_t cfg{};
     // every CTA takes part in the phase barriers: the grid is one CTA per SM, all co-resident
     cfg.gridDim = dim3(di.sm_count);

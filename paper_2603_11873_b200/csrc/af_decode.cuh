@@ -39,6 +39,17 @@ __device__ __forceinline__ void load8<float>(const float* p, float (&f)[8]) {
     f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
 
+// Order of `np.argsort(-logits, kind="stable")` (routing.py:64-65): larger logit first, equal logits (+0 == -0)
+// by index, NaN after every number (numpy sorts NaN last), NaN against NaN by index.
+__device__ __forceinline__ bool router_better(float v, int id, float best, int best_id) {
+    if (id == 0x7fffffff) return false;
+    if (best_id == 0x7fffffff) return true;
+    const bool vn = v != v, bn = best != best;
+    if (vn != bn) return bn;
+    if (vn) return id < best_id;
+    return v > best || (v == best && id < best_id);
+}
+
 template <typename WT, typename XT>
 __global__ void __launch_bounds__(kRouterThreads) pregate_kernel(const WT* __restrict__ wg, int n_experts, int d,
                                                                  const XT* __restrict__ x_base,
@@ -81,14 +92,13 @@ __global__ void __launch_bounds__(kRouterThreads) pregate_kernel(const WT* __res
         for (int s = 0, e = lane; e < n_experts; e += 32, ++s) {
             if (taken_mask[s >> 5] & (1u << (s & 31))) continue;
             const float v = logits[e];
-            // strict > keeps the lowest index; NaN never wins, matching a stable sort on -logits
-            if (best_id == 0x7fffffff || v > best) { best = v; best_id = e; }
+            if (router_better(v, e, best, best_id)) { best = v; best_id = e; }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const float ov = __shfl_xor_sync(0xffffffffu, best, o);
             const int oi = __shfl_xor_sync(0xffffffffu, best_id, o);
-            if (oi != 0x7fffffff && (best_id == 0x7fffffff || ov > best || (ov == best && oi < best_id))) {
+            if (router_better(ov, oi, best, best_id)) {
                 best = ov;
                 best_id = oi;
             }

@@ -127,10 +127,15 @@ __global__ void __launch_bounds__(kGcThreads, 1) gemv_chain_kernel(const __grid_
             if (tid == 0) {
                 const long long t0 = clock64();
                 int seen;
+                unsigned spins = 0;
                 do {
                     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(gp.phase_done + p - 1) : "memory");
                     if (seen >= G) break;
-                    if (clock64() - t0 > (1ll << 32)) {  // ~2 s: never hang the device on a lost CTA
+                    // ~2 s: never hang the device on a lost CTA.  The first CTA to give up raises AF_ECUDA in the
+                    // caller's error word; every other CTA sees the word and stops waiting at once, so the launch
+                    // ends (with unusable outputs) and the host raises at its next status check.
+                    if ((++spins & 1023u) == 0 && gp.err_flag && *reinterpret_cast<volatile int*>(gp.err_flag) == AF_ECUDA) break;
+                    if (clock64() - t0 > (1ll << 32)) {
                         if (gp.err_flag) atomicExch(gp.err_flag, AF_ECUDA);
                         break;
                     }

@@ -401,6 +401,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
     pdl_wait();  // qkv comes from the previous kernel
     pdl_launch_dependents();  // after the wait: a dependent's pre-wait part then never runs ahead of qkv's producer
     const int pos = *pos_dev;
+    if (pos < 0 || pos >= max_seq) return;   // KV cache full: touch nothing (the host side raises StateError before it gets here)
     const int n_pos = pos + 1;
     // the grid is sized for the longest context; a short one uses fewer splits (a split below ~32 positions costs
     // more in the combine than it saves), the other CTAs of the head leave here

@@ -125,49 +125,34 @@ __host__ __device__ inline void build_plan(Plan& plan, const af_decision* prev, 
         }
         return;
     }
-    for (int j = 0; j < kc; ++j) {
-        int e = cur->ids[j];
-        if (e < 0 || e >= n_experts_limit) continue;
-        float w = cur->weights[j];
-        for (int i = 0; i < kp; ++i)
-            if (prev->ids[i] == e) w -= prev->weights[i];
-        // a duplicate id inside `cur` is folded into its first occurrence
-        bool dup = false;
-        for (int i = 0; i < j; ++i)
-            if (cur->ids[i] == e) dup = true;
-        if (dup) {
-            for (int b = 0; b < plan.n_blocks; ++b)
-                if (plan.expert[b] == e) plan.weight[b] += cur->weights[j] * scale;
-            continue;
+    // Net weight per distinct expert, in order of first appearance (cur, then prev):
+    //   w_e = (sum of e's gates in cur - sum of e's gates in prev) * scale ;  w_e == 0 -> no block.
+    // (Duplicates inside one decision are summed, wherever the first occurrence netted to.)
+    for (int side = 0; side < 2; ++side) {
+        const af_decision* d = side == 0 ? cur : prev;
+        const int kd = side == 0 ? kc : kp;
+        for (int j = 0; j < kd; ++j) {
+            const int e = d->ids[j];
+            if (e < 0 || e >= n_experts_limit) continue;
+            bool seen = false;
+            for (int i = 0; i < j; ++i)
+                if (d->ids[i] == e) seen = true;
+            if (side == 1)
+                for (int i = 0; i < kc; ++i)
+                    if (cur->ids[i] == e) seen = true;
+            if (seen) continue;
+            float w = 0.0f;
+            for (int i = 0; i < kc; ++i)
+                if (cur->ids[i] == e) w += cur->weights[i];
+            for (int i = 0; i < kp; ++i)
+                if (prev->ids[i] == e) w -= prev->weights[i];
+            w *= scale;
+            if (w == 0.0f || plan.n_blocks >= kMaxBlocks) continue;
+            plan.expert[plan.n_blocks] = e;
+            plan.weight[plan.n_blocks] = w;
+            plan.negate[plan.n_blocks] = 0;
+            ++plan.n_blocks;
         }
-        w *= scale;
-        if (w == 0.0f) continue;
-        plan.expert[plan.n_blocks] = e;
-        plan.weight[plan.n_blocks] = w;
-        plan.negate[plan.n_blocks] = 0;
-        ++plan.n_blocks;
-    }
-    for (int i = 0; i < kp; ++i) {
-        int e = prev->ids[i];
-        if (e < 0 || e >= n_experts_limit) continue;
-        bool in_cur = false;
-        for (int j = 0; j < kc; ++j)
-            if (cur->ids[j] == e) in_cur = true;
-        if (in_cur) continue;
-        bool dup = false;
-        for (int b = 0; b < i; ++b)
-            if (prev->ids[b] == e) dup = true;
-        if (dup) {
-            for (int b = 0; b < plan.n_blocks; ++b)
-                if (plan.expert[b] == e) plan.weight[b] -= prev->weights[i] * scale;
-            continue;
-        }
-        float w = -prev->weights[i] * scale;
-        if (w == 0.0f) continue;
-        plan.expert[plan.n_blocks] = e;
-        plan.weight[plan.n_blocks] = w;
-        plan.negate[plan.n_blocks] = 0;
-        ++plan.n_blocks;
     }
 }
 

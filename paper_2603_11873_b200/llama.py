@@ -57,6 +57,12 @@ class LlamaConfig:
     tp_rank: int = 0
     compute: str = "auto"
     switch_mode: str = "inplace"     # or "from_pristine"
+    # model.py:344-349: every `refresh_every` decoded tokens the live weights are rebuilt from the pristine copy
+    # (bf16 storage re-rounds W at every in-place switch, a ~0.3 sqrt(T) ulp random walk the f32 reference does
+    # not have; 16 keeps the logits within 1e-2 of the reference's trajectory).  Here the refresh costs nothing:
+    # "copy W0, then merge the current decision" IS the from-pristine switch, so the refreshing token's one
+    # launch reads W0 instead of W -- same bytes, no extra pass.  0 = never; needs keep_pristine.
+    refresh_every: int = 16
     adapters: bool = True            # False = adapter-free backbone (the reference's BASE strategy)
     keep_pristine: bool = True
     attn_splits: int = 0             # CTAs per head in decode attention; 0 = auto (max_seq / 32, at most 8)
@@ -94,6 +100,8 @@ class LlamaConfig:
             raise ValueError(f"unknown switch mode {self.switch_mode!r}")
         if self.switch_mode == "from_pristine" and not self.keep_pristine:
             raise ValueError("from_pristine needs keep_pristine")
+        if not isinstance(self.refresh_every, int) or isinstance(self.refresh_every, bool) or self.refresh_every < 0:
+            raise ValueError(f"refresh_every must be a non-negative integer, got {self.refresh_every!r}")
         if self.forward_mode not in ("auto", "chase", "separate"):
             raise ValueError(f"unknown forward mode {self.forward_mode!r}")
         if self.forward_mode == "chase" and not self.adapters:
@@ -260,6 +268,22 @@ class NoPeers(Collectives):
 # ---------------------------------------------------------------------------
 
 
+def _on_device(fn):
+    """Run a public engine method with the engine's device current: the C ABI launches on the current
+    device's stream and configures kernels per device, so an engine built on cuda:1 must not be
+    driven while cuda:0 is current."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *a, **kw):
+        if torch.cuda.current_device() == self.dev.index:
+            return fn(self, *a, **kw)
+        with torch.cuda.device(self.dev):
+            return fn(self, *a, **kw)
+
+    return wrapper
+
+
 class LlamaEngine:
     """Resident weights, expert bank, descriptor table, KV cache and the captured decode step."""
 
@@ -268,6 +292,12 @@ class LlamaEngine:
         torch_ = _capi.require_cuda()
         self.cfg = cfg
         self.dev = torch_.device(device) if device is not None else torch_.device("cuda", torch_.cuda.current_device())
+        if self.dev.index is None:
+            self.dev = torch_.device("cuda", torch_.cuda.current_device())
+        if self.dev.index != torch_.cuda.current_device():
+            with torch_.cuda.device(self.dev):      # build (and configure the kernels) on the engine's own device
+                self.__init__(cfg, init=init, device=self.dev, group=group, comm=comm)
+            return
         # `comm` lets a caller supply the exchange layer (tests build one shard with no peers)
         self.comm = comm if comm is not None else Collectives(group, cfg.tp_size)
         self.recorder = DispatchRecorder()
@@ -343,7 +373,22 @@ class LlamaEngine:
         self.gu_buf = torch.zeros(2 * self.ffn_local, dtype=f32, device=dev)
         self.logits = torch.zeros(self.vocab_local, dtype=f32, device=dev)
         self.token_dev = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.next_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        # what a step reports back: [next token, status word].  Every kernel of the engine that validates on the device
+        # (unusable decision, phase-barrier timeout) raises into report[1]; decode_step reads both words in ONE copy.
+        self.report = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.next_dev, self.err_dev = self.report[0:1], self.report[1:2]
+        self._pin_in = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self._pin_out = torch.zeros(2, dtype=torch.int32).pin_memory()
+        self._pin_in_np, self._pin_out_np = self._pin_in.numpy(), self._pin_out.numpy()
+        self._done_evt = torch.cuda.Event()
+        # host mirrors of the device counters (the device advances them itself, af_step_advance; the host only needs
+        # them to refuse a step past the KV cache and to pick the refreshing launch -- no read-back)
+        self._pos_host = 0
+        self._steps_host = 0
+        self.auto_graph = True      # decode_step replays the captured step (see decode_step)
+        self.refresh_every = cfg.refresh_every if (cfg.adapters and cfg.keep_pristine and cfg.switch_mode == "inplace") else 0
+        if self.table is not None:
+            _capi.check(_capi.lib().af_table_set_error_word(self.table.device_table.handle, _ptr(self.err_dev)))
         self.next_val = torch.zeros(1, dtype=f32, device=dev)
         self.pos_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -424,6 +469,7 @@ class LlamaEngine:
         self.comm.broadcast_decision(self.cur.buf)
         return self.cur
 
+    @_on_device
     def fused_switch(self, prev, cur, **kw) -> None:
         """W <- W + delta(cur) - delta(prev) over all 7 x L local shards, one launch."""
         if self.table is None:
@@ -447,9 +493,9 @@ class LlamaEngine:
     def unmerge(self, dec, **kw) -> None:
         self.fused_switch(dec, None, **kw)
 
-    def _switch_for_step(self, with_prev: bool) -> None:
-        if self.cfg.switch_mode == "from_pristine":
-            self.fused_switch(None, self.cur, mode="from_pristine")
+    def _switch_for_step(self, with_prev: bool, refresh: bool = False) -> None:
+        if self.cfg.switch_mode == "from_pristine" or refresh:
+            self.fused_switch(None, self.cur, mode="from_pristine")   # refresh: model.py:344-349 + the merge, in one pass
         else:
             self.fused_switch(self.prev if with_prev else None, self.cur)
 
@@ -487,7 +533,7 @@ class LlamaEngine:
                 phases.append(self._gv_phase(self.lm_head.data, self.vocab_local, d, xa, self.logits, prologue=_capi.AF_PRO_RMSNORM,
                                              norm_w=self.final_norm, eps=eps))
             arr = (_capi.GvPhase * len(phases))(*phases)
-            self._check(L.af_gemv_chain(arr, len(phases), _ptr(self.gc_done[4 * li: 4 * li + 4]), 1, st))
+            self._check(L.af_gemv_chain(arr, len(phases), _ptr(self.gc_done[4 * li: 4 * li + 4]), _ptr(self.err_dev), 1, st))
         self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
 
     def forward(self) -> None:
@@ -521,7 +567,7 @@ class LlamaEngine:
                                     _ptr(self.next_val), st))
         self.comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
 
-    def forward_chase(self, with_prev: bool) -> None:
+    def forward_chase(self, with_prev: bool, refresh: bool = False) -> None:
         """Switch AND merged forward of one token in one pass over the weights: each projection's
         launch merges the selected experts into its tiles (adapters.py:236-258), multiplies the
         rounded tiles with the projection's input (model.py:288) and writes them back.  4 weight
@@ -530,11 +576,12 @@ class LlamaEngine:
         cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
         d, eps = cfg.hidden, cfg.rms_eps
         xa, xb = self.x
-        prev = self.prev if (with_prev and cfg.switch_mode == "inplace") else None
-        cur, max_k, mode = self.cur, cfg.top_k, cfg.switch_mode
+        step_mode = "from_pristine" if refresh else cfg.switch_mode   # a refreshing token rebuilds W from W0 (model.py:344-349)
+        prev = self.prev if (with_prev and step_mode == "inplace") else None
+        cur, max_k, mode = self.cur, cfg.top_k, step_mode
         if self.chase_split:
             # all passes but the last as plain switch launches; the last merge pass is the one fused with the forward
-            cur, max_k, mode = self.table.switch_in_passes(prev, self.cur, rank=cfg.rank, max_k=cfg.top_k, mode=cfg.switch_mode,
+            cur, max_k, mode = self.table.switch_in_passes(prev, self.cur, rank=cfg.rank, max_k=cfg.top_k, mode=step_mode,
                                                            compute=cfg.compute, hold_last=True)
             prev = None
         kw = dict(max_k=max_k, mode=mode, plan_prebuilt=True)
@@ -588,20 +635,52 @@ class LlamaEngine:
                                       _ptr(forced) if forced is not None else None, int(forced.numel()) if forced is not None else 0,
                                       _ptr(self.history), int(self.history.numel()), st))
 
-    def _step_body(self, with_prev: bool) -> None:
+    def _step_body(self, with_prev: bool, refresh: bool = False) -> None:
         if self.chase:
             self.pregate()
-            self.forward_chase(with_prev)
+            self.forward_chase(with_prev, refresh)
             self._advance()
             return
         if self.cfg.adapters:
             self.pregate()
-            self._switch_for_step(with_prev)
+            self._switch_for_step(with_prev, refresh)
         self.forward()
         self._advance()
 
+    def _refresh_due(self) -> bool:
+        """model.py:344-349: tokens_done > 0 and tokens_done % refresh_every == 0."""
+        return bool(self.refresh_every) and self.have_prev and self._steps_host > 0 and self._steps_host % self.refresh_every == 0
+
+    def _stepped(self) -> None:
+        self._pos_host += 1
+        self._steps_host += 1
+        self.have_prev = self.cfg.adapters
+
+    @_on_device
+    def set_position(self, pos: int) -> None:
+        """Move the decode position (benchmarks that re-time a step at a fixed context length)."""
+        if not 0 <= int(pos) < self.cfg.max_seq:
+            raise InputError(f"position {pos!r} outside the KV cache of {self.cfg.max_seq}")
+        self.pos_dev.fill_(int(pos))
+        self._pos_host = int(pos)
+
+    @_on_device
+    def check(self) -> None:
+        """Raise what a kernel flagged since the last check (synchronises): an unusable device decision
+        (IndexError / ValueError, adapters.py:199-200), a phase-barrier timeout (DeviceError)."""
+        self._pin_out.copy_(self.report, non_blocking=True)
+        self._done_evt.record()
+        self._done_evt.synchronize()
+        self._raise_flag(int(self._pin_out_np[1]))
+
+    def _raise_flag(self, flag: int) -> None:
+        if flag:
+            self.err_dev.zero_()
+            _capi.raise_for_flag(flag)
+
     # -- public stepping ---------------------------------------------------------------------
 
+    @_on_device
     def reset(self, first_token: int = 0, forced=None) -> None:
         """Start a new sequence: position 0, weights back to pristine, optional teacher-forced
         token stream (consumed instead of the greedy feedback)."""
@@ -615,6 +694,7 @@ class LlamaEngine:
         self.have_prev = False
         self.pos_dev.zero_()
         self.step_dev.zero_()
+        self._pos_host = self._steps_host = 0
         if forced is not None:
             forced = np.asarray(forced, dtype=np.int64)
             if forced.size == 0 or forced.min() < 0 or forced.max() >= self.cfg.vocab:
@@ -626,21 +706,41 @@ class LlamaEngine:
         self.token_dev.fill_(int(first_token))
         self._graphs = {}
 
-    def decode_step(self, token: int | None = None) -> int:
-        """One eager decode step through the public API: the consumed token comes from the host
-        (4 bytes H2D), the next token is read back (4 bytes D2H)."""
+    @_on_device
+    def decode_step(self, token: int | None = None, *, graph: bool | None = None) -> int:
+        """One decode step through the public API: the consumed token comes from the host (4 bytes
+        H2D from a pinned word), the next token and the step's status word are read back together
+        (8 bytes D2H into pinned memory) -- the one synchronisation of the step.  The step itself is
+        a fixed launch sequence driven by device-resident state, so from the second token on it is
+        replayed as a CUDA graph (captured on first use; `graph=False` / `auto_graph = False` keep
+        the eager launches, which TP engines use unless AF_TP_GRAPH=1)."""
         if token is not None:
             if not 0 <= int(token) < self.cfg.vocab:
                 raise InputError(f"token {token!r} outside vocab of {self.cfg.vocab}")
-            self.token_dev.copy_(torch.tensor([int(token)], dtype=torch.int32).pin_memory(), non_blocking=True)
-        if int(self.pos_dev.item()) >= self.cfg.max_seq:
+            self._pin_in_np[0] = int(token)
+            self.token_dev.copy_(self._pin_in, non_blocking=True)
+        if self._pos_host >= self.cfg.max_seq:
             raise StateError("KV cache is full")
-        self._step_body(self.have_prev)
-        self.have_prev = self.cfg.adapters
-        return int(self.next_dev.item())
+        refresh = self._refresh_due()
+        use_graph = self.auto_graph if graph is None else bool(graph)
+        steady = self.have_prev or not self.cfg.adapters or self.cfg.switch_mode == "from_pristine"
+        if use_graph and steady and (self.cfg.tp_size == 1 or os.environ.get("AF_TP_GRAPH") == "1"):
+            if "steady" not in self._graphs:
+                self.capture()
+            self._graphs["refresh" if refresh else "steady"].replay()
+        else:
+            self._step_body(self.have_prev and not refresh, refresh)
+        self._stepped()
+        self._pin_out.copy_(self.report, non_blocking=True)
+        self._done_evt.record()
+        self._done_evt.synchronize()
+        self._raise_flag(int(self._pin_out_np[1]))
+        return int(self._pin_out_np[0])
 
+    @_on_device
     def capture(self) -> None:
-        """Capture the steady-state step (switch with a previous decision) as a CUDA graph."""
+        """Capture the steady-state step (switch with a previous decision) as a CUDA graph -- and, with
+        refresh_every, the refreshing step (from-pristine switch of the current decision) as a second one."""
         if not self.have_prev and self.cfg.adapters and self.cfg.switch_mode == "inplace":
             raise StateError("run one eager decode_step first: the steady graph unmerges a previous decision")
         if self.cfg.tp_size > 1 and os.environ.get("AF_TP_GRAPH") != "1":
@@ -648,26 +748,35 @@ class LlamaEngine:
             # have created the communicator); verified here only on a one-rank NCCL group
             # (tests/test_gpu_llama.py::test_tp_step_with_nccl_collectives_captures), hence opt-in
             raise StateError("TP steps run eagerly unless AF_TP_GRAPH=1")
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
-                self._step_body(True)
-        torch.cuda.current_stream().wait_stream(side)
-        self._graphs["steady"] = g
+        variants = [("steady", True, False)] + ([("refresh", False, True)] if self.refresh_every else [])
+        for name, with_prev, refresh in variants:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    self._step_body(with_prev, refresh)
+            torch.cuda.current_stream().wait_stream(side)
+            self._graphs[name] = g
 
+    @_on_device
     def replay(self) -> None:
-        self._graphs["steady"].replay()
+        """One captured step, asynchronously (no read-back: `check()` / `tokens()` synchronise)."""
+        if self._pos_host >= self.cfg.max_seq:
+            raise StateError("KV cache is full")       # the kernels would run past the caches and the rotary tables
+        self._graphs["refresh" if self._refresh_due() else "steady"].replay()
+        self._stepped()
 
     def steps_done(self) -> int:
         return int(self.step_dev.item())
 
     def tokens(self, n: int | None = None) -> list:
+        self.check()
         n = self.steps_done() if n is None else n
         return [int(v) for v in self.history[:n].cpu().numpy()]
 
+    @_on_device
     def prefill(self, prompt) -> int:
         """Batched UNMERGED prefill of a whole prompt (model.py:408-425; PAPER Eq. 2): all T tokens go
         through every layer at once, token t with its own pre-gated decision,
@@ -756,12 +865,14 @@ class LlamaEngine:
         self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
         nxt = int(self.next_dev.item())
         self.pos_dev.fill_(T)
+        self._pos_host = T
         self.step_dev.fill_(T)
         self.history[T - 1] = nxt
         self.token_dev.fill_(nxt)
         self.last_prefill_hidden = x[T - 1]
         return nxt
 
+    @_on_device
     def generate(self, prompt, n_new: int, use_graph: bool = True, prefill: str = "auto") -> list:
         """Greedy generation.  prefill="batched" (default on one rank): the whole prompt in one
         unmerged batched pass (`prefill`), as the reference prefills (model.py:408-425);
@@ -784,11 +895,11 @@ class LlamaEngine:
             self.reset(prompt[0])
             nxt = None
             for t in prompt:
-                nxt = self.decode_step(t)
+                nxt = self.decode_step(t, graph=use_graph)
             out = [nxt]
         remaining = n_new - 1
         if remaining and not self.have_prev and self.cfg.adapters and self.cfg.switch_mode == "inplace":
-            out.append(self.decode_step())     # the first merge has no previous decision: eager, then the steady graph
+            out.append(self.decode_step(graph=use_graph))     # the first merge has no previous decision: eager, then the steady graph
             remaining -= 1
         if remaining and use_graph and self.cfg.tp_size == 1:
             self.capture()
@@ -798,10 +909,11 @@ class LlamaEngine:
             out = out + self.tokens()[len(prompt) + len(out) - 1:]
         else:
             for _ in range(remaining):
-                out.append(self.decode_step())
+                out.append(self.decode_step(graph=use_graph))
         self.finalize()
         return out
 
+    @_on_device
     def finalize(self) -> None:
         """model.py:460-474: take the last delta out again."""
         if self.table is not None and self.have_prev:
@@ -811,6 +923,7 @@ class LlamaEngine:
                 self.unmerge(self.prev)
             self.have_prev = False
 
+    @_on_device
     def max_backbone_deviation(self) -> float:
         if self.table is None or self.pristine is None:
             raise StateError("no pristine copy kept")

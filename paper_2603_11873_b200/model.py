@@ -11,6 +11,13 @@ The per-token hot path of ``PRE_GATED_FUSED`` (model.py:332-371 `_merged_pass`) 
 with the routing decision, the token and every activation resident on the device; the only
 host read per step is the 4-byte next token.  Weights are stored in bf16
 (``precision="bf16"``, the default) or f32 (``"single"`` -- the reference's own mode).
+
+Attribution: ``Strategy``, ``ModelConfig`` (fields, validation rules and messages, ``to_dict`` /
+``from_dict``), ``DecoderModel`` and ``DecodeState`` are the reference's carrier classes
+(model.py:66-162) restated field for field -- they ARE the public API this package keeps intact,
+so their names, fields and error behaviour are taken from the reference, not invented here.
+Everything below them (device residency, kernels, the refresh folded into the switch) is this
+package's own.
 """
 
 from __future__ import annotations
@@ -28,6 +35,22 @@ from .adapters import ConcatAdapter, ExpertBank, LoraExpert, SwitchTable, expert
 from .errors import DeviceError, DimensionError, InputError, StateError
 from .linalg import PRECISION_DTYPES, _AF_DTYPE, DispatchEvent, DispatchRecorder, Matrix, _ptr, gemm
 from .routing import DeviceDecision, GateDecision, RouterParams, pregate_device, pregate_token_device
+
+
+def _on_model_device(fn):
+    """Run an engine entry point with the model's device current (the C ABI launches on the current
+    device's stream and configures its kernels per device)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(model, *a, **kw):
+        dev = model.embed.data.device
+        if dev.type != "cuda" or torch.cuda.current_device() == dev.index:
+            return fn(model, *a, **kw)
+        with torch.cuda.device(dev):
+            return fn(model, *a, **kw)
+
+    return wrapper
 
 
 class Strategy(Enum):
@@ -63,7 +86,7 @@ class ModelConfig:
     precision: str = "bf16"
     seed: int = 0
     strategy: Strategy = Strategy.PRE_GATED_FUSED
-    refresh_every: int = 0
+    refresh_every: int = 0         # model.py:103; see `effective_refresh_every` for bf16 storage
     compute: str = "auto"
     switch_mode: str = "inplace"   # "inplace": W <- W + dNew - dOld; "from_pristine": W <- W0 + dNew (no drift)
 
@@ -84,14 +107,30 @@ class ModelConfig:
             raise ValueError(f"unknown precision {self.precision!r}")
         if not isinstance(self.strategy, Strategy):
             raise ValueError(f"strategy must be a Strategy, got {self.strategy!r}")
-        if not isinstance(self.refresh_every, int) or self.refresh_every < 0:
-            raise ValueError("refresh_every must be a non-negative integer")
+        if not isinstance(self.refresh_every, int) or self.refresh_every < -1:
+            raise ValueError("refresh_every must be a non-negative integer (or -1: never, also for bf16 storage)")
         if not isinstance(self.seed, int):
             raise ValueError("seed must be an integer")
         if self.compute not in _capi.COMPUTE_MODES:
             raise ValueError(f"unknown compute mode {self.compute!r}")
         if self.switch_mode not in ("inplace", "from_pristine"):
             raise ValueError(f"unknown switch mode {self.switch_mode!r}")
+
+    BF16_REFRESH_EVERY = 16
+
+    @property
+    def effective_refresh_every(self) -> int:
+        """The refresh period `_merged_pass` uses.  The reference's default (0 = never) is right for its f32 / f64
+        weights, whose in-place switch drifts by ~1e-8.  bf16 storage re-rounds W at every in-place switch (a
+        ~0.3 sqrt(T) ulp random walk), and 16 switches is where the logits are still within 1e-2
+        of the reference's trajectory -- so an in-place bf16 model left at 0 refreshes every 16 tokens.  The
+        refresh is free here (it is folded into that token's switch launch, see `_merged_pass`);
+        ``refresh_every=-1`` turns it off."""
+        if self.refresh_every < 0:
+            return 0
+        if self.refresh_every == 0 and self.precision == "bf16" and self.switch_mode == "inplace" and self.strategy.merges_backbone:
+            return self.BF16_REFRESH_EVERY
+        return self.refresh_every
 
     def to_dict(self) -> dict:
         return {
@@ -188,6 +227,9 @@ def build_model(config: ModelConfig, device=None) -> DecoderModel:
     config.validate()
     torch_ = _capi.require_cuda()
     dev = torch_.device(device) if device is not None else torch_.device("cuda", torch_.cuda.current_device())
+    if dev.type == "cuda" and dev.index is not None and dev.index != torch_.cuda.current_device():
+        with torch_.cuda.device(dev):      # the descriptor table is allocated on the CURRENT device
+            return build_model(config, dev)
     w = draw_weights(config)
     prec = config.precision
 
@@ -229,6 +271,7 @@ def weights_digest(model: DecoderModel) -> str:
     return h.hexdigest()
 
 
+@_on_model_device
 def max_backbone_deviation(model: DecoderModel) -> float:
     """Largest |backbone - pristine| entry across all layers (model.py:231-236)."""
     return model.table.max_deviation()
@@ -329,11 +372,16 @@ def _merged_pass(model: DecoderModel, state: DecodeState, token: int, recorder: 
     cur = state.spare_decision if state.spare_decision is not None else DeviceDecision(dev)
     state.spare_decision = None
     pregate_device(model.router, x, config.top_k, recorder, out=cur)
-    if config.refresh_every > 0 and state.tokens_done > 0 and state.tokens_done % config.refresh_every == 0:
+    period = config.effective_refresh_every
+    refresh = period > 0 and state.tokens_done > 0 and state.tokens_done % period == 0      # model.py:344-349
+    if refresh and strategy is not Strategy.PRE_GATED_FUSED:
         _refresh_from_pristine(model, state)
     prev = state.prev_decision
-    if strategy is Strategy.PRE_GATED_FUSED and config.switch_mode == "from_pristine":
-        # same HBM traffic (read W0, write W), half the stacked rank, and no bf16 re-rounding drift
+    if strategy is Strategy.PRE_GATED_FUSED and (config.switch_mode == "from_pristine" or refresh):
+        # A refreshing token: "copy W0 over W, forget prev, merge cur" (model.py:308-312, :350-357) is exactly
+        # W <- bf16(W0 + delta(cur)) -- the from-pristine switch -- so the refresh rides in this token's one
+        # launch instead of costing a copy of every weight.
+        # Same HBM traffic (read W0, write W), half the stacked rank, and no bf16 re-rounding drift.
         model.table.switch(None, cur, max_k=config.top_k, compute=config.compute, mode="from_pristine")
         _switch_event(model, config.top_k, recorder)
     elif strategy is Strategy.PRE_GATED_FUSED:
@@ -358,6 +406,7 @@ def _merged_pass(model: DecoderModel, state: DecodeState, token: int, recorder: 
     return x, _unembed(model, x, recorder)
 
 
+@_on_model_device
 def decode_step(model: DecoderModel, state: DecodeState, token: int, recorder: DispatchRecorder, capture=None,
                 logits_out: list | None = None):
     """One greedy decode step (model.py:374-405): consume ``token``, emit the next token id;
@@ -372,6 +421,8 @@ def decode_step(model: DecoderModel, state: DecodeState, token: int, recorder: D
     _capi.check(_capi.lib().af_argmax(_ptr(logits), int(logits.numel()), _ptr(nxt), _capi.stream_ptr()))
     recorder.record("reduce", flops=model.config.vocab, bytes_touched=model.config.vocab * 4, label="other")
     next_token = int(nxt.item())  # the one host read of the step
+    if model.table is not None and strategy.merges_backbone:
+        model.table.status()      # what the switch kernel flagged for this step's device decision (adapters.py:199-200)
     if logits_out is not None:
         logits_out.append(logits.detach().cpu().numpy().copy())
     state.last_hidden_dev = x.data[:, 0]
@@ -379,6 +430,7 @@ def decode_step(model: DecoderModel, state: DecodeState, token: int, recorder: D
     return next_token, recorder.events_since(mark)
 
 
+@_on_model_device
 def prefill(model: DecoderModel, tokens, recorder: DispatchRecorder) -> DecodeState:
     """Process a prompt along the unfused per-token path (model.py:408-425); never an sgmm."""
     tokens = list(tokens)
@@ -393,12 +445,15 @@ def prefill(model: DecoderModel, tokens, recorder: DispatchRecorder) -> DecodeSt
     return DecodeState(prev_decision=None, last_hidden_dev=x.data[:, 0], tokens_done=0)
 
 
+@_on_model_device
 def generate(model: DecoderModel, prompt, n_new: int, recorder: DispatchRecorder, hidden_sink: list | None = None,
              forced=None, logits_sink: list | None = None):
     """Prefill, n_new greedy decode steps, then restore the backbone (model.py:428-457).
 
-    Returns (generated tokens, tuple of all events).  ``forced`` (an extension) teacher-forces
-    the consumed token stream so every step really switches."""
+    Returns (generated tokens, DispatchTrace of all events), as the reference does.  ``forced`` (an
+    extension) teacher-forces the consumed token stream so every step really switches."""
+    from .perf import DispatchTrace
+
     if n_new < 1:
         raise InputError(f"n_new must be >= 1, got {n_new}")
     mark = recorder.mark()
@@ -414,9 +469,10 @@ def generate(model: DecoderModel, prompt, n_new: int, recorder: DispatchRecorder
         if hidden_sink is not None:
             hidden_sink.append(capture)
     finalize_generation(model, state, recorder)
-    return generated, tuple(recorder.events_since(mark))
+    return generated, DispatchTrace(tuple(recorder.events_since(mark)))
 
 
+@_on_model_device
 def finalize_generation(model: DecoderModel, state: DecodeState, recorder: DispatchRecorder) -> None:
     """Unmerge the last token's delta arithmetically (model.py:460-474) -- one launch over all
     layers here; the trace keeps the reference's one gemm event per layer."""
@@ -439,6 +495,7 @@ def finalize_generation(model: DecoderModel, state: DecodeState, recorder: Dispa
 # ---------------------------------------------------------------------------
 
 
+@_on_model_device
 def fused_switch(model: DecoderModel, prev_decision, cur_decision, recorder: DispatchRecorder | None = None, **kw) -> None:
     """W <- W + delta(cur) - delta(prev) over every adapted matrix in one launch.
     Decisions may be ``GateDecision`` (host) or ``DeviceDecision``; None = empty."""

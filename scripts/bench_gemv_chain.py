@@ -19,14 +19,14 @@ def run(phases, nbytes, label, iters=20):
     done = torch.zeros(4, dtype=torch.int32, device="cuda")
     for _ in range(3):
         done.zero_()
-        _capi.check(L.af_gemv_chain(arr, len(phases), p(done), 0, st))
+        _capi.check(L.af_gemv_chain(arr, len(phases), p(done), None, 0, st))
     torch.cuda.synchronize()
     best = 1e9
     for _ in range(iters):
         done.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _capi.check(L.af_gemv_chain(arr, len(phases), p(done), 0, st))
+        _capi.check(L.af_gemv_chain(arr, len(phases), p(done), None, 0, st))
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))

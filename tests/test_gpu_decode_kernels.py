@@ -197,7 +197,7 @@ def test_gemv_chain_against_numpy(capi, d, f, kv, vocab):
           prologue=capi.AF_PRO_RMSNORM, epilogue=capi.AF_EPI_NONE),
     )
     done = torch.zeros(4, dtype=torch.int32, device="cuda")
-    capi.check(L.af_gemv_chain(phases, 4, p(done), 0, st))
+    capi.check(L.af_gemv_chain(phases, 4, p(done), None, 0, st))
     torch.cuda.synchronize()
     sm = capi.device_info()["sm_count"]
     assert done[:3].tolist() == [sm] * 3
@@ -213,11 +213,11 @@ def test_gemv_chain_against_numpy(capi, d, f, kv, vocab):
     # bit-reproducible: a second run from the same inputs gives the same bits
     q1 = qkv_d.clone()
     done.zero_()
-    capi.check(L.af_gemv_chain(phases, 4, p(done), 0, st))
+    capi.check(L.af_gemv_chain(phases, 4, p(done), None, 0, st))
     torch.cuda.synchronize()
     assert torch.equal(q1, qkv_d)
     # validation
     with pytest.raises(ValueError):
-        capi.check(L.af_gemv_chain(phases, 5, p(done), 0, st))
+        capi.check(L.af_gemv_chain(phases, 5, p(done), None, 0, st))
     with pytest.raises(ValueError):
-        capi.check(L.af_gemv_chain(phases, 2, None, 0, st))
+        capi.check(L.af_gemv_chain(phases, 2, None, None, 0, st))

@@ -93,7 +93,7 @@ def test_graph_replay_equals_eager(llama, forward_mode):
     a = llama.LlamaEngine(cfg, init="host")
     a.reset(forced=forced)
     for _ in range(20):
-        a.decode_step()
+        a.decode_step(graph=False)      # eager launches (decode_step replays a captured graph by default)
     eager = a.tokens()
     b = llama.LlamaEngine(cfg, init="host")
     b.reset(forced=forced)
@@ -129,8 +129,10 @@ def test_split_attention_and_pdl_do_not_change_results(llama, forward_mode):
     # Split attention reorders f32 sums (1e-7 on the attention output).  In the one-pass forward the
     # activations enter the tensor pipe as bf16 hi + lo pairs -- x is reproduced to 2^-18, by a
     # rounding that a 1e-7 change re-rolls -- so bf16 roundings of cached k/v flip more often and
-    # the schedules drift apart faster (still 20x inside the 1e-2 logit criterion).
-    atol = 1e-5 if forward_mode == "separate" else 1e-3
+    # the schedules drift apart faster (still 20x inside the 1e-2 logit criterion).  The plain forward has the same
+    # mechanism one level down: the KV cache stores bf16, and a 1e-7 change of k or v flips the occasional rounding
+    # (2^-9 of one cached element: a few 1e-5 on a logit over 80 positions).
+    atol = 1e-4 if forward_mode == "separate" else 1e-3
     for toks, lg in outs[1:]:
         np.testing.assert_allclose(lg, outs[0][1], rtol=1e-4, atol=atol)
     assert outs[2][0] == outs[0][0]          # PDL on/off: bit-identical schedule-independent arithmetic
@@ -383,10 +385,10 @@ def test_switch_in_passes_for_more_than_64_stacked_ranks(llama, switch_mode, for
     n_pass = 8 if switch_mode == "inplace" else 2
     for step in range(len(forced)):
         before = _capi.launch_count()
-        a = one.decode_step()
+        a = one.decode_step(graph=False)        # eager: the launches are counted
         single = _capi.launch_count() - before
         before = _capi.launch_count()
-        b = many.decode_step()
+        b = many.decode_step(graph=False)
         launches = _capi.launch_count() - before
         assert many.decision() == one.decision()
         want_passes = (2 if switch_mode == "from_pristine" else (4 if step else 2))    # 2 experts of rank 32 per pass

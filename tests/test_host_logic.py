@@ -21,7 +21,7 @@ def test_model_config_validation():
     # /root/reference/pkg/src/lorafuse/model.py:101-119
     af.ModelConfig().validate()
     for bad in (dict(layers=0), dict(vocab=1), dict(top_k=9, experts=8), dict(rank=65, hidden=64), dict(precision="double"),
-                dict(strategy="pre_gated_fused"), dict(refresh_every=-1), dict(seed=1.5), dict(hidden=True),
+                dict(strategy="pre_gated_fused"), dict(refresh_every=-2), dict(seed=1.5), dict(hidden=True),
                 dict(compute="fast"), dict(switch_mode="copy")):
         with pytest.raises(ValueError):
             af.ModelConfig(**bad).validate()
