@@ -322,13 +322,22 @@ class SwitchTable:
             )
         )
 
-    TENSOR_PATH_RANKS = 64   # stacked ranks one tensor-path launch holds (include/adafuse_b200.h, af_fused_switch)
+    TENSOR_PATH_RANKS = 64   # stacked ranks one mma.sync tensor-path launch holds (include/adafuse_b200.h, af_fused_switch)
+    UMMA_PATH_RANKS = 256    # ... and one K-chunked tcgen05 launch (tables of one rank in {8, 16, 32} on 128-multiples)
+
+    def one_launch_ranks(self) -> int:
+        """Stacked ranks (blocks x rank) ONE tensor-path launch over this table takes -- the reference's merge is
+        one sgmm whatever the stacked rank (adapters.py:236-258); beyond this the engine falls back to passes."""
+        if self.info()["umma_path"] and self.rank in (8, 16, 32):
+            return self.UMMA_PATH_RANKS
+        return self.TENSOR_PATH_RANKS
 
     def switch_in_passes(self, prev, cur, *, rank: int, max_k: int, scale: float = 1.0, mode: str = "inplace",
                          compute: str = "auto", hold_last: bool = False):
         """The switch of `switch`, for decisions whose stacked rank (blocks x rank) exceeds what one
-        tensor-path launch holds (Llama-2-70B: r = 32, k = 4 -> 256): the experts are taken
-        `TENSOR_PATH_RANKS // rank` at a time -- first the previous decision's (unmerged), then the
+        tensor-path launch holds (`one_launch_ranks`: 256 on the tcgen05 path, which covers every
+        BASELINE configuration in ONE launch; 64 for rank-64 tables and off the tcgen05 path): the
+        experts are taken `one_launch_ranks() // rank` at a time -- first the previous decision's (unmerged), then the
         current one's (merged; the first of them from pristine in that mode) -- each pass one
         tensor-path launch over all segments.  The sub-decisions are cut on the device (no host
         round trip, capturable).  Costs one pass over W per launch and rounds W to bf16 once per
@@ -341,7 +350,7 @@ class SwitchTable:
         for dec in (prev, cur):
             if dec is not None and not isinstance(dec, DeviceDecision):
                 raise TypeError("switch_in_passes takes device-resident decisions (DeviceDecision) or None")
-        per = max(1, self.TENSOR_PATH_RANKS // int(rank))
+        per = max(1, self.one_launch_ranks() // int(rank))
         chunks = [(start, min(per, max_k - start)) for start in range(0, max_k, per)]
         if not hasattr(self, "_sub_decisions"):
             self._sub_decisions = {}

@@ -497,18 +497,20 @@ static int launch_mma(const MmaParams& mp, int grid, cudaStream_t st) {
     return AF_OK;
 }
 
-// Stacked ranks (2 k r in the steady switch) up to which the tcgen05 kernel is used.  The plain switch gains
-// 2-3 % over mma.sync at 64 (four W stages, three UP stages); the fused switch + GEMV loses 4 % there (measured on
-// Llama-3-8B, profiles/README.md), so chains stay on mma.sync above 32.  AF_UMMA_MAX_RANKS[_CHAIN] override (A/B runs).
-static const int kUmmaMaxRanks = [] { const char* e = getenv("AF_UMMA_MAX_RANKS"); return e ? atoi(e) : 64; }();
-static const int kUmmaMaxRanksChain = [] { const char* e = getenv("AF_UMMA_MAX_RANKS_CHAIN"); return e ? atoi(e) : 32; }();
-// tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = k-groups of 8 stacked ranks per half.
-template <int NB, bool GEMV>
+// Stacked ranks (2 k r in the steady switch) up to which the tcgen05 kernel is used: 256, K-chunked above 32
+// (af_switch_umma.cuh), for tables of rank 8 / 16 / 32; rank 64 up to 64.  AF_UMMA_MAX_RANKS[_CHAIN] override (A/B runs).
+static const int kUmmaMaxRanks = [] { const char* e = getenv("AF_UMMA_MAX_RANKS"); return e ? atoi(e) : 256; }();
+static const int kUmmaMaxRanksChain = [] { const char* e = getenv("AF_UMMA_MAX_RANKS_CHAIN"); return e ? atoi(e) : 256; }();
+// 1: launches of 33..64 stacked ranks stream the UP operand in 32-rank chunks too (same shared memory, twice the
+// barrier traffic: measured 1.5 % slower on Llama-3-8B shapes, so off)
+static const int kUmmaChunk64 = [] { const char* e = getenv("AF_UMMA_CHUNK64"); return e ? atoi(e) : 0; }();
+// tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = k-groups of 8 stacked ranks per half, CH = k-groups per UP stage.
+template <int NB, bool GEMV, int CH = NB>
 static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
-    using L = UmmaLayout<NB, GEMV>;
+    using L = UmmaLayout<NB, GEMV, CH>;
     static PerDevice configured;
     if (!configured.cur()) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured.cur() = 1;
     }
     cudaLaunchConfig_t cfg{};
@@ -521,10 +523,23 @@ static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = mp.pdl ? 1 : 0;
-    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV>, mp));
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV, CH>, mp));
     AF_LAUNCH_CHECK("switch_umma_kernel");
-    note_kernel("switch_umma_kernel<NB=%d,GEMV=%d> (tcgen05 + TMEM)", NB, (int)GEMV);
+    note_kernel("switch_umma_kernel<NB=%d,GEMV=%d,CH=%d> (tcgen05 + TMEM)", NB, (int)GEMV, CH);
     return AF_OK;
+}
+
+// Largest stacked rank ONE tcgen05 launch over this table takes (0: the table is not eligible at all)
+static int umma_rank_limit(const af_table* t) {
+    if (!t->umma_ok || !g_umma.load()) return 0;
+    return t->max_rank <= 32 ? 256 : 64;
+}
+template <bool GEMV>
+static int dispatch_umma(const af_table* t, int s_bound, const MmaParams& mp, int grid, cudaStream_t st) {
+    if (s_bound <= 32) return launch_umma<4, GEMV>(mp, grid, st);
+    if (s_bound <= 64) return (kUmmaChunk64 && t->max_rank <= 32) ? launch_umma<8, GEMV, 4>(mp, grid, st) : launch_umma<8, GEMV>(mp, grid, st);
+    if (s_bound <= 128) return launch_umma<16, GEMV, 4>(mp, grid, st);
+    return launch_umma<32, GEMV, 4>(mp, grid, st);
 }
 
 template <typename FT, bool EXACT, bool F2>
@@ -610,12 +625,13 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
     const int s_bound = n_blocks_bound * t->max_rank;
 
     const bool want_mma = compute == AF_COMPUTE_MMA || compute == AF_COMPUTE_AUTO;
+    const bool umma_fits = t->fast_mma && t->n_units_umma && !host_plan_override && s_bound <= std::min(kUmmaMaxRanks, umma_rank_limit(t));
     const bool mma_fits = t->fast_mma && s_bound <= kMmaMaxKS * 16;
-    if (compute == AF_COMPUTE_MMA && !mma_fits)
-        return fail(AF_EVALUE, "tensor path needs bf16 targets and factors, rank % 8 == 0, 16-byte aligned rows and "
-                               "at most 64 stacked ranks");
+    if (compute == AF_COMPUTE_MMA && !mma_fits && !umma_fits)
+        return fail(AF_EVALUE, "tensor path needs bf16 targets and factors, rank % 8 == 0, 16-byte aligned rows and at most 64 stacked "
+                               "ranks (256 on the tcgen05 path: one rank of 8 / 16 / 32 per table, matrices multiples of 128)");
     const int S = t->n_segments;
-    if (want_mma && mma_fits && g_umma.load() && t->umma_ok && t->n_units_umma && s_bound <= kUmmaMaxRanks && !host_plan_override) {
+    if (want_mma && umma_fits) {
         MmaParams mp{};
         mp.base = p;
         mp.base.units = t->d_units_umma;
@@ -626,7 +642,9 @@ static int run_switch(af_table* t, const af_decision* prev_dev, const af_decisio
         mp.n_chain_segs = 0;
         mp.n_phases = 1;
         const int grid = std::min(t->n_units_umma, t->sm_count);
-        return s_bound <= 32 ? launch_umma<4, false>(mp, grid, st) : launch_umma<8, false>(mp, grid, st);
+        static const int env_dbg3 = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
+        mp.dbg = env_dbg3 ^ 24;
+        return dispatch_umma<false>(t, s_bound, mp, grid, st);
     }
     if (want_mma && mma_fits) {
         MmaParams mp{};
@@ -978,7 +996,9 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     const int n_blocks_bound = use_dev ? ((from_pristine || !prev_dev ? 0 : max_k) + (cur_dev ? max_k : 0)) : 0;
     p.max_blocks = std::min(n_blocks_bound, kMaxBlocks);
     const int s_bound = n_blocks_bound * t->max_rank;
-    if (s_bound > kMmaMaxKS * 16) return fail(AF_EVALUE, "the fused switch + GEMV holds at most 64 stacked ranks");
+    const bool umma_launch = g->d_units_umma && s_bound <= std::min(kUmmaMaxRanksChain, umma_rank_limit(t));
+    if (s_bound > kMmaMaxKS * 16 && !umma_launch)
+        return fail(AF_EVALUE, "the fused switch + GEMV holds at most 64 stacked ranks (256 on the tcgen05 path)");
     const int S = t->n_segments;
     mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 3 : 2) * S;
     mp.tmaps_st = t->d_maps + (size_t)2 * S;
@@ -1008,9 +1028,6 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     static const int env_dbg = [] { const char* e = getenv("AF_DBG"); return e ? atoi(e) : 0; }();
     mp.dbg = env_dbg ^ 24;
     const int ks_tl = std::max(1, (s_bound + 15) / 16);
-    // At most 32 stacked ranks: with 64 the hi + lo slab (32 KB) and the UP stage (16 KB) leave the tcgen05
-    // kernel three ring stages and it loses to the mma.sync kernel (Llama-3-8B shapes, r = 16: 7.93 vs 7.04 ms)
-    const bool umma_launch = g_umma.load() && t->umma_ok && g->d_units_umma && s_bound <= kUmmaMaxRanksChain;
     if (g_timeline && g_timeline_left > 0 && (ks_tl == 2 || umma_launch)) {  // mma.sync: the probe is compiled into the KS = 2 hi/lo variant only
         mp.timeline = g_timeline;
         g_timeline += g_timeline_stride;
@@ -1032,8 +1049,7 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 6 : 5) * S;
         mp.tmaps_st = t->d_maps + (size_t)5 * S;
         mp.tmaps_up = t->d_maps + (size_t)7 * S;
-        // 4 (8) k-groups of 8 stacked ranks per half
-        return s_bound <= 32 ? launch_umma<4, true>(mp, g->grid_umma, st) : launch_umma<8, true>(mp, g->grid_umma, st);
+        return dispatch_umma<true>(t, s_bound, mp, g->grid_umma, st);
     }
     if (mp.timeline && ks == 2) return launch_mma<2, false, true, true>(mp, g->grid, st);
     switch (ks) {

@@ -18,9 +18,17 @@
 // (no cross-warp reduction: a thread holds the whole 128-column row strip).
 //
 // Scope: tables of ONE rank in {8, 16, 32, 64}, matrices multiples of 128 in both directions (every
-// Llama shape of BASELINE.json), launches of at most 64 stacked ranks (plain switch) / 32 (fused switch +
-// GEMV, where mma.sync still wins at 64: af_api.cu kUmmaMaxRanks[Chain]); anything else keeps the mma.sync
-// kernel.  (scripts/micro/umma_test.cu pins the descriptor encodings in isolation.)
+// Llama shape of BASELINE.json).  Stacked ranks: up to 256 in ONE launch (K-chunked, below) for ranks 8 / 16 /
+// 32; rank 64 up to 64.  (scripts/micro/umma_test.cu pins the descriptor encodings in isolation.)
+//
+// K-chunking (template argument CH < NB): the reference's merge is ONE sgmm whatever the stacked rank
+// (adapters.py:236-258 -> linalg.py:306-346).  With more than 32 stacked ranks the UP operand of a tile no
+// longer fits the ring next to the W tiles, so it streams through the UP ring in CHUNKS of 32 ranks (8 KB:
+// CH = 4 k-groups of 8) while the tile's accumulator stays in tensor memory: per chunk 2 x 2 tcgen05.mma
+// (hi and lo halves of the resident slab, K = 16 each), a commit that frees the chunk's stage, and after
+// the last chunk the commit that hands the accumulator to the epilogue.  One read and one write of W and
+// ONE bf16 rounding per token at any stacked rank up to 256 (Llama-2-70B, r = 32, k = 4) -- the multi-pass
+// schedule this replaces read and rounded W once per 64 ranks.
 #pragma once
 
 #include "af_switch_mma.cuh"
@@ -44,21 +52,29 @@ constexpr int kUXSlots = 4;
 #endif
 constexpr int kUPrefetch = AF_UMMA_PF;             // W tiles prefetched into L2 beyond the shared-memory ring (0 = off)
 
-template <int NB, bool GEMV>   // NB = block slots (2 * top_k, even)
+// NB = k-groups of 8 stacked ranks the slab holds per half; CH = k-groups per UP ring stage (CH == NB: the whole
+// UP operand of a tile is one stage; CH < NB: K-chunked, NB / CH chunks per tile)
+template <int NB, bool GEMV, int CH = NB>
 struct UmmaLayout {
-    static constexpr int up_stage = NB * kUBlockBytes;
+    static_assert(NB % CH == 0 && CH % 2 == 0, "chunks are whole rank-16 steps");
+    static constexpr bool chunked = CH < NB;
+    static constexpr int up_stage = CH * kUBlockBytes;
     static constexpr int slab_bytes = 2 * NB * kUSlabBlock;            // hi + lo
     static constexpr int xs_bytes = GEMV ? kUXSlots * kUN * 4 : 0;
     static constexpr int misc = 1024 /*barriers*/ + (int)sizeof(Plan) + 256 + kUnitCache * (int)sizeof(UnitDev) + kSegCache * (int)sizeof(SegDev);
     static constexpr int fixed = slab_bytes + xs_bytes + misc + 2048;
     // Two rings.  W tiles (32 KB, from HBM) live from their load until their store has read them; UP stages
-    // (from L2) only until the tile's MMAs have completed, two tiles ahead of the epilogue at most -- three UP
-    // stages are enough, which leaves a 64-rank launch (16 KB UP stages, 32 KB slab) four W stages instead of three.
-    static constexpr int up_stages_wanted = NB > 4 ? 3 : 6;
+    // (from L2) only until the MMAs that read them have completed, two tiles ahead of the epilogue at most.
+    // Whole-operand stages: three are enough, which leaves a 64-rank launch (16 KB UP stages, 32 KB slab) four
+    // W stages instead of three.  Chunked (8 KB stages): a tile consumes NB / CH stages in a burst, each an L2
+    // round trip: six stages (measured at 128 stacked ranks on Llama-2-70B shard shapes: six UP + three W stages
+    // 2.59 ms, three UP + four W stages 2.85 ms) -- except at 256, where the 128 KB slab leaves room for three
+    // UP and two W stages.
+    static constexpr int up_stages_wanted = chunked ? (NB >= 32 ? 3 : 6) : (NB > 4 ? 3 : 6);
     static constexpr int by_smem = (227 * 1024 - fixed) / (kUWStage + up_stage);          // equal depths
     static constexpr int by_smem_w = (227 * 1024 - fixed - up_stages_wanted * up_stage) / kUWStage;
-    static constexpr int stages = NB > 4 ? (by_smem_w < 6 ? by_smem_w : 6) : (by_smem < 6 ? by_smem : 6);
-    static constexpr int up_stages = NB > 4 ? up_stages_wanted : stages;
+    static constexpr int stages = (NB > 4 || chunked) ? (by_smem_w < 6 ? by_smem_w : 6) : (by_smem < 6 ? by_smem : 6);
+    static constexpr int up_stages = (NB > 4 || chunked) ? up_stages_wanted : stages;
     static constexpr int off_w = 0;
     static constexpr int off_up = off_w + stages * kUWStage;
     static constexpr int off_slab = off_up + up_stages * up_stage;     // 1024-aligned (multiples of 2 KB)
@@ -69,7 +85,7 @@ struct UmmaLayout {
     static constexpr int off_units = off_red + 256;
     static constexpr int off_segs = off_units + kUnitCache * (int)sizeof(UnitDev);
     static constexpr int total = off_segs + kSegCache * (int)sizeof(SegDev) + 1024;
-    static_assert(stages >= 3 && up_stages >= 3 && up_stages <= 8 && total <= 227 * 1024, "shared memory budget");
+    static_assert(stages >= 2 && up_stages >= 3 && up_stages <= 8 && total <= 227 * 1024, "shared memory budget");
 };
 
 // ---- tcgen05 wrappers ----
@@ -230,9 +246,61 @@ __device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const uint
     }
 }
 
-template <int NB, bool GEMV>
+// The same staging without the register hand-over, for slabs too large to park in registers across a unit
+// (NB > 8: 16 and more 16-byte words per thread): loaded and committed four words at a time at the unit's start.
+template <int NB>
+__device__ __forceinline__ void umma_slab_direct(unsigned char* slab, const SegDev& sg, const Plan& plan, int S, int col0, int tid) {
+    constexpr int chunks = kUN / 8;
+    constexpr int per_thread = NB * 8 * chunks / kUEpi;
+    static_assert(per_thread % 4 == 0, "four words in flight");
+    const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(sg.down);
+#pragma unroll 1
+    for (int j0 = 0; j0 < per_thread; j0 += 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = tid + (j0 + u) * kUEpi;
+            const int q = i / chunks, c = (i % chunks) * 8;
+            v[u] = make_uint4(0u, 0u, 0u, 0u);
+            if (q < S && col0 + c < sg.d_in) {
+                int qb, qr;
+                rank_divmod(q, sg.rank, qb, qr);
+                v[u] = __ldg(reinterpret_cast<const uint4*>(base + (long long)plan.expert[qb] * sg.down_estride + (long long)qr * sg.ld_down + col0 + c));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = tid + (j0 + u) * kUEpi;
+            const int q = i / chunks, c = (i % chunks) * 8;
+            uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
+            if (q < S) {
+                int wb, wr;
+                rank_divmod(q, sg.rank, wb, wr);
+                const float w = plan.weight[wb];
+                const uint32_t in[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                uint32_t oh[4], ol[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float f0 = __fmul_rn(w, bf16lo_to_f32(in[e]));
+                    const float f1 = __fmul_rn(w, bf16hi_to_f32(in[e]));
+                    const uint32_t h = pack_bf16x2(f0, f1);
+                    oh[e] = h;
+                    ol[e] = pack_bf16x2(f0 - bf16lo_to_f32(h), f1 - bf16hi_to_f32(h));
+                }
+                hi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+                lo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+            }
+            const int off = (q >> 3) * kUSlabBlock + (c >> 3) * 128 + (q & 7) * 16;
+            *reinterpret_cast<uint4*>(slab + off) = hi;
+            *reinterpret_cast<uint4*>(slab + NB * kUSlabBlock + off) = lo;
+        }
+    }
+}
+
+template <int NB, bool GEMV, int CH = NB>
 __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_constant__ MmaParams mp) {
-    using L = UmmaLayout<NB, GEMV>;
+    using L = UmmaLayout<NB, GEMV, CH>;
+    constexpr bool kPrefetchSlab = NB <= 8;   // the next unit's DOWN rows wait in registers (umma_slab_prefetch)
     constexpr int kSt = L::stages, kUpSt = L::up_stages;
     extern __shared__ unsigned char smem_dyn[];
     const SwitchParams& p = mp.base;
@@ -345,32 +413,43 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 }
             }
         } else if (warp == kUEpiWarps + 1) {
-            // ============ UP producer: one 2 KB bulk copy per selected expert block ============
+            // ============ UP producer: one 2 KB bulk copy per selected expert block (rank 8), one swizzled box per
+            // block otherwise; a tile's blocks go to one stage, or -- K-chunked -- to one stage per CH k-groups ============
             if (lane == 0) {
                 UmmaIter ti;
                 ti.init(p, unit_cache);
                 SegDev sg;
                 int cur_seg = -1;
+                int uit = 0;
                 for (int it = 0; ti.valid(p); ++it) {
-                    const int stage = it % kUpSt;
-                    const uint32_t ph = (it / kUpSt) & 1;
                     if (ti.un.seg != cur_seg) {
                         cur_seg = ti.un.seg;
                         sg = seg_of(ti.un);
                     }
-                    mbar_wait(&up_empty[stage], ph ^ 1);
                     const uint32_t blk_bytes = (uint32_t)kUM * sg.rank * 2;
-                    mbar_expect_tx(&up_full[stage], n_blocks * blk_bytes);
-                    if (sg.rank == 8) {   // an expert block is 128 contiguous 16-byte rows: one bulk copy
-                        const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
-                        for (int b = 0; b < n_blocks; ++b)
-                            bulk_load_1d(up_base + stage * L::up_stage + b * kUBlockBytes,
-                                         upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &up_full[stage]);
-                    } else {              // 128 rows x rank through the tensor map whose swizzle span is the row
-                        const CUtensorMap* tm = mp.tmaps_up + ti.un.seg;
-                        for (int b = 0; b < n_blocks; ++b)
-                            tma_load_2d_addr(up_base + stage * L::up_stage + b * blk_bytes, tm, 0, plan.expert[b] * sg.d_out + ti.m0,
-                                             &up_full[stage]);
+                    const int per_chunk = (CH * 8) / sg.rank;                      // expert blocks per stage
+                    const int n_ch = n_blocks > 0 ? (n_blocks + per_chunk - 1) / per_chunk : 1;
+                    for (int c = 0; c < n_ch; ++c, ++uit) {
+                        const int stage = uit % kUpSt;
+                        const uint32_t ph = (uit / kUpSt) & 1;
+                        const int b0 = c * per_chunk, b1 = min(n_blocks, b0 + per_chunk);
+                        mbar_wait(&up_empty[stage], ph ^ 1);
+                        if (mp.dbg & 64) {   // timing experiment: no UP traffic at all
+                            mbar_expect_tx(&up_full[stage], 0);
+                            continue;
+                        }
+                        mbar_expect_tx(&up_full[stage], (uint32_t)max(0, b1 - b0) * blk_bytes);
+                        if (sg.rank == 8) {   // an expert block is 128 contiguous 16-byte rows: one bulk copy
+                            const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
+                            for (int b = b0; b < b1; ++b)
+                                bulk_load_1d(up_base + stage * L::up_stage + (b - b0) * kUBlockBytes,
+                                             upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &up_full[stage]);
+                        } else {              // 128 rows x rank through the tensor map whose swizzle span is the row
+                            const CUtensorMap* tm = mp.tmaps_up + ti.un.seg;
+                            for (int b = b0; b < b1; ++b)
+                                tma_load_2d_addr(up_base + stage * L::up_stage + (b - b0) * blk_bytes, tm, 0, plan.expert[b] * sg.d_out + ti.m0,
+                                                 &up_full[stage]);
+                        }
                     }
                     ti.next(p);
                 }
@@ -384,33 +463,54 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 ti.init(p, unit_cache);
                 const int rank = ti.valid(p) ? seg_of(ti.un).rank : 8;   // one rank for the whole table (eligibility)
                 const int ksteps = (n_blocks * rank + 15) >> 4;          // rank-16 steps over the stacked ranks
-                int unit_j = -1;
+                const int per_chunk = (CH * 8) / rank;
+                const int n_ch = n_blocks > 0 ? (n_blocks + per_chunk - 1) / per_chunk : 1;
+                // ONE thread issues every MMA of the CTA, so what it executes per MMA is on the tile's critical path:
+                // the descriptors are a per-table prototype plus a precomputed 16-byte-unit offset per rank-16 step
+                // (computing them from scratch -- divisions by the run-time rank -- cost ~2x the MMA itself).
+                constexpr int kStepsPerChunk = CH / 2;
+                uint32_t a_inc[kStepsPerChunk];
+#pragma unroll
+                for (int k2 = 0; k2 < kStepsPerChunk; ++k2)
+                    a_inc[k2] = (uint32_t)(umma_a_desc(0u, rank, k2) & 0x3fffu);          // (offset inside a stage) >> 4
+                const uint64_t a_proto = umma_a_desc(0u, rank, 0);                           // layout / LBO / SBO of the table's rank
+                const uint64_t b_proto = umma_desc(0u, kUSlabBlock, 128);
+                const uint32_t slab16 = slab_base >> 4;
+                int unit_j = -1, uit = 0;
                 for (int it = 0; ti.valid(p); ++it) {
-                    const int stage = it % kUpSt, buf = it & 1;
-                    const uint32_t ph = (it / kUpSt) & 1, aph = (it >> 1) & 1;
+                    const int buf = it & 1;
+                    const uint32_t aph = (it >> 1) & 1;
                     if (ti.j != unit_j) {   // the unit's slab has been written (and made visible to the tensor core)
                         unit_j = ti.j;
                         mbar_wait(slab_bar, (uint32_t)unit_j & 1);
                     }
-                    mbar_wait(&up_full[stage], ph);
                     mbar_wait(&acc_empty[buf], aph ^ 1);
-                    tc_fence_after();
-                    const uint32_t a0 = up_base + stage * L::up_stage;
+                    const uint32_t d_tmem = tmem + buf * kUN;
                     uint32_t accumulate = 0;
-                    for (int half = 0; half < 2; ++half)
-                        for (int ks = 0; ks < ksteps; ++ks) {
-                            const uint64_t da = umma_a_desc(a0, rank, ks);
-                            const uint64_t db = umma_desc(slab_base + (half * NB + ks * 2) * kUSlabBlock, kUSlabBlock, 128);
-                            umma_bf16(tmem + buf * kUN, da, db, idesc, accumulate);
-                            accumulate = 1;
+                    for (int c = 0; c < n_ch; ++c, ++uit) {
+                        const int stage = uit % kUpSt;
+                        const uint32_t ph = (uit / kUpSt) & 1;
+                        mbar_wait(&up_full[stage], ph);
+                        tc_fence_after();
+                        const uint32_t a16 = (up_base + stage * L::up_stage) >> 4;
+                        const int ks0 = c * kStepsPerChunk;
+                        const int n_half = (mp.dbg & 32) ? 1 : 2;   // (dbg 32: timing experiment without the lo half)
+                        for (int half = 0; half < n_half; ++half) {
+                            const uint32_t b16 = slab16 + (uint32_t)((half * NB + ks0 * 2) * (kUSlabBlock >> 4));
+#pragma unroll
+                            for (int k2 = 0; k2 < kStepsPerChunk; ++k2) {
+                                if (ks0 + k2 < ksteps) {
+                                    umma_bf16(d_tmem, a_proto + (a16 + a_inc[k2]), b_proto + (b16 + (uint32_t)(k2 * 2 * (kUSlabBlock >> 4))), idesc,
+                                              accumulate);
+                                    accumulate = 1;
+                                }
+                            }
                         }
-                    if (ksteps == 0) {   // nothing selected (plain GEMV): D = 0 through a K = 16 product with the zeroed slot
-                        const uint64_t da = umma_a_desc(a0, rank, 0);
-                        const uint64_t db = umma_desc(slab_base, kUSlabBlock, 128);
-                        umma_bf16(tmem + buf * kUN, da, db, idesc, 0);
+                        if (ksteps == 0)   // nothing selected (plain GEMV): D = 0 through a K = 16 product with the zeroed slot
+                            umma_bf16(d_tmem, a_proto + a16, b_proto + slab16, idesc, 0);
+                        umma_commit(smem_u32(&up_empty[stage]));   // the UP stage is free once these MMAs have read it
                     }
-                    umma_commit(smem_u32(&acc_full[buf]));
-                    umma_commit(smem_u32(&up_empty[stage]));   // the UP stage is free once these MMAs have read it
+                    umma_commit(smem_u32(&acc_full[buf]));          // every MMA of the tile has completed: the epilogue may read D
                     ti.next(p);
                 }
             }
@@ -570,8 +670,8 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
 
                 const int rank = seg_of(ti.un).rank;
                 const int S = n_blocks * rank;
-                uint4 dn_regs[NB * 8 * (kUN / 8) / kUEpi];
-                umma_slab_prefetch<NB>(dn_regs, seg_of(ti.un), plan, S, ti.un.col0, tid);
+                uint4 dn_regs[kPrefetchSlab ? NB * 8 * (kUN / 8) / kUEpi : 1];
+                if constexpr (kPrefetchSlab) umma_slab_prefetch<NB>(dn_regs, seg_of(ti.un), plan, S, ti.un.col0, tid);
                 bool new_unit = true;
                 int yoff = 0;
                 unsigned long long* acc_out = nullptr;
@@ -594,11 +694,12 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                 published = ti.un.phase;
                             }
                         }
-                        umma_slab_commit<NB>(slab, dn_regs, plan, S, rank, tid);
+                        if constexpr (kPrefetchSlab) umma_slab_commit<NB>(slab, dn_regs, plan, S, rank, tid);
+                        else if (!(mp.dbg & 128) || it == 0) umma_slab_direct<NB>(slab, seg_of(ti.un), plan, S, ti.un.col0, tid);   // (dbg 128: timing experiment)
                         fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
                         __syncwarp();
                         if (lane == 0) mbar_arrive(slab_bar);
-                        {   // start fetching the NEXT unit's DOWN rows; they are committed at its start
+                        if constexpr (kPrefetchSlab) {   // start fetching the NEXT unit's DOWN rows; they are committed at its start
                             const UnitDev nu = ti.peek(p);
                             if (nu.rows > 0) umma_slab_prefetch<NB>(dn_regs, seg_of(nu), plan, S, nu.col0, tid);
                         }

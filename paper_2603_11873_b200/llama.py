@@ -359,8 +359,11 @@ class LlamaEngine:
         self.targets, self.bank_down, self.bank_up = targets, downs, ups
         self.pristine = [t.copy() for t in targets] if (cfg.adapters and cfg.keep_pristine) else None
         self.table = SwitchTable(targets, downs, ups, pristine=self.pristine) if cfg.adapters else None
+        # stacked ranks one launch takes: 256 on the tcgen05 path (K-chunked), 64 otherwise; beyond it the switch
+        # runs as several tensor-path passes (rank-64 tables, tables off the tcgen05 path)
+        self.rank_limit = self.table.one_launch_ranks() if self.table is not None else 0
         self.split_switch = bool(self.table is not None and cfg.split_switch and self.table.info()["tensor_path"]
-                                 and cfg.rank <= SwitchTable.TENSOR_PATH_RANKS)
+                                 and cfg.rank <= self.rank_limit)
         cos, sin = rope_tables(cfg)
         self.cos, self.sin = put(cos, torch.float32), put(sin, torch.float32)
         self.k_cache = [torch.zeros((self.kv_local, cfg.max_seq, hd), dtype=bf, device=dev) for _ in range(cfg.layers)]
@@ -410,12 +413,14 @@ class LlamaEngine:
         self.gc_done = torch.zeros(4 * cfg.layers, dtype=torch.int32, device=dev)
         # ---- fused switch + GEMV ("chase") ----
         want = cfg.forward_mode
-        # more than 64 stacked ranks: the switch runs in tensor-path passes and the LAST pass carries the GEMVs
-        self.chase_split = bool(self.split_switch and 2 * cfg.top_k * cfg.rank > SwitchTable.TENSOR_PATH_RANKS)
+        # more stacked ranks than one launch takes: the switch runs in tensor-path passes and the LAST pass carries the GEMVs
+        steady_ranks = (1 if cfg.switch_mode == "from_pristine" else 2) * cfg.top_k * cfg.rank
+        self.chase_split = bool(self.split_switch and steady_ranks > self.rank_limit)
         can = cfg.adapters and self.table is not None and self.table.info()["tensor_path"] \
-            and (2 * cfg.top_k * cfg.rank <= 64 or self.chase_split) and cfg.compute in ("auto", "mma")
+            and (steady_ranks <= self.rank_limit or self.chase_split) and cfg.compute in ("auto", "mma")
         if want == "chase" and not can:
-            raise ConfigError("forward_mode='chase' needs the tensor path (bf16, rank % 8 == 0) and 2*top_k*rank <= 64")
+            raise ConfigError("forward_mode='chase' needs the tensor path (bf16, rank % 8 == 0) and a steady switch of at most "
+                              f"{self.rank_limit} stacked ranks in one launch")
         self.chase = can and want in ("auto", "chase")
         if self.chase:
             # launches of one token: [qkv(0)] attn [o gu down qkv(1)] attn ... [o gu down (L-1)]
@@ -443,7 +448,8 @@ class LlamaEngine:
             # tcgen05 path: RMSNorm scales are deferred -- one CTA computes them, the consumers of q|k|v
             # (attention) and gate|up (the SiLU prologue of the down projection) apply them
             stacked = (1 if cfg.switch_mode == "from_pristine" else 2) * cfg.top_k * cfg.rank   # ranks of a steady switch
-            umma_ranks = int(os.environ.get("AF_UMMA_MAX_RANKS_CHAIN", "32"))   # af_api.cu: stacked ranks the tcgen05 chain kernel takes
+            # af_api.cu: stacked ranks the tcgen05 chain kernel takes
+            umma_ranks = min(int(os.environ.get("AF_UMMA_MAX_RANKS_CHAIN", "256")), self.rank_limit)
             self.defer_norm = bool(self.table.info().get("umma_path")) and cfg.defer_norm and stacked <= umma_ranks
             self.inv_qkv = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
             self.inv_gu = torch.ones(cfg.layers, dtype=torch.float32, device=dev)
@@ -478,7 +484,7 @@ class LlamaEngine:
         kw.setdefault("compute", self.cfg.compute)
         cfg = self.cfg
         blocks = (cfg.top_k if (prev is not None and kw.get("mode", "inplace") == "inplace") else 0) + (cfg.top_k if cur is not None else 0)
-        if self.split_switch and blocks * cfg.rank > SwitchTable.TENSOR_PATH_RANKS and kw["compute"] in ("auto", "mma") \
+        if self.split_switch and blocks * cfg.rank > self.rank_limit and kw["compute"] in ("auto", "mma") \
                 and all(isinstance(dec, DeviceDecision) for dec in (prev, cur) if dec is not None):
             # more stacked ranks than one tensor-path launch holds (Llama-2-70B): a few tensor-path passes
             # instead of one FMA-bound CUDA-core pass

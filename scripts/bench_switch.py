@@ -22,10 +22,15 @@ CONFIGS = {
     "7b": dict(layers=32, d=4096, ffn=11008, kv=4096, experts=8, rank=8, k=2),
     "8b": dict(layers=32, d=4096, ffn=14336, kv=1024, experts=16, rank=16, k=2),
     "13b": dict(layers=40, d=5120, ffn=13824, kv=5120, experts=8, rank=8, k=2),
+    # one tensor-parallel shard of Llama-2-70B (tp 8): explicit (d_out, d_in) of q k v o gate up down
+    "70b-tp8": dict(layers=80, experts=8, rank=32, k=4,
+                    shapes=[(1024, 8192), (128, 8192), (128, 8192), (8192, 1024), (3584, 8192), (3584, 8192), (8192, 3584)]),
 }
 
 
 def shapes(c):
+    if "shapes" in c:
+        return c["shapes"]
     d, ffn, kv = c["d"], c["ffn"], c["kv"]
     if ffn == 0:
         return [(d, d)]
@@ -40,8 +45,11 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--pristine", action="store_true")
+    ap.add_argument("--k", type=int, default=0, help="override top-k (stacked ranks of the steady switch = 2 k rank)")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
+    if args.k:
+        c["k"] = args.k
     if args.layers:
         c["layers"] = args.layers
     dev = torch.device("cuda", 0)
@@ -89,7 +97,7 @@ def main():
             ms = float(np.mean(times))
             s = 2 * k * c["rank"]
             gbs = table.switch_bytes(s) / ms / 1e6
-            print(json.dumps({"mode": mode, "ms": round(ms, 4), "min_ms": round(min(times), 4), "GBps": round(gbs, 1),
+            print(json.dumps({"mode": mode, "kernel": af._capi.lib().af_last_switch_kernel().decode(), "stacked_ranks": s, "ms": round(ms, 4), "min_ms": round(min(times), 4), "GBps": round(gbs, 1),
                               "frac_of_measured_peak": round(gbs / peaks["hbm_gbs"], 4), "bytes": table.switch_bytes(s),
                               "TFLOPs": round(table.switch_flops(s) / ms / 1e9, 1)}), flush=True)
         except Exception as e:  # noqa: BLE001

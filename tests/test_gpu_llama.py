@@ -39,12 +39,13 @@ def _oracle_for(eng, llama):
                           rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps, max_seq=cfg.max_seq)
 
 
-@pytest.mark.parametrize("shape", ["r8", "r16-gqa"])
+@pytest.mark.parametrize("shape", ["r8", "r16-gqa", "r32-k4"])
 @pytest.mark.parametrize("forward_mode", ["chase", "separate"])
 @pytest.mark.parametrize("switch_mode", ["inplace", "from_pristine"])
 def test_decode_steps_against_oracle(llama, switch_mode, forward_mode, shape):
     # "r16-gqa": BASELINE configs[2]-like -- 16 experts of rank 16, 4 query heads on 1 kv head
-    extra = dict(experts=16, rank=16, n_heads=4, n_kv_heads=1) if shape == "r16-gqa" else {}
+    # "r32-k4": BASELINE configs[4]-like -- rank 32, top-4: 256 stacked ranks in a steady switch, ONE K-chunked launch
+    extra = {"r16-gqa": dict(experts=16, rank=16, n_heads=4, n_kv_heads=1), "r32-k4": dict(experts=8, rank=32, top_k=4)}.get(shape, {})
     cfg = llama.preset("tiny", switch_mode=switch_mode, max_seq=32, forward_mode=forward_mode, **extra)
     eng = llama.LlamaEngine(cfg, init="host")
     assert eng.table.info()["tensor_path"]
@@ -369,12 +370,14 @@ def test_tp_forward_in_lockstep_equals_the_full_model(llama, tp, forward_mode):
 @pytest.mark.parametrize("forward_mode", ["separate", "chase"])
 @pytest.mark.parametrize("switch_mode", ["inplace", "from_pristine"])
 def test_switch_in_passes_for_more_than_64_stacked_ranks(llama, switch_mode, forward_mode):
-    """BASELINE configs[4]-like (rank 32, top-4: 256 stacked ranks in a steady switch): the engine cuts the
-    switch into tensor-path passes of 64 stacked ranks.  Against the single CUDA-core pass over all ranks
-    the weights differ by at most one bf16 rounding per pass, the logits agree, the backbone is restored."""
+    """The fallback for tables whose stacked rank exceeds what ONE launch takes (rank-64 tables: 64; every
+    BASELINE configuration fits one K-chunked tcgen05 launch and never gets here): the engine cuts the switch
+    into tensor-path passes.  Rank 64, top-2 -- 256 stacked ranks in a steady switch, one expert per pass.
+    Against the single CUDA-core pass over all ranks the weights differ by at most one bf16 rounding per
+    pass, the logits agree, the backbone is restored."""
     from paper_2603_11873_b200 import _capi
 
-    base = dict(max_seq=16, experts=8, rank=32, top_k=4, switch_mode=switch_mode)
+    base = dict(max_seq=16, experts=8, rank=64, top_k=2, switch_mode=switch_mode, refresh_every=0)
     forced = np.random.Generator(np.random.PCG64(41)).integers(0, 512, 6)
     one = llama.LlamaEngine(llama.preset("tiny", split_switch=False, forward_mode="separate", **base), init="host")
     many = llama.LlamaEngine(llama.preset("tiny", forward_mode=forward_mode, **base), init="host")
@@ -391,7 +394,7 @@ def test_switch_in_passes_for_more_than_64_stacked_ranks(llama, switch_mode, for
         b = many.decode_step(graph=False)
         launches = _capi.launch_count() - before
         assert many.decision() == one.decision()
-        want_passes = (2 if switch_mode == "from_pristine" else (4 if step else 2))    # 2 experts of rank 32 per pass
+        want_passes = (2 if switch_mode == "from_pristine" else (4 if step else 2))    # 1 expert of rank 64 per pass
         if forward_mode == "separate":
             assert launches - single == want_passes - 1, f"step {step}: {launches} launches against {single}"
         for i, (ta, tb) in enumerate(zip(one.targets, many.targets)):
