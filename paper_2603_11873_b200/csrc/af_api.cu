@@ -1379,6 +1379,21 @@ static int attn_decode_impl(const float* qkv, const long long* qkv_fix, const fl
     AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode_kernel<EL>, qkv, qkv_fix, qkv_scale, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,  \
                                    (int)n_kv_heads, (int)head_dim, (int)max_seq, scale, (int)n_split, workspace,           \
                                    reinterpret_cast<int*>(tickets), out))
+    // hd 64 / 128: the latency-oriented form (KV chunk staged in shared memory ahead of the dependency wait, 64-position splits)
+    static const int env_attn2 = [] { const char* e = getenv("AF_ATTN2"); return e ? atoi(e) : 1; }();
+    if (env_attn2 && aligned && (head_dim == 64 || head_dim == 128) && n_split <= kAt2MaxSplit) {
+        cfg.gridDim = dim3(n_heads * n_split);
+        cfg.blockDim = dim3(kAt2Threads);
+        cfg.dynamicSmemBytes = 2 * kAt2Chunk * head_dim * 2;
+        if (head_dim == 128)
+            AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode2_kernel<128>, qkv, qkv_fix, qkv_scale, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,
+                                           (int)n_kv_heads, (int)max_seq, scale, (int)n_split, workspace, reinterpret_cast<int*>(tickets), out));
+        else
+            AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_decode2_kernel<64>, qkv, qkv_fix, qkv_scale, kc, vc, cos_table, sin_table, pos_dev, (int)n_heads,
+                                           (int)n_kv_heads, (int)max_seq, scale, (int)n_split, workspace, reinterpret_cast<int*>(tickets), out));
+        AF_LAUNCH_CHECK("attn_decode2_kernel");
+        return AF_OK;
+    }
     if (aligned && head_dim == 64) AF_ATTN(2);
     else if (aligned && head_dim == 128) AF_ATTN(4);
     else if (aligned && head_dim == 256) AF_ATTN(8);

@@ -556,6 +556,223 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const float* 
     if (tid == 0) tickets[h] = 0;  // ready for the next launch (graph replay)
 }
 
+// ---- decode attention, second form: the KV chunk of a split is staged in shared memory with asynchronous
+// 16-byte copies issued BEFORE griddepcontrol.wait ----
+// The attention sits between two fused weight launches on the critical path of every layer, so what counts is
+// its latency, not its bandwidth (16.8 MB of KV at 1024 positions of Llama-2-7B are 2.6 us of HBM time; the first
+// kernel above takes 22.7 us there, 11 us at 128 positions: a chain of ~8 dependent global round trips).  Here:
+//   * everything that does not depend on the previous kernel -- the position, the rotary row, and the split's
+//     whole K/V chunk (positions < pos are static during a step) -- is requested before the wait for it;
+//   * splits are 64 positions (16 at 1024, up to 32 per head), one position per warp and step, four steps
+//     of dot products in flight per warp, so the serial online-softmax chain is 4 long per warp at 64 positions;
+//   * the combine of a head's splits reads every partial in one batch of independent loads.
+// hd = 64 or 128 (16-byte aligned caches); other head sizes keep attn_decode_kernel.
+constexpr int kAt2Threads = 128;
+constexpr int kAt2Warps = kAt2Threads / 32;
+constexpr int kAt2Chunk = 64;          // positions per split (and per shared-memory chunk)
+constexpr int kAt2MaxSplit = 32;
+
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int HD>
+__global__ void __launch_bounds__(kAt2Threads) attn_decode2_kernel(const float* __restrict__ qkv, const long long* __restrict__ qkv_fix,
+                                                                   const float* __restrict__ qkv_scale, __nv_bfloat16* __restrict__ k_cache,
+                                                                   __nv_bfloat16* __restrict__ v_cache, const float* __restrict__ cos_t,
+                                                                   const float* __restrict__ sin_t, const int32_t* __restrict__ pos_dev,
+                                                                   int n_heads, int n_kv, int max_seq, float scale, int n_split,
+                                                                   float* __restrict__ ws, int* __restrict__ tickets, float* __restrict__ out) {
+    constexpr int EL = HD / 32;            // dims per lane (contiguous)
+    constexpr int RC = HD / 8;             // 16-byte chunks per cached row
+    constexpr int half = HD / 2;
+    extern __shared__ __align__(16) unsigned char at2_smem[];
+    __nv_bfloat16* kbuf = reinterpret_cast<__nv_bfloat16*>(at2_smem);                    // [kAt2Chunk][HD]
+    __nv_bfloat16* vbuf = kbuf + kAt2Chunk * HD;
+    __shared__ float q_s[HD], k_s[HD], v_s[HD];
+    __shared__ float m_s[kAt2Warps], l_s[kAt2Warps];
+    __shared__ float acc_s[kAt2Warps][HD];
+    __shared__ float pm_s[kAt2MaxSplit], pl_s[kAt2MaxSplit];
+    __shared__ int is_last;
+    const int h = blockIdx.x / n_split, sp = blockIdx.x % n_split;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int group = n_heads / n_kv, kvh = h / group;
+    // The position was written by the previous token's bookkeeping launch, which completed before this token's
+    // first kernel started (the token boundary has plain launches): reading it ahead of the wait is safe.
+    const int pos = *pos_dev;
+    if (pos < 0 || pos >= max_seq) return;   // KV cache full: touch nothing (the host side raises StateError before it gets here)
+    const int n_pos = pos + 1;
+    n_split = min(n_split, max(1, (n_pos + kAt2Chunk - 1) / kAt2Chunk));
+    if (sp >= n_split) return;
+    const int per = (n_pos + n_split - 1) / n_split;
+    const int t0 = sp * per, t1 = min(n_pos, t0 + per);
+    const __nv_bfloat16* kbase = k_cache + (long long)kvh * max_seq * HD;
+    const __nv_bfloat16* vbase = v_cache + (long long)kvh * max_seq * HD;
+    auto prefetch = [&](int base) {
+        const int n = min(kAt2Chunk, t1 - base);
+        const uint32_t ks = smem_u32(kbuf), vs = smem_u32(vbuf);
+        for (int idx = tid; idx < n * RC; idx += kAt2Threads) {
+            const int r = idx / RC, c = idx % RC;
+            const int t = base + r;
+            if (t != pos) {   // the new position is not in the cache yet: it is used from k_s / v_s
+                cp_async16(ks + (r * HD + c * 8) * 2, kbase + (long long)t * HD + c * 8);
+                cp_async16(vs + (r * HD + c * 8) * 2, vbase + (long long)t * HD + c * 8);
+            }
+        }
+        cp_async_commit();
+    };
+    prefetch(t0);
+    float rc_ = 1.f, rs_ = 0.f;
+    if (tid < half) {
+        rc_ = __ldg(cos_t + (long long)pos * half + tid);
+        rs_ = __ldg(sin_t + (long long)pos * half + tid);
+    }
+    pdl_wait();               // q | k | v of the new token come from the previous kernel
+    pdl_launch_dependents();
+    const long long oq = (long long)h * HD, ok = (long long)n_heads * HD + (long long)kvh * HD,
+                    ov = (long long)(n_heads + n_kv) * HD + (long long)kvh * HD;
+    const float fix_scale = (qkv_scale ? *qkv_scale : 1.0f) * (1.0f / (float)(1ll << AF_FIX_SHIFT));
+    auto ld = [&](long long i) { return qkv_fix ? __ll2float_rn(__ldcg(qkv_fix + i)) * fix_scale : __ldcg(qkv + i); };
+    if (tid < half) {   // RoPE (rotate-half); the cache stores bf16, and the new position uses the rounded values too
+        const float q0 = ld(oq + tid), q1 = ld(oq + tid + half), k0 = ld(ok + tid), k1 = ld(ok + tid + half);
+        q_s[tid] = q0 * rc_ - q1 * rs_;
+        q_s[tid + half] = q1 * rc_ + q0 * rs_;
+        k_s[tid] = __bfloat162float(__float2bfloat16_rn(k0 * rc_ - k1 * rs_));
+        k_s[tid + half] = __bfloat162float(__float2bfloat16_rn(k1 * rc_ + k0 * rs_));
+    }
+    for (int i = tid; i < HD; i += kAt2Threads) v_s[i] = __bfloat162float(__float2bfloat16_rn(ld(ov + i)));
+    __syncthreads();
+    if (h % group == 0 && pos >= t0 && pos < t1) {  // one CTA per kv head appends to the cache
+        __nv_bfloat16* kc = k_cache + ((long long)kvh * max_seq + pos) * HD;
+        __nv_bfloat16* vc = v_cache + ((long long)kvh * max_seq + pos) * HD;
+        for (int i = tid; i < HD; i += kAt2Threads) {
+            kc[i] = __float2bfloat16_rn(k_s[i]);
+            vc[i] = __float2bfloat16_rn(v_s[i]);
+        }
+    }
+    float qr[EL], acc[EL];
+#pragma unroll
+    for (int j = 0; j < EL; ++j) {
+        qr[j] = q_s[lane * EL + j] * scale;
+        acc[j] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    for (int base = t0; base < t1; base += kAt2Chunk) {
+        if (base > t0) {          // contexts beyond n_split * 64 positions: further chunks through the same buffer
+            __syncthreads();
+            prefetch(base);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        const int n = min(kAt2Chunk, t1 - base);
+        constexpr int kFly = 4;   // positions per warp whose dot products are in flight together
+        for (int r0 = warp; r0 < n; r0 += kAt2Warps * kFly) {
+            float kf[kFly][EL], vf[kFly][EL], dot[kFly];
+#pragma unroll
+            for (int u = 0; u < kFly; ++u) {
+                const int r = r0 + u * kAt2Warps;
+                if (r < n && base + r != pos) {
+                    load_bf16_vec<EL>(kbuf + r * HD + lane * EL, kf[u]);
+                    load_bf16_vec<EL>(vbuf + r * HD + lane * EL, vf[u]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < EL; ++j) {
+                        kf[u][j] = r < n ? k_s[lane * EL + j] : 0.f;
+                        vf[u][j] = r < n ? v_s[lane * EL + j] : 0.f;
+                    }
+                }
+                float d = 0.f;
+#pragma unroll
+                for (int j = 0; j < EL; ++j) d = fmaf(qr[j], kf[u][j], d);
+                dot[u] = d;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < kFly; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+            float m_new = m;
+#pragma unroll
+            for (int u = 0; u < kFly; ++u)
+                if (r0 + u * kAt2Warps < n) m_new = fmaxf(m_new, dot[u]);
+            const float corr = expf(m - m_new);   // exp(-inf) = 0 on the first group
+            l *= corr;
+#pragma unroll
+            for (int j = 0; j < EL; ++j) acc[j] *= corr;
+#pragma unroll
+            for (int u = 0; u < kFly; ++u)
+                if (r0 + u * kAt2Warps < n) {     // warp-uniform
+                    const float pw = expf(dot[u] - m_new);
+                    l += pw;
+#pragma unroll
+                    for (int j = 0; j < EL; ++j) acc[j] = fmaf(pw, vf[u][j], acc[j]);
+                }
+            m = m_new;
+        }
+    }
+    if (lane == 0) {
+        m_s[warp] = m;
+        l_s[warp] = l;
+    }
+#pragma unroll
+    for (int j = 0; j < EL; ++j) acc_s[warp][lane * EL + j] = acc[j];
+    __syncthreads();
+    // ---- merge the warps of this CTA ----
+    float mm = -INFINITY;
+#pragma unroll
+    for (int wv = 0; wv < kAt2Warps; ++wv) mm = fmaxf(mm, m_s[wv]);
+    float ll = 0.f;
+#pragma unroll
+    for (int wv = 0; wv < kAt2Warps; ++wv) ll += (m_s[wv] == -INFINITY) ? 0.f : l_s[wv] * expf(m_s[wv] - mm);
+    float o_part = 0.f;      // element tid of this split's un-normalised output (HD <= kAt2Threads)
+    if (tid < HD) {
+#pragma unroll
+        for (int wv = 0; wv < kAt2Warps; ++wv)
+            if (m_s[wv] != -INFINITY) o_part += acc_s[wv][tid] * expf(m_s[wv] - mm);
+    }
+    if (n_split == 1) {
+        if (tid < HD) out[(long long)h * HD + tid] = o_part / ll;
+        return;
+    }
+    // ---- partial of this split -> workspace; the last CTA of the head to arrive combines ----
+    float* my = ws + ((long long)h * n_split + sp) * (HD + 2);
+    if (tid < HD) my[2 + tid] = o_part;
+    if (tid == 0) {
+        my[0] = mm;
+        my[1] = ll;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = (atomicAdd(&tickets[h], 1) == n_split - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const float* hp = ws + (long long)h * n_split * (HD + 2);
+    if (tid < n_split) {     // one batch of independent loads: every split's (max, sum) ...
+        pm_s[tid] = __ldcg(hp + (long long)tid * (HD + 2));
+        pl_s[tid] = __ldcg(hp + (long long)tid * (HD + 2) + 1);
+    }
+    float pv[kAt2MaxSplit];
+    if (tid < HD) {          // ... and this thread's element of every partial
+#pragma unroll
+        for (int s2 = 0; s2 < kAt2MaxSplit; ++s2) pv[s2] = s2 < n_split ? __ldcg(hp + (long long)s2 * (HD + 2) + 2 + tid) : 0.f;
+    }
+    __syncthreads();
+    float gm = -INFINITY;
+    for (int s2 = 0; s2 < n_split; ++s2) gm = fmaxf(gm, pm_s[s2]);
+    float gl = 0.f, o = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < kAt2MaxSplit; ++s2)
+        if (s2 < n_split && pm_s[s2] != -INFINITY) {
+            const float e = expf(pm_s[s2] - gm);
+            gl += pl_s[s2] * e;
+            o += pv[s2] * e;
+        }
+    if (tid < HD) out[(long long)h * HD + tid] = o / gl;
+    if (tid == 0) tickets[h] = 0;  // ready for the next launch (graph replay)
+}
+
 // out[i] = (res ? res[i] : 0) + fixed-point accumulator i (the residual stream after the last fused
 // switch + GEMV launch, as a plain f32 vector for the lm_head GEMV).
 __global__ void accum_to_f32_kernel(const long long* __restrict__ acc, const float* __restrict__ res, float* __restrict__ out, int n) {

@@ -65,7 +65,7 @@ class LlamaConfig:
     refresh_every: int = 16
     adapters: bool = True            # False = adapter-free backbone (the reference's BASE strategy)
     keep_pristine: bool = True
-    attn_splits: int = 0             # CTAs per head in decode attention; 0 = auto (max_seq / 32, at most 8)
+    attn_splits: int = 0             # CTAs per head in decode attention; 0 = auto (one per 64 positions of max_seq, at most 32)
     # "chase": the forward GEMV of every projection is fused into the switch of its weights (one pass
     # over W per token instead of switch + forward); "separate": one switch launch, then plain GEMVs;
     # "auto": chase when it applies (adapters, single rank, tensor path)
@@ -403,7 +403,12 @@ class LlamaEngine:
         # grid of the decode attention: sized for the longest context (one split per 32 positions, at most 8 --
         # measured: 1 split costs 13 % of the step at 400 positions, 12 or 16 cost more than 8 even at 1800);
         # the kernel itself uses fewer splits while the context is short
-        self.attn_splits = cfg.attn_splits if cfg.attn_splits > 0 else (1 if cfg.max_seq <= 64 else min(8, -(-cfg.max_seq // 32)))
+        if cfg.attn_splits > 0:
+            self.attn_splits = cfg.attn_splits
+        elif hd in (64, 128):    # attn_decode2_kernel: 64-position splits staged in shared memory, up to 32 per head
+            self.attn_splits = max(1, min(32, -(-cfg.max_seq // 64)))
+        else:
+            self.attn_splits = 1 if cfg.max_seq <= 64 else min(8, -(-cfg.max_seq // 32))
         self.attn_ws = torch.zeros(self.heads_local * self.attn_splits * (hd + 2), dtype=f32, device=dev)
         self.attn_tickets = torch.zeros(self.heads_local, dtype=torch.int32, device=dev)
         self.forced_dev = None
