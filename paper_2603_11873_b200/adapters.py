@@ -12,6 +12,12 @@ Host-side mirror of /root/reference/pkg/src/lorafuse/adapters.py.  Two forms liv
   memory) selects bank blocks inside the kernel.  Nothing is concatenated, negated or copied
   per token: the gate is folded into the DOWN rows while they are staged in shared memory
   (adapters.py:202), previous blocks are negated there (adapters.py:230).
+
+Attribution: ``LoraExpert``, ``ExpertBank`` and ``ConcatAdapter`` (fields, ``validate`` rules and their
+messages, ``ConcatAdapter.empty``) and the bodies of ``concat_gated`` / ``build_switch`` are the
+reference's (adapters.py:49-233) restated on torch tensors -- they are the public API this package
+keeps intact and exist here for parity tests and reference-style callers.  ``SwitchTable``,
+``SegmentGroup`` and the packed bank layout are this package's own and are what the decode loop runs.
 """
 
 from __future__ import annotations

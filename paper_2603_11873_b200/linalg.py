@@ -16,6 +16,13 @@ Differences that follow from the device carrier (documented in DESIGN.md):
   * A ``Segment`` may pair a ``"bf16"`` target with ``"single"`` factors (gate folding is an
     f32 multiply, adapters.py:202).
 There is no CPU fallback: any kernel call on a non-CUDA tensor raises ``DeviceError``.
+
+Attribution: the accounting and table carriers -- ``DispatchEvent``, ``DispatchSummary``,
+``DispatchRecorder`` (``record`` / ``mark`` / ``events_since`` / ``counts``), ``TileConfig``, ``Segment`` and
+``SegmentTable`` with their validation rules and messages -- are the reference's classes
+(linalg.py:110-231) restated: they are the public API this package keeps intact, so names, fields and
+error behaviour come from the reference.  ``Matrix`` on a torch tensor, ``DeviceTable`` and every
+kernel call are this package's own.
 """
 
 from __future__ import annotations
