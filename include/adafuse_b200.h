@@ -323,6 +323,13 @@ int af_group_create(af_table* table, const int32_t* seg_ids, int32_t n, af_group
 /* seg_ids: the phases' segment lists back to back; phase_len[p] segments belong to phase p. */
 int af_chain_create(af_table* table, const int32_t* seg_ids, const int32_t* phase_len, int32_t n_phases,
                     af_group** out);
+/* af_chain_create with a measured work split: cta_share[ph * n_cta + c] > 0 is the relative share of phase ph's
+ * tiles CTA c gets (NULL = equal shares).  Every CTA of a chained launch meets the others at each phase barrier,
+ * so the slowest SM sets the pace; SM rates differ by a few per cent with their position on the chip, identically
+ * in every launch, and a caller that has timed them (af_set_timeline) can hand the split back.  The schedule
+ * changes which CTA takes which tile and nothing else: weights and accumulators are bit-identical. */
+int af_chain_create_weighted(af_table* table, const int32_t* seg_ids, const int32_t* phase_len, int32_t n_phases,
+                             const float* cta_share, int32_t n_cta, af_group** out);
 int af_group_destroy(af_group* group);
 /* x_len / y_rows: arrays of n_phases entries (4 is always enough). */
 int af_group_info(const af_group* group, int32_t* n_phases, int32_t* x_len, int32_t* y_rows, int32_t* n_units,

@@ -144,6 +144,7 @@ SIGNATURES = {
     "af_group_create": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_vp)]),
     "af_group_destroy": (ctypes.c_int, [_vp]),
     "af_chain_create": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _i32, ctypes.POINTER(_vp)]),
+    "af_chain_create_weighted": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _i32, ctypes.POINTER(_f32), _i32, ctypes.POINTER(_vp)]),
     "af_group_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
     "af_switch_gemv_chain": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, ctypes.POINTER(GemvPhase), _i32, _vp, _i32, _vp]),
     "af_switch_gemv": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _i32, _vp]),
@@ -154,6 +155,7 @@ SIGNATURES = {
     "af_attn_decode_fix": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 AF_FIX_SHIFT = 40
+AF_TIMELINE_SLOTS = 42
 AF_CHAIN_PDL, AF_CHAIN_PLAN_PREBUILT = 1, 2
 AF_PRO_NONE, AF_PRO_RMSNORM, AF_PRO_SILU_MUL, AF_PRO_RMSNORM_DEFERRED = 0, 1, 2, 3
 

@@ -510,7 +510,9 @@ class SegmentGroup:
     PROLOGUES = {"none": _capi.AF_PRO_NONE, "rmsnorm": _capi.AF_PRO_RMSNORM, "silu_mul": _capi.AF_PRO_SILU_MUL,
                  "rmsnorm_deferred": _capi.AF_PRO_RMSNORM_DEFERRED}
 
-    def __init__(self, table: SwitchTable, seg_ids):
+    def __init__(self, table: SwitchTable, seg_ids, cta_share=None):
+        """`cta_share` (optional): [n_phases][n_cta] positive floats -- the measured share of each phase's tiles every
+        CTA of the launch should get (`af_chain_create_weighted`; `LlamaEngine.calibrate_schedule` produces it)."""
         import ctypes
 
         seg_ids = list(seg_ids)
@@ -519,7 +521,16 @@ class SegmentGroup:
         arr = (ctypes.c_int32 * max(1, len(ids)))(*ids)
         lens = (ctypes.c_int32 * len(phases))(*[len(p) for p in phases])
         handle = ctypes.c_void_p()
-        _capi.check(_capi.lib().af_chain_create(table.device_table.handle, arr, lens, len(phases), ctypes.byref(handle)))
+        if cta_share is None:
+            _capi.check(_capi.lib().af_chain_create(table.device_table.handle, arr, lens, len(phases), ctypes.byref(handle)))
+        else:
+            rows = [[float(v) for v in row] for row in cta_share]
+            if len(rows) != len(phases) or len({len(r) for r in rows}) != 1:
+                raise DimensionError("cta_share must hold one row of per-CTA shares per phase")
+            flat = [v for r in rows for v in r]
+            share = (ctypes.c_float * len(flat))(*flat)
+            _capi.check(_capi.lib().af_chain_create_weighted(table.device_table.handle, arr, lens, len(phases), share, len(rows[0]),
+                                                             ctypes.byref(handle)))
         self.handle = handle
         self.table = table  # keeps the af_table (and the tensors it points at) alive
         n_ph, n_units, grid, tiles = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()

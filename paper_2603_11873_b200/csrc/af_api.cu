@@ -312,7 +312,10 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
     for (int i = 0; i < n_segments; ++i) {
         const af_segment_desc& s = segments[i];
         const bool rank_ok = s.rank == segments[0].rank && (s.rank == 8 || s.rank == 16 || s.rank == 32 || s.rank == 64);
-        if (!rank_ok || s.d_out % kUM != 0 || s.d_in % kUN != 0) t->umma_ok = false;
+        // Any matrix of at least one 128 x 128 tile: ragged edges (tensor-parallel shards: ffn / tp = 2752, 1376, 1728 ...)
+        // are partial tiles -- TMA zero-fills what it loads out of bounds and clips what it stores, the UP copy
+        // of a partial row tile is cut at d_out, slab and input-vector columns past d_in are zeros.
+        if (!rank_ok || s.d_out < kUM || s.d_in < kUN) t->umma_ok = false;
     }
 
     // ---- work units: column strips of kTN columns cut into runs of row tiles ----
@@ -342,7 +345,8 @@ int af_table_create(const af_segment_desc* segments, int32_t n_segments, int32_t
     std::vector<UnitDev> units_u;
     if (t->umma_ok) {
         long long tiles_u = 0;
-        for (int i = 0; i < n_segments; ++i) tiles_u += (long long)(segments[i].d_out / kUM) * (segments[i].d_in / kUN);
+        for (int i = 0; i < n_segments; ++i)
+            tiles_u += (long long)((segments[i].d_out + kUM - 1) / kUM) * ((segments[i].d_in + kUN - 1) / kUN);
         long long per_u = std::max(1LL, std::min(32LL, tiles_u / ((long long)std::max(1, t->sm_count) * 32)));
         for (int i = 0; i < n_segments; ++i) {
             const af_segment_desc& s = segments[i];
@@ -512,6 +516,21 @@ static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
     if (!configured.cur()) {
         AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured.cur() = 1;
+    }
+    if (mp.n_phases > 1) {
+        // The phases of a chained launch meet at in-kernel grid barriers: every CTA must be resident at once.  One CTA
+        // per SM by construction; refuse the launch when the device cannot hold it (a smaller partition, MIG) instead
+        // of running into the barrier timeout.
+        static PerDevice occ_checked;
+        if (!occ_checked.cur()) {
+            int per_sm = 0;
+            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, switch_umma_kernel<NB, GEMV, CH>, kUThreads, L::total));
+            const DeviceInfo& di = device_info();
+            if (per_sm < 1 || grid > di.sm_count * per_sm)
+                return fail(AF_ESTATE, "a chained launch needs all its CTAs co-resident: " + std::to_string(grid) + " CTAs, device holds " +
+                                           std::to_string(di.sm_count * per_sm));
+            occ_checked.cur() = 1;
+        }
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -760,7 +779,16 @@ int af_group_destroy(af_group* g) {
 }
 
 int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_len, int32_t n_phases, af_group** out) {
+    return af_chain_create_weighted(t, seg_ids, phase_len, n_phases, nullptr, 0, out);
+}
+
+int af_chain_create_weighted(af_table* t, const int32_t* seg_ids, const int32_t* phase_len, int32_t n_phases, const float* cta_share,
+                             int32_t n_cta, af_group** out) {
     if (!out) return fail(AF_EVALUE, "out is NULL");
+    if (cta_share && n_cta < 1) return fail(AF_EVALUE, "cta_share needs n_cta >= 1");
+    if (cta_share)
+        for (int i = 0; i < n_phases * n_cta; ++i)
+            if (!(cta_share[i] > 0.0f) || !std::isfinite(cta_share[i])) return fail(AF_EVALUE, "cta_share entries must be positive and finite");
     *out = nullptr;
     if (!t || !seg_ids || !phase_len || n_phases < 1) return fail(AF_EDIM, "segment group is empty");
     if (n_phases > kMaxPhases) return fail(AF_EVALUE, "a chain holds at most 4 phases");
@@ -836,6 +864,12 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
             // Spans end at multiples of a fractional per-CTA budget (total cost / Gp), so every CTA gets
             // its share to within one tile; the total cost depends on how many spans cross a strip
             // boundary, which depends on the cut -- three fixed-point rounds settle it.
+            // Share of the phase each CTA gets: equal, or the caller's measured shares (af_chain_create_weighted: an SM's
+            // rate depends on where it sits -- its L2 die, its distance to the memory partitions -- by a few per cent,
+            // the same in every launch; all CTAs meet at the phase barrier, so the slowest one sets the phase's time).
+            std::vector<double> cum(Gp + 1, 0.0);
+            for (int c = 0; c < Gp; ++c) cum[c + 1] = cum[c] + ((cta_share && c < n_cta) ? (double)cta_share[(size_t)ph * n_cta + c] : 1.0);
+            for (int c = 1; c <= Gp; ++c) cum[c] *= (double)Gp / cum[Gp];     // in units of the equal share
             auto cut = [&](double budget, std::vector<std::vector<UnitDev>>* out) -> int {
                 int cta = 0, crossings = 0;
                 // cumulative cost of everything emitted so far; CTA 0 starts with its extra duties on the books,
@@ -846,7 +880,7 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
                     int r = 0;
                     bool entered = false;
                     while (r < st.rt) {
-                        const double span_end = (cta + 1) * budget;
+                        const double span_end = cum[cta + 1] * budget;
                         if (!entered) {
                             entered = true;
                             if (in_span > 0) {   // the span continues into this strip: a unit change
@@ -855,6 +889,7 @@ int af_chain_create(af_table* t, const int32_t* seg_ids, const int32_t* phase_le
                             }
                         }
                         long long room = (long long)std::floor(span_end - cost + 1e-6);
+                        if (room < 1 && cta == 0 && in_span == 0) room = 1;   // CTA 0 owns a tile of every phase (it writes h_out / the deferred scale)
                         if (room < 1) {
                             if (cta < Gp - 1) {
                                 ++cta;
@@ -1313,6 +1348,15 @@ int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_do
     if (smem > configured.cur()) {
         AF_CUDA_TRY(cudaFuncSetAttribute(gemv_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         configured.cur() = smem;
+    }
+    if (n_phases > 1) {   // co-residency of the whole grid (in-kernel phase barriers), checked once per device
+        static PerDevice occ_checked;
+        if (occ_checked.cur() < smem) {
+            int per_sm = 0;
+            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_chain_kernel, kGcThreads, smem));
+            if (per_sm < 1) return fail(AF_ESTATE, "a chained GEMV launch needs one resident CTA per SM; this device cannot hold it");
+            occ_checked.cur() = smem;
+        }
     }
     gp.n_phases = n_phases;
     gp.phase_done = phase_done_dev;

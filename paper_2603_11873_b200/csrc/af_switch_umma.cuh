@@ -51,6 +51,14 @@ constexpr int kUXSlots = 4;
 #define AF_UMMA_PF 0   /* measured: prefetching W into L2 beyond the ring costs 20 % (profiles/README.md) */
 #endif
 constexpr int kUPrefetch = AF_UMMA_PF;             // W tiles prefetched into L2 beyond the shared-memory ring (0 = off)
+#ifndef AF_UMMA_BURST
+#define AF_UMMA_BURST 4
+#endif
+#ifndef AF_UMMA_BURST_AFTER
+#define AF_UMMA_BURST_AFTER 5000   /* cycles (~2.5 us) the ring must have stayed full before the loader prefetches ahead */
+#endif
+constexpr int kUBurst = AF_UMMA_BURST;             // tiles pulled into L2 when the consumers stall (phase boundary)
+constexpr long long kUBurstAfterCycles = AF_UMMA_BURST_AFTER;
 
 // NB = k-groups of 8 stacked ranks the slab holds per half; CH = k-groups per UP ring stage (CH == NB: the whole
 // UP operand of a tile is one stage; CH < NB: K-chunked, NB / CH chunks per tile)
@@ -399,10 +407,39 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 const uint64_t pol = l2_evict_first_policy();
                 UmmaIter ti;
                 ti.init(p, unit_cache);
+                // Stall burst (EXPERIMENT, off: AF_DBG=256 turns it on): when the ring has stayed full for longer than a
+                // tile's worth of back-pressure the consumers sit at a phase boundary, and HBM idles until they are back
+                // and the first stage comes free; the loader then pulls the next kUBurst tiles into L2 (TMA prefetch), so
+                // that the ring would refill from L2 afterwards.  Measured on Llama-2-7B (round 2, A/B on one box, twice):
+                // 5.58 against 5.52 ms per token WITHOUT it -- like the standing prefetcher of round 1 (-20 %), pulling W
+                // into L2 ahead of the ring does not pay on this part; the boundary cost is not recoverable this way.
+                UmmaIter tp = ti;
+                int pf_it = 0;
+                const bool burst_on = GEMV && kUBurst > 0 && (mp.dbg & 256);
                 for (int it = 0; ti.valid(p); ++it) {
                     const int stage = it % kSt;
                     const uint32_t ph = (it / kSt) & 1;
                     *reinterpret_cast<volatile int*>(full + 31) = it + kSt;   // tiles up to it + kSt are the ring's business
+                    if (burst_on && !mbar_test(&empty[stage], ph ^ 1)) {
+                        const long long t0 = clock64();
+                        bool fired = false;
+                        while (!mbar_test(&empty[stage], ph ^ 1)) {
+                            if (!fired && clock64() - t0 > kUBurstAfterCycles) {
+                                fired = true;
+                                if (pf_it < it) {   // the cursor never falls behind the loader
+                                    pf_it = it;
+                                    tp = ti;
+                                }
+                                while (pf_it < it + kUBurst && tp.valid(p)) {
+                                    const CUtensorMap* tmp_ = mp.tmaps_ld + tp.un.seg;
+#pragma unroll
+                                    for (int b = 0; b < kUBoxes; ++b) tma_prefetch_l2_2d(tmp_, tp.un.col0 + b * kUBoxCols, tp.m0);
+                                    tp.next(p);
+                                    ++pf_it;
+                                }
+                            }
+                        }
+                    }
                     mbar_wait(&empty[stage], ph ^ 1);
                     mbar_expect_tx(&full[stage], kUWStage);
                     const CUtensorMap* tm = mp.tmaps_ld + ti.un.seg;
@@ -438,13 +475,17 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                             mbar_expect_tx(&up_full[stage], 0);
                             continue;
                         }
-                        mbar_expect_tx(&up_full[stage], (uint32_t)max(0, b1 - b0) * blk_bytes);
                         if (sg.rank == 8) {   // an expert block is 128 contiguous 16-byte rows: one bulk copy
+                            // (a partial last row tile is cut at d_out: the rows behind it belong to the next expert, or to nobody;
+                            //  what stays in the stage for them is finite and feeds accumulator rows that are never stored)
+                            const uint32_t bytes = (uint32_t)min(kUM, sg.d_out - ti.m0) * 16u;
+                            mbar_expect_tx(&up_full[stage], (uint32_t)max(0, b1 - b0) * bytes);
                             const __nv_bfloat16* upb = reinterpret_cast<const __nv_bfloat16*>(sg.up);
                             for (int b = b0; b < b1; ++b)
                                 bulk_load_1d(up_base + stage * L::up_stage + (b - b0) * kUBlockBytes,
-                                             upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, kUBlockBytes, &up_full[stage]);
+                                             upb + (long long)plan.expert[b] * sg.up_estride + (long long)ti.m0 * 8, bytes, &up_full[stage]);
                         } else {              // 128 rows x rank through the tensor map whose swizzle span is the row
+                            mbar_expect_tx(&up_full[stage], (uint32_t)max(0, b1 - b0) * blk_bytes);
                             const CUtensorMap* tm = mp.tmaps_up + ti.un.seg;
                             for (int b = b0; b < b1; ++b)
                                 tma_load_2d_addr(up_base + stage * L::up_stage + (b - b0) * blk_bytes, tm, 0, plan.expert[b] * sg.d_out + ti.m0,

@@ -74,6 +74,11 @@ class LlamaConfig:
     split_switch: bool = True        # > 64 stacked ranks: several tensor-path passes instead of one CUDA-core pass
     defer_norm: bool = True          # chase on the tcgen05 path: RMSNorm scales computed by one CTA, applied by the consumers
     gemv_chain: bool = True          # plain forward (separate / adapter-free): the same four projections as one persistent GEMV launch
+    # chained chase launches: time every CTA's phases once at engine build and split each phase's tiles by the measured
+    # rates (`calibrate_schedule`).  Off: measured on Llama-2-7B, the spread of the CTAs' arrival at a phase barrier
+    # (~4 us) is tile granularity (+-1 tile of 1.6 us) and unit changes, not a per-SM rate -- recalibrating moves it to
+    # other CTAs without shrinking it (5.50 ms per token either way).
+    calibrate: bool = False
 
     def validate(self) -> None:
         for name in ("layers", "hidden", "ffn", "n_heads", "n_kv_heads", "vocab", "experts", "rank", "top_k", "max_seq", "tp_size"):
@@ -441,6 +446,11 @@ class LlamaEngine:
                     mid = [sg["o"], sg["gu"], sg["down"]] + ([seg(li + 1)["qkv"]] if li + 1 < cfg.layers else [])
                     self.groups.append({"qkv": SegmentGroup(self.table, sg["qkv"]) if li == 0 else None,
                                         "mid": SegmentGroup(self.table, mid)})
+                elif cfg.chain:
+                    # TP: the chain breaks only where a collective sits -- after o and after down.  gate|up -> down has
+                    # none in between (column-parallel outputs feed the row-parallel input shard locally): one launch.
+                    self.groups.append({"qkv": SegmentGroup(self.table, sg["qkv"]), "o": SegmentGroup(self.table, sg["o"]),
+                                        "gudown": SegmentGroup(self.table, [sg["gu"], sg["down"]])})
                 else:
                     self.groups.append({k: SegmentGroup(self.table, v) for k, v in sg.items()})
             # fixed-point accumulators of every launch of a token and the chains' phase counters:
@@ -465,6 +475,10 @@ class LlamaEngine:
                                  "gu": self.acc_arena[o + n_qkv + d: o + n_qkv + d + n_gu],
                                  "down": self.acc_arena[o + n_qkv + d + n_gu: o + per_layer]})
                 self.phase_done.append(counters[4 * li: 4 * li + 4])
+            self.schedule_shares = None
+            if cfg.calibrate and self.chase_chained and self.pristine is not None and cfg.layers >= 4 \
+                    and os.environ.get("AF_CALIBRATE", "1") != "0":
+                self.calibrate_schedule()
 
     # -- the pieces of one step ---------------------------------------------------------
 
@@ -509,6 +523,59 @@ class LlamaEngine:
             self.fused_switch(None, self.cur, mode="from_pristine")   # refresh: model.py:344-349 + the merge, in one pass
         else:
             self.fused_switch(self.prev if with_prev else None, self.cur)
+
+    def calibrate_schedule(self, rounds: int = 2) -> None:
+        """Measure how long every CTA of the chained launches spends in each phase (the library's timeline probe,
+        `af_set_timeline`) and rebuild the launches' schedules with the phases' tiles split by the measured rates
+        (`af_chain_create_weighted`).  A launch's CTAs meet at every phase barrier, so the slowest SM sets the pace of
+        the phase; the rates differ by a few per cent with an SM's position and are the same in every launch.  Changes
+        which CTA takes which tile and nothing else (weights and accumulators bit-identical).  Runs a few decode steps
+        on a scratch token stream and restores the engine (pristine weights, position 0) afterwards."""
+        cfg, L = self.cfg, _capi.lib()
+        if not (self.chase and self.chase_chained and self.pristine is not None):
+            raise StateError("schedule calibration applies to the chained one-pass schedule with a pristine copy")
+        grid = _capi.device_info()["sm_count"]
+        slots = _capi.AF_TIMELINE_SLOTS
+        n_launch = cfg.layers + 1
+        shares = np.ones((4, grid), dtype=np.float64)
+        scratch = np.random.Generator(np.random.PCG64(12345)).integers(0, cfg.vocab, 16)
+        for _ in range(rounds):
+            self.reset(forced=scratch)
+            for _ in range(2):
+                self.decode_step(graph=False)
+            buf = torch.zeros(n_launch * grid * slots, dtype=torch.int64, device=self.dev)
+            self._check(L.af_set_timeline(_ptr(buf), n_launch, grid * slots))
+            try:
+                self.decode_step(graph=False)
+            finally:
+                self._check(L.af_set_timeline(None, 0, 0))
+            tl = buf.cpu().numpy().reshape(n_launch, grid, slots).astype(np.float64)
+            tl[tl == 0] = np.nan
+            mid = tl[2:cfg.layers - 1]                                    # the four-phase launches of the inner layers
+            new = shares.copy()
+            for ph in range(1, 4):                                        # (phase 0, o, is a handful of tiles: start skew, not rate)
+                start = mid[:, :, 9 + 4 * ph]                             # barrier passed
+                end = mid[:, :, 8 + 4 * (ph + 1)] if ph < 3 else mid[:, :, 7]   # next phase's wait begins / consumers done
+                dur = np.nanmean(end - start, axis=0)                     # [cta]
+                if not np.all(np.isfinite(dur)) or np.nanmin(dur) <= 0:
+                    continue
+                rel = np.nanmedian(dur) / dur                             # > 1: this CTA was early and can take more
+                new[ph] = shares[ph] * (1.0 + 0.8 * (np.clip(rel, 0.8, 1.25) - 1.0))
+            shares = new / new.mean(axis=1, keepdims=True)
+            self._rebuild_mid_groups(shares)
+        self.schedule_shares = shares
+        self.reset()
+
+    def _rebuild_mid_groups(self, shares) -> None:
+        cfg = self.cfg
+        seg = lambda li: {"qkv": [7 * li, 7 * li + 1, 7 * li + 2], "o": [7 * li + 3], "gu": [7 * li + 4, 7 * li + 5], "down": [7 * li + 6]}  # noqa: E731
+        for li in range(cfg.layers):
+            sg = seg(li)
+            mid = [sg["o"], sg["gu"], sg["down"]] + ([seg(li + 1)["qkv"]] if li + 1 < cfg.layers else [])
+            old = self.groups[li]["mid"]
+            self.groups[li]["mid"] = SegmentGroup(self.table, mid, cta_share=[list(shares[ph]) for ph in range(len(mid))])
+            old.close()
+        self._graphs = {}
 
     def _gv_phase(self, w, rows, cols, x, out, prologue=0, norm_w=None, eps=0.0, epilogue=0, res=None):
         return _capi.GvPhase(w=_ptr(w), rows=rows, cols=cols, ld=cols, x=_ptr(x), out=_ptr(out), res=_ptr(res) if res is not None else None,
@@ -611,7 +678,8 @@ class LlamaEngine:
             elif not self.chase_chained:
                 g["qkv"].switch_gemv(prev, cur, a["qkv"], acc_in=self.acc[li - 1]["down"], res=xb, h_out=xa, prologue=norm,
                                      norm_w=self.attn_norm[li], eps=eps, inv_out=iq, pdl=True, **kw)
-            self._check(L.af_attn_decode_fix(_ptr(a["qkv"]), _ptr(iq) if iq is not None else None, _ptr(self.k_cache[li]),
+            if os.environ.get("AF_SKIP_ATTN") != "1":   # (timing experiment: AF_SKIP_ATTN=1 leaves the attention launches out -- wrong results)
+              self._check(L.af_attn_decode_fix(_ptr(a["qkv"]), _ptr(iq) if iq is not None else None, _ptr(self.k_cache[li]),
                                              _ptr(self.v_cache[li]), _ptr(self.cos), _ptr(self.sin), _ptr(self.pos_dev),
                                              self.heads_local, self.kv_local, cfg.head_dim, cfg.max_seq, self.attn_splits,
                                              _ptr(self.attn_ws), _ptr(self.attn_tickets), _ptr(self.attn_buf), st))
@@ -628,8 +696,11 @@ class LlamaEngine:
             else:
                 g["o"].switch_gemv(prev, cur, pdl=True, **ph_o, **kw)
                 self.comm.all_reduce_sum(a["o"])          # TP: partial sums of the row-parallel o, as int64 (no-op on one rank)
-                g["gu"].switch_gemv(prev, cur, pdl=True, **ph_gu, **kw)
-                g["down"].switch_gemv(prev, cur, pdl=True, **ph_down, **kw)
+                if "gudown" in g:
+                    g["gudown"].switch_gemv_chain(prev, cur, [ph_gu, ph_down], self.phase_done[li], pdl=True, **kw)
+                else:
+                    g["gu"].switch_gemv(prev, cur, pdl=True, **ph_gu, **kw)
+                    g["down"].switch_gemv(prev, cur, pdl=True, **ph_down, **kw)
                 self.comm.all_reduce_sum(a["down"])
         self._check(L.af_accum_to_f32(_ptr(self.acc[-1]["down"]), _ptr(xb), _ptr(xa), d, st))
         self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),

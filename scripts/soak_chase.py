@@ -21,7 +21,7 @@ for rep in range(2):
     for _ in range(n):
         eng.replay()
     torch.cuda.synchronize()
-    eng.table.status()
+    eng.check()          # the engine's status word: unusable decision / phase-barrier timeout
     runs.append(eng.tokens())
     del eng
     torch.cuda.empty_cache()

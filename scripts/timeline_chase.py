@@ -17,14 +17,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("workload", nargs="?", default="llama2-7b")
 ap.add_argument("--no-chain", action="store_true")
 ap.add_argument("--show", default="0,1,2,17,32")
+ap.add_argument("--ctx", type=int, default=0, help="positions already in the KV cache")
 args = ap.parse_args()
 
-cfg = llama.preset(args.workload, max_seq=64, forward_mode="chase", chain=not args.no_chain)
+cfg = llama.preset(args.workload, max_seq=args.ctx + 64, forward_mode="chase", chain=not args.no_chain)
 eng = llama.LlamaEngine(cfg, init="device")
 forced = np.random.Generator(np.random.PCG64(1)).integers(0, cfg.vocab, 64)
 eng.reset(forced=forced)
 for _ in range(4):
-    eng.decode_step()
+    eng.decode_step(graph=False)
+if args.ctx:
+    eng.set_position(args.ctx)
 SLOTS = 42
 n_launch = (cfg.layers + 1) if not args.no_chain else 4 * cfg.layers
 grid = _capi.device_info()["sm_count"]

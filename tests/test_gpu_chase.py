@@ -189,6 +189,50 @@ def test_chain_equals_separate_launches(af):
     assert float(outs[0][0][3].abs().max()) > 0
 
 
+def test_weighted_schedule_changes_nothing_but_the_split(af):
+    """af_chain_create_weighted: per-CTA shares of each phase (what `LlamaEngine.calibrate_schedule` measures) move
+    tiles between CTAs; weights, accumulators and residual streams stay bit-identical to the equal split."""
+    from paper_2603_11873_b200 import _capi
+    from paper_2603_11873_b200.adapters import SegmentGroup
+
+    d, f = 512, 1280
+    shapes = [(d, d), (f, d), (f, d), (d, f), (d, d), (128, d), (128, d)]
+    phases_ids = [[0], [1, 2], [3], [4, 5, 6]]
+    n_cta = _capi.device_info()["sm_count"]
+    rng = np.random.Generator(np.random.PCG64(5))
+    outs = []
+    for weighted in (False, True):
+        tg, tab = _mk_table(af, shapes, seed=7)
+        prev = _decision(af, (1, 4), (0.7, 0.3))
+        cur = _decision(af, (4, 2), (0.55, 0.45))
+        tab.switch(None, prev, max_k=2)
+        g = torch.Generator(device="cuda").manual_seed(2)
+        attn = torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        xa = torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        nw1 = 1.0 + 0.1 * torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        nw2 = 1.0 + 0.1 * torch.empty(d, device="cuda").uniform_(-1, 1, generator=g)
+        xb, xa2 = torch.zeros(d, device="cuda"), torch.zeros(d, device="cuda")
+        acc = [torch.zeros(n, dtype=torch.int64, device="cuda") for n in (d, 2 * f, d, d + 256)]
+        phases = [dict(acc_out=acc[0], xin=attn),
+                  dict(acc_out=acc[1], acc_in=acc[0], res=xa, h_out=xb, prologue="rmsnorm", norm_w=nw1, eps=1e-5),
+                  dict(acc_out=acc[2], acc_in=acc[1], prologue="silu_mul"),
+                  dict(acc_out=acc[3], acc_in=acc[2], res=xb, h_out=xa2, prologue="rmsnorm", norm_w=nw2, eps=1e-5)]
+        share = rng.uniform(0.5, 1.5, (4, n_cta)).tolist() if weighted else None
+        grp = SegmentGroup(tab, phases_ids, cta_share=share)
+        done = torch.zeros(4, dtype=torch.int32, device="cuda")
+        grp.switch_gemv_chain(prev, cur, phases, done, max_k=2)
+        tab.status()
+        outs.append(([a.clone() for a in acc], xb.clone(), xa2.clone(), [t.data.clone() for t in tg]))
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert torch.equal(a, b)
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
+    for a, b in zip(outs[0][3], outs[1][3]):
+        assert torch.equal(a, b)
+    tg, tab = _mk_table(af, shapes, seed=7)
+    with pytest.raises(ValueError):
+        SegmentGroup(tab, phases_ids, cta_share=[[1.0] * n_cta] * 3 + [[0.0] * n_cta])
+
+
 def test_group_validation(af):
     from paper_2603_11873_b200.adapters import SegmentGroup
     from paper_2603_11873_b200.errors import AliasingError, DimensionError
