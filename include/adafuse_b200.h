@@ -260,6 +260,38 @@ typedef struct af_gv_phase {
 } af_gv_phase;
 int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_done_dev,
                   int32_t* err_flag_dev, int32_t pdl, void* stream);
+/* af_forward_persistent : the whole merged-path forward of one token (model.py:367-371 on the Llama block) as ONE
+ *    persistent launch driven by a device-side phase table: q|k|v(0), then per layer attention (two phases: partials
+ *    per (head, 64-position chunk), combine), o, gate|up, down and the next layer's q|k|v (the lm_head after the last
+ *    layer).  GEMV phases (kind AF_FW_GEMV) follow af_gemv_chain's contract; AF_FW_ATTN_PARTIAL reads q|k|v of the new
+ *    token from `x` (f32, [n_heads*hd | n_kv*hd | n_kv*hd]), applies RoPE at *pos_dev, appends k / v to this layer's
+ *    bf16 caches and writes per-chunk softmax partials to `workspace` (n_heads * ceil(max_seq / 64) * (head_dim + 2)
+ *    floats); AF_FW_ATTN_COMBINE writes the n_heads * head_dim attention outputs to `out`.  head_dim 64 or 128.
+ *    The table lives in DEVICE memory (phases_dev) and is validated from its host copy by af_forward_validate, which
+ *    also returns the shared-memory vector length the launch needs (max_cols).  phase_done_dev: n_phases int32
+ *    counters zeroed by the caller; err_flag_dev as in af_gemv_chain. */
+#define AF_FW_GEMV 0
+#define AF_FW_ATTN_PARTIAL 1
+#define AF_FW_ATTN_COMBINE 2
+typedef struct af_fw_phase {
+    const void* w;
+    const float* x;
+    float* out;
+    const float* res;
+    const float* norm_w;
+    void* k_cache;
+    void* v_cache;
+    int64_t ld;
+    int32_t rows, cols;
+    float eps;
+    int32_t prologue, epilogue, kind;
+} af_fw_phase;
+int af_forward_validate(const af_fw_phase* phases_host, int32_t n_phases, int32_t n_heads, int32_t n_kv_heads,
+                        int32_t head_dim, int32_t* max_cols_out);
+int af_forward_persistent(const af_fw_phase* phases_dev, int32_t n_phases, int32_t max_cols, const float* cos_table,
+                          const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
+                          int32_t head_dim, int32_t max_seq, float* workspace, int32_t* phase_done_dev,
+                          int32_t* err_flag_dev, int32_t pdl, void* stream);
 int af_attn_decode(const float* qkv, void* k_cache, void* v_cache, const float* cos_table,
                    const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads,
                    int32_t head_dim, int32_t max_seq, int32_t n_split, float* workspace,

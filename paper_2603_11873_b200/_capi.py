@@ -103,6 +103,29 @@ class GvPhase(ctypes.Structure):
     ]
 
 
+class FwPhase(ctypes.Structure):
+    """`af_fw_phase`: one record of the persistent forward's device-side phase table."""
+
+    _fields_ = [
+        ("w", ctypes.c_void_p),
+        ("x", ctypes.c_void_p),
+        ("out", ctypes.c_void_p),
+        ("res", ctypes.c_void_p),
+        ("norm_w", ctypes.c_void_p),
+        ("k_cache", ctypes.c_void_p),
+        ("v_cache", ctypes.c_void_p),
+        ("ld", ctypes.c_int64),
+        ("rows", ctypes.c_int32),
+        ("cols", ctypes.c_int32),
+        ("eps", ctypes.c_float),
+        ("prologue", ctypes.c_int32),
+        ("epilogue", ctypes.c_int32),
+        ("kind", ctypes.c_int32),
+    ]
+
+
+AF_FW_GEMV, AF_FW_ATTN_PARTIAL, AF_FW_ATTN_COMBINE = 0, 1, 2
+
 assert ctypes.sizeof(Decision) == 128
 
 _vp = ctypes.c_void_p
@@ -149,6 +172,8 @@ SIGNATURES = {
     "af_switch_gemv_chain": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, ctypes.POINTER(GemvPhase), _i32, _vp, _i32, _vp]),
     "af_switch_gemv": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _f32, _vp, _i32, _vp]),
     "af_gemv_chain": (ctypes.c_int, [ctypes.POINTER(GvPhase), _i32, _vp, _vp, _i32, _vp]),
+    "af_forward_validate": (ctypes.c_int, [ctypes.POINTER(FwPhase), _i32, _i32, _i32, _i32, ctypes.POINTER(_i32)]),
+    "af_forward_persistent": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
     "af_plan_build": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp]),
     "af_set_timeline": (ctypes.c_int, [_vp, _i32, _i64]),
     "af_accum_to_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp]),

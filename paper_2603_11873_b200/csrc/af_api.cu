@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "af_decode.cuh"
+#include "af_forward.cuh"
 #include "af_gemv_chain.cuh"
 #include "af_llama.cuh"
 #include "af_switch_mma.cuh"
@@ -1376,6 +1377,98 @@ int af_gemv_chain(const af_gv_phase* phases, int32_t n_phases, int32_t* phase_do
     cfg.numAttrs = gp.pdl ? 1 : 0;
     AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemv_chain_kernel, gp));
     AF_LAUNCH_CHECK("gemv_chain_kernel");
+    return AF_OK;
+}
+
+int af_forward_validate(const af_fw_phase* ph, int32_t n_phases, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                        int32_t* max_cols_out) {
+    if (!ph || n_phases < 1) return fail(AF_EVALUE, "a forward needs at least one phase");
+    if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads != 0) return fail(AF_EDIM, "heads must be a multiple of kv heads");
+    if (head_dim != 64 && head_dim != 128) return fail(AF_EDIM, "the persistent forward takes head_dim 64 or 128");
+    static_assert(sizeof(af_fw_phase) == sizeof(FwPhase), "af_fw_phase mirrors FwPhase");
+    int max_cols = 0;
+    for (int i = 0; i < n_phases; ++i) {
+        const af_fw_phase& f = ph[i];
+        if (f.kind == AF_FW_GEMV) {
+            if (f.rows < 1 || f.cols < 1 || f.ld < f.cols) return fail(AF_EDIM, "bad GEMV shape");
+            if (f.cols % 8 != 0 || f.ld % 8 != 0 || (reinterpret_cast<uintptr_t>(f.w) & 15) != 0)
+                return fail(AF_EDIM, "GEMV phases need 16-byte aligned bf16 rows (cols % 8 == 0)");
+            if (f.prologue < AF_PRO_NONE || f.prologue > AF_PRO_SILU_MUL) return fail(AF_EVALUE, "unknown prologue");
+            if (f.prologue == AF_PRO_RMSNORM && !f.norm_w) return fail(AF_EVALUE, "RMSNorm prologue needs its weight vector");
+            if (f.epilogue < AF_EPI_NONE || f.epilogue > AF_EPI_RESIDUAL) return fail(AF_EVALUE, "unknown epilogue");
+            if (f.epilogue != AF_EPI_NONE && !f.res) return fail(AF_EVALUE, "epilogue needs a residual vector");
+            if (!f.w || !f.x || !f.out) return fail(AF_EVALUE, "NULL argument");
+            if (f.out == f.x) return fail(AF_EALIAS, "GEMV output aliases its input");
+            if ((reinterpret_cast<uintptr_t>(f.x) & 15) != 0 || (f.norm_w && (reinterpret_cast<uintptr_t>(f.norm_w) & 15) != 0))
+                return fail(AF_EDIM, "GEMV phases need 16-byte aligned f32 vectors");
+            max_cols = std::max(max_cols, (int)f.cols);
+        } else if (f.kind == AF_FW_ATTN_PARTIAL) {
+            if (!f.x || !f.k_cache || !f.v_cache) return fail(AF_EVALUE, "attention phase: NULL argument");
+            if ((reinterpret_cast<uintptr_t>(f.k_cache) & 15) != 0 || (reinterpret_cast<uintptr_t>(f.v_cache) & 15) != 0)
+                return fail(AF_EDIM, "KV caches must be 16-byte aligned");
+        } else if (f.kind == AF_FW_ATTN_COMBINE) {
+            if (!f.out) return fail(AF_EVALUE, "attention combine: NULL output");
+            if (i == 0 || ph[i - 1].kind != AF_FW_ATTN_PARTIAL) return fail(AF_EVALUE, "an attention combine follows its partials phase");
+        } else {
+            return fail(AF_EVALUE, "unknown phase kind");
+        }
+    }
+    if (max_cols_out) *max_cols_out = max_cols;
+    return AF_OK;
+}
+
+int af_forward_persistent(const af_fw_phase* phases_dev, int32_t n_phases, int32_t max_cols, const float* cos_table,
+                          const float* sin_table, const int32_t* pos_dev, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                          int32_t max_seq, float* workspace, int32_t* phase_done_dev, int32_t* err_flag_dev, int32_t pdl, void* stream) {
+    if (!phases_dev || n_phases < 1 || !phase_done_dev) return fail(AF_EVALUE, "NULL argument");
+    if (head_dim != 64 && head_dim != 128) return fail(AF_EDIM, "the persistent forward takes head_dim 64 or 128");
+    if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads != 0 || max_seq < 1) return fail(AF_EDIM, "bad attention geometry");
+    if (!cos_table || !sin_table || !pos_dev || !workspace) return fail(AF_EVALUE, "NULL argument");
+    if (max_cols < 8) return fail(AF_EDIM, "max_cols comes from af_forward_validate");
+    const DeviceInfo& di = device_info();
+    if (!di.ok) return fail(AF_ECUDA, "no CUDA device");
+    // the input-vector area doubles as the attention teams' merge buffers
+    const int xs_bytes = std::max(max_cols * 4, kFwTeams * kFwTeamWarps * (head_dim + 2) * 4);
+    int n_stages = (di.max_smem_optin - 2048 - xs_bytes) / kGcStage;
+    n_stages = std::min(n_stages, kGcMaxStages);
+    if (n_stages < 2) return fail(AF_EDIM, "GEMV input vector does not fit in shared memory next to the weight ring");
+    const int smem = n_stages * kGcStage + xs_bytes;
+    static PerDevice configured;
+    if (smem > configured.cur()) {
+        AF_CUDA_TRY(cudaFuncSetAttribute(forward_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;   // every CTA takes part in the phase barriers: the grid must be co-resident
+        AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, forward_persistent_kernel, kGcThreads, smem));
+        if (per_sm < 1) return fail(AF_ESTATE, "the persistent forward needs one resident CTA per SM; this device cannot hold it");
+        configured.cur() = smem;
+    }
+    FwParams gp{};
+    gp.table = reinterpret_cast<const FwPhase*>(phases_dev);
+    gp.n_phases = n_phases;
+    gp.phase_done = phase_done_dev;
+    gp.n_stages = n_stages;
+    gp.pdl = (pdl && g_pdl.load()) ? 1 : 0;
+    gp.err_flag = err_flag_dev;
+    gp.cos_t = cos_table;
+    gp.sin_t = sin_table;
+    gp.pos_dev = pos_dev;
+    gp.n_heads = n_heads;
+    gp.n_kv = n_kv_heads;
+    gp.head_dim = head_dim;
+    gp.max_seq = max_seq;
+    gp.scale = 1.0f / sqrtf((float)head_dim);
+    gp.ws = workspace;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(di.sm_count);
+    cfg.blockDim = dim3(kGcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = gp.pdl ? 1 : 0;
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, forward_persistent_kernel, gp));
+    AF_LAUNCH_CHECK("forward_persistent_kernel");
     return AF_OK;
 }
 

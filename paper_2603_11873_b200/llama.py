@@ -74,6 +74,12 @@ class LlamaConfig:
     split_switch: bool = True        # > 64 stacked ranks: several tensor-path passes instead of one CUDA-core pass
     defer_norm: bool = True          # chase on the tcgen05 path: RMSNorm scales computed by one CTA, applied by the consumers
     gemv_chain: bool = True          # plain forward (separate / adapter-free): the same four projections as one persistent GEMV launch
+    # ... and the whole forward of a token -- attention included -- as ONE launch over a device-side phase table
+    # (af_forward_persistent).  Correct and tested, but OFF: measured on Llama-2-7B at 1024 positions the adapter-free
+    # decode is 3.51 ms per token against 2.82 ms for one chained launch per layer + the attention kernel -- inside one
+    # launch the attention is two more phases, and a phase boundary (grid barrier + input vector + pipeline restart
+    # ~ 4-5 us) costs as much as the programmatic-dependent-launch hand-over it replaces (~14 us per layer for three).
+    persistent_forward: bool = False
     # chained chase launches: time every CTA's phases once at engine build and split each phase's tiles by the measured
     # rates (`calibrate_schedule`).  Off: measured on Llama-2-7B, the spread of the CTAs' arrival at a phase barrier
     # (~4 us) is tile granularity (+-1 tile of 1.6 us) and unit changes, not a per-SM rate -- recalibrating moves it to
@@ -421,6 +427,12 @@ class LlamaEngine:
         # phase counters of the chained plain-GEMV launches (4 per layer), zeroed once per forward
         self.use_gemv_chain = cfg.gemv_chain and cfg.tp_size == 1
         self.gc_done = torch.zeros(4 * cfg.layers, dtype=torch.int32, device=dev)
+        # the whole plain forward as one launch over a device-side phase table (head_dim 64 / 128, single rank)
+        self.use_fw_persistent = bool(self.use_gemv_chain and cfg.persistent_forward and hd in (64, 128)
+                                      and os.environ.get("AF_FW_PERSISTENT", "1") != "0")
+        self._fw = None
+        if self.use_fw_persistent:
+            self._fw_build()            # (uploads the phase table: not something to do lazily inside a graph capture)
         # ---- fused switch + GEMV ("chase") ----
         want = cfg.forward_mode
         # more stacked ranks than one launch takes: the switch runs in tensor-path passes and the LAST pass carries the GEMVs
@@ -614,8 +626,63 @@ class LlamaEngine:
             self._check(L.af_gemv_chain(arr, len(phases), _ptr(self.gc_done[4 * li: 4 * li + 4]), _ptr(self.err_dev), 1, st))
         self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
 
+    def _fw_build(self):
+        """The device-side phase table of `forward_persistent`: q|k|v(0), then per layer attention partials, attention
+        combine, o, gate|up, down and the next layer's q|k|v (the lm_head after the last layer)."""
+        import ctypes
+
+        cfg, L = self.cfg, _capi.lib()
+        d, eps = cfg.hidden, cfg.rms_eps
+        xa, xb = self.x
+        n_qkv, n_gu = self.q_rows + 2 * self.kv_rows, 2 * self.ffn_local
+        P = _capi.FwPhase
+
+        def gemv(w, rows, cols, x, out, prologue=_capi.AF_PRO_NONE, norm_w=None, epilogue=_capi.AF_EPI_NONE, res=None):
+            return P(w=_ptr(w), x=_ptr(x), out=_ptr(out), res=_ptr(res) if res is not None else None,
+                     norm_w=_ptr(norm_w) if norm_w is not None else None, k_cache=None, v_cache=None, ld=cols, rows=rows, cols=cols,
+                     eps=float(eps), prologue=prologue, epilogue=epilogue, kind=_capi.AF_FW_GEMV)
+
+        ph = [gemv(self.wqkv[0], n_qkv, d, xa, self.qkv_buf, _capi.AF_PRO_RMSNORM, self.attn_norm[0])]
+        for li in range(cfg.layers):
+            ph.append(P(w=None, x=_ptr(self.qkv_buf), out=None, res=None, norm_w=None, k_cache=_ptr(self.k_cache[li]),
+                        v_cache=_ptr(self.v_cache[li]), ld=0, rows=0, cols=0, eps=0.0, prologue=0, epilogue=0, kind=_capi.AF_FW_ATTN_PARTIAL))
+            ph.append(P(w=None, x=None, out=_ptr(self.attn_buf), res=None, norm_w=None, k_cache=None, v_cache=None, ld=0, rows=0, cols=0,
+                        eps=0.0, prologue=0, epilogue=0, kind=_capi.AF_FW_ATTN_COMBINE))
+            ph.append(gemv(self.wo[li], d, self.q_rows, self.attn_buf, xb, epilogue=_capi.AF_EPI_RESIDUAL, res=xa))
+            ph.append(gemv(self.wgu[li], n_gu, d, xb, self.gu_buf, _capi.AF_PRO_RMSNORM, self.ffn_norm[li]))
+            ph.append(gemv(self.wdown[li], d, self.ffn_local, self.gu_buf, xa, _capi.AF_PRO_SILU_MUL, epilogue=_capi.AF_EPI_RESIDUAL, res=xb))
+            if li + 1 < cfg.layers:
+                ph.append(gemv(self.wqkv[li + 1], n_qkv, d, xa, self.qkv_buf, _capi.AF_PRO_RMSNORM, self.attn_norm[li + 1]))
+            else:
+                ph.append(gemv(self.lm_head.data, self.vocab_local, d, xa, self.logits, _capi.AF_PRO_RMSNORM, self.final_norm))
+        arr = (P * len(ph))(*ph)
+        max_cols = ctypes.c_int32()
+        self._check(L.af_forward_validate(arr, len(ph), self.heads_local, self.kv_local, cfg.head_dim, ctypes.byref(max_cols)))
+        raw = np.frombuffer(ctypes.string_at(ctypes.addressof(arr), ctypes.sizeof(arr)), dtype=np.uint8).copy()
+        chunks = -(-cfg.max_seq // 64)
+        self._fw = {"table": torch.from_numpy(raw).to(self.dev), "n": len(ph), "max_cols": int(max_cols.value),
+                    "done": torch.zeros(len(ph), dtype=torch.int32, device=self.dev),
+                    "ws": torch.zeros(self.heads_local * chunks * (cfg.head_dim + 2), dtype=torch.float32, device=self.dev)}
+
+    def forward_persistent(self) -> None:
+        """The same forward as `forward`, as ONE persistent launch over all layers (af_forward_persistent): the CTAs
+        never leave between projections and attentions; the weights of the next projection fill the ring while the
+        attention of the layer runs as two phases of the same kernel."""
+        cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
+        if self._fw is None:
+            self._fw_build()
+        fw = self._fw
+        fw["done"].zero_()
+        self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, cfg.hidden, _ptr(self.token_dev), _ptr(self.x[0]), st))
+        self._check(L.af_forward_persistent(_ptr(fw["table"]), fw["n"], fw["max_cols"], _ptr(self.cos), _ptr(self.sin), _ptr(self.pos_dev),
+                                            self.heads_local, self.kv_local, cfg.head_dim, cfg.max_seq, _ptr(fw["ws"]), _ptr(fw["done"]),
+                                            _ptr(self.err_dev), 1, st))
+        self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
+
     def forward(self) -> None:
         """Merged-path forward of one token (model.py:367-371 on the Llama block)."""
+        if self.use_fw_persistent:
+            return self.forward_persistent()
         if self.use_gemv_chain:
             return self.forward_chained()
         cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()

@@ -140,6 +140,40 @@ def test_split_attention_and_pdl_do_not_change_results(llama, forward_mode):
     assert np.array_equal(outs[2][1], outs[0][1])
 
 
+@pytest.mark.parametrize("shape", ["mha-hd64", "gqa-hd64", "hd128"])
+def test_persistent_forward_equals_chained_forward(llama, shape):
+    """af_forward_persistent (the whole forward of a token -- attention included -- as ONE launch over a device-side
+    phase table) against the chained forward with the standalone attention kernel: same tokens, logits to f32
+    round-off of the different attention chunking (plus the occasional flipped bf16 rounding of a cached k / v),
+    over 150 positions (three 64-position chunks per head, several rounds of work items per team)."""
+    extra = {"mha-hd64": {}, "gqa-hd64": dict(n_heads=4, n_kv_heads=1), "hd128": dict(hidden=512, n_heads=4, n_kv_heads=2, ffn=1024)}[shape]
+    forced = np.random.Generator(np.random.PCG64(17)).integers(0, 512, 150)
+    outs = []
+    for persistent in (False, True):
+        eng = llama.LlamaEngine(llama.preset("tiny", max_seq=160, forward_mode="separate", persistent_forward=persistent, **extra), init="host")
+        assert eng.use_fw_persistent == persistent and eng.cfg.head_dim == (128 if shape == "hd128" else 64)
+        eng.reset(forced=forced)
+        logits = []
+        for step in range(150):
+            eng.decode_step(graph=(step % 2 == 1))      # eager and replayed steps alternate
+            logits.append(eng.logits.cpu().numpy().copy())
+        eng.check()
+        outs.append((eng.tokens(), np.stack(logits), [k.clone() for k in eng.k_cache], [v.clone() for v in eng.v_cache]))
+    (ta, la, ka, va), (tb, lb, kb, vb) = outs
+    scale = np.max(np.abs(la))
+    assert np.max(np.abs(la - lb)) <= 2e-4 * scale
+    agree = sum(a == b for a, b in zip(ta, tb))
+    assert agree >= len(ta) - 2                          # a near-tie may flip on 1e-4 logits
+    for a, b in zip(ka + va, kb + vb):                   # caches: same bf16 values up to a flipped rounding here and there
+        assert (a.float() - b.float()).abs().max().item() <= 2.0 ** -6 * a.float().abs().max().item()
+        assert (a != b).float().mean().item() < 0.02
+    # the adapter-free backbone runs the same launch
+    base = llama.LlamaEngine(llama.preset("tiny", max_seq=32, adapters=False, persistent_forward=True, **extra), init="host")
+    assert base.use_fw_persistent
+    ref = llama.LlamaEngine(llama.preset("tiny", max_seq=32, adapters=False, persistent_forward=False, **extra), init="host")
+    assert base.generate([5, 17, 300], 12) == ref.generate([5, 17, 300], 12)
+
+
 def test_chained_plain_forward_equals_per_projection_launches(llama):
     """af_gemv_chain (one persistent launch per layer) against one af_gemv_fused launch per projection:
     same tokens, logits equal to f32 summation-order round-off; adapter-free and separate schedules."""
