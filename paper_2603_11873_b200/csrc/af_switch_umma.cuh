@@ -758,9 +758,12 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     const int m0 = ti.m0, row_end = ti.row_end, col0 = ti.un.col0;
                     new_unit = ti.next(p);
                     if ((it & 1) == group) {
+                        const bool probe = GEMV && tl && tl_first && cur_phase == 1 && tid == (it & 1) * 128;   // timeline: first tile of phase 1, one thread per group
+                        if (probe) tl_stamp(tl, 26 + 3 * (it & 1));
                         mbar_wait(&full[stage], ph);        // the W tile (TMA) is in shared memory
                         mbar_wait(&acc_full[buf], aph);     // the MMAs of this tile have completed
                         tc_fence_after();
+                        if (probe) tl_stamp(tl, 27 + 3 * (it & 1));
                         const uint32_t wrow = w_base + stage * kUWStage + row_in_tile * 128;
                         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * kUN;
                         float y = 0.f;
@@ -806,6 +809,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                             tmem_ld_wait();
                             chunk(da, c4);
                         }
+                        if (probe) tl_stamp(tl, 28 + 3 * (it & 1));
                         tc_fence_before();
                         fence_proxy_async_smem();   // tile written back -> visible to the TMA store
                         __syncwarp();

@@ -140,6 +140,7 @@ def main():
                       open(os.path.join(PROF, "chase_traffic.json"), "w"), indent=1)
             print("chase traffic per launch", (rd + wr) / 1e6, "MB")
         full(tag, "switch_umma", "prof_switch_umma.ncu-rep")
+        full(tag, "tp_shard", "prof_shard.ncu-rep")      # one fused launch of a Llama-2-7B tp4 shard (partial tiles)
         for name, dst in (("chase_timeline.txt", "chase_timeline.txt"), ("umma_ab.txt", "umma_ab.txt"), ("umma_switch_ab.txt", "umma_switch_ab.txt"), ("bench.json", "bench.json"), ("bench_separate.json", "bench_separate.json"),
                           ("chase_kernel.txt", "chase_kernel.txt"), ("ab.txt", "consumer_loop_ab.txt")):
             pth = os.path.join(OUT, name)

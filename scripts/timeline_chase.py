@@ -79,6 +79,14 @@ if not args.no_chain:
         same_sm = np.all(tl[1:-1, :, 24] == smid[None, :])
         print("   CTA -> SM mapping identical in every launch:", bool(same_sm))
 if not args.no_chain:
+    # tcgen05 kernel: the first tile of phase 1 by each epilogue group: loop entry -> operands ready -> chunks done
+    for grp in (0, 1):
+        a, b, c = (tl[1:-1, :, 26 + 3 * grp + k] for k in range(3))
+        pr = tl[1:-1, :, 10 + 4]     # p1.prolog
+        if not np.all(np.isnan(a)):
+            print(f"phase 1, first tile of epilogue group {grp}: prolog -> loop entry med {np.nanmedian(a - pr) / 1e3:.2f} us, "
+                  f"entry -> W tile + accumulator ready med {np.nanmedian(b - a) / 1e3:.2f} us, ready -> four chunks done med {np.nanmedian(c - b) / 1e3:.2f} us")
+if not args.no_chain and False:
     # first unit change inside phase 1 (CTAs whose span crosses a strip boundary)
     uc = tl[1:-1, :, 26:32]
     has = ~np.isnan(uc[:, :, 0])
