@@ -37,13 +37,16 @@ def main():
     ap.add_argument("--steps", type=int, default=48)
     ap.add_argument("--switch-mode", default="inplace")
     ap.add_argument("--forward-mode", default="auto", choices=["auto", "chase", "separate"])
+    ap.add_argument("--context", type=int, default=1024, help="positions already in the KV cache")
     args = ap.parse_args()
-    cfg = llama.preset(args.workload, max_seq=8 * args.steps + 64, switch_mode=args.switch_mode, forward_mode=args.forward_mode)
+    # (refresh_every = 0: the sweep's graphs are captured by hand; the refreshing step costs the same as a steady one)
+    cfg = llama.preset(args.workload, max_seq=args.context + 8 * args.steps + 64, switch_mode=args.switch_mode, forward_mode=args.forward_mode,
+                       refresh_every=0)
     eng = llama.LlamaEngine(cfg, init="device")
     forced = np.random.Generator(np.random.PCG64(7)).integers(0, cfg.vocab, 4096)
     eng.reset(forced=forced)
     for _ in range(3):
-        eng.decode_step()
+        eng.decode_step(graph=False)
     g_switch = capture(lambda: eng._step_body(True))
 
     def hold():
@@ -60,11 +63,11 @@ def main():
     # a switching step moves the switch bytes and, in the separate schedule, the forward's bytes on top;
     # in the chase schedule the forward rides on the switch's pass (only lm_head is extra)
     switch_step_bytes = cfg.switch_bytes() + (lm_head_bytes if eng.chase else cfg.decode_bytes())
-    print(json.dumps({"workload": args.workload, "switch_mode": args.switch_mode, "forward_mode": "chase" if eng.chase else "separate",
+    print(json.dumps({"workload": args.workload, "context_positions": args.context, "switch_mode": args.switch_mode, "forward_mode": "chase" if eng.chase else "separate",
                       "segments": eng.table.info()["n_segments"],
                       "switch_bytes": cfg.switch_bytes(), "decode_bytes": cfg.decode_bytes()}), flush=True)
     for period in (1, 2, 4, 8, 16, 0):
-        eng.pos_dev.fill_(4)
+        eng.set_position(args.context)
         for _ in range(2):
             g_switch.replay()
         torch.cuda.synchronize()
@@ -84,7 +87,7 @@ def main():
         print(json.dumps({"switch_period": period if period else "inf", "switches": n_sw, "ms_per_token": round(ms, 4),
                           "tok_s": round(1e3 / ms, 1), "hbm_GBps": round(bytes_per_tok / ms / 1e6, 1),
                           "frac_of_measured_peak": round(bytes_per_tok / ms / 1e6 / peak, 4)}), flush=True)
-    eng.table.status()
+    eng.check()
 
 
 if __name__ == "__main__":
