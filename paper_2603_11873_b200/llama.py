@@ -926,7 +926,7 @@ class LlamaEngine:
         return [int(v) for v in self.history[:n].cpu().numpy()]
 
     @_on_device
-    def prefill(self, prompt) -> int:
+    def prefill(self, prompt, use_graph: bool = True) -> int:
         """Batched UNMERGED prefill of a whole prompt (model.py:408-425; PAPER Eq. 2): all T tokens go
         through every layer at once, token t with its own pre-gated decision,
 
@@ -939,7 +939,12 @@ class LlamaEngine:
         paper, not tuned; the router decisions come from the same `pregate_kernel` the decode uses.
         Fills the KV cache for positions 0 .. T-1 (bf16, rotated, as the decode kernel stores
         them), leaves the engine at position T with pristine weights, and returns the token
-        emitted after the prompt.  Single rank."""
+        emitted after the prompt.  Single rank.
+
+        The pass is ~100 small device operations per layer and was bound by their host launches (54 of 61 ms for
+        512 tokens of Llama-2-7B): with `use_graph` (default) the whole pass is captured once per prompt LENGTH as a
+        CUDA graph (after one eager run that also warms the library handles) and replayed -- the prompt's tokens are
+        the graph's only input."""
         cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
         prompt = [int(t) for t in prompt]
         if not prompt:
@@ -951,9 +956,47 @@ class LlamaEngine:
         if cfg.tp_size != 1:
             raise StateError("batched prefill is single-rank; TP engines consume the prompt step by step")
         self.reset(prompt[0])
-        T, d, hd, f32 = len(prompt), cfg.hidden, cfg.head_dim, torch.float32
+        T = len(prompt)
+        if not hasattr(self, "_prefill_graphs"):
+            self._prefill_graphs = {}
+            self._prefill_hidden = torch.zeros(cfg.hidden, dtype=torch.float32, device=self.dev)
+        host_tok = torch.tensor(prompt, dtype=torch.int32)
+        entry = self._prefill_graphs.get(T) if use_graph else None
+        if entry is None:
+            tok = host_tok.to(self.dev)
+            self._prefill_body(tok, T)                      # eager (first use of a length; also the non-graph path)
+            if use_graph:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(g, stream=side):
+                        self._prefill_body(tok, T)
+                torch.cuda.current_stream().wait_stream(side)
+                if len(self._prefill_graphs) >= 4:          # a few prompt lengths at a time (each graph owns its activations)
+                    self._prefill_graphs.pop(next(iter(self._prefill_graphs)))
+                self._prefill_graphs[T] = (g, tok)
+        else:
+            g, tok = entry
+            tok.copy_(host_tok)
+            g.replay()
+        nxt = int(self.next_dev.item())
+        self.pos_dev.fill_(T)
+        self._pos_host = T
+        self.step_dev.fill_(T)
+        self.history[T - 1] = nxt
+        self.token_dev.fill_(nxt)
+        self.last_prefill_hidden = self._prefill_hidden
+        return nxt
+
+    def _prefill_body(self, tok, T: int) -> None:
+        """Every device operation of `prefill` for a prompt of T tokens held in `tok` (int32, device): router decisions,
+        the unmerged batched layers, the KV cache rows, the emitted token in `next_dev`.  No host synchronisation, static
+        shapes: capturable as a CUDA graph per prompt length."""
+        cfg, L, st = self.cfg, _capi.lib(), _capi.stream_ptr()
+        d, hd, f32 = cfg.hidden, cfg.head_dim, torch.float32
         nh, nkv = self.heads_local, self.kv_local
-        tok = torch.tensor(prompt, dtype=torch.int32, device=self.dev)
         gates = None
         if cfg.adapters:
             decs = torch.zeros((T, DECISION_BYTES), dtype=torch.uint8, device=self.dev)
@@ -1008,18 +1051,11 @@ class LlamaEngine:
             u = linear(xn, li, 5, self.wgu[li][self.ffn_local:])
             x = x + linear(torch.nn.functional.silu(g) * u, li, 6, self.wdown[li])
         # the emitted token: the decode's own lm_head + argmax kernels on the last position
+        self._prefill_hidden[:] = x[T - 1]
         self.x[0].copy_(x[T - 1])
         self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(self.x[0]), _ptr(self.logits),
                                     _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), cfg.rms_eps, _capi.AF_EPI_NONE, None, st))
         self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, 0, _ptr(self.next_dev), _ptr(self.next_val), st))
-        nxt = int(self.next_dev.item())
-        self.pos_dev.fill_(T)
-        self._pos_host = T
-        self.step_dev.fill_(T)
-        self.history[T - 1] = nxt
-        self.token_dev.fill_(nxt)
-        self.last_prefill_hidden = x[T - 1]
-        return nxt
 
     @_on_device
     def generate(self, prompt, n_new: int, use_graph: bool = True, prefill: str = "auto") -> list:
