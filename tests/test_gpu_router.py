@@ -99,3 +99,28 @@ def test_device_decision_round_trip(af):
     dd = af.DeviceDecision.from_host(gd)
     assert dd.to_host() == gd
     assert torch.cuda.is_available()
+
+
+def test_nan_logits_sort_last_like_numpy(af):
+    """routing.py:64-65 is `np.argsort(-logits, kind="stable")`: numpy sorts NaN after every number (and NaN against NaN
+    by index).  A router row that produces NaN must therefore never be selected while k numbers exist."""
+    import torch
+
+    n, d, k = 8, 64, 3
+    rng = np.random.Generator(np.random.PCG64(77))
+    w = rng.uniform(-1, 1, (n, d)).astype(np.float32)
+    x = rng.uniform(-1, 1, d).astype(np.float32)
+    w[0, 5] = np.nan            # the very first expert: "first seen in a lane" must not stick as the lane's best
+    w[6, 1] = np.nan
+    router = af.RouterParams(weight=af.Matrix(torch.from_numpy(w).cuda(), "single"))
+    dec = af.route(router, af.Matrix(torch.from_numpy(x.reshape(-1, 1)).cuda(), "single"), k, af.DispatchRecorder())
+    logits = (w.astype(np.float64) @ x.astype(np.float64)).astype(np.float32)
+    want = tuple(int(i) for i in np.argsort(-logits, kind="stable")[:k])
+    assert 0 not in dec.expert_ids and 6 not in dec.expert_ids
+    assert dec.expert_ids == want
+    # with fewer than k numbers the NaN rows fill the tail, lowest index first
+    w2 = np.full((4, d), np.nan, np.float32)
+    w2[2] = rng.uniform(-1, 1, d)
+    router2 = af.RouterParams(weight=af.Matrix(torch.from_numpy(w2).cuda(), "single"))
+    dec2 = af.route(router2, af.Matrix(torch.from_numpy(x.reshape(-1, 1)).cuda(), "single"), 3, af.DispatchRecorder())
+    assert dec2.expert_ids == (2, 0, 1)
