@@ -236,3 +236,89 @@ def test_collectives_need_an_initialised_group():
     with pytest.raises(af.StateError):
         llama.Collectives(None, 2)
     llama.Collectives(None, 1).all_reduce_sum(torch.zeros(1))       # tp=1: no-ops
+
+
+# ------------------------------------------------------------------ round-2 host logic ----
+
+
+def test_refresh_period_defaults_and_validation():
+    """model.py:344-349 `refresh_every`: the reference's default (never) stays for f32; bf16 storage refreshes every 16
+    tokens unless told otherwise; -1 turns it off."""
+    assert af.ModelConfig(precision="single").effective_refresh_every == 0
+    assert af.ModelConfig(precision="bf16").effective_refresh_every == 16
+    assert af.ModelConfig(precision="bf16", refresh_every=5).effective_refresh_every == 5
+    assert af.ModelConfig(precision="bf16", refresh_every=-1).effective_refresh_every == 0
+    assert af.ModelConfig(precision="bf16", switch_mode="from_pristine").effective_refresh_every == 0
+    assert af.ModelConfig(precision="bf16", strategy=af.Strategy.BASE).effective_refresh_every == 0
+    with pytest.raises(ValueError):
+        af.ModelConfig(refresh_every=-2).validate()
+    assert llama.preset("tiny").refresh_every == 16
+    with pytest.raises(ValueError):
+        llama.preset("tiny", refresh_every=-1)
+    with pytest.raises(ValueError):
+        llama.preset("tiny", refresh_every=True)
+
+
+def test_status_word_messages_and_exception_classes():
+    """af_flag_message / _capi.raise_for_flag: what a kernel raised on the device maps onto the reference's classes."""
+    from paper_2603_11873_b200 import _capi, errors
+
+    L = _capi.lib()
+    assert b"outside the bank" in L.af_flag_message(_capi.AF_EINDEX)
+    assert b"phase barrier" in L.af_flag_message(_capi.AF_ECUDA)
+    _capi.raise_for_flag(0)
+    with pytest.raises(IndexError):
+        _capi.raise_for_flag(_capi.AF_EINDEX)
+    with pytest.raises(ValueError):
+        _capi.raise_for_flag(_capi.AF_EVALUE)
+    with pytest.raises(errors.StateError):
+        _capi.raise_for_flag(_capi.AF_ESTATE)
+    with pytest.raises(errors.DeviceError):
+        _capi.raise_for_flag(_capi.AF_ECUDA)
+
+
+def test_forward_phase_table_validation():
+    """af_forward_validate checks the HOST copy of the persistent forward's phase table before it is uploaded
+    (no device needed): shapes, alignment, prologue / epilogue operands, phase order."""
+    import ctypes
+
+    from paper_2603_11873_b200 import _capi, errors
+
+    L = _capi.lib()
+    P = _capi.FwPhase
+    assert ctypes.sizeof(P) == 88
+
+    def gemv(**kw):
+        base = dict(w=0x1000, x=0x2000, out=0x3000, res=None, norm_w=None, k_cache=None, v_cache=None, ld=256, rows=64, cols=256,
+                    eps=1e-5, prologue=_capi.AF_PRO_NONE, epilogue=_capi.AF_EPI_NONE, kind=_capi.AF_FW_GEMV)
+        base.update(kw)
+        return P(**base)
+
+    att_p = P(w=None, x=0x2000, out=None, res=None, norm_w=None, k_cache=0x4000, v_cache=0x5000, ld=0, rows=0, cols=0, eps=0.0,
+              prologue=0, epilogue=0, kind=_capi.AF_FW_ATTN_PARTIAL)
+    att_c = P(w=None, x=None, out=0x6000, res=None, norm_w=None, k_cache=None, v_cache=None, ld=0, rows=0, cols=0, eps=0.0,
+              prologue=0, epilogue=0, kind=_capi.AF_FW_ATTN_COMBINE)
+
+    def check(phases, heads=4, kv=2, hd=64):
+        arr = (P * len(phases))(*phases)
+        mc = ctypes.c_int32()
+        _capi.check(L.af_forward_validate(arr, len(phases), heads, kv, hd, ctypes.byref(mc)))
+        return mc.value
+
+    assert check([gemv(), att_p, att_c, gemv(cols=512, ld=512)]) == 512
+    with pytest.raises(errors.DimensionError):
+        check([gemv()], hd=96)                                      # head_dim 64 or 128
+    with pytest.raises(errors.DimensionError):
+        check([gemv(cols=250, ld=250)])                             # 16-byte rows
+    with pytest.raises(ValueError):
+        check([gemv(prologue=_capi.AF_PRO_RMSNORM)])                # RMSNorm without its weight
+    with pytest.raises(ValueError):
+        check([gemv(epilogue=_capi.AF_EPI_RESIDUAL)])               # residual epilogue without a residual
+    with pytest.raises(errors.AliasingError):
+        check([gemv(out=0x2000)])
+    with pytest.raises(ValueError):
+        check([gemv(), att_c])                                      # a combine needs its partials phase in front
+    with pytest.raises(ValueError):
+        check([gemv(kind=7)])
+    with pytest.raises(errors.DimensionError):
+        check([gemv()], heads=3, kv=2)
