@@ -74,11 +74,11 @@ struct UmmaLayout {
     // Two rings.  W tiles (32 KB, from HBM) live from their load until their store has read them; UP stages
     // (from L2) only until the MMAs that read them have completed, two tiles ahead of the epilogue at most.
     // Whole-operand stages: three are enough, which leaves a 64-rank launch (16 KB UP stages, 32 KB slab) four
-    // W stages instead of three.  Chunked (8 KB stages): a tile consumes NB / CH stages in a burst, each an L2
-    // round trip: six stages (measured at 128 stacked ranks on Llama-2-70B shard shapes: six UP + three W stages
-    // 2.59 ms, three UP + four W stages 2.85 ms) -- except at 256, where the 128 KB slab leaves room for three
-    // UP and two W stages.
-    static constexpr int up_stages_wanted = chunked ? (NB >= 32 ? 3 : 6) : (NB > 4 ? 3 : 6);
+    // W stages instead of three.  Chunked: a tile consumes NB / CH stages in a burst, each an L2 round trip.  With
+    // 32-rank chunks (8 KB): six stages (measured at 128 stacked ranks on Llama-2-70B shard shapes: six UP + three W
+    // stages 2.59 ms, three UP + four W stages 2.85 ms) -- except at 256, where the 128 KB slab leaves room for three
+    // UP and two W stages.  With 64-rank chunks (16 KB, the choice at 128 stacked ranks: 2.41 ms): three stages.
+    static constexpr int up_stages_wanted = chunked ? ((NB >= 32 || CH >= 8) ? 3 : 6) : (NB > 4 ? 3 : 6);
     static constexpr int by_smem = (227 * 1024 - fixed) / (kUWStage + up_stage);          // equal depths
     static constexpr int by_smem_w = (227 * 1024 - fixed - up_stages_wanted * up_stage) / kUWStage;
     static constexpr int stages = (NB > 4 || chunked) ? (by_smem_w < 6 ? by_smem_w : 6) : (by_smem < 6 ? by_smem : 6);
