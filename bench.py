@@ -209,6 +209,8 @@ def main():
     ap.add_argument("--no-chain", action="store_true", help="chase: one launch per projection instead of chained phases")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--attn-splits", type=int, default=0, help="KV splits of the decode attention (0 = the engine's choice)")
+    ap.add_argument("--persistent-forward", action="store_true",
+                    help="plain forward (separate schedule, decode_only) as ONE launch per token (af_forward_persistent) instead of one chained launch per layer")
     ap.add_argument("--context", type=int, default=1024, help="positions already in the KV cache when the timed regions start")
     ap.add_argument("--refresh-every", type=int, default=16,
                     help="in-place mode: rebuild W from the pristine copy every N tokens (reference model.py:344-349; folded into "
@@ -253,7 +255,7 @@ def main():
     max_seq = args.context + 3 * (args.steps + args.warmup) + 64
     cfg = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
                        compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain,
-                       attn_splits=args.attn_splits, refresh_every=args.refresh_every)
+                       attn_splits=args.attn_splits, refresh_every=args.refresh_every, persistent_forward=args.persistent_forward)
     eng = llama.LlamaEngine(cfg, init="device")
     info = eng.table.info()
     forced = np.random.Generator(np.random.PCG64(cfg.seed + 1)).integers(0, cfg.vocab, 4096)

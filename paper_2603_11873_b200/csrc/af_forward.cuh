@@ -62,7 +62,7 @@ struct FwParams {
 
 // ---- attention partials of one phase: every team loops over its (head, chunk) items ----
 template <int HD>
-__device__ __forceinline__ void fw_attn_partials(const FwPhase& f, const FwParams& A, float* sm_f, int tid, int G) {
+__device__ __noinline__ void fw_attn_partials(const FwPhase& f, const FwParams& A, float* sm_f, int tid, int G) {
     constexpr int EL = HD / 32, half = HD / 2;
     const int lane = tid & 31, warp = tid >> 5;
     const int team = warp / kFwTeamWarps, tw = warp % kFwTeamWarps, tid_t = tid - team * kFwTeamWarps * 32;
@@ -202,7 +202,7 @@ __device__ __forceinline__ void fw_attn_partials(const FwPhase& f, const FwParam
 
 // ---- attention combine: one thread per output element folds the chunks of its head ----
 template <int HD>
-__device__ __forceinline__ void fw_attn_combine(const FwPhase& f, const FwParams& A, int tid, int G, int n_threads) {
+__device__ __noinline__ void fw_attn_combine(const FwPhase& f, const FwParams& A, int tid, int G, int n_threads) {
     const int pos = __ldcg(A.pos_dev);
     if (pos < 0 || pos >= A.max_seq) return;
     const int n_chunks = (pos + kFwChunk) / kFwChunk, chunks_max = (A.max_seq + kFwChunk - 1) / kFwChunk;
