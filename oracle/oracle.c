@@ -362,3 +362,45 @@ int32_t orc_max_ulp_diff_bf16(const uint16_t* a, const uint16_t* b, int64_t n, i
     if (n_diff) *n_diff = cnt;
     return worst;
 }
+
+/* One pass over a merged matrix for the parity report of tests/test_gpu_true_shapes.py (the numpy form of
+ * oracle.strict_ulp_report takes seconds per 45M-element matrix; this takes tens of milliseconds):
+ *   out[0] = elements that differ, out[1] = elements off by more than one ulp OF THE RESULT,
+ *   out[2] = max |got - want| / ulp(max(|want|, |got|))            (the literal criterion)
+ *   out[3] = max |got - want| / ulp(max(|want|, |ref_k|...))       (the operand-magnitude criterion)
+ *   out[4] = over the strict violators, max |want| / max(|want|, |ref_k| ...)               (how deep they cancelled)
+ * ulp(x) = 2^(floor(log2 x) - 7), with the smallest normal's spacing below it. */
+static inline double orc_bf16_ulp(double mag) {
+    if (mag < 1.1754943508222875e-38) mag = 1.1754943508222875e-38;
+    int e;
+    frexp(mag, &e);
+    return ldexp(1.0, e - 1 - 7);
+}
+void orc_ulp_report_bf16(const uint16_t* got, const uint16_t* want, const uint16_t* const* refs, int n_refs, int64_t n, double* out) {
+    int64_t n_diff = 0, n_viol = 0;
+    double max_strict = 0.0, max_relaxed = 0.0, worst_ratio = 0.0;
+#pragma omp parallel for reduction(+ : n_diff, n_viol) reduction(max : max_strict, max_relaxed, worst_ratio) schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        if (got[i] == want[i]) continue;
+        const double g = (double)orc_bf16_to_f32(got[i]), w = (double)orc_bf16_to_f32(want[i]);
+        const double diff = fabs(g - w);
+        if (diff == 0.0) continue; /* +0 against -0 */
+        n_diff += 1;
+        const double res = fmax(fabs(g), fabs(w));
+        double mag = fabs(w);
+        for (int k = 0; k < n_refs; ++k) mag = fmax(mag, fabs((double)orc_bf16_to_f32(refs[k][i])));
+        const double strict = diff / orc_bf16_ulp(res), relaxed = diff / orc_bf16_ulp(mag);
+        if (strict > max_strict) max_strict = strict;
+        if (relaxed > max_relaxed) max_relaxed = relaxed;
+        if (strict > 1.0) {
+            n_viol += 1;
+            const double ratio = mag > 0.0 ? fabs(w) / mag : 1.0;
+            if (ratio > worst_ratio) worst_ratio = ratio;
+        }
+    }
+    out[0] = (double)n_diff;
+    out[1] = (double)n_viol;
+    out[2] = max_strict;
+    out[3] = max_relaxed;
+    out[4] = worst_ratio;
+}

@@ -932,7 +932,10 @@ int af_chain_create_weighted(af_table* t, const int32_t* seg_ids, const int32_t*
     g->n_units = (int)units.size();
     bool umma = t->umma_ok;
     if (umma) {
-        build(kUM, kUN, 1, 2, units_umma, g->grid_umma, nullptr);   // a 128 x 128 tile is 4x the bytes: a unit change weighs about one tile
+        static const int env_penalty_u = [] { const char* e = getenv("AF_UNIT_PENALTY_UMMA"); return e ? atoi(e) : 2; }();
+        // a 128 x 128 tile is 4x the bytes of the mma.sync kernel's: a unit change weighs about two tiles (swept 0 .. 3 on
+        // Llama-2-7B: 5.59 / 5.53 / 5.50 / 5.53 ms per token)
+        build(kUM, kUN, env_penalty_u, 2, units_umma, g->grid_umma, nullptr);
         g->n_units_umma = (int)units_umma.size();
     }
     cudaError_t e = cudaMalloc(&g->d_units, sizeof(UnitDev) * units.size());

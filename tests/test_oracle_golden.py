@@ -234,3 +234,22 @@ def test_oracle_thread_override_under_torchrun_env():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_ulp_report_c_pass_equals_numpy():
+    """oracle.strict_ulp_report (one OpenMP pass in oracle.c, what the true-shape GPU tests call on 45M-element
+    matrices) against its plain numpy statement."""
+    rng = np.random.default_rng(0)
+    want = orc.to_bf16_bits(rng.normal(size=(300, 257)).astype(np.float32) * 0.01)
+    got = want.copy()
+    idx = rng.integers(0, want.size, 2000)
+    got.reshape(-1)[idx] += rng.integers(-3, 4, 2000).astype(np.uint16)
+    got.reshape(-1)[7] = want.reshape(-1)[7] ^ 0x8000 if want.reshape(-1)[7] & 0x7FFF == 0 else got.reshape(-1)[7]
+    r1 = orc.to_bf16_bits(rng.normal(size=want.shape).astype(np.float32) * 0.05)
+    r2 = orc.to_bf16_bits(rng.normal(size=want.shape).astype(np.float32) * 0.001)
+    a, b = orc.strict_ulp_report(got, want, r1, r2), orc.strict_ulp_report_numpy(got, want, r1, r2)
+    assert a["n"] == b["n"] and a["n_diff"] == b["n_diff"] and a["n_violations"] == b["n_violations"]
+    for k in ("max_strict", "max_relaxed", "worst_ratio"):
+        assert abs(a[k] - b[k]) <= 1e-12 * max(1.0, abs(b[k])), k
+    same = orc.strict_ulp_report(want, want, r1)
+    assert same["n_diff"] == 0 and same["max_strict"] == 0.0 and same["n_violations"] == 0
