@@ -112,13 +112,20 @@ int af_set_pdl(int32_t enable);
  * Results are identical up to f32 summation order.  Env: AF_GEMV, AF_GEMV_FULL_SM. */
 int af_set_gemv_variant(int32_t variant, int32_t full_sm);
 /* Tensor path of the fused switch (+ GEMV) on eligible tables (one rank in {8, 16, 32, 64} everywhere,
- * every matrix a multiple of 128 x 128; launches of at most 64 stacked ranks for af_fused_switch, 32 for
- * af_switch_gemv[_chain]): 1 = tcgen05.mma with the accumulators in tensor memory
- * (csrc/af_switch_umma.cuh; default), 0 = mma.sync kernels (what every other table and launch uses).
+ * every matrix at least 128 x 128 with rows a multiple of 8; launches of up to 256 stacked ranks):
+ * 1 = tcgen05.mma with the accumulators in tensor memory (csrc/af_switch_umma.cuh; default),
+ * 0 = mma.sync kernels (what every other table and launch uses).
  * Both are within 1 bf16 ulp of the f32 merge; they round differently in the last bit, so do not mix
  * them inside one comparison.  Env: AF_UMMA=0 turns the tcgen05 path off at load;
- * AF_UMMA_MAX_RANKS / AF_UMMA_MAX_RANKS_CHAIN move the two limits (A/B runs). */
+ * AF_UMMA_MAX_RANKS / AF_UMMA_MAX_RANKS_CHAIN move the limits (A/B runs). */
 int af_set_umma(int32_t enable);
+/* bf16 pieces the tcgen05 kernels split a gated DOWN row (g * a, an f32 value) into before the tensor
+ * cores multiply it with UP: 2 (default; g*a reproduced to 2^-17 relative) or 3 (g*a exact: the merge
+ * then differs from the reference's f32 `B @ (g*A)` of linalg.py:150-168 only by the order of the f32
+ * sums -- 8x fewer last-bit differences, ~2 % more time per token at Llama-2-7B).  Three pieces apply
+ * to launches of at most 32 stacked ranks (rank 8, top-2: every BASELINE config but configs[2..4]);
+ * larger launches keep two.  AF_EVALUE for anything but 2 or 3.  Env: AF_UMMA_PIECES. */
+int af_set_umma_pieces(int32_t pieces);
 
 /* ---- segment table: built once at model load -------------------------------------
  * Replaces: linalg.py:207-231 `SegmentTable` + `.validate()` (shape, precision and

@@ -143,6 +143,7 @@ SIGNATURES = {
     "af_set_pdl": (ctypes.c_int, [_i32]),
     "af_set_gemv_variant": (ctypes.c_int, [_i32, _i32]),
     "af_set_umma": (ctypes.c_int, [_i32]),
+    "af_set_umma_pieces": (ctypes.c_int, [_i32]),
     "af_table_create": (ctypes.c_int, [ctypes.POINTER(SegmentDesc), _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     "af_table_destroy": (ctypes.c_int, [_vp]),
     "af_table_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),

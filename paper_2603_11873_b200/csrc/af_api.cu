@@ -58,6 +58,11 @@ static std::atomic<int> g_umma{[] {
     const char* e = getenv("AF_UMMA");
     return e ? atoi(e) : 1;
 }()};
+// bf16 pieces of the gated DOWN rows in launches of at most 32 stacked ranks (af_set_umma_pieces; env AF_UMMA_PIECES)
+static std::atomic<int> g_umma_pieces{[] {
+    const char* e = getenv("AF_UMMA_PIECES");
+    return e && atoi(e) == 3 ? 3 : 2;
+}()};
 static const bool g_force_hilo = [] { const char* e = getenv("AF_FORCE_HILO"); return e && e[0] == '1'; }();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and occupancy are per DEVICE: what has been configured is
 // remembered per device id, so a second GPU in the same process gets its own attribute call.
@@ -194,6 +199,12 @@ int af_set_pdl(int32_t enable) {
 
 int af_set_umma(int32_t enable) {
     g_umma.store(enable ? 1 : 0);
+    return AF_OK;
+}
+
+int af_set_umma_pieces(int32_t pieces) {
+    if (pieces != 2 && pieces != 3) return fail(AF_EVALUE, "the gated DOWN rows split into 2 or 3 bf16 pieces");
+    g_umma_pieces.store(pieces);
     return AF_OK;
 }
 
@@ -510,12 +521,12 @@ static const int kUmmaMaxRanksChain = [] { const char* e = getenv("AF_UMMA_MAX_R
 // barrier traffic: measured 1.5 % slower on Llama-3-8B shapes, so off)
 static const int kUmmaChunk64 = [] { const char* e = getenv("AF_UMMA_CHUNK64"); return e ? atoi(e) : 0; }();
 // tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = k-groups of 8 stacked ranks per half, CH = k-groups per UP stage.
-template <int NB, bool GEMV, int CH = NB>
+template <int NB, bool GEMV, int CH = NB, int PC = 2>
 static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
-    using L = UmmaLayout<NB, GEMV, CH>;
+    using L = UmmaLayout<NB, GEMV, CH, PC>;
     static PerDevice configured;
     if (!configured.cur()) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV, CH, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured.cur() = 1;
     }
     if (mp.n_phases > 1) {
@@ -525,7 +536,7 @@ static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
         static PerDevice occ_checked;
         if (!occ_checked.cur()) {
             int per_sm = 0;
-            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, switch_umma_kernel<NB, GEMV, CH>, kUThreads, L::total));
+            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, switch_umma_kernel<NB, GEMV, CH, PC>, kUThreads, L::total));
             const DeviceInfo& di = device_info();
             if (per_sm < 1 || grid > di.sm_count * per_sm)
                 return fail(AF_ESTATE, "a chained launch needs all its CTAs co-resident: " + std::to_string(grid) + " CTAs, device holds " +
@@ -543,9 +554,10 @@ static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = mp.pdl ? 1 : 0;
-    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV, CH>, mp));
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV, CH, PC>, mp));
     AF_LAUNCH_CHECK("switch_umma_kernel");
-    note_kernel("switch_umma_kernel<NB=%d,GEMV=%d,CH=%d> (tcgen05 + TMEM)", NB, (int)GEMV, CH);
+    note_kernel(PC == 3 ? "switch_umma_kernel<NB=%d,GEMV=%d,CH=%d,PC=3> (tcgen05 + TMEM)" : "switch_umma_kernel<NB=%d,GEMV=%d,CH=%d> (tcgen05 + TMEM)", NB,
+                (int)GEMV, CH);
     return AF_OK;
 }
 
@@ -556,7 +568,8 @@ static int umma_rank_limit(const af_table* t) {
 }
 template <bool GEMV>
 static int dispatch_umma(const af_table* t, int s_bound, const MmaParams& mp, int grid, cudaStream_t st) {
-    if (s_bound <= 32) return launch_umma<4, GEMV>(mp, grid, st);
+    // up to 32 stacked ranks: the gated DOWN rows in two or three bf16 pieces (af_set_umma_pieces; see UmmaLayout)
+    if (s_bound <= 32) return g_umma_pieces.load() == 3 ? launch_umma<4, GEMV, 4, 3>(mp, grid, st) : launch_umma<4, GEMV>(mp, grid, st);
     if (s_bound <= 64) return (kUmmaChunk64 && t->max_rank <= 32) ? launch_umma<8, GEMV, 4>(mp, grid, st) : launch_umma<8, GEMV>(mp, grid, st);
     // 128 stacked ranks: UP chunks of 64 ranks (three 16 KB stages) beat chunks of 32 (six 8 KB stages) -- half the chunk
     // barriers per tile: 2.41 against 2.61 ms on 24 layers of a Llama-2-70B tp8 shard, 13.0 against 14.5 ms per shard step

@@ -62,12 +62,16 @@ constexpr long long kUBurstAfterCycles = AF_UMMA_BURST_AFTER;
 
 // NB = k-groups of 8 stacked ranks the slab holds per half; CH = k-groups per UP ring stage (CH == NB: the whole
 // UP operand of a tile is one stage; CH < NB: K-chunked, NB / CH chunks per tile)
-template <int NB, bool GEMV, int CH = NB>
+// PC = bf16 pieces the gated DOWN rows are split into: 2 (hi + lo: g*a reproduced to 2^-17) or 3 (hi + mid + lo: the f32 value
+// of g*a exactly -- 24 bits in three 8-bit pieces -- so that the product differs from the reference's f32 merge only by the
+// order of the f32 sums).  Three pieces need 50 % more slab and MMAs: offered where both are cheap, at up to 32 stacked ranks.
+template <int NB, bool GEMV, int CH = NB, int PC = 2>
 struct UmmaLayout {
     static_assert(NB % CH == 0 && CH % 2 == 0, "chunks are whole rank-16 steps");
+    static_assert(PC == 2 || (PC == 3 && NB <= 4 && CH == NB), "three pieces: launches of at most 32 stacked ranks");
     static constexpr bool chunked = CH < NB;
     static constexpr int up_stage = CH * kUBlockBytes;
-    static constexpr int slab_bytes = 2 * NB * kUSlabBlock;            // hi + lo
+    static constexpr int slab_bytes = PC * NB * kUSlabBlock;           // hi + lo (+ a third piece)
     static constexpr int xs_bytes = GEMV ? kUXSlots * kUN * 4 : 0;
     static constexpr int misc = 1024 /*barriers*/ + (int)sizeof(Plan) + 256 + kUnitCache * (int)sizeof(UnitDev) + kSegCache * (int)sizeof(SegDev);
     static constexpr int fixed = slab_bytes + xs_bytes + misc + 2048;
@@ -81,8 +85,9 @@ struct UmmaLayout {
     static constexpr int up_stages_wanted = chunked ? ((NB >= 32 || CH >= 8) ? 3 : 6) : (NB > 4 ? 3 : 6);
     static constexpr int by_smem = (227 * 1024 - fixed) / (kUWStage + up_stage);          // equal depths
     static constexpr int by_smem_w = (227 * 1024 - fixed - up_stages_wanted * up_stage) / kUWStage;
-    static constexpr int stages = (NB > 4 || chunked) ? (by_smem_w < 6 ? by_smem_w : 6) : (by_smem < 6 ? by_smem : 6);
-    static constexpr int up_stages = (NB > 4 || chunked) ? up_stages_wanted : stages;
+    // (three pieces at 32 stacked ranks: the 24 KB slab would cost a W stage at equal depths; four UP stages keep five W stages)
+    static constexpr int stages = PC == 3 ? 5 : (NB > 4 || chunked) ? (by_smem_w < 6 ? by_smem_w : 6) : (by_smem < 6 ? by_smem : 6);
+    static constexpr int up_stages = PC == 3 ? 4 : (NB > 4 || chunked) ? up_stages_wanted : stages;
     static constexpr int off_w = 0;
     static constexpr int off_up = off_w + stages * kUWStage;
     static constexpr int off_slab = off_up + up_stages * up_stage;     // 1024-aligned (multiples of 2 KB)
@@ -222,7 +227,7 @@ __device__ __forceinline__ void umma_slab_prefetch(uint4 (&regs)[NB * 8 * (kUN /
             : "l"(ok ? src : base), "r"((int)ok));
     }
 }
-template <int NB>
+template <int NB, int PC>
 __device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const uint4 (&regs)[NB * 8 * (kUN / 8) / kUEpi], const Plan& plan, int S,
                                                  int rank, int tid) {
     constexpr int chunks = kUN / 8;
@@ -230,27 +235,32 @@ __device__ __forceinline__ void umma_slab_commit(unsigned char* slab, const uint
     for (int j = 0; j < NB * 8 * chunks / kUEpi; ++j) {
         const int i = tid + j * kUEpi;
         const int q = i / chunks, c = (i % chunks) * 8;
-        uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi;
+        uint4 hi = make_uint4(0u, 0u, 0u, 0u), lo = hi, lo2 = hi;
         if (q < S) {
             int wb, wr;
             rank_divmod(q, rank, wb, wr);
             const float w = plan.weight[wb];
             const uint32_t in[4] = {regs[j].x, regs[j].y, regs[j].z, regs[j].w};
-            uint32_t oh[4], ol[4];
+            uint32_t oh[4], ol[4], ol2[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const float f0 = __fmul_rn(w, bf16lo_to_f32(in[e]));
+                const float f0 = __fmul_rn(w, bf16lo_to_f32(in[e]));       // one rounding, as the reference folds the gate (adapters.py:202)
                 const float f1 = __fmul_rn(w, bf16hi_to_f32(in[e]));
                 const uint32_t h = pack_bf16x2(f0, f1);
                 oh[e] = h;
-                ol[e] = pack_bf16x2(f0 - bf16lo_to_f32(h), f1 - bf16hi_to_f32(h));
+                const float r0 = f0 - bf16lo_to_f32(h), r1 = f1 - bf16hi_to_f32(h);   // exact in f32
+                const uint32_t m = pack_bf16x2(r0, r1);
+                ol[e] = m;
+                if constexpr (PC == 3) ol2[e] = pack_bf16x2(r0 - bf16lo_to_f32(m), r1 - bf16hi_to_f32(m));   // exact: 24 bits = 8 + 8 + 8
             }
             hi = make_uint4(oh[0], oh[1], oh[2], oh[3]);
             lo = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+            if constexpr (PC == 3) lo2 = make_uint4(ol2[0], ol2[1], ol2[2], ol2[3]);
         }
         const int off = (q >> 3) * kUSlabBlock + (c >> 3) * 128 + (q & 7) * 16;
         *reinterpret_cast<uint4*>(slab + off) = hi;
         *reinterpret_cast<uint4*>(slab + NB * kUSlabBlock + off) = lo;
+        if constexpr (PC == 3) *reinterpret_cast<uint4*>(slab + 2 * NB * kUSlabBlock + off) = lo2;
     }
 }
 
@@ -305,9 +315,9 @@ __device__ __forceinline__ void umma_slab_direct(unsigned char* slab, const SegD
     }
 }
 
-template <int NB, bool GEMV, int CH = NB>
+template <int NB, bool GEMV, int CH = NB, int PC = 2>
 __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_constant__ MmaParams mp) {
-    using L = UmmaLayout<NB, GEMV, CH>;
+    using L = UmmaLayout<NB, GEMV, CH, PC>;
     constexpr bool kPrefetchSlab = NB <= 8;   // the next unit's DOWN rows wait in registers (umma_slab_prefetch)
     constexpr int kSt = L::stages, kUpSt = L::up_stages;
     extern __shared__ unsigned char smem_dyn[];
@@ -535,7 +545,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                         tc_fence_after();
                         const uint32_t a16 = (up_base + stage * L::up_stage) >> 4;
                         const int ks0 = c * kStepsPerChunk;
-                        const int n_half = (mp.dbg & 32) ? 1 : 2;   // (dbg 32: timing experiment without the lo half)
+                        const int n_half = (mp.dbg & 32) ? 1 : PC;  // (dbg 32: timing experiment without the lo pieces)
                         for (int half = 0; half < n_half; ++half) {
                             const uint32_t b16 = slab16 + (uint32_t)((half * NB + ks0 * 2) * (kUSlabBlock >> 4));
 #pragma unroll
@@ -735,7 +745,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                 published = ti.un.phase;
                             }
                         }
-                        if constexpr (kPrefetchSlab) umma_slab_commit<NB>(slab, dn_regs, plan, S, rank, tid);
+                        if constexpr (kPrefetchSlab) umma_slab_commit<NB, PC>(slab, dn_regs, plan, S, rank, tid);
                         else if (!(mp.dbg & 128) || it == 0) umma_slab_direct<NB>(slab, seg_of(ti.un), plan, S, ti.un.col0, tid);   // (dbg 128: timing experiment)
                         fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
                         __syncwarp();
