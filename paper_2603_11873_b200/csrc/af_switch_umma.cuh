@@ -129,6 +129,20 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t
         "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// The same, for a converged warp: every lane executes it, elect.sync picks the one that issues.
+__device__ __forceinline__ void umma_bf16_elect(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|q, 0xffffffff;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\telect.sync _|q, 0xffffffff;\n\t"
+        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -335,7 +349,8 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
     Plan& plan = *reinterpret_cast<Plan*>(sm + L::off_plan);
     UnitDev* unit_cache = reinterpret_cast<UnitDev*>(sm + L::off_units);
     SegDev* seg_cache = reinterpret_cast<SegDev*>(sm + L::off_segs);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // (the warp index through a shuffle: the compiler then knows the role branches are warp-uniform)
+    const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
 
     unsigned long long* const tl = GEMV ? mp.timeline : nullptr;   // probe: a few stamps per phase, none per tile
     if (tid == 0) tl_stamp(tl, 0);
@@ -384,8 +399,10 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const int n_blocks = plan.n_blocks;
+    // (block-wide values read from shared memory, broadcast with a shuffle: the compiler cannot see that a load is
+    //  warp-uniform, and only code under provably uniform branches gets the uniform datapath -- see the MMA issuer)
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const int n_blocks = __shfl_sync(0xffffffffu, plan.n_blocks, 0);
     const bool store_w = n_blocks > 0 || p.from_pristine;
     const bool bail = n_blocks < 0 || (!GEMV && !store_w);
     const uint32_t w_base = smem_u32(sm + L::off_w), up_base = smem_u32(sm + L::off_up), slab_base = smem_u32(sm + L::off_slab);
@@ -506,19 +523,41 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 }
             }
         } else if (warp == kUEpiWarps + 2) {
-            // ============ MMA issuer: D[buf] = U . hi + U . lo, one thread ============
-            if (lane == 0) {
+            // ============ MMA issuer: D[buf] = U . hi + U . lo ============
+            // The WHOLE warp runs this loop and elect.sync picks the lane that issues (umma_bf16_elect): with the warp
+            // provably converged and every descriptor input warp-uniform (loop counters, shared-memory bases, values
+            // broadcast with a shuffle), the compiler keeps the descriptors in uniform registers and an MMA costs the
+            // issuing warp UIADD3 + UTCHMMA.  Under `if (lane == 0)` the same code compiled to an election loop with
+            // five R2UR per MMA: 135 cycles of issue against the tensor core's 65 for M128 N128 K16
+            // (scripts/micro/umma_rate.cu) -- the MMA stream, not HBM, was what bounded launches of 64+ stacked ranks.
+            {
                 // D f32, A / B bf16, A K-major, B MN-major, N = 128, M = 128
                 constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(kUN >> 3) << 17) | ((uint32_t)(kUM >> 4) << 24);
-                UmmaIter ti;
-                ti.init(p, unit_cache);
-                const int rank = ti.valid(p) ? seg_of(ti.un).rank : 8;   // one rank for the whole table (eligibility)
-                const int ksteps = (n_blocks * rank + 15) >> 4;          // rank-16 steps over the stacked ranks
+                // The walk over this CTA's units (UmmaIter's order) with every branch condition warp-uniform: per unit
+                // only its number of row tiles is needed, read by all lanes and broadcast.
+                auto unit_tiles = [&](int jj, int uu) -> int {
+                    int nt = 0;
+                    if (uu < p.n_units) {
+                        const int rows = jj < kUnitCache ? unit_cache[jj].rows : p.units[uu].rows;
+                        nt = rows > 0 ? (rows + kUM - 1) / kUM : 0;
+                    }
+                    return __shfl_sync(0xffffffffu, nt, 0);
+                };
+                int unit_j = 0, unit_u = blockIdx.x;
+                int nt = unit_tiles(unit_j, unit_u);
+                int rank = 8;                                            // one rank for the whole table (eligibility)
+                if (nt > 0) {
+                    const UnitDev un0 = unit_cache[0];
+                    rank = seg_of(un0).rank;
+                }
+                rank = __shfl_sync(0xffffffffu, rank, 0);
+                const int nb_u = n_blocks;
+                const uint32_t tmem_u = tmem;
+                const int ksteps = (nb_u * rank + 15) >> 4;              // rank-16 steps over the stacked ranks
                 const int per_chunk = (CH * 8) / rank;
-                const int n_ch = n_blocks > 0 ? (n_blocks + per_chunk - 1) / per_chunk : 1;
-                // ONE thread issues every MMA of the CTA, so what it executes per MMA is on the tile's critical path:
+                const int n_ch = nb_u > 0 ? (nb_u + per_chunk - 1) / per_chunk : 1;
                 // the descriptors are a per-table prototype plus a precomputed 16-byte-unit offset per rank-16 step
-                // (computing them from scratch -- divisions by the run-time rank -- cost ~2x the MMA itself).
+                // (computing them from scratch -- divisions by the run-time rank -- cost ~2x the MMA itself)
                 constexpr int kStepsPerChunk = CH / 2;
                 uint32_t a_inc[kStepsPerChunk];
 #pragma unroll
@@ -527,42 +566,43 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 const uint64_t a_proto = umma_a_desc(0u, rank, 0);                           // layout / LBO / SBO of the table's rank
                 const uint64_t b_proto = umma_desc(0u, kUSlabBlock, 128);
                 const uint32_t slab16 = slab_base >> 4;
-                int unit_j = -1, uit = 0;
-                for (int it = 0; ti.valid(p); ++it) {
-                    const int buf = it & 1;
-                    const uint32_t aph = (it >> 1) & 1;
-                    if (ti.j != unit_j) {   // the unit's slab has been written (and made visible to the tensor core)
-                        unit_j = ti.j;
-                        mbar_wait(slab_bar, (uint32_t)unit_j & 1);
-                    }
-                    mbar_wait(&acc_empty[buf], aph ^ 1);
-                    const uint32_t d_tmem = tmem + buf * kUN;
-                    uint32_t accumulate = 0;
-                    for (int c = 0; c < n_ch; ++c, ++uit) {
-                        const int stage = uit % kUpSt;
-                        const uint32_t ph = (uit / kUpSt) & 1;
-                        mbar_wait(&up_full[stage], ph);
-                        tc_fence_after();
-                        const uint32_t a16 = (up_base + stage * L::up_stage) >> 4;
-                        const int ks0 = c * kStepsPerChunk;
-                        const int n_half = (mp.dbg & 32) ? 1 : PC;  // (dbg 32: timing experiment without the lo pieces)
-                        for (int half = 0; half < n_half; ++half) {
-                            const uint32_t b16 = slab16 + (uint32_t)((half * NB + ks0 * 2) * (kUSlabBlock >> 4));
+                const int n_half = (mp.dbg & 32) ? 1 : PC;   // (dbg 32: timing experiment without the lo pieces)
+                int it = 0, uit = 0;
+                while (nt > 0) {
+                    mbar_wait(slab_bar, (uint32_t)unit_j & 1);   // the unit's slab has been written (and made visible to the tensor core)
+                    for (int t = 0; t < nt; ++t, ++it) {
+                        const int buf = it & 1;
+                        const uint32_t aph = (it >> 1) & 1;
+                        mbar_wait(&acc_empty[buf], aph ^ 1);
+                        const uint32_t d_tmem = tmem_u + buf * kUN;
+                        uint32_t accumulate = 0;
+                        for (int c = 0; c < n_ch; ++c, ++uit) {
+                            const int stage = uit % kUpSt;
+                            const uint32_t ph = (uit / kUpSt) & 1;
+                            mbar_wait(&up_full[stage], ph);
+                            tc_fence_after();
+                            const uint32_t a16 = (up_base + stage * L::up_stage) >> 4;
+                            const int ks0 = c * kStepsPerChunk;
+                            for (int half = 0; half < n_half; ++half) {
+                                const uint32_t b16 = slab16 + (uint32_t)((half * NB + ks0 * 2) * (kUSlabBlock >> 4));
 #pragma unroll
-                            for (int k2 = 0; k2 < kStepsPerChunk; ++k2) {
-                                if (ks0 + k2 < ksteps) {
-                                    umma_bf16(d_tmem, a_proto + (a16 + a_inc[k2]), b_proto + (b16 + (uint32_t)(k2 * 2 * (kUSlabBlock >> 4))), idesc,
-                                              accumulate);
-                                    accumulate = 1;
+                                for (int k2 = 0; k2 < kStepsPerChunk; ++k2) {
+                                    if (ks0 + k2 < ksteps) {
+                                        umma_bf16_elect(d_tmem, a_proto + (a16 + a_inc[k2]), b_proto + (b16 + (uint32_t)(k2 * 2 * (kUSlabBlock >> 4))),
+                                                        idesc, accumulate);
+                                        accumulate = 1;
+                                    }
                                 }
                             }
+                            if (ksteps == 0)   // nothing selected (plain GEMV): D = 0 through a K = 16 product with the zeroed slot
+                                umma_bf16_elect(d_tmem, a_proto + a16, b_proto + slab16, idesc, 0);
+                            umma_commit_elect(smem_u32(&up_empty[stage]));   // the UP stage is free once these MMAs have read it
                         }
-                        if (ksteps == 0)   // nothing selected (plain GEMV): D = 0 through a K = 16 product with the zeroed slot
-                            umma_bf16(d_tmem, a_proto + a16, b_proto + slab16, idesc, 0);
-                        umma_commit(smem_u32(&up_empty[stage]));   // the UP stage is free once these MMAs have read it
+                        umma_commit_elect(smem_u32(&acc_full[buf]));          // every MMA of the tile has completed: the epilogue may read D
                     }
-                    umma_commit(smem_u32(&acc_full[buf]));          // every MMA of the tile has completed: the epilogue may read D
-                    ti.next(p);
+                    unit_u += gridDim.x;
+                    ++unit_j;
+                    nt = unit_tiles(unit_j, unit_u);
                 }
             }
         } else if (warp == kUEpiWarps + 3) {

@@ -16,13 +16,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint3
     d |= (uint64_t)(layout & 7) << 61;
     return d;
 }
-struct Cfg { uint32_t a_lbo, a_sbo, a_layout, a_step, b_lbo, b_sbo, b_layout, b_step, b_mn_major, commit_every; };
+struct Cfg { uint32_t a_lbo, a_sbo, a_layout, a_step, b_lbo, b_sbo, b_layout, b_step, b_mn_major, commit_every, n = 128, a_in_tmem = 0, alt_d = 0; };
 
 __global__ void __launch_bounds__(288) rate(Cfg c, int nm, long long* out, int busy_smem) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint32_t tmem_base_s;
     __shared__ uint64_t bar;
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
     for (int i = tid * 16; i < 200 * 1024; i += blockDim.x * 16) *reinterpret_cast<uint4*>(sm + i) = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
@@ -30,36 +30,54 @@ __global__ void __launch_bounds__(288) rate(Cfg c, int nm, long long* out, int b
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)), "n"(256));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)), "n"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = tmem_base_s;
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((c.b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_base_s, 0);
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((c.b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(c.n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t a_base = smem_u32(sm), b_base = smem_u32(sm) + 65536;
     uint32_t phase = 0;
-    if (tid == 0) {
+    if (warp == 0) {
         const long long t0 = clock64();
-        for (int i = 0; i < nm; ++i) {
-            const uint64_t da = make_desc(a_base + (i & 7) * c.a_step, c.a_lbo, c.a_sbo, c.a_layout);
-            const uint64_t db = make_desc(b_base + (i & 7) * c.b_step, c.b_lbo, c.b_sbo, c.b_layout);
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                         "l"(da), "l"(db), "r"(idesc), "r"(i > 0 ? 1u : 0u));
-            if (c.commit_every && (i + 1) % c.commit_every == 0 && i + 1 < nm) {
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
-                if (c.commit_every >= 1000) {   // and wait for it (drain) -- not used
+        // descriptors of the eight operand positions precomputed: the loop body is nothing but the MMAs (the issuing thread's
+        // own instruction stream was the limit of the first version of this benchmark: 135 cycles per MMA whatever N)
+        uint64_t da[8], db[8];
+        uint32_t ta[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            da[j] = make_desc(a_base + j * c.a_step, c.a_lbo, c.a_sbo, c.a_layout);
+            db[j] = make_desc(b_base + j * c.b_step, c.b_lbo, c.b_sbo, c.b_layout);
+            ta[j] = tmem + 256 + j * 8;
+        }
+        const bool a_tm = c.a_in_tmem != 0;
+        const uint32_t tmem0 = tmem, alt = c.alt_d ? 128u : 0u;
+        const uint32_t every = c.commit_every;
+        for (int i = 0; i < nm; i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t accumulate = (i | (j >> 1)) ? 1u : 0u;
+                const uint32_t tmem = tmem0 + ((j & 1) ? alt : 0u);   // alt_d: consecutive MMAs go to two different accumulators
+                if (a_tm)   // A: 128 lanes x 8 columns (16 bf16 per row) of tensor memory, columns 256..
+                    asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|q, 0xffffffff;\n\t@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem),
+                                 "r"(ta[j]), "l"(db[j]), "r"(idesc), "r"(accumulate));
+                else
+                    asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|q, 0xffffffff;\n\t@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                                 "l"(da[j]), "l"(db[j]), "r"(idesc), "r"(accumulate));
+                if (every && (j + 1) % 4 == 0 && i + j + 1 < nm) {
+                    asm volatile("{\n\t.reg .pred q;\n\telect.sync _|q, 0xffffffff;\n\t@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar)) : "memory");
+                    asm volatile("{\n.reg .pred p;\nW1:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@p bra D1;\nbra W1;\nD1:\n}\n" ::"r"(smem_u32(&bar)), "r"(phase) : "memory");
+                    phase ^= 1;
                 }
-                asm volatile("{\n.reg .pred p;\nW1:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@p bra D1;\nbra W1;\nD1:\n}\n" ::"r"(smem_u32(&bar)), "r"(phase) : "memory");
-                phase ^= 1;
             }
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+        asm volatile("{\n\t.reg .pred q;\n\telect.sync _|q, 0xffffffff;\n\t@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar)) : "memory");
         asm volatile("{\n.reg .pred p;\nW2:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@p bra D2;\nbra W2;\nD2:\n}\n" ::"r"(smem_u32(&bar)), "r"(phase) : "memory");
         const long long t1 = clock64();
-        out[blockIdx.x] = t1 - t0;
-        *reinterpret_cast<volatile int*>(sm + 200 * 1024) = 1;
+        if (tid == 0) out[blockIdx.x] = t1 - t0;
+        if (tid == 0) *reinterpret_cast<volatile int*>(sm + 200 * 1024) = 1;
     } else if (busy_smem && warp >= 1) {
         // the other warps do what an epilogue does until thread 0 is done:
         //   bit 1: stream shared memory (16-byte loads + stores over a 64 KB region, conflict-free)
@@ -82,7 +100,7 @@ __global__ void __launch_bounds__(288) rate(Cfg c, int nm, long long* out, int b
 #pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
                     uint32_t r[32];
-                    const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + 128 + c4 * 32;
+                    const uint32_t addr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 384 + c4 * 32;
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
@@ -100,7 +118,7 @@ __global__ void __launch_bounds__(288) rate(Cfg c, int nm, long long* out, int b
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
 int main() {
@@ -117,10 +135,18 @@ int main() {
         {"A K-major 128B swizzle       | B MN-major 128B swizzle       ", {16, 1024, 2, 32, 8192, 1024, 2, 2048, 1, 0}},
         {"A K-major 128B swizzle       | B K-major 128B swizzle (GEMM) ", {16, 1024, 2, 32, 16, 1024, 2, 32, 0, 0}},
         {"current, commit + wait every 4 MMAs                          ", {2048, 128, 0, 4096, 2048, 128, 0, 4096, 1, 4}},
+        {"N=256: A K-major none | B MN-major none                      ", {2048, 128, 0, 4096, 4096, 128, 0, 8192, 1, 0, 256, 0}},
+        {"N=64:  A K-major none | B MN-major none                      ", {2048, 128, 0, 4096, 1024, 128, 0, 2048, 1, 0, 64, 0}},
+        {"A in TMEM | B MN-major none (current slab)  N=128            ", {2048, 128, 0, 4096, 2048, 128, 0, 4096, 1, 0, 128, 1}},
+        {"two accumulators alternating: SS N=128                       ", {2048, 128, 0, 4096, 2048, 128, 0, 4096, 1, 0, 128, 0, 1}},
+        {"two accumulators alternating: A in TMEM N=128                ", {2048, 128, 0, 4096, 2048, 128, 0, 4096, 1, 0, 128, 1, 1}},
+        {"two accumulators alternating: SS N=64                        ", {2048, 128, 0, 4096, 1024, 128, 0, 2048, 1, 0, 64, 0, 1}},
+        {"A in TMEM | B MN-major none                 N=256            ", {2048, 128, 0, 4096, 4096, 128, 0, 8192, 1, 0, 256, 1}},
+        {"A in TMEM | B K-major 128B swizzle          N=128            ", {16, 1024, 2, 32, 16, 1024, 2, 32, 0, 0, 128, 1}},
     };
-    for (int busy = 0; busy < 4; ++busy)
+    for (int busy = 0; busy < 1; busy += 3)
         for (auto& n : v) {
-            for (int grid : {148}) {
+            for (int grid : {1, 148}) {
                 cudaMemset(out, 0, 2048 * sizeof(long long));
                 rate<<<grid, 288, 220 * 1024>>>(n.c, 512, out, busy);
                 cudaError_t e = cudaDeviceSynchronize();
