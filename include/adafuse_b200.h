@@ -370,7 +370,8 @@ int af_chain_create(af_table* table, const int32_t* seg_ids, const int32_t* phas
 int af_chain_create_weighted(af_table* table, const int32_t* seg_ids, const int32_t* phase_len, int32_t n_phases,
                              const float* cta_share, int32_t n_cta, af_group** out);
 int af_group_destroy(af_group* group);
-/* x_len / y_rows: arrays of n_phases entries (4 is always enough). */
+/* x_len / y_rows: arrays of n_phases entries (4 is always enough).  grid: CTAs of a launch over the group (the
+ * tcgen05 schedule's when the table is on that path; what a peer counter is compared against, times n_peers). */
 int af_group_info(const af_group* group, int32_t* n_phases, int32_t* x_len, int32_t* y_rows, int32_t* n_units,
                   int32_t* grid, int64_t* tiles);
 /* flags of af_switch_gemv_chain (af_switch_gemv takes AF_CHAIN_PDL as its `pdl` argument) */
@@ -380,6 +381,27 @@ int af_group_info(const af_group* group, int32_t* n_phases, int32_t* x_len, int3
 int af_switch_gemv_chain(af_group* group, const af_decision* prev_dev, const af_decision* cur_dev,
                          int32_t max_k, float scale, int32_t mode, const af_gemv_phase* phases,
                          int32_t n_phases, int32_t* phase_done_dev, int32_t flags, void* stream);
+/* ---- tensor parallelism without a collective between the launches ----------------------------
+ * No reference counterpart (the reference is single-process; BASELINE configs[3..4] name TP 2 / 4 / 8).
+ * Every rank maps one buffer holding the fixed-point accumulators and phase counters of every other rank
+ * (NVLink peer memory: torch symmetric memory / CUDA IPC on the host side) at own address + peer_offset_bytes[w];
+ * the list includes the rank itself (offset 0) and has the same ORDER on every rank only by convention -- the
+ * kernels never use the index.  af_group_set_peers marks the row-parallel phases of a chain (bit ph of
+ * reduce_phase_mask: o and down): a marked phase adds its partial sums into EVERY rank's acc_out with system-scope
+ * integer atomics (exact in any order -- the all-reduce is part of the GEMV epilogue) and is reported on every
+ * rank's phase counter, so the next phase starts on the reduced vector once grid * n_peers CTAs have reported.
+ * Requirements: tcgen05 path; identical chain shapes (hence grids) on all ranks; acc_out of the marked phases and
+ * phase_done_dev inside the mapped buffer; phase_done_dev then holds n_phases counters when the LAST phase is
+ * marked (its consumer is a later launch: af_peer_wait on counter n_phases - 1 for grid * n_peers).
+ * n_peers == 0 clears the setting.  Errors: AF_EVALUE, AF_EDIM (alignment), AF_EALIAS, AF_ESTATE (not tcgen05). */
+int af_group_set_peers(af_group* group, int32_t n_peers, const int64_t* peer_offset_bytes, int32_t reduce_phase_mask);
+/* Once per token, after this rank has zeroed its accumulators / counters and before any rank may push into them:
+ * bumps counter_dev on every rank (a monotonic count, never reset) and waits until all n_peers ranks have bumped
+ * this rank's; *epoch_dev (device-resident, zero-initialised, private to the rank) counts the barriers so far. */
+int af_peer_barrier(int32_t* counter_dev, int32_t* epoch_dev, int32_t n_peers, const int64_t* peer_offset_bytes,
+                    int32_t* err_flag_dev, void* stream);
+/* Stream-ordered wait until *counter_dev >= target (system-scope acquire); ~2 s -> AF_ECUDA in *err_flag_dev. */
+int af_peer_wait(const int32_t* counter_dev, int32_t target, int32_t* err_flag_dev, void* stream);
 /* adapters.py:188-233 (`concat_gated` + `build_switch` bookkeeping) once per token: turns the two
  * device decisions into the table's block list (experts present on both sides collapse to one block
  * of weight g_new - g_old).  The launches of the token that pass AF_CHAIN_PLAN_PREBUILT read it

@@ -178,6 +178,9 @@ SIGNATURES = {
     "af_plan_build": (ctypes.c_int, [_vp, _vp, _vp, _i32, _f32, _i32, _vp]),
     "af_set_timeline": (ctypes.c_int, [_vp, _i32, _i64]),
     "af_accum_to_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp]),
+    "af_group_set_peers": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_int64), _i32]),
+    "af_peer_barrier": (ctypes.c_int, [_vp, _vp, _i32, ctypes.POINTER(ctypes.c_int64), _vp, _vp]),
+    "af_peer_wait": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
     "af_attn_decode_fix": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 AF_FIX_SHIFT = 40

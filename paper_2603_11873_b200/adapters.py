@@ -573,14 +573,33 @@ class SegmentGroup:
                 raise TypeError("the fused switch + GEMV takes device-resident decisions (DeviceDecision) or None")
         if len(phases) != self.n_phases:
             raise DimensionError(f"chain has {self.n_phases} phases, got {len(phases)} descriptions")
-        if self.n_phases > 1:
-            if phase_done is None or phase_done.dtype != torch.int32 or not phase_done.is_cuda or phase_done.numel() < self.n_phases - 1:
-                raise DimensionError("phase_done must be a CUDA int32 tensor of n_phases - 1 zeroed counters")
+        n_counters = self.n_phases - 1 + ((getattr(self, "reduce_mask", 0) >> (self.n_phases - 1)) & 1)
+        if n_counters > 0:
+            if phase_done is None or phase_done.dtype != torch.int32 or not phase_done.is_cuda or phase_done.numel() < n_counters:
+                raise DimensionError(f"phase_done must be a CUDA int32 tensor of {n_counters} zeroed counters")
         structs = (_capi.GemvPhase * self.n_phases)(*[self._phase_struct(i, **ph) for i, ph in enumerate(phases)])
         _capi.check(_capi.lib().af_switch_gemv_chain(
             self.handle, prev.ptr if prev is not None else None, cur.ptr if cur is not None else None, int(max_k), float(scale),
             _MODES[mode], structs, self.n_phases, _ptr(phase_done) if phase_done is not None else None,
             (_capi.AF_CHAIN_PDL if pdl else 0) | (_capi.AF_CHAIN_PLAN_PREBUILT if plan_prebuilt else 0), _capi.stream_ptr()))
+
+    def set_peers(self, peer_offsets, reduce_phases) -> None:
+        """Tensor parallelism without a collective between the launches (`af_group_set_peers`; no reference
+        counterpart).  `peer_offsets`: byte offsets from this rank's accumulator buffer to every rank's mapping of
+        it, this rank included as 0; `reduce_phases`: the row-parallel phases of the chain (o, down) -- their partial
+        sums go into EVERY rank's accumulators and the phase is reported on every rank's counter, so the next phase
+        starts on the all-reduced vector.  An empty offset list clears the setting."""
+        import ctypes
+
+        offs = [int(o) for o in peer_offsets]
+        mask = 0
+        for ph in reduce_phases:
+            if not 0 <= int(ph) < self.n_phases:
+                raise ValueError(f"chain has no phase {ph}")
+            mask |= 1 << int(ph)
+        arr = (ctypes.c_int64 * max(1, len(offs)))(*offs)
+        _capi.check(_capi.lib().af_group_set_peers(self.handle, len(offs), arr, mask))
+        self.n_peers, self.reduce_mask = len(offs), mask
 
     def switch_gemv(self, prev, cur, acc_out, *, max_k: int = _capi.AF_MAX_K, scale: float = 1.0, mode: str = "inplace",
                     pdl: bool = False, plan_prebuilt: bool = False, **phase) -> None:
@@ -598,3 +617,20 @@ class SegmentGroup:
             self.close()
         except Exception:
             pass
+
+
+def peer_barrier(counter: torch.Tensor, epoch: torch.Tensor, peer_offsets, err_flag: torch.Tensor | None = None) -> None:
+    """`af_peer_barrier`: once per token, after this rank zeroed its accumulators and before any rank may push into
+    them.  `counter` (int32[1], inside the buffer the peers map) is bumped on every rank and never reset; `epoch`
+    (int32[1], private, zero-initialised) counts this rank's barriers on the device, so a captured graph replays."""
+    import ctypes
+
+    offs = [int(o) for o in peer_offsets]
+    arr = (ctypes.c_int64 * len(offs))(*offs)
+    _capi.check(_capi.lib().af_peer_barrier(_ptr(counter), _ptr(epoch), len(offs), arr, _ptr(err_flag) if err_flag is not None else None,
+                                            _capi.stream_ptr()))
+
+
+def peer_wait(counter: torch.Tensor, target: int, err_flag: torch.Tensor | None = None) -> None:
+    """`af_peer_wait`: the stream waits until the counter the peers bump has reached `target`."""
+    _capi.check(_capi.lib().af_peer_wait(_ptr(counter), int(target), _ptr(err_flag) if err_flag is not None else None, _capi.stream_ptr()))

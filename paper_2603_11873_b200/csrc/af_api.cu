@@ -12,6 +12,7 @@
 #include "af_forward.cuh"
 #include "af_gemv_chain.cuh"
 #include "af_llama.cuh"
+#include "af_peer.cuh"
 #include "af_switch_mma.cuh"
 #include "af_switch_umma.cuh"
 
@@ -172,6 +173,9 @@ struct af_group {
     int n_phases = 1;
     int x_len[kMaxPhases] = {0, 0, 0, 0}, y_rows[kMaxPhases] = {0, 0, 0, 0};
     long long tiles = 0;
+    // tensor-parallel peers (af_group_set_peers): 0 = none
+    int n_peers = 0, reduce_mask = 0;
+    long long peer_off[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 extern "C" {
@@ -979,7 +983,7 @@ int af_group_info(const af_group* g, int32_t* n_phases, int32_t* x_len, int32_t*
         if (y_rows) y_rows[ph] = g->y_rows[ph];
     }
     if (n_units) *n_units = g->n_units;
-    if (grid) *grid = g->grid;
+    if (grid) *grid = g->d_units_umma ? g->grid_umma : g->grid;   // the launch size: tcgen05 schedule when the table has one
     if (tiles) *tiles = g->tiles;
     return AF_OK;
 }
@@ -1098,12 +1102,17 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
     for (int ph = 0; ph < n_phases; ++ph)
         if ((phases[ph].prologue == AF_PRO_RMSNORM_DEFERRED || phases[ph].inv_in) && !umma_launch)
             return fail(AF_ESTATE, "deferred RMSNorm scales are implemented by the tcgen05 kernel only (table info: umma_path)");
+    if (g->n_peers > 0 && !umma_launch)
+        return fail(AF_ESTATE, "peer accumulation (af_group_set_peers) is implemented by the tcgen05 kernel only (table info: umma_path)");
     if (umma_launch) {
         p.units = g->d_units_umma;
         p.n_units = g->n_units_umma;
         mp.tmaps_ld = t->d_maps + (size_t)(from_pristine ? 6 : 5) * S;
         mp.tmaps_st = t->d_maps + (size_t)5 * S;
         mp.tmaps_up = t->d_maps + (size_t)7 * S;
+        mp.n_peers = g->n_peers;
+        mp.reduce_mask = g->reduce_mask;
+        for (int w = 0; w < g->n_peers; ++w) mp.peer_off[w] = g->peer_off[w];
         return dispatch_umma<true>(t, s_bound, mp, g->grid_umma, st);
     }
     if (mp.timeline && ks == 2) return launch_mma<2, false, true, true>(mp, g->grid, st);
@@ -1113,6 +1122,58 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         case 3: return ba ? launch_mma<3, true, true>(mp, g->grid, st) : launch_mma<3, false, true>(mp, g->grid, st);
         default: return ba ? launch_mma<4, true, true>(mp, g->grid, st) : launch_mma<4, false, true>(mp, g->grid, st);
     }
+}
+
+int af_group_set_peers(af_group* g, int32_t n_peers, const int64_t* peer_offset_bytes, int32_t reduce_phase_mask) {
+    if (!g) return fail(AF_EVALUE, "group is NULL");
+    if (n_peers == 0) {   // back to a single rank
+        g->n_peers = 0;
+        g->reduce_mask = 0;
+        return AF_OK;
+    }
+    if (n_peers < 1 || n_peers > 8) return fail(AF_EVALUE, "1 .. 8 peers (this rank included)");
+    if (!peer_offset_bytes) return fail(AF_EVALUE, "peer offsets are NULL");
+    if (!g->d_units_umma) return fail(AF_ESTATE, "peer accumulation needs the tcgen05 path (table info: umma_path)");
+    if (reduce_phase_mask < 0 || reduce_phase_mask >= (1 << g->n_phases)) return fail(AF_EVALUE, "reduce mask names a phase the chain does not have");
+    int zeros = 0;
+    for (int w = 0; w < n_peers; ++w) {
+        if (peer_offset_bytes[w] % 8 != 0) return fail(AF_EDIM, "peer offsets must keep the 8-byte alignment of the accumulators");
+        zeros += peer_offset_bytes[w] == 0;
+        for (int v = 0; v < w; ++v)
+            if (peer_offset_bytes[v] == peer_offset_bytes[w]) return fail(AF_EALIAS, "two peers at the same address");
+    }
+    if (zeros != 1) return fail(AF_EVALUE, "the list must contain this rank itself (offset 0) exactly once");
+    g->n_peers = n_peers;
+    g->reduce_mask = reduce_phase_mask;
+    for (int w = 0; w < n_peers; ++w) g->peer_off[w] = peer_offset_bytes[w];
+    return AF_OK;
+}
+
+static int peer_list(int32_t n_peers, const int64_t* peer_offset_bytes, PeerList& pl) {
+    if (n_peers < 1 || n_peers > 8 || !peer_offset_bytes) return fail(AF_EVALUE, "1 .. 8 peers (this rank included)");
+    pl.n = n_peers;
+    for (int w = 0; w < n_peers; ++w) {
+        if (peer_offset_bytes[w] % 4 != 0) return fail(AF_EDIM, "peer offsets must keep the counters aligned");
+        pl.off[w] = peer_offset_bytes[w];
+    }
+    return AF_OK;
+}
+
+int af_peer_barrier(int32_t* counter_dev, int32_t* epoch_dev, int32_t n_peers, const int64_t* peer_offset_bytes,
+                    int32_t* err_flag_dev, void* stream) {
+    if (!counter_dev || !epoch_dev) return fail(AF_EVALUE, "counter / epoch is NULL");
+    PeerList pl{};
+    if (int rc = peer_list(n_peers, peer_offset_bytes, pl)) return rc;
+    peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(counter_dev, epoch_dev, pl, err_flag_dev);
+    AF_LAUNCH_CHECK("peer_barrier_kernel");
+    return AF_OK;
+}
+
+int af_peer_wait(const int32_t* counter_dev, int32_t target, int32_t* err_flag_dev, void* stream) {
+    if (!counter_dev) return fail(AF_EVALUE, "counter is NULL");
+    peer_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(counter_dev, target, err_flag_dev);
+    AF_LAUNCH_CHECK("peer_wait_kernel");
+    return AF_OK;
 }
 
 int af_switch_gemv(af_group* g, const af_decision* prev_dev, const af_decision* cur_dev, int32_t max_k, float scale,

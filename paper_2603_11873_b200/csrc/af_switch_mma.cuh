@@ -229,6 +229,14 @@ struct MmaParams {
     int up_swizzle_ok;             // 0: always plain bulk copies for UP (A/B switch, env AF_UP_SWIZZLE=0)
     int n_stages;                  // ring depth actually used (<= MmaLayout<KS>::stages)
     int store_depth;               // tile stores that may still be reading shared memory (0..3)
+    // Tensor parallelism without a collective between the launches (af_group_set_peers, tcgen05 kernel): the
+    // fixed-point accumulators and the phase counters live in a buffer every rank maps at
+    // (own address + peer_off[w]).  A phase in reduce_mask (row-parallel: o, down) adds its partial sums into EVERY
+    // rank's accumulators and is published on every rank's counter, so the next phase starts on the all-reduced
+    // vector when gridDim.x * n_peers CTAs have reported -- integer adds, so the sum is exact in any order.
+    int n_peers;                   // 0 = single rank (no peer traffic); peer_off[] includes this rank (offset 0)
+    int reduce_mask;               // bit ph: phase ph pushes to the peers
+    long long peer_off[8];
 };
 
 // Gated DOWN slab for one unit: rows [0, S) hold hi(g*a), rows [s_pad, s_pad+S) hold lo; the

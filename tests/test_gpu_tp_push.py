@@ -1,0 +1,261 @@
+"""Tensor parallelism without a collective between the launches (include/adafuse_b200.h `af_group_set_peers`,
+`af_peer_barrier`, `af_peer_wait`; no reference counterpart -- the reference is single-process and BASELINE
+configs[3..4] only name TP 2 / 4 / 8).
+
+One B200 plays both ranks: two shard tables, two streams, two chained launches of 40 CTAs each that are resident
+TOGETHER and push the partial sums of their row-parallel phases (o, down) into each other's accumulators -- the
+same system-scope atomics and cross-rank phase counters that run over NVLink peer mappings between GPUs; here the
+"peer mapping" is a second region of one allocation.
+
+The sums are integers (fixed point, 2^-40), the 128-column strips of a row are the same whether the row lives on
+one rank or is split over two, and a merged tile depends on its own rows / columns of the factors only: so the
+two-rank result must be BIT-IDENTICAL to the single-rank chain on the unsharded matrices -- accumulators, residual
+streams and merged weights."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+D, F, N_EXP, RANK = 512, 1280, 6, 8      # a shard's largest phase is 40 tiles: two launches of 40 CTAs are resident together
+
+
+@pytest.fixture(scope="module")
+def af():
+    import paper_2603_11873_b200 as af
+
+    return af
+
+
+def _decision(ids, weights):
+    from paper_2603_11873_b200.routing import DeviceDecision, GateDecision
+
+    return DeviceDecision.from_host(GateDecision(tuple(ids), tuple(weights)), torch.device("cuda"))
+
+
+def _full_model(seed=11):
+    """Unsharded matrices and factors of one block: o | gate up | down | q k v (all `d_out x d_in`)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+
+    def u(shape, fan):
+        return (torch.empty(shape, device="cuda").uniform_(-1, 1, generator=g) * fan ** -0.5).to(torch.bfloat16)
+
+    shapes = [(D, D), (F, D), (F, D), (D, F), (D, D), (D, D), (D, D)]
+    w = [u((o, i), i) for o, i in shapes]
+    down = [u((N_EXP, RANK, i), i) for o, i in shapes]      # A: rank x d_in
+    up = [u((N_EXP, o, RANK), RANK) for o, i in shapes]      # B: d_out x rank
+    return shapes, w, down, up
+
+
+def _shard(w, down, up, rank, tp):
+    """Row-parallel (split d_in: o, down) and column-parallel (split d_out: gate, up, q, k, v) shards of rank `rank`."""
+    row_parallel = [True, False, False, True, False, False, False]
+    ws, dns, ups = [], [], []
+    for i, rp in enumerate(row_parallel):
+        if rp:
+            n = w[i].shape[1] // tp
+            sl = slice(rank * n, (rank + 1) * n)
+            ws.append(w[i][:, sl].contiguous())
+            dns.append(down[i][:, :, sl].contiguous())
+            ups.append(up[i].clone())
+        else:
+            n = w[i].shape[0] // tp
+            sl = slice(rank * n, (rank + 1) * n)
+            ws.append(w[i][sl].contiguous())
+            dns.append(down[i].clone())
+            ups.append(up[i][:, sl].contiguous())
+    return ws, dns, ups
+
+
+def _table(ws, dns, ups):
+    from paper_2603_11873_b200.adapters import SwitchTable
+    from paper_2603_11873_b200.linalg import Matrix
+
+    targets = [Matrix(t.clone(), "bf16") for t in ws]
+    return targets, SwitchTable(targets, [t.clone() for t in dns], [t.clone() for t in ups])
+
+
+PHASE_IDS = [[0], [1, 2], [3], [4, 5, 6]]
+
+
+def _inputs():
+    g = torch.Generator(device="cuda").manual_seed(2)
+    attn = torch.empty(D, device="cuda").uniform_(-1, 1, generator=g)
+    xa = torch.empty(D, device="cuda").uniform_(-1, 1, generator=g)
+    nw1 = 1.0 + 0.1 * torch.empty(D, device="cuda").uniform_(-1, 1, generator=g)
+    nw2 = 1.0 + 0.1 * torch.empty(D, device="cuda").uniform_(-1, 1, generator=g)
+    return attn, xa, nw1, nw2
+
+
+def _phases(acc, attn_in, xa, xb, xa2, nw1, nw2):
+    return [dict(acc_out=acc[0], xin=attn_in),
+            dict(acc_out=acc[1], acc_in=acc[0], res=xa, h_out=xb, prologue="rmsnorm", norm_w=nw1, eps=1e-5),
+            dict(acc_out=acc[2], acc_in=acc[1], prologue="silu_mul"),
+            dict(acc_out=acc[3], acc_in=acc[2], res=xb, h_out=xa2, prologue="rmsnorm", norm_w=nw2, eps=1e-5)]
+
+
+def test_two_ranks_on_one_gpu_equal_the_single_rank_chain(af):
+    from paper_2603_11873_b200.adapters import SegmentGroup
+
+    tp = 2
+    shapes, w, down, up = _full_model()
+    prev, cur = _decision((1, 4), (0.7, 0.3)), _decision((4, 2), (0.55, 0.45))
+    attn, xa, nw1, nw2 = _inputs()
+
+    # ---- single rank, unsharded ----
+    tg, tab = _table(w, down, up)
+    tab.switch(None, prev, max_k=2)
+    xb, xa2 = torch.zeros(D, device="cuda"), torch.zeros(D, device="cuda")
+    acc = [torch.zeros(n, dtype=torch.int64, device="cuda") for n in (D, 2 * F, D, 3 * D)]
+    done = torch.zeros(4, dtype=torch.int32, device="cuda")
+    grp = SegmentGroup(tab, PHASE_IDS)
+    grp.switch_gemv_chain(prev, cur, _phases(acc, attn, xa, xb, xa2, nw1, nw2), done, max_k=2)
+    tab.status()
+    want = dict(acc=[a.clone() for a in acc], xb=xb.clone(), xa2=xa2.clone(), w=[t.data.clone() for t in tg])
+
+    # ---- two ranks: one buffer, one region per rank, holding what the peers write: o and down sums + the counters ----
+    region = 2 * D + 16                                  # int64 words: acc o | acc down | 4 int32 counters (+ pad)
+    shared = torch.zeros(tp * region, dtype=torch.int64, device="cuda")
+    ranks = []
+    for r in range(tp):
+        ws, dns, ups = _shard(w, down, up, r, tp)
+        tg_r, tab_r = _table(ws, dns, ups)
+        assert tab_r.info()["umma_path"]
+        tab_r.switch(None, prev, max_k=2)
+        reg = shared[r * region: (r + 1) * region]
+        acc_r = [reg[:D], torch.zeros(2 * F // tp, dtype=torch.int64, device="cuda"), reg[D: 2 * D],
+                 torch.zeros(3 * D // tp, dtype=torch.int64, device="cuda")]
+        done_r = reg[2 * D: 2 * D + 2].view(torch.int32)
+        grp_r = SegmentGroup(tab_r, PHASE_IDS)
+        assert 2 * grp_r.grid <= 148
+        offs = [(q - r) * region * 8 for q in range(tp)]
+        grp_r.set_peers(offs, reduce_phases=[0, 2])
+        n_local = D // tp                                 # this rank's heads: its slice of the attention output
+        ranks.append(dict(tg=tg_r, tab=tab_r, grp=grp_r, acc=acc_r, done=done_r, xb=torch.zeros(D, device="cuda"),
+                          xa2=torch.zeros(D, device="cuda"), attn=attn[r * n_local: (r + 1) * n_local].contiguous(),
+                          stream=torch.cuda.Stream()))
+    torch.cuda.synchronize()
+    for rk in ranks:                                      # both launches in flight together, neither can finish alone
+        with torch.cuda.stream(rk["stream"]):
+            rk["grp"].switch_gemv_chain(prev, cur, _phases(rk["acc"], rk["attn"], xa, rk["xb"], rk["xa2"], nw1, nw2), rk["done"], max_k=2)
+    torch.cuda.synchronize()
+    for r, rk in enumerate(ranks):
+        rk["tab"].status()
+        # counters: a reduced phase is reported by the CTAs of both ranks, a local one by this rank's
+        n_cta = rk["grp"].grid
+        assert rk["done"][:3].tolist() == [tp * n_cta, n_cta, tp * n_cta]
+        assert torch.equal(rk["acc"][0], want["acc"][0]) and torch.equal(rk["acc"][2], want["acc"][2])      # all-reduced sums
+        f_loc, d_loc = F // tp, D // tp
+        gate_up = torch.cat([want["acc"][1][r * f_loc: (r + 1) * f_loc], want["acc"][1][F + r * f_loc: F + (r + 1) * f_loc]])
+        assert torch.equal(rk["acc"][1], gate_up)
+        qkv = torch.cat([want["acc"][3][m * D + r * d_loc: m * D + (r + 1) * d_loc] for m in range(3)])
+        assert torch.equal(rk["acc"][3], qkv)
+        assert torch.equal(rk["xb"], want["xb"]) and torch.equal(rk["xa2"], want["xa2"])                    # residual streams
+        ws, _, _ = _shard(want["w"], down, up, r, tp)                                                        # merged weights
+        for got, ref in zip(rk["tg"], ws):
+            assert torch.equal(got.data, ref)
+    assert float(want["acc"][3].abs().max()) > 0
+
+
+def test_last_phase_reduced_needs_its_own_counter_and_wait(af):
+    """A chain that ENDS in a row-parallel phase (the last layer: o -> gate|up -> down) reports that phase too; the
+    consumer is a later launch, ordered behind `peer_wait` on the extra counter."""
+    from paper_2603_11873_b200.adapters import SegmentGroup, peer_wait
+    from paper_2603_11873_b200.errors import DimensionError
+
+    tp = 2
+    shapes, w, down, up = _full_model(seed=12)
+    prev, cur = _decision((0, 3), (0.6, 0.4)), _decision((3, 5), (0.5, 0.5))
+    attn, xa, nw1, _ = _inputs()
+    ids = PHASE_IDS[:3]
+
+    tg, tab = _table(w, down, up)
+    tab.switch(None, prev, max_k=2)
+    xb = torch.zeros(D, device="cuda")
+    acc = [torch.zeros(n, dtype=torch.int64, device="cuda") for n in (D, 2 * F, D)]
+    done = torch.zeros(4, dtype=torch.int32, device="cuda")
+    SegmentGroup(tab, ids).switch_gemv_chain(
+        prev, cur, _phases(acc + [None], attn, xa, xb, None, nw1, None)[:3], done, max_k=2)
+    tab.status()
+
+    region = 2 * D + 16
+    shared = torch.zeros(tp * region, dtype=torch.int64, device="cuda")
+    ranks = []
+    for r in range(tp):
+        ws, dns, ups = _shard(w, down, up, r, tp)
+        tg_r, tab_r = _table(ws, dns, ups)
+        tab_r.switch(None, prev, max_k=2)
+        reg = shared[r * region: (r + 1) * region]
+        acc_r = [reg[:D], torch.zeros(2 * F // tp, dtype=torch.int64, device="cuda"), reg[D: 2 * D]]
+        done_r = reg[2 * D: 2 * D + 2].view(torch.int32)
+        grp_r = SegmentGroup(tab_r, ids)
+        grp_r.set_peers([(q - r) * region * 8 for q in range(tp)], reduce_phases=[0, 2])
+        with pytest.raises(DimensionError):              # three counters now: two boundaries + the reduced last phase
+            grp_r.switch_gemv_chain(prev, cur, _phases(acc_r + [None], attn[:D // tp].contiguous(), xa, xb, None, nw1, None)[:3],
+                                    torch.zeros(2, dtype=torch.int32, device="cuda"), max_k=2)
+        n_local = D // tp
+        ranks.append(dict(tab=tab_r, grp=grp_r, acc=acc_r, done=done_r, xb=torch.zeros(D, device="cuda"),
+                          attn=attn[r * n_local: (r + 1) * n_local].contiguous(), stream=torch.cuda.Stream(),
+                          out=torch.zeros(D, dtype=torch.int64, device="cuda")))
+    torch.cuda.synchronize()
+    # (one GPU plays both ranks: launches that wait for each other are enqueued back to back, so that even if the two
+    #  streams share a hardware queue nothing a launch waits for sits behind one of its own successors)
+    for rk in ranks:
+        with torch.cuda.stream(rk["stream"]):
+            rk["grp"].switch_gemv_chain(prev, cur, _phases(rk["acc"] + [None], rk["attn"], xa, rk["xb"], None, nw1, None)[:3], rk["done"], max_k=2)
+    for rk in ranks:
+        with torch.cuda.stream(rk["stream"]):
+            peer_wait(rk["done"][2:3], tp * rk["grp"].grid)        # ... then the consumer of the reduced sums, on the same stream
+            rk["out"].copy_(rk["acc"][2])
+    torch.cuda.synchronize()
+    for rk in ranks:
+        rk["tab"].status()
+        n_cta = rk["grp"].grid
+        assert rk["done"][:3].tolist() == [tp * n_cta, n_cta, tp * n_cta]
+        assert torch.equal(rk["out"], acc[2])
+
+
+def test_peer_barrier_between_two_streams(af):
+    """`af_peer_barrier`: a monotonic counter every rank bumps on every rank; round k completes when the own counter
+    has reached k * n_peers.  Two streams play the ranks; a rank that is alone times out with an error flag instead of
+    hanging -- not exercised here (2 s), only the happy path over several rounds."""
+    from paper_2603_11873_b200.adapters import peer_barrier
+
+    tp = 2
+    shared = torch.zeros(tp * 4, dtype=torch.int32, device="cuda")         # one 16-byte region per rank
+    epochs = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(tp)]
+    streams = [torch.cuda.Stream() for _ in range(tp)]
+    marks = torch.zeros(tp, 3, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    for rnd in range(3):
+        for r in range(tp):                                   # (the two barriers of a round back to back, see above)
+            with torch.cuda.stream(streams[r]):
+                peer_barrier(shared[r * 4: r * 4 + 1], epochs[r], [(q - r) * 16 for q in range(tp)])
+        for r in range(tp):
+            with torch.cuda.stream(streams[r]):
+                marks[r, rnd] = rnd + 1
+    torch.cuda.synchronize()
+    assert shared[0].item() == 3 * tp and shared[4].item() == 3 * tp
+    assert [e.item() for e in epochs] == [3, 3] and marks.tolist() == [[1, 2, 3]] * tp
+
+
+def test_set_peers_validation(af):
+    from paper_2603_11873_b200.adapters import SegmentGroup
+    from paper_2603_11873_b200.errors import AliasingError, DimensionError
+
+    shapes, w, down, up = _full_model(seed=13)
+    tg, tab = _table(w, down, up)
+    grp = SegmentGroup(tab, PHASE_IDS)
+    with pytest.raises(ValueError):
+        grp.set_peers([0, 4096], reduce_phases=[4])          # the chain has phases 0..3
+    with pytest.raises(ValueError):
+        grp.set_peers([8, 4096], reduce_phases=[0])          # this rank (offset 0) is missing
+    with pytest.raises(AliasingError):
+        grp.set_peers([0, 4096, 4096], reduce_phases=[0])
+    with pytest.raises(DimensionError):
+        grp.set_peers([0, 4100], reduce_phases=[0])          # accumulators are 8-byte words
+    with pytest.raises(ValueError):
+        grp.set_peers([0] + [4096 * i for i in range(1, 9)], reduce_phases=[0])   # at most 8 ranks
+    grp.set_peers([0, 4096], reduce_phases=[0, 2])
+    grp.set_peers([], reduce_phases=[])                        # cleared: a single rank again
+    assert grp.n_peers == 0
