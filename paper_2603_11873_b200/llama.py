@@ -30,7 +30,7 @@ import torch
 
 from . import _capi
 from .adapters import SegmentGroup, SwitchTable
-from .errors import ConfigError, InputError, StateError
+from .errors import ConfigError, DimensionError, InputError, StateError
 from .linalg import DispatchRecorder, Matrix, _ptr
 from .routing import DECISION_BYTES, DeviceDecision, GateDecision
 
@@ -73,6 +73,11 @@ class LlamaConfig:
     chain: bool = True               # chase: o -> gate|up -> down -> next q|k|v as ONE launch with in-kernel phase barriers
     split_switch: bool = True        # > 64 stacked ranks: several tensor-path passes instead of one CUDA-core pass
     defer_norm: bool = True          # chase on the tcgen05 path: RMSNorm scales computed by one CTA, applied by the consumers
+    # Tensor parallelism: True = the row-parallel projections (o, down) push their fixed-point partial sums into every
+    # rank's accumulators from the GEMV epilogue (peer memory over NVLink; `PeerBuffer`), so the chained launch carries
+    # to TP and no collective sits between the launches of a layer; False = one NCCL all-reduce after o and after down;
+    # None = push when tp_size > 1, the tcgen05 path applies and the ranks can map each other's buffer (env AF_TP_PUSH=0: never)
+    tp_push: bool | None = None
     gemv_chain: bool = True          # plain forward (separate / adapter-free): the same four projections as one persistent GEMV launch
     # ... and the whole forward of a token -- attention included -- as ONE launch over a device-side phase table
     # (af_forward_persistent).  Correct and tested, but OFF: measured on Llama-2-7B at 1024 positions the adapter-free
@@ -231,6 +236,39 @@ def rope_tables(cfg: LlamaConfig):
 # ---------------------------------------------------------------------------
 
 
+class PeerBuffer:
+    """int64 words of device memory that every tensor-parallel rank maps (`include/adafuse_b200.h`, af_group_set_peers):
+    `tensor` is this rank's region, `offsets[w]` the byte distance from it to rank w's region as THIS process sees it
+    (own rank: 0).  The engine puts its fixed-point accumulators, phase counters and the token barrier's counter there."""
+
+    def __init__(self, tensor: torch.Tensor, offsets, keep=None):
+        if tensor.dtype != torch.int64 or not tensor.is_contiguous():
+            raise DimensionError("a peer buffer is a contiguous int64 tensor")
+        self.tensor, self.offsets, self._keep = tensor, [int(o) for o in offsets], keep
+        if self.offsets.count(0) != 1:
+            raise ValueError("peer offsets must contain this rank (0) exactly once")
+
+    @classmethod
+    def local(cls, n_words: int, device) -> "PeerBuffer":
+        """A single rank: the only peer is the rank itself (tests; the same kernels and counters run)."""
+        return cls(torch.zeros(n_words, dtype=torch.int64, device=device), [0])
+
+    @classmethod
+    def symmetric(cls, n_words: int, device, group=None) -> "PeerBuffer":
+        """One buffer per rank of `group`, mapped by every other rank through torch symmetric memory (CUDA VMM / NVLink
+        peer access).  A collective call: every rank of the group makes it with the same size."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        t = symm.empty(n_words, dtype=torch.int64, device=device)
+        t.zero_()
+        hdl = symm.rendezvous(t, group if group is not None else dist.group.WORLD)
+        ptrs = [int(p) for p in hdl.buffer_ptrs]
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)                      # every region is zeroed before anybody pushes into it
+        return cls(t, [p - ptrs[hdl.rank] for p in ptrs], keep=hdl)
+
+
 class Collectives:
     """torch.distributed plumbing of the TP path.  With tp_size == 1 every method is a no-op."""
 
@@ -298,7 +336,7 @@ def _on_device(fn):
 class LlamaEngine:
     """Resident weights, expert bank, descriptor table, KV cache and the captured decode step."""
 
-    def __init__(self, cfg: LlamaConfig, init: str = "host", device=None, group=None, comm=None):
+    def __init__(self, cfg: LlamaConfig, init: str = "host", device=None, group=None, comm=None, peers=None):
         cfg.validate()
         torch_ = _capi.require_cuda()
         self.cfg = cfg
@@ -307,7 +345,7 @@ class LlamaEngine:
             self.dev = torch_.device("cuda", torch_.cuda.current_device())
         if self.dev.index != torch_.cuda.current_device():
             with torch_.cuda.device(self.dev):      # build (and configure the kernels) on the engine's own device
-                self.__init__(cfg, init=init, device=self.dev, group=group, comm=comm)
+                self.__init__(cfg, init=init, device=self.dev, group=group, comm=comm, peers=peers)
             return
         # `comm` lets a caller supply the exchange layer (tests build one shard with no peers)
         self.comm = comm if comm is not None else Collectives(group, cfg.tp_size)
@@ -448,7 +486,38 @@ class LlamaEngine:
             # launches of one token: [qkv(0)] attn [o gu down qkv(1)] attn ... [o gu down (L-1)]
             # TP: the row-parallel projections (o, down) end in an all-reduce of their fixed-point accumulators
             # (exact: integer sums), so the phases cannot share one launch -- one launch per projection
-            self.chase_chained = cfg.chain and cfg.tp_size == 1
+            # ... unless the epilogue does the all-reduce itself (tp_push): o and down add their partial sums into EVERY
+            # rank's accumulators over peer memory and the phase counters count the CTAs of all ranks -- the single-rank
+            # chain, unchanged, is then the TP step
+            n_qkv, n_gu = self.q_rows + 2 * self.kv_rows, 2 * self.ffn_local
+            per_layer = n_qkv + d + n_gu + d
+            arena_words = cfg.layers * (per_layer + 2)
+            self.tp_push, self.peer_buf = False, None
+            env_push = os.environ.get("AF_TP_PUSH", "1") != "0"
+            if cfg.tp_push is not None:
+                want_push = cfg.tp_push
+            else:   # automatic: a real process group whose ranks are this engine's TP ranks (or a caller-supplied buffer)
+                import torch.distributed as dist
+                have_group = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) == cfg.tp_size
+                want_push = cfg.tp_size > 1 and env_push and (peers is not None or have_group)
+            push_ok = cfg.chain and bool(self.table.info().get("umma_path")) and not self.chase_split
+            if cfg.tp_push and not push_ok:
+                raise ConfigError("tp_push needs the chained launches on the tcgen05 path (chain=True, umma_path, one-launch switch)")
+            if want_push and push_ok:
+                try:
+                    # (+ 2 words behind the arena: the token barrier's counter, which is never zeroed)
+                    self.peer_buf = peers(arena_words + 2) if peers is not None else (
+                        PeerBuffer.symmetric(arena_words + 2, dev, group) if cfg.tp_size > 1 else PeerBuffer.local(arena_words + 2, dev))
+                    if len(self.peer_buf.offsets) != cfg.tp_size or self.peer_buf.tensor.numel() < arena_words + 2:
+                        raise ConfigError(f"the peer buffer maps {len(self.peer_buf.offsets)} rank(s) for tp_size {cfg.tp_size}, "
+                                          "or is smaller than the arena")
+                    self.tp_push = True
+                except (RuntimeError, ImportError, AttributeError, TypeError, ConfigError) as e:   # no peer access between the ranks:
+                    if cfg.tp_push:                                                       # NCCL all-reduces instead
+                        raise
+                    self.peer_buf = None
+                    self.tp_push_unavailable = f"{type(e).__name__}: {e}"
+            self.chase_chained = cfg.chain and (cfg.tp_size == 1 or self.tp_push)
             seg = lambda li: {"qkv": [7 * li, 7 * li + 1, 7 * li + 2], "o": [7 * li + 3], "gu": [7 * li + 4, 7 * li + 5],  # noqa: E731
                               "down": [7 * li + 6]}                                 # SEGMENT_NAMES order: q k v o gate up down
             self.groups = []
@@ -458,6 +527,8 @@ class LlamaEngine:
                     mid = [sg["o"], sg["gu"], sg["down"]] + ([seg(li + 1)["qkv"]] if li + 1 < cfg.layers else [])
                     self.groups.append({"qkv": SegmentGroup(self.table, sg["qkv"]) if li == 0 else None,
                                         "mid": SegmentGroup(self.table, mid)})
+                    if self.tp_push:            # phases 0 (o) and 2 (down) are row-parallel
+                        self.groups[-1]["mid"].set_peers(self.peer_buf.offsets, reduce_phases=[0, 2])
                 elif cfg.chain:
                     # TP: the chain breaks only where a collective sits -- after o and after down.  gate|up -> down has
                     # none in between (column-parallel outputs feed the row-parallel input shard locally): one launch.
@@ -467,9 +538,12 @@ class LlamaEngine:
                     self.groups.append({k: SegmentGroup(self.table, v) for k, v in sg.items()})
             # fixed-point accumulators of every launch of a token and the chains' phase counters:
             # one arena, zeroed once per step
-            n_qkv, n_gu = self.q_rows + 2 * self.kv_rows, 2 * self.ffn_local
-            per_layer = n_qkv + d + n_gu + d
-            self.acc_arena = torch.zeros(cfg.layers * (per_layer + 2), dtype=torch.int64, device=dev)
+            if self.tp_push:
+                self.acc_arena = self.peer_buf.tensor[:arena_words]
+                self.peer_counter = self.peer_buf.tensor[arena_words: arena_words + 1].view(torch.int32)[:1]
+                self.peer_epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+            else:
+                self.acc_arena = torch.zeros(arena_words, dtype=torch.int64, device=dev)
             self.acc = []
             self.phase_done = []
             # tcgen05 path: RMSNorm scales are deferred -- one CTA computes them, the consumers of q|k|v
@@ -732,6 +806,11 @@ class LlamaEngine:
         kw = dict(max_k=max_k, mode=mode, plan_prebuilt=True)
         self.table.build_plan(prev, cur, max_k=max_k, mode=mode)
         self.acc_arena.zero_()
+        if self.tp_push:
+            # nobody pushes into these accumulators before every rank has zeroed its own (af_peer_barrier: a monotonic
+            # counter behind the arena, bumped on every rank by every rank)
+            from .adapters import peer_barrier
+            peer_barrier(self.peer_counter, self.peer_epoch, self.peer_buf.offsets, self.err_dev)
         self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
         norm = "rmsnorm_deferred" if self.defer_norm else "rmsnorm"
         # timing experiment only (wrong results): AF_SKIP_ATTN=1 leaves the attention launches out -- how much of the step
@@ -772,6 +851,11 @@ class LlamaEngine:
                     g["gu"].switch_gemv(prev, cur, pdl=True, **ph_gu, **kw)
                     g["down"].switch_gemv(prev, cur, pdl=True, **ph_down, **kw)
                 self.comm.all_reduce_sum(a["down"])
+        if self.tp_push:
+            # the last layer's down projection has no consumer inside its launch: wait until the CTAs of every rank
+            # have reported it (counter 2 of the last chain) before reading the reduced sums
+            from .adapters import peer_wait
+            peer_wait(self.phase_done[-1][2:3], cfg.tp_size * self.groups[-1]["mid"].grid, self.err_dev)
         self._check(L.af_accum_to_f32(_ptr(self.acc[-1]["down"]), _ptr(xb), _ptr(xa), d, st))
         self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),
                                     _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))

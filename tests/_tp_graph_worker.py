@@ -16,8 +16,35 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_11873_b200 import llama  # noqa: E402
 
 
+def push_over_symmetric_memory(port):
+    """`push` mode: the TP-push step with its accumulators in torch SYMMETRIC MEMORY (what maps the ranks' buffers into
+    each other over NVLink), on a one-rank NCCL group: allocation, rendezvous and the peer offsets are the real ones,
+    the only peer is the rank itself.  Bit-identical to the plain engine."""
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
+    forced = np.random.Generator(np.random.PCG64(13)).integers(0, 512, 12)
+    runs = []
+    for push in (False, True):
+        cfg = llama.preset("tiny", forward_mode="chase", max_seq=48, tp_push=push)
+        eng = llama.LlamaEngine(cfg, init="host", peers=(lambda n: llama.PeerBuffer.symmetric(n, dev)) if push else None)
+        assert eng.tp_push == push
+        if push:
+            assert eng.peer_buf.offsets == [0] and eng.peer_buf._keep is not None
+        eng.reset(forced=forced)
+        toks = [eng.decode_step() for _ in forced]
+        runs.append((toks, [t.data.clone() for t in eng.targets]))
+    assert runs[0][0] == runs[1][0], runs
+    for ta, tb in zip(runs[0][1], runs[1][1]):
+        assert torch.equal(ta, tb)
+    dist.destroy_process_group()
+    print("TP_PUSH_SYMM_OK")
+
+
 def main():
     forward_mode, port = sys.argv[1], sys.argv[2]
+    if forward_mode == "push":
+        return push_over_symmetric_memory(port)
     os.environ["AF_TP_GRAPH"] = "1"
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,

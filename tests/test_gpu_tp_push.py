@@ -259,3 +259,70 @@ def test_set_peers_validation(af):
     grp.set_peers([0, 4096], reduce_phases=[0, 2])
     grp.set_peers([], reduce_phases=[])                        # cleared: a single rank again
     assert grp.n_peers == 0
+
+
+def test_engine_with_push_enabled_equals_the_plain_engine(af):
+    """`LlamaConfig.tp_push=True` on ONE rank (the only peer is the rank itself): the engine runs the TP-push step --
+    accumulators and counters in the peer buffer, the token barrier, o and down pushed with system-scope atomics, the
+    wait for the last layer's down projection -- and must reproduce the plain engine bit for bit: tokens, logits and
+    the weights the switches leave behind."""
+    import numpy as np
+
+    from paper_2603_11873_b200 import llama
+
+    forced = np.random.Generator(np.random.PCG64(5)).integers(0, 512, 12)
+    outs = []
+    for push in (False, True):
+        cfg = llama.preset("tiny", max_seq=32, forward_mode="chase", tp_push=push)
+        eng = llama.LlamaEngine(cfg, init="host")
+        assert eng.chase and eng.chase_chained and eng.tp_push == push
+        if push:
+            assert eng.peer_buf.offsets == [0] and eng.groups[0]["mid"].n_peers == 1
+        eng.reset(forced=forced)
+        toks, logits = [], []
+        for _ in forced:
+            toks.append(eng.decode_step(graph=False))
+            logits.append(eng.logits.clone())
+        eng.check()
+        if push:
+            assert int(eng.peer_epoch.item()) == len(forced) and int(eng.peer_counter.item()) == len(forced)
+        outs.append((toks, logits, [t.data.clone() for t in eng.targets]))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert torch.equal(a, b)
+    for a, b in zip(outs[0][2], outs[1][2]):
+        assert torch.equal(a, b)
+
+
+def test_engine_push_step_replays_as_a_graph(af):
+    """The push step has no library collective inside the layers: it captures and replays like the single-rank step
+    (the barrier's epoch lives on the device)."""
+    import numpy as np
+
+    from paper_2603_11873_b200 import llama
+
+    forced = np.random.Generator(np.random.PCG64(6)).integers(0, 512, 10)
+    runs = []
+    for graph in (False, True):
+        eng = llama.LlamaEngine(llama.preset("tiny", max_seq=32, forward_mode="chase", tp_push=True), init="host")
+        eng.reset(forced=forced)
+        runs.append([eng.decode_step(graph=graph) for _ in forced])
+        eng.check()
+        assert int(eng.peer_epoch.item()) == len(forced)
+    assert runs[0] == runs[1]
+
+
+def test_engine_push_over_torch_symmetric_memory():
+    """The accumulators in torch symmetric memory (one-rank NCCL group in a worker process): the buffer and the peer
+    offsets are obtained the way a multi-GPU run obtains them."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_tp_graph_worker.py")
+    r = subprocess.run([sys.executable, worker, "push", str(port)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "TP_PUSH_SYMM_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
