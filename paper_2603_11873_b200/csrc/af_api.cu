@@ -525,12 +525,12 @@ static const int kUmmaMaxRanksChain = [] { const char* e = getenv("AF_UMMA_MAX_R
 // barrier traffic: measured 1.5 % slower on Llama-3-8B shapes, so off)
 static const int kUmmaChunk64 = [] { const char* e = getenv("AF_UMMA_CHUNK64"); return e ? atoi(e) : 0; }();
 // tcgen05 / TMEM kernel (af_switch_umma.cuh).  NB = k-groups of 8 stacked ranks per half, CH = k-groups per UP stage.
-template <int NB, bool GEMV, int CH = NB, int PC = 2>
-static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
+template <int NB, bool GEMV, int CH, int PC, bool PEERS>
+static int launch_umma_k(const MmaParams& mp, int grid, cudaStream_t st) {
     using L = UmmaLayout<NB, GEMV, CH, PC>;
     static PerDevice configured;
     if (!configured.cur()) {
-        AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV, CH, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        AF_CUDA_TRY(cudaFuncSetAttribute(switch_umma_kernel<NB, GEMV, CH, PC, PEERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
         configured.cur() = 1;
     }
     if (mp.n_phases > 1) {
@@ -540,7 +540,7 @@ static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
         static PerDevice occ_checked;
         if (!occ_checked.cur()) {
             int per_sm = 0;
-            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, switch_umma_kernel<NB, GEMV, CH, PC>, kUThreads, L::total));
+            AF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, switch_umma_kernel<NB, GEMV, CH, PC, PEERS>, kUThreads, L::total));
             const DeviceInfo& di = device_info();
             if (per_sm < 1 || grid > di.sm_count * per_sm)
                 return fail(AF_ESTATE, "a chained launch needs all its CTAs co-resident: " + std::to_string(grid) + " CTAs, device holds " +
@@ -558,11 +558,19 @@ static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = mp.pdl ? 1 : 0;
-    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV, CH, PC>, mp));
+    AF_CUDA_TRY(cudaLaunchKernelEx(&cfg, switch_umma_kernel<NB, GEMV, CH, PC, PEERS>, mp));
     AF_LAUNCH_CHECK("switch_umma_kernel");
-    note_kernel(PC == 3 ? "switch_umma_kernel<NB=%d,GEMV=%d,CH=%d,PC=3> (tcgen05 + TMEM)" : "switch_umma_kernel<NB=%d,GEMV=%d,CH=%d> (tcgen05 + TMEM)", NB,
-                (int)GEMV, CH);
+    note_kernel(PC == 3 ? "switch_umma_kernel<NB=%d,GEMV=%d,CH=%d,PC=3> (tcgen05 + TMEM)"
+                        : (PEERS ? "switch_umma_kernel<NB=%d,GEMV=%d,CH=%d,PEERS> (tcgen05 + TMEM)" : "switch_umma_kernel<NB=%d,GEMV=%d,CH=%d> (tcgen05 + TMEM)"),
+                NB, (int)GEMV, CH);
     return AF_OK;
+}
+
+template <int NB, bool GEMV, int CH = NB, int PC = 2>
+static int launch_umma(const MmaParams& mp, int grid, cudaStream_t st) {
+    // tensor-parallel pushes (af_group_set_peers) are a separate instantiation of the GEMV kernels
+    if (GEMV && mp.n_peers > 0) return launch_umma_k<NB, GEMV, CH, PC, GEMV>(mp, grid, st);
+    return launch_umma_k<NB, GEMV, CH, PC, false>(mp, grid, st);
 }
 
 // Largest stacked rank ONE tcgen05 launch over this table takes (0: the table is not eligible at all)

@@ -175,12 +175,13 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 // tile walk with 128-row tiles (units are cut at multiples of kUM)
 // This CTA's partial sums of phases [from, to) are out: bump their counters (after the fence that orders the atomics
 // before the bump).  A phase that was pushed to the peers (MmaParams::reduce_mask) is reported on every rank's counter.
+template <bool PEERS>
 __device__ __forceinline__ void umma_publish_phases(const MmaParams& mp, int from, int to) {
     if (from >= to) return;
-    if (mp.n_peers > 0) __threadfence_system();
+    if (PEERS && mp.n_peers > 0) __threadfence_system();
     else __threadfence();
     for (int ph = from; ph < to; ++ph) {
-        if (mp.n_peers > 0 && ((mp.reduce_mask >> ph) & 1)) {
+        if (PEERS && mp.n_peers > 0 && ((mp.reduce_mask >> ph) & 1)) {
             for (int w = 0; w < mp.n_peers; ++w)
                 atomicAdd_system(reinterpret_cast<int*>(reinterpret_cast<char*>(mp.phase_done + ph) + mp.peer_off[w]), 1);
         } else {
@@ -190,8 +191,9 @@ __device__ __forceinline__ void umma_publish_phases(const MmaParams& mp, int fro
 }
 // Counters a launch bumps: one per phase boundary, plus the last phase's when that one is reduced over the peers
 // (its consumer is a later launch, which waits for it with af_peer_wait).
+template <bool PEERS>
 __device__ __forceinline__ int umma_phases_to_publish(const MmaParams& mp) {
-    const bool last_reduced = mp.n_peers > 0 && ((mp.reduce_mask >> (mp.n_phases - 1)) & 1);
+    const bool last_reduced = PEERS && mp.n_peers > 0 && ((mp.reduce_mask >> (mp.n_phases - 1)) & 1);
     return mp.n_phases - 1 + (last_reduced ? 1 : 0);
 }
 
@@ -351,7 +353,9 @@ __device__ __forceinline__ void umma_slab_direct(unsigned char* slab, const SegD
     }
 }
 
-template <int NB, bool GEMV, int CH = NB, int PC = 2>
+// PEERS: the tensor-parallel pushes (MmaParams::n_peers) are compiled in -- a separate instantiation, so that a single
+// rank's kernel carries none of it (measured: 0.4 % of the Llama-2-7B step otherwise)
+template <int NB, bool GEMV, int CH = NB, int PC = 2, bool PEERS = false>
 __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_constant__ MmaParams mp) {
     using L = UmmaLayout<NB, GEMV, CH, PC>;
     constexpr bool kPrefetchSlab = NB <= 8;   // the next unit's DOWN rows wait in registers (umma_slab_prefetch)
@@ -683,12 +687,12 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                     if (ph > 0) {
                         if (tid == 0) {
                             // (a reduced phase: the CTAs of EVERY rank report on this rank's counter)
-                            const bool reduced = mp.n_peers > 0 && ((mp.reduce_mask >> (ph - 1)) & 1);
+                            const bool reduced = PEERS && mp.n_peers > 0 && ((mp.reduce_mask >> (ph - 1)) & 1);
                             const int target = (int)gridDim.x * (reduced ? mp.n_peers : 1);
                             const long long t0 = clock64();
                             int seen;
                             do {
-                                if (mp.n_peers > 0)
+                                if (PEERS && mp.n_peers > 0)
                                     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(mp.phase_done + ph - 1) : "memory");
                                 else
                                     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(mp.phase_done + ph - 1) : "memory");
@@ -805,7 +809,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                             // the phases this CTA has finished (or has no tiles in) are complete on its side: every
                             // epilogue warp issued its atomics before the barrier above -- publish before anything else
                             if (ti.un.phase != cur_phase) {
-                                if (tid == 0 && published < ti.un.phase) umma_publish_phases(mp, published, min(ti.un.phase, mp.n_phases - 1));
+                                if (tid == 0 && published < ti.un.phase) umma_publish_phases<PEERS>(mp, published, min(ti.un.phase, mp.n_phases - 1));
                                 published = ti.un.phase;
                             }
                         }
@@ -895,7 +899,7 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                             if (m0 + row_in_tile < row_end) {
                                 unsigned long long* dst = acc_out + yoff + m0 + row_in_tile;
                                 const unsigned long long v = (unsigned long long)f32_to_fix(y);
-                                if (mp.n_peers > 0 && ((mp.reduce_mask >> cur_phase) & 1)) {   // row-parallel phase: into every rank's sums
+                                if (PEERS && mp.n_peers > 0 && ((mp.reduce_mask >> cur_phase) & 1)) {   // row-parallel phase: into every rank's sums
                                     for (int w = 0; w < mp.n_peers; ++w)
                                         atomicAdd_system(reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(dst) + mp.peer_off[w]), v);
                                 } else {
@@ -910,11 +914,11 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                 if (tid == 0) tl_stamp(tl, 7);
                 if constexpr (GEMV) {   // the remaining phases of the chain
                     named_bar_sync(1, kUEpi);
-                    if (tid == 0) umma_publish_phases(mp, published, umma_phases_to_publish(mp));
+                    if (tid == 0) umma_publish_phases<PEERS>(mp, published, umma_phases_to_publish<PEERS>(mp));
                 }
             } else if constexpr (GEMV) {
                 // a CTA without work still takes part in the phase barriers
-                if (tid == 0) umma_publish_phases(mp, 0, umma_phases_to_publish(mp));
+                if (tid == 0) umma_publish_phases<PEERS>(mp, 0, umma_phases_to_publish<PEERS>(mp));
             }
         }
     }

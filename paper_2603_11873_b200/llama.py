@@ -508,7 +508,8 @@ class LlamaEngine:
                     # (+ 2 words behind the arena: the token barrier's counter, which is never zeroed)
                     self.peer_buf = peers(arena_words + 2) if peers is not None else (
                         PeerBuffer.symmetric(arena_words + 2, dev, group) if cfg.tp_size > 1 else PeerBuffer.local(arena_words + 2, dev))
-                    if len(self.peer_buf.offsets) != cfg.tp_size or self.peer_buf.tensor.numel() < arena_words + 2:
+                    # (a one-entry list on a TP shard: the shard runs ALONE -- scripts/bench_shard.py times a rank's step that way)
+                    if len(self.peer_buf.offsets) not in (1, cfg.tp_size) or self.peer_buf.tensor.numel() < arena_words + 2:
                         raise ConfigError(f"the peer buffer maps {len(self.peer_buf.offsets)} rank(s) for tp_size {cfg.tp_size}, "
                                           "or is smaller than the arena")
                     self.tp_push = True
@@ -855,7 +856,7 @@ class LlamaEngine:
             # the last layer's down projection has no consumer inside its launch: wait until the CTAs of every rank
             # have reported it (counter 2 of the last chain) before reading the reduced sums
             from .adapters import peer_wait
-            peer_wait(self.phase_done[-1][2:3], cfg.tp_size * self.groups[-1]["mid"].grid, self.err_dev)
+            peer_wait(self.phase_done[-1][2:3], len(self.peer_buf.offsets) * self.groups[-1]["mid"].grid, self.err_dev)
         self._check(L.af_accum_to_f32(_ptr(self.acc[-1]["down"]), _ptr(xb), _ptr(xa), d, st))
         self._check(L.af_gemv_fused(_ptr(self.lm_head.data), self.vocab_local, d, d, _ptr(xa), _ptr(self.logits),
                                     _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))

@@ -17,6 +17,7 @@ ap.add_argument("--tp", type=int, default=2)
 ap.add_argument("--steps", type=int, default=30)
 ap.add_argument("--forward-mode", default="auto")
 ap.add_argument("--switch-mode", default="inplace")
+ap.add_argument("--push", action="store_true", help="tp_push step (chained launches, sums pushed from the epilogue) with the rank as its only peer")
 args = ap.parse_args()
 
 
@@ -35,8 +36,9 @@ class Alone(llama.Collectives):
 
 
 cfg = llama.preset(args.workload, tp_size=args.tp, tp_rank=0, max_seq=2 * args.steps + 32, forward_mode=args.forward_mode,
-                   switch_mode=args.switch_mode)
-eng = llama.LlamaEngine(cfg, init="device", comm=Alone(args.tp))
+                   switch_mode=args.switch_mode, tp_push=True if args.push else False)
+dev = torch.device("cuda", 0)
+eng = llama.LlamaEngine(cfg, init="device", comm=Alone(args.tp), peers=(lambda n: llama.PeerBuffer.local(n, dev)) if args.push else None)
 forced = np.random.Generator(np.random.PCG64(1)).integers(0, cfg.vocab, 256)
 eng.reset(forced=forced)
 for _ in range(4):
@@ -69,6 +71,6 @@ graph = timed(g.replay, args.steps)
 info = eng.table.info()
 w_gb = sum(t.data.numel() for t in eng.targets) * 2 / 1e9
 print(f"{args.workload} tp{args.tp} rank 0 alone: W {w_gb:.2f} GB/rank, stacked ranks {2 * cfg.top_k * cfg.rank}, "
-      f"schedule {'chase' if eng.chase else 'separate'}, tensor path {bool(info.get('tensor_path'))}, tcgen05 {bool(info.get('umma_path'))}: "
+      f"schedule {'chase' if eng.chase else 'separate'}{' chained + push (alone)' if getattr(eng, 'tp_push', False) else ''}, tensor path {bool(info.get('tensor_path'))}, tcgen05 {bool(info.get('umma_path'))}: "
       f"eager {eager:.3f} ms/token, graph {graph:.3f} ms/token ({1e3 / graph:.0f} tok/s per rank-step; "
       f"{(3 if not eng.chase else 2) * w_gb / graph * 1e3:.0f} GB/s of W traffic at 2 (chase) / 3 (separate) passes over W)", flush=True)

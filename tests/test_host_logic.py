@@ -322,3 +322,27 @@ def test_forward_phase_table_validation():
         check([gemv(kind=7)])
     with pytest.raises(errors.DimensionError):
         check([gemv()], heads=3, kv=2)
+
+
+def test_peer_buffer_contract_and_peer_calls_validate_without_a_device():
+    """`llama.PeerBuffer` (what a TP rank hands the engine for tp_push) and the argument checks of the peer calls of the
+    C ABI, which run before anything touches a device."""
+    import ctypes
+
+    from paper_2603_11873_b200 import _capi
+    from paper_2603_11873_b200.errors import DimensionError
+
+    buf = llama.PeerBuffer(torch.zeros(16, dtype=torch.int64), [-4096, 0, 4096])
+    assert buf.offsets == [-4096, 0, 4096] and buf.tensor.numel() == 16
+    with pytest.raises(ValueError):
+        llama.PeerBuffer(torch.zeros(16, dtype=torch.int64), [4096, 8192])      # this rank (0) is missing
+    with pytest.raises(ValueError):
+        llama.PeerBuffer(torch.zeros(16, dtype=torch.int64), [0, 0])
+    with pytest.raises(DimensionError):
+        llama.PeerBuffer(torch.zeros(16, dtype=torch.int32), [0])
+    assert llama.LlamaConfig().tp_push is None
+    L = _capi.lib()
+    offs = (ctypes.c_int64 * 2)(0, 4096)
+    assert L.af_group_set_peers(None, 2, offs, 1) == _capi.AF_EVALUE             # no group
+    assert L.af_peer_barrier(None, None, 2, offs, None, None) == _capi.AF_EVALUE
+    assert L.af_peer_wait(None, 1, None, None) == _capi.AF_EVALUE
