@@ -253,10 +253,40 @@ def main():
         torch.cuda.synchronize()
 
     max_seq = args.context + 3 * (args.steps + args.warmup) + 64
-    cfg = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
-                       compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain,
-                       attn_splits=args.attn_splits, refresh_every=args.refresh_every, persistent_forward=args.persistent_forward)
-    eng = llama.LlamaEngine(cfg, init="device")
+    def build_engine(tp_push):
+        c = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
+                         compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain,
+                         attn_splits=args.attn_splits, refresh_every=args.refresh_every, persistent_forward=args.persistent_forward,
+                         tp_push=tp_push)
+        return c, llama.LlamaEngine(c, init="device")
+
+    # N > 1: the row-parallel sums are pushed into the peers' accumulators from the GEMV epilogue (LlamaConfig.tp_push:
+    # torch symmetric memory over NVLink) when the ranks can map each other's buffers -- probed with two eager steps on
+    # every rank, all ranks agreeing; otherwise one NCCL all-reduce after o and after down.  AF_TP_PUSH=0 skips the probe.
+    tp_collective = "none"
+    eng = None
+    if world > 1:
+        tp_collective = "nccl all-reduce"
+        if backend == "nccl" and os.environ.get("AF_TP_PUSH", "1") != "0" and args.forward_mode != "separate" and not args.no_chain:
+            ok = 1
+            try:
+                cfg, eng = build_engine(True)
+                eng.reset(forced=[1, 2, 3, 4])
+                for _ in range(2):
+                    eng.decode_step(graph=False)
+                eng.check()
+            except Exception as e:   # noqa: BLE001 -- whatever it is, the NCCL path is the fallback
+                ok = 0
+                print(f"[bench rank {rank}] tp_push unavailable: {type(e).__name__}: {e}", file=sys.stderr, flush=True)
+            flag = torch.tensor([ok], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:
+                tp_collective = "pushed from the GEMV epilogue (peer memory)"
+            else:
+                eng = None
+                torch.cuda.empty_cache()
+    if eng is None:
+        cfg, eng = build_engine(False if world > 1 else None)
     info = eng.table.info()
     forced = np.random.Generator(np.random.PCG64(cfg.seed + 1)).integers(0, cfg.vocab, 4096)
     peak, peak_kind = load_peaks()
@@ -464,7 +494,8 @@ def main():
                         "forward_mode": "chase (GEMV fused into the switch: W read and written once per token)" if chase
                         else "separate (one switch launch, then plain GEMVs)",
                         "refresh": "every %d-th token switches from the pristine copy (same bytes, same launch)" % eng.refresh_every
-                        if eng.refresh_every else "none"},
+                        if eng.refresh_every else "none",
+                        "tp_collective": tp_collective},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 8,
                 "ms_per_step": e2e_ms / args.steps,
                 "api": "LlamaEngine.decode_step(token): pinned H2D of the token, the step (a CUDA graph replay from the second token on), "
