@@ -22,6 +22,8 @@ for tp in 1 2 4 8; do timeout 300 python scripts/bench_shard.py llama2-7b --tp $
 for tp in 2 4 8; do timeout 300 python scripts/bench_shard.py llama2-13b --tp $tp --steps 20 2>&1 | tail -1; done
 timeout 300 python scripts/bench_shard.py llama2-70b --tp 8 --steps 10 2>&1 | tail -1
 timeout 300 python scripts/bench_shard.py llama2-70b --tp 8 --steps 10 --switch-mode from_pristine 2>&1 | tail -1
+echo "# tp_push step of a shard timed alone (chained launches; the rank is its own and only peer: no NVLink traffic, no peers to wait for)"
+for w in "llama2-7b --tp 8" "llama2-7b --tp 4" "llama2-13b --tp 8" "llama2-13b --tp 4"; do timeout 300 python scripts/bench_shard.py $w --steps 20 --push 2>&1 | tail -1; done
 } > $O/tp_shard_alone.txt 2>&1
 {
 timeout 200 python scripts/bench_switch.py --config 7b --modes mma --iters 4 2>&1 | grep '"mode"'
@@ -31,6 +33,8 @@ for k in 1 2 4; do timeout 200 python scripts/bench_switch.py --config 70b-tp8 -
 } > $O/switch_by_stacked_rank.txt 2>&1
 { timeout 200 python scripts/bench_attn.py --ctx 128 --splits 1,2,4; timeout 200 python scripts/bench_attn.py --ctx 1024 --splits 8,16,17,32; timeout 200 python scripts/bench_attn.py --ctx 4096 --splits 16,32;
   AF_ATTN2=0 timeout 200 python scripts/bench_attn.py --ctx 1024 --splits 8; } > $O/attn.txt 2>&1
+{ for pc in 2 3; do AF_UMMA_PIECES=$pc timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('AF_UMMA_PIECES=$pc', 'ms_per_step', round(d['ms_per_step'],4), 'e2e', round(d['e2e']['value'],2), 'tok/s; roofline frac', round(d['roofline']['frac'],4), d['roofline']['kernel'][:70])"; done
+  for pc in 2 3; do echo "AF_UMMA_PIECES=$pc:"; AF_UMMA_PIECES=$pc timeout 600 python -m pytest tests/test_gpu_true_shapes.py -q -s -k "bench" 2>&1 | grep -E "elements checked|passed|failed" | cut -c1-330; done; } > $O/three_pieces.txt 2>&1
 timeout 300 python scripts/timeline_chase.py --ctx 1024 --show 0,1,17,32 > $O/chase_timeline.txt 2>&1
 timeout 200 ./scripts/micro/_bin/umma_rate > $O/umma_rate.txt 2>&1
 if [ "$1" != "noncu" ]; then
