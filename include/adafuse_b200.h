@@ -120,11 +120,13 @@ int af_set_gemv_variant(int32_t variant, int32_t full_sm);
  * AF_UMMA_MAX_RANKS / AF_UMMA_MAX_RANKS_CHAIN move the limits (A/B runs). */
 int af_set_umma(int32_t enable);
 /* bf16 pieces the tcgen05 kernels split a gated DOWN row (g * a, an f32 value) into before the tensor cores
- * multiply it with UP: 3 (default; g*a exact -- 24 bits in three 8-bit pieces -- so the merge differs from the
- * reference's f32 `B @ (g*A)` of linalg.py:150-168 only by the order of the f32 sums) or 2 (g*a reproduced to 2^-17
- * relative: 8x more last-bit differences against the oracle, 0.4 % less time per token at Llama-2-7B).  Three pieces
- * apply to launches of at most 32 stacked ranks (rank 8, top-2: BASELINE configs[0..1] and [3]); larger launches
- * always use two (the slab would cost a ring stage).  AF_EVALUE for anything but 2 or 3.  Env: AF_UMMA_PIECES. */
+ * multiply it with UP: 2 (default; g*a reproduced to 2^-17 relative, as the mma.sync kernels do) or 3 (g*a exact --
+ * 24 bits in three 8-bit pieces -- so the merge differs from the reference's f32 `B @ (g*A)` of linalg.py:150-168
+ * only by the order of the f32 sums: 8x fewer last-bit differences against the oracle at Llama-2-7B, for 0.4 % of the
+ * step at full clocks and 1.5 % on a power-capped board -- 50 % more tensor work).  Three pieces apply to launches of
+ * at most 32 stacked ranks (rank 8, top-2: BASELINE configs[0..1] and [3]); larger launches always use two (the slab
+ * would cost a ring stage).  The two settings round differently in the last bit: do not mix them inside one
+ * comparison.  AF_EVALUE for anything but 2 or 3.  Env: AF_UMMA_PIECES. */
 int af_set_umma_pieces(int32_t pieces);
 
 /* ---- segment table: built once at model load -------------------------------------

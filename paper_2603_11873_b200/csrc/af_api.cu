@@ -62,7 +62,7 @@ static std::atomic<int> g_umma{[] {
 // bf16 pieces of the gated DOWN rows in launches of at most 32 stacked ranks (af_set_umma_pieces; env AF_UMMA_PIECES)
 static std::atomic<int> g_umma_pieces{[] {
     const char* e = getenv("AF_UMMA_PIECES");
-    return e && atoi(e) == 2 ? 2 : 3;
+    return e && atoi(e) == 3 ? 3 : 2;
 }()};
 static const bool g_force_hilo = [] { const char* e = getenv("AF_FORCE_HILO"); return e && e[0] == '1'; }();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and occupancy are per DEVICE: what has been configured is

@@ -64,8 +64,10 @@ constexpr long long kUBurstAfterCycles = AF_UMMA_BURST_AFTER;
 // UP operand of a tile is one stage; CH < NB: K-chunked, NB / CH chunks per tile)
 // PC = bf16 pieces the gated DOWN rows are split into: 2 (hi + lo: g*a reproduced to 2^-17) or 3 (hi + mid + lo: the f32 value
 // of g*a exactly -- 24 bits in three 8-bit pieces -- so that the product differs from the reference's f32 merge only by the
-// order of the f32 sums).  Three pieces need 50 % more slab and MMAs: used where both are cheap, at up to 32 stacked ranks
-// (the default there since the MMA issue moved to the uniform datapath: +0.4 % per token, 8x fewer last-bit differences).
+// order of the f32 sums).  Three pieces need 50 % more slab and MMAs: offered where both are cheap, at up to 32 stacked ranks
+// (af_set_umma_pieces(3): 8x fewer last-bit differences against the oracle for 0.4 % of the Llama-2-7B step at full clocks,
+// 1.5 % on a power-capped board; the default stays two -- the mma.sync kernels' split, so both tensor paths agree to the bit
+// count the tests pin).
 template <int NB, bool GEMV, int CH = NB, int PC = 2>
 struct UmmaLayout {
     static_assert(NB % CH == 0 && CH % 2 == 0, "chunks are whole rank-16 steps");
