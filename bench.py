@@ -253,12 +253,12 @@ def main():
         torch.cuda.synchronize()
 
     max_seq = args.context + 3 * (args.steps + args.warmup) + 64
-    def build_engine(tp_push):
+    def build_engine(tp_push, peers=None):
         c = llama.preset(args.workload, tp_size=world, tp_rank=rank, max_seq=max_seq, switch_mode=args.switch_mode,
                          compute=args.compute, keep_pristine=True, forward_mode=args.forward_mode, chain=not args.no_chain,
                          attn_splits=args.attn_splits, refresh_every=args.refresh_every, persistent_forward=args.persistent_forward,
                          tp_push=tp_push)
-        return c, llama.LlamaEngine(c, init="device")
+        return c, llama.LlamaEngine(c, init="device", peers=peers)
 
     # N > 1: the row-parallel sums are pushed into the peers' accumulators from the GEMV epilogue (LlamaConfig.tp_push:
     # torch symmetric memory over NVLink) when the ranks can map each other's buffers -- probed with two eager steps on
@@ -267,10 +267,22 @@ def main():
     eng = None
     if world > 1:
         tp_collective = "nccl all-reduce"
-        if backend == "nccl" and os.environ.get("AF_TP_PUSH", "1") != "0" and args.forward_mode != "separate" and not args.no_chain:
+        # (AF_TP_PUSH=1 forces the probe on any backend: the one-GPU rehearsal uses it to walk this very code)
+        push_env = os.environ.get("AF_TP_PUSH", "auto")
+        if (backend == "nccl" or push_env == "1") and push_env != "0" and args.forward_mode != "separate" and not args.no_chain:
             ok = 1
             try:
-                cfg, eng = build_engine(True)
+                try:
+                    cfg, eng = build_engine(True)                      # the ranks' buffers in torch symmetric memory
+                    tp_how = "torch symmetric memory"
+                except RuntimeError:
+                    # one node: CUDA IPC handles over the process group instead (also what maps two ranks that share a
+                    # GPU, which symmetric memory refuses -- the one-GPU rehearsal)
+                    if int(os.environ.get("LOCAL_WORLD_SIZE", "0")) != world:
+                        raise
+                    dev_ = torch.device("cuda", local_rank)
+                    cfg, eng = build_engine(True, peers=lambda n: llama.PeerBuffer.ipc(n, dev_))
+                    tp_how = "CUDA IPC"
                 eng.reset(forced=[1, 2, 3, 4])
                 for _ in range(2):
                     eng.decode_step(graph=False)
@@ -281,7 +293,7 @@ def main():
             flag = torch.tensor([ok], device="cuda")
             dist.all_reduce(flag, op=dist.ReduceOp.MIN)
             if int(flag.item()) == 1:
-                tp_collective = "pushed from the GEMV epilogue (peer memory)"
+                tp_collective = f"pushed from the GEMV epilogue (peer memory: {tp_how})"
             else:
                 eng = None
                 torch.cuda.empty_cache()

@@ -386,7 +386,7 @@ int af_switch_gemv_chain(af_group* group, const af_decision* prev_dev, const af_
 /* ---- tensor parallelism without a collective between the launches ----------------------------
  * No reference counterpart (the reference is single-process; BASELINE configs[3..4] name TP 2 / 4 / 8).
  * Every rank maps one buffer holding the fixed-point accumulators and phase counters of every other rank
- * (NVLink peer memory: torch symmetric memory / CUDA IPC on the host side) at own address + peer_offset_bytes[w];
+ * (NVLink peer memory: torch symmetric memory or CUDA IPC handles on the host side, `llama.PeerBuffer`) at own address + peer_offset_bytes[w];
  * the list includes the rank itself (offset 0) and has the same ORDER on every rank only by convention -- the
  * kernels never use the index.  af_group_set_peers marks the row-parallel phases of a chain (bit ph of
  * reduce_phase_mask: o and down): a marked phase adds its partial sums into EVERY rank's acc_out with system-scope

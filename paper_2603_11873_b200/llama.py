@@ -269,6 +269,34 @@ class PeerBuffer:
         return cls(t, [p - ptrs[hdl.rank] for p in ptrs], keep=hdl)
 
 
+def _ipc_peer_buffer(cls, n_words: int, device, group=None):
+    import torch.distributed as dist
+
+    t = torch.zeros(n_words, dtype=torch.int64, device=device)
+    meta = t.untyped_storage()._share_cuda_()          # cudaIpcGetMemHandle of the block + this storage's offset in it
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    metas = [None] * world
+    dist.all_gather_object(metas, meta, group=group)
+    views, offsets = [], []
+    for w, m in enumerate(metas):
+        if w == rank:
+            offsets.append(0)
+            continue
+        storage = torch.UntypedStorage._new_shared_cuda(*m)     # cudaIpcOpenMemHandle (peer access enabled lazily)
+        view = torch.empty(0, dtype=torch.int64, device=device).set_(storage)
+        views.append(view)
+        offsets.append(view.data_ptr() - t.data_ptr())
+    torch.cuda.synchronize(device)
+    dist.barrier(group=group)                          # every region exists, is zeroed and is mapped everywhere
+    return cls(t, offsets, keep=views)
+
+
+PeerBuffer.ipc = classmethod(_ipc_peer_buffer)
+PeerBuffer.ipc.__func__.__doc__ = """One buffer per rank of `group`, mapped by the other ranks through CUDA IPC handles exchanged over the
+process group (any backend): the ranks of one node -- on different GPUs with peer access, or, for tests, on the SAME
+GPU, which torch symmetric memory refuses.  A collective call."""
+
+
 class Collectives:
     """torch.distributed plumbing of the TP path.  With tp_size == 1 every method is a no-op."""
 
@@ -506,8 +534,12 @@ class LlamaEngine:
             if want_push and push_ok:
                 try:
                     # (+ 2 words behind the arena: the token barrier's counter, which is never zeroed)
-                    self.peer_buf = peers(arena_words + 2) if peers is not None else (
-                        PeerBuffer.symmetric(arena_words + 2, dev, group) if cfg.tp_size > 1 else PeerBuffer.local(arena_words + 2, dev))
+                    if peers is not None:
+                        self.peer_buf = peers(arena_words + 2)
+                    elif cfg.tp_size == 1:
+                        self.peer_buf = PeerBuffer.local(arena_words + 2, dev)
+                    else:
+                        self.peer_buf = PeerBuffer.symmetric(arena_words + 2, dev, group)
                     # (a one-entry list on a TP shard: the shard runs ALONE -- scripts/bench_shard.py times a rank's step that way)
                     if len(self.peer_buf.offsets) not in (1, cfg.tp_size) or self.peer_buf.tensor.numel() < arena_words + 2:
                         raise ConfigError(f"the peer buffer maps {len(self.peer_buf.offsets)} rank(s) for tp_size {cfg.tp_size}, "

@@ -2,7 +2,9 @@
 `python -m torch.distributed.run --nproc-per-node TP`, one process per rank.  Every rank sits on cuda:0
 (the test box has one GPU) and the process group is gloo, so the engine's real exchange layer
 (`llama.Collectives` on torch.distributed: decision broadcast, int64/f32 all-reduces, argmax all-gather)
-carries the calls between PROCESSES; on a multi-GPU box the same calls go over NCCL."""
+carries the calls between PROCESSES; on a multi-GPU box the same calls go over NCCL.  Mode "push": no all-reduce calls at
+all inside the layers -- each rank's chained launches add their partial sums into the other PROCESS's accumulators through a
+CUDA IPC mapping (`llama.PeerBuffer.ipc`) and wait on cross-process phase counters; the two contexts time-slice one GPU."""
 
 import os
 import sys
@@ -22,8 +24,12 @@ def main():
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
     forced = np.random.Generator(np.random.PCG64(31)).integers(0, 512, 8)
-    cfg = llama.preset("tiny", tp_size=world, tp_rank=rank, forward_mode=forward_mode, max_seq=16, n_heads=4, n_kv_heads=4)
-    eng = llama.LlamaEngine(cfg, init="host")
+    push = forward_mode == "push"      # the chase schedule with the all-reduce pushed from the epilogues over CUDA IPC mappings
+    cfg = llama.preset("tiny", tp_size=world, tp_rank=rank, forward_mode="chase" if push else forward_mode, max_seq=16, n_heads=4,
+                       n_kv_heads=4, tp_push=True if push else False)
+    dev = torch.device("cuda", 0)
+    eng = llama.LlamaEngine(cfg, init="host", peers=(lambda n: llama.PeerBuffer.ipc(n, dev)) if push else None)
+    assert getattr(eng, "tp_push", False) == push and bool(getattr(eng, "chase_chained", False)) == push
     eng.reset(forced=forced)
     tokens, logits = [], []
     for _ in range(len(forced)):

@@ -448,11 +448,14 @@ def test_switch_in_passes_for_more_than_64_stacked_ranks(llama, switch_mode, for
 
 
 
-@pytest.mark.parametrize("forward_mode", ["separate", "chase"])
+@pytest.mark.parametrize("forward_mode", ["separate", "chase", "push"])
 def test_tp_two_processes_over_torch_distributed(llama, forward_mode, tmp_path):
     """The lockstep test above with real processes and the engine's own exchange layer: two ranks launched
     by torch.distributed.run, `llama.Collectives` over a gloo group (both ranks on cuda:0 — one GPU here;
-    NCCL carries the same calls on a multi-GPU box), decode the unsharded engine's tokens."""
+    NCCL carries the same calls on a multi-GPU box), decode the unsharded engine's tokens.  "push": the chase schedule with
+    `tp_push` -- no all-reduce inside the layers; each rank's chained launches add their partial sums into the other
+    PROCESS's accumulators through CUDA IPC mappings and wait on cross-process phase counters (two contexts time-slicing
+    one GPU: slow, but the real cross-process path -- handles, offsets, system-scope atomics, the token barrier)."""
     import os
     import socket
     import subprocess
