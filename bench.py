@@ -392,7 +392,7 @@ def main():
 
     kernel_name = _capi.lib().af_last_switch_kernel().decode()
     # ---------------- (2) value: inputs resident, the step replayed as one CUDA graph ----
-    graph_ok = world == 1 or os.environ.get("AF_TP_GRAPH") == "1"   # TP capture is opt-in (llama.LlamaEngine.capture)
+    graph_ok = eng.graph_ok()   # one rank, the push step (no library collective inside), or AF_TP_GRAPH=1 (llama.LlamaEngine.graph_ok)
     eng.set_position(args.context)
     if graph_ok:
         eng.capture()
@@ -418,7 +418,8 @@ def main():
         eng.forward()
         eng._advance()
 
-    if graph_ok:
+    # (the adapter-free forward of a TP engine still ends its row-parallel GEMVs in library all-reduces: eager unless opted in)
+    if world == 1 or os.environ.get("AF_TP_GRAPH") == "1":
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())

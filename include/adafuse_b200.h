@@ -402,6 +402,20 @@ int af_group_set_peers(af_group* group, int32_t n_peers, const int64_t* peer_off
  * this rank's; *epoch_dev (device-resident, zero-initialised, private to the rank) counts the barriers so far. */
 int af_peer_barrier(int32_t* counter_dev, int32_t* epoch_dev, int32_t n_peers, const int64_t* peer_offset_bytes,
                     int32_t* err_flag_dev, void* stream);
+/* The two exchanges of a tensor-parallel token that are not sums, over the same peer mappings, so that a step holds no
+ * library collective (and captures as a CUDA graph without one):
+ * af_peer_bcast  -- rank 0's decision record (`llama.Collectives.broadcast_decision`; SURVEY.md 8b `af_bcast_decision`):
+ *    the root (is_root != 0) copies `bytes` from src_dev into slot_dev of EVERY rank and bumps every rank's counter; each
+ *    rank waits until its counter has reached its own number of broadcasts so far (*epoch_dev) and copies its slot to dst_dev.
+ * af_peer_argmax -- the vocab-parallel argmax (model.py:396 over the ranks' lm_head slices): every rank writes its
+ *    (value, index) pair into slot my_slot of every rank's slots_dev (n_peers 8-byte words), bumps every rank's counter,
+ *    waits for the n pairs of this round and writes the index of the largest value (lowest index on ties) to out_idx_dev.
+ * slot_dev / slots_dev / counter_dev live in the mapped buffer, each call kind with its own counter and epoch word. */
+int af_peer_bcast(const void* src_dev, void* slot_dev, void* dst_dev, int32_t bytes, int32_t is_root, int32_t* counter_dev,
+                  int32_t* epoch_dev, int32_t n_peers, const int64_t* peer_offset_bytes, int32_t* err_flag_dev, void* stream);
+int af_peer_argmax(const float* val_dev, const int32_t* idx_dev, void* slots_dev, int32_t my_slot, int32_t* counter_dev,
+                   int32_t* epoch_dev, int32_t n_peers, const int64_t* peer_offset_bytes, int32_t* out_idx_dev,
+                   int32_t* err_flag_dev, void* stream);
 /* Stream-ordered wait until *counter_dev >= target (system-scope acquire); ~2 s -> AF_ECUDA in *err_flag_dev. */
 int af_peer_wait(const int32_t* counter_dev, int32_t target, int32_t* err_flag_dev, void* stream);
 /* adapters.py:188-233 (`concat_gated` + `build_switch` bookkeeping) once per token: turns the two

@@ -181,6 +181,8 @@ SIGNATURES = {
     "af_group_set_peers": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_int64), _i32]),
     "af_peer_barrier": (ctypes.c_int, [_vp, _vp, _i32, ctypes.POINTER(ctypes.c_int64), _vp, _vp]),
     "af_peer_wait": (ctypes.c_int, [_vp, _i32, _vp, _vp]),
+    "af_peer_bcast": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32, ctypes.POINTER(ctypes.c_int64), _vp, _vp]),
+    "af_peer_argmax": (ctypes.c_int, [_vp, _vp, _vp, _i32, _vp, _vp, _i32, ctypes.POINTER(ctypes.c_int64), _vp, _vp, _vp]),
     "af_attn_decode_fix": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 AF_FIX_SHIFT = 40

@@ -634,3 +634,28 @@ def peer_barrier(counter: torch.Tensor, epoch: torch.Tensor, peer_offsets, err_f
 def peer_wait(counter: torch.Tensor, target: int, err_flag: torch.Tensor | None = None) -> None:
     """`af_peer_wait`: the stream waits until the counter the peers bump has reached `target`."""
     _capi.check(_capi.lib().af_peer_wait(_ptr(counter), int(target), _ptr(err_flag) if err_flag is not None else None, _capi.stream_ptr()))
+
+
+def peer_bcast(src, slot: torch.Tensor, dst: torch.Tensor, is_root: bool, counter: torch.Tensor, epoch: torch.Tensor, peer_offsets,
+               err_flag: torch.Tensor | None = None) -> None:
+    """`af_peer_bcast`: the root's record (`src`, same byte size as `dst`) lands in `slot` of every rank and is copied to
+    `dst` on every rank -- rank 0's decision of the token, without a library collective."""
+    import ctypes
+
+    offs = [int(o) for o in peer_offsets]
+    arr = (ctypes.c_int64 * len(offs))(*offs)
+    nbytes = dst.numel() * dst.element_size()
+    _capi.check(_capi.lib().af_peer_bcast(_ptr(src) if src is not None else None, _ptr(slot), _ptr(dst), nbytes, 1 if is_root else 0,
+                                          _ptr(counter), _ptr(epoch), len(offs), arr, _ptr(err_flag) if err_flag is not None else None,
+                                          _capi.stream_ptr()))
+
+
+def peer_argmax(val: torch.Tensor, idx: torch.Tensor, slots: torch.Tensor, my_slot: int, counter: torch.Tensor, epoch: torch.Tensor,
+                peer_offsets, out_idx: torch.Tensor, err_flag: torch.Tensor | None = None) -> None:
+    """`af_peer_argmax`: every rank's (value, index) pair to every rank; the largest value wins, the lowest index on ties."""
+    import ctypes
+
+    offs = [int(o) for o in peer_offsets]
+    arr = (ctypes.c_int64 * len(offs))(*offs)
+    _capi.check(_capi.lib().af_peer_argmax(_ptr(val), _ptr(idx), _ptr(slots), int(my_slot), _ptr(counter), _ptr(epoch), len(offs), arr,
+                                           _ptr(out_idx), _ptr(err_flag) if err_flag is not None else None, _capi.stream_ptr()))

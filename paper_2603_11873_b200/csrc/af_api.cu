@@ -1177,6 +1177,34 @@ int af_peer_barrier(int32_t* counter_dev, int32_t* epoch_dev, int32_t n_peers, c
     return AF_OK;
 }
 
+int af_peer_bcast(const void* src_dev, void* slot_dev, void* dst_dev, int32_t bytes, int32_t is_root, int32_t* counter_dev,
+                  int32_t* epoch_dev, int32_t n_peers, const int64_t* peer_offset_bytes, int32_t* err_flag_dev, void* stream) {
+    if (!slot_dev || !dst_dev || !counter_dev || !epoch_dev || (is_root && !src_dev)) return fail(AF_EVALUE, "NULL argument");
+    if (bytes < 4 || bytes > 4096 || bytes % 4 != 0) return fail(AF_EDIM, "a broadcast record is 4 .. 4096 bytes, a multiple of 4");
+    PeerList pl{};
+    if (int rc = peer_list(n_peers, peer_offset_bytes, pl)) return rc;
+    peer_bcast_kernel<<<1, 128, 0, as_stream(stream)>>>(static_cast<const uint32_t*>(src_dev), static_cast<uint32_t*>(slot_dev),
+                                                         static_cast<uint32_t*>(dst_dev), bytes / 4, is_root ? 1 : 0, counter_dev, epoch_dev, pl,
+                                                         err_flag_dev);
+    AF_LAUNCH_CHECK("peer_bcast_kernel");
+    return AF_OK;
+}
+
+int af_peer_argmax(const float* val_dev, const int32_t* idx_dev, void* slots_dev, int32_t my_slot, int32_t* counter_dev, int32_t* epoch_dev,
+                   int32_t n_peers, const int64_t* peer_offset_bytes, int32_t* out_idx_dev, int32_t* err_flag_dev, void* stream) {
+    if (!val_dev || !idx_dev || !slots_dev || !counter_dev || !epoch_dev || !out_idx_dev) return fail(AF_EVALUE, "NULL argument");
+    if (reinterpret_cast<uintptr_t>(slots_dev) % 8 != 0) return fail(AF_EDIM, "the pair slots are 8-byte words");
+    PeerList pl{};
+    if (int rc = peer_list(n_peers, peer_offset_bytes, pl)) return rc;
+    if (my_slot < 0 || my_slot >= n_peers) return fail(AF_EVALUE, "my_slot outside [0, n_peers)");
+    for (int w = 0; w < n_peers; ++w)
+        if (pl.off[w] % 8 != 0) return fail(AF_EDIM, "peer offsets must keep the 8-byte alignment of the pair slots");
+    peer_argmax_kernel<<<1, 32, 0, as_stream(stream)>>>(val_dev, idx_dev, static_cast<unsigned long long*>(slots_dev), my_slot, counter_dev,
+                                                        epoch_dev, pl, out_idx_dev, err_flag_dev);
+    AF_LAUNCH_CHECK("peer_argmax_kernel");
+    return AF_OK;
+}
+
 int af_peer_wait(const int32_t* counter_dev, int32_t target, int32_t* err_flag_dev, void* stream) {
     if (!counter_dev) return fail(AF_EVALUE, "counter is NULL");
     peer_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(counter_dev, target, err_flag_dev);

@@ -5,7 +5,9 @@
 //   * af_peer_barrier : once per token, after a rank has zeroed its accumulators and before anybody may push into
 //     them -- a monotonic counter (never reset, so there is no reset race) that every rank bumps on every rank;
 //   * af_peer_wait    : a stream-ordered wait for a counter the peers bump (the last phase of the last layer has
-//     no consumer inside its own launch).
+//     no consumer inside its own launch);
+//   * af_peer_bcast / af_peer_argmax : the two small exchanges of a token that are not sums -- rank 0's decision record
+//     and the vocab-parallel argmax -- so that a tensor-parallel step contains no library collective at all.
 // Both are one thread spinning with system-scope acquire loads; a wait of ~2 s raises AF_ECUDA in *err_flag
 // instead of hanging (a rank that died, or ranks whose launches disagree).
 #pragma once
@@ -44,6 +46,62 @@ __global__ void peer_barrier_kernel(int* counter, int* epoch_dev, PeerList peers
 __global__ void peer_wait_kernel(const int* counter, int target, int* err_flag) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     peer_spin_until(counter, target, err_flag);
+}
+
+// af_peer_bcast: the root writes `words` 32-bit words into `slot` of EVERY rank (its own included), then bumps every
+// rank's counter; each rank waits for its counter to reach its own count of broadcasts so far and copies the slot out.
+// (The 128-byte decision record of the switch path: llama.Collectives.broadcast_decision without a library call.)
+__global__ void peer_bcast_kernel(const uint32_t* src, uint32_t* slot, uint32_t* dst, int words, int is_root, int* counter, int* epoch_dev,
+                                  PeerList peers, int* err_flag) {
+    const int tid = threadIdx.x;
+    if (is_root) {
+        for (int w = 0; w < peers.n; ++w) {
+            volatile uint32_t* s = reinterpret_cast<volatile uint32_t*>(reinterpret_cast<char*>(slot) + peers.off[w]);
+            for (int i = tid; i < words; i += blockDim.x) s[i] = src[i];
+        }
+        __threadfence_system();
+    }
+    __syncthreads();
+    __shared__ int ok;
+    if (tid == 0) {
+        const int epoch = *epoch_dev + 1;
+        *epoch_dev = epoch;
+        if (is_root)
+            for (int w = 0; w < peers.n; ++w) atomicAdd_system(reinterpret_cast<int*>(reinterpret_cast<char*>(counter) + peers.off[w]), 1);
+        ok = peer_spin_until(counter, epoch, err_flag) ? 1 : 0;
+    }
+    __syncthreads();
+    if (!ok) return;
+    const volatile uint32_t* s = slot;
+    for (int i = tid; i < words; i += blockDim.x) dst[i] = s[i];
+}
+
+// af_peer_argmax: vocab-parallel argmax (model.py:396 over the ranks' slices).  Every rank writes its (value, index)
+// pair into slot `my_slot` of every rank, bumps every rank's counter, waits for all n pairs of this round and keeps the
+// largest value, the lowest index on ties -- every rank computes the same answer from the same n pairs.
+__global__ void peer_argmax_kernel(const float* val, const int* idx, unsigned long long* slots, int my_slot, int* counter, int* epoch_dev,
+                                   PeerList peers, int* out_idx, int* err_flag) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long pair = ((unsigned long long)__float_as_uint(*val) << 32) | (unsigned int)(*idx);
+    for (int w = 0; w < peers.n; ++w)
+        atomicExch_system(reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(slots + my_slot) + peers.off[w]), pair);
+    __threadfence_system();
+    const int epoch = *epoch_dev + 1;
+    *epoch_dev = epoch;
+    for (int w = 0; w < peers.n; ++w) atomicAdd_system(reinterpret_cast<int*>(reinterpret_cast<char*>(counter) + peers.off[w]), 1);
+    if (!peer_spin_until(counter, (long long)epoch * peers.n, err_flag)) return;
+    float best = 0.f;
+    int best_i = 0;
+    for (int r = 0; r < peers.n; ++r) {
+        const unsigned long long q = *reinterpret_cast<volatile unsigned long long*>(slots + r);
+        const float v = __uint_as_float((unsigned int)(q >> 32));
+        const int i = (int)(unsigned int)q;
+        if (r == 0 || v > best || (v == best && i < best_i)) {
+            best = v;
+            best_i = i;
+        }
+    }
+    *out_idx = best_i;
 }
 
 }  // namespace af

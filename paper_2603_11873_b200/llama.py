@@ -361,6 +361,44 @@ def _on_device(fn):
     return wrapper
 
 
+PEER_TAIL_WORDS = 32     # int64 words behind the accumulator arena in a PeerBuffer: counters, decision slot, argmax slots
+
+
+class PeerCollectives:
+    """The exchanges of a tp_push step that are not sums, over the ranks' peer mappings instead of a library collective
+    (`af_peer_bcast`, `af_peer_argmax`): rank 0's decision record and the vocab-parallel argmax.  With the all-reduces
+    pushed from the GEMV epilogues this leaves a tensor-parallel token without any NCCL call.  Layout of the tail
+    (int64 words): 0 = barrier | bcast counters (int32 each), 1 = gather counter, 2..17 = decision slot, 18..25 = pairs."""
+
+    def __init__(self, tail: torch.Tensor, offsets, rank: int, err_flag: torch.Tensor):
+        if tail.numel() < PEER_TAIL_WORDS:
+            raise DimensionError("the peer buffer's tail is too small")
+        c32 = tail[:2].view(torch.int32)
+        self.barrier_counter, self.bcast_counter, self.gather_counter = c32[0:1], c32[1:2], c32[2:3]
+        self.decision_slot = tail[2: 2 + DECISION_BYTES // 8]
+        self.pair_slots = tail[18: 18 + 8]
+        self.offsets, self.rank, self.err = [int(o) for o in offsets], int(rank), err_flag
+        self.epochs = torch.zeros(4, dtype=torch.int32, device=tail.device)    # barrier, bcast, gather (private, on the device)
+        self.tp_size = len(self.offsets)
+        if self.tp_size > 8:
+            raise DimensionError("at most 8 ranks")
+
+    def barrier(self) -> None:
+        from .adapters import peer_barrier
+        peer_barrier(self.barrier_counter, self.epochs[0:1], self.offsets, self.err)
+
+    def broadcast_decision(self, buf: torch.Tensor) -> None:
+        from .adapters import peer_bcast
+        peer_bcast(buf, self.decision_slot, buf, self.rank == 0, self.bcast_counter, self.epochs[1:2], self.offsets, self.err)
+
+    def argmax_pairs(self, val: torch.Tensor, idx: torch.Tensor, out_idx: torch.Tensor) -> None:
+        from .adapters import peer_argmax
+        peer_argmax(val, idx, self.pair_slots, self.rank, self.gather_counter, self.epochs[2:3], self.offsets, out_idx, self.err)
+
+    def all_reduce_sum(self, t: torch.Tensor) -> None:   # pragma: no cover - the push step has no separate all-reduce
+        raise StateError("tp_push: the sums are pushed from the GEMV epilogues")
+
+
 class LlamaEngine:
     """Resident weights, expert bank, descriptor table, KV cache and the captured decode step."""
 
@@ -377,6 +415,7 @@ class LlamaEngine:
             return
         # `comm` lets a caller supply the exchange layer (tests build one shard with no peers)
         self.comm = comm if comm is not None else Collectives(group, cfg.tp_size)
+        self.step_comm = self.comm          # what the decode step calls; a tp_push engine swaps in PeerCollectives
         self.recorder = DispatchRecorder()
         d, hd = cfg.hidden, cfg.head_dim
         shp = cfg.segment_shapes()
@@ -533,15 +572,16 @@ class LlamaEngine:
                 raise ConfigError("tp_push needs the chained launches on the tcgen05 path (chain=True, umma_path, one-launch switch)")
             if want_push and push_ok:
                 try:
-                    # (+ 2 words behind the arena: the token barrier's counter, which is never zeroed)
+                    # (+ a tail behind the arena that is never zeroed: the counters of the barrier / broadcast / argmax, their slots)
+                    n_buf = arena_words + PEER_TAIL_WORDS
                     if peers is not None:
-                        self.peer_buf = peers(arena_words + 2)
+                        self.peer_buf = peers(n_buf)
                     elif cfg.tp_size == 1:
-                        self.peer_buf = PeerBuffer.local(arena_words + 2, dev)
+                        self.peer_buf = PeerBuffer.local(n_buf, dev)
                     else:
-                        self.peer_buf = PeerBuffer.symmetric(arena_words + 2, dev, group)
+                        self.peer_buf = PeerBuffer.symmetric(n_buf, dev, group)
                     # (a one-entry list on a TP shard: the shard runs ALONE -- scripts/bench_shard.py times a rank's step that way)
-                    if len(self.peer_buf.offsets) not in (1, cfg.tp_size) or self.peer_buf.tensor.numel() < arena_words + 2:
+                    if len(self.peer_buf.offsets) not in (1, cfg.tp_size) or self.peer_buf.tensor.numel() < arena_words + PEER_TAIL_WORDS:
                         raise ConfigError(f"the peer buffer maps {len(self.peer_buf.offsets)} rank(s) for tp_size {cfg.tp_size}, "
                                           "or is smaller than the arena")
                     self.tp_push = True
@@ -573,8 +613,12 @@ class LlamaEngine:
             # one arena, zeroed once per step
             if self.tp_push:
                 self.acc_arena = self.peer_buf.tensor[:arena_words]
-                self.peer_counter = self.peer_buf.tensor[arena_words: arena_words + 1].view(torch.int32)[:1]
-                self.peer_epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.peer_comm = PeerCollectives(self.peer_buf.tensor[arena_words: arena_words + PEER_TAIL_WORDS], self.peer_buf.offsets,
+                                                 cfg.tp_rank if len(self.peer_buf.offsets) > 1 else 0, self.err_dev)
+                self.peer_counter, self.peer_epoch = self.peer_comm.barrier_counter, self.peer_comm.epochs[0:1]
+                # the engine's own exchange layer is replaced too (a caller-supplied `comm` -- tests, a shard timed alone -- stays)
+                if comm is None:
+                    self.step_comm = self.peer_comm
             else:
                 self.acc_arena = torch.zeros(arena_words, dtype=torch.int64, device=dev)
             self.acc = []
@@ -610,7 +654,7 @@ class LlamaEngine:
         if cfg.tp_rank == 0 or cfg.tp_size == 1:
             self._check(L.af_pregate(_ptr(self.router.data), _capi.AF_BF16, cfg.experts, cfg.hidden, _ptr(self.embed.data),
                                      _capi.AF_BF16, _ptr(self.token_dev), cfg.top_k, self.cur.ptr, None, st))
-        self.comm.broadcast_decision(self.cur.buf)
+        self.step_comm.broadcast_decision(self.cur.buf)
         return self.cur
 
     @_on_device
@@ -817,7 +861,7 @@ class LlamaEngine:
                                     _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))
         self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, cfg.tp_rank * self.vocab_local, _ptr(self.next_dev),
                                     _ptr(self.next_val), st))
-        self.comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
+        self.step_comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
 
     def forward_chase(self, with_prev: bool, refresh: bool = False) -> None:
         """Switch AND merged forward of one token in one pass over the weights: each projection's
@@ -842,8 +886,7 @@ class LlamaEngine:
         if self.tp_push:
             # nobody pushes into these accumulators before every rank has zeroed its own (af_peer_barrier: a monotonic
             # counter behind the arena, bumped on every rank by every rank)
-            from .adapters import peer_barrier
-            peer_barrier(self.peer_counter, self.peer_epoch, self.peer_buf.offsets, self.err_dev)
+            self.peer_comm.barrier()
         self._check(L.af_embed(_ptr(self.embed.data), _capi.AF_BF16, d, _ptr(self.token_dev), _ptr(xa), st))
         norm = "rmsnorm_deferred" if self.defer_norm else "rmsnorm"
         # timing experiment only (wrong results): AF_SKIP_ATTN=1 leaves the attention launches out -- how much of the step
@@ -894,7 +937,7 @@ class LlamaEngine:
                                     _capi.AF_PRO_RMSNORM, _ptr(self.final_norm), eps, _capi.AF_EPI_NONE, None, st))
         self._check(L.af_argmax_val(_ptr(self.logits), self.vocab_local, cfg.tp_rank * self.vocab_local, _ptr(self.next_dev),
                                     _ptr(self.next_val), st))
-        self.comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
+        self.step_comm.argmax_pairs(self.next_val, self.next_dev, self.next_dev)
 
     def _advance(self) -> None:
         L, st = _capi.lib(), _capi.stream_ptr()
@@ -993,7 +1036,7 @@ class LlamaEngine:
         refresh = self._refresh_due()
         use_graph = self.auto_graph if graph is None else bool(graph)
         steady = self.have_prev or not self.cfg.adapters or self.cfg.switch_mode == "from_pristine"
-        if use_graph and steady and (self.cfg.tp_size == 1 or os.environ.get("AF_TP_GRAPH") == "1"):
+        if use_graph and steady and self.graph_ok():
             if "steady" not in self._graphs:
                 self.capture()
             self._graphs["refresh" if refresh else "steady"].replay()
@@ -1006,13 +1049,21 @@ class LlamaEngine:
         self._raise_flag(int(self._pin_out_np[1]))
         return int(self._pin_out_np[0])
 
+    def graph_ok(self) -> bool:
+        """May the step be captured as a CUDA graph?  One rank: yes.  Tensor parallel: when the step holds no library
+        collective -- the push step with the engine's own peer exchanges -- or when AF_TP_GRAPH=1 opts torch's NCCL
+        collectives into the capture."""
+        if self.cfg.tp_size == 1 or os.environ.get("AF_TP_GRAPH") == "1":
+            return True
+        return bool(getattr(self, "tp_push", False)) and self.step_comm is getattr(self, "peer_comm", None)
+
     @_on_device
     def capture(self) -> None:
         """Capture the steady-state step (switch with a previous decision) as a CUDA graph -- and, with
         refresh_every, the refreshing step (from-pristine switch of the current decision) as a second one."""
         if not self.have_prev and self.cfg.adapters and self.cfg.switch_mode == "inplace":
             raise StateError("run one eager decode_step first: the steady graph unmerges a previous decision")
-        if self.cfg.tp_size > 1 and os.environ.get("AF_TP_GRAPH") != "1":
+        if not self.graph_ok():
             # torch's NCCL collectives can be captured (each rank captures its own graph after eager warm-up steps
             # have created the communicator); verified here only on a one-rank NCCL group
             # (tests/test_gpu_llama.py::test_tp_step_with_nccl_collectives_captures), hence opt-in

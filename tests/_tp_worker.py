@@ -35,6 +35,9 @@ def main():
     for _ in range(len(forced)):
         tokens.append(int(eng.decode_step()))
         logits.append(eng.logits.float().cpu().numpy().copy())
+    if push:   # no library collective inside the step: the exchanges are the engine's own, and the step replays as a graph
+        assert type(eng.step_comm) is llama.PeerCollectives and eng.graph_ok() and "steady" in eng._graphs
+        assert int(eng.peer_comm.epochs[0].item()) == len(forced) and int(eng.peer_comm.epochs[2].item()) == len(forced)
     eng.finalize()
     dev = float(eng.max_backbone_deviation())
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), tokens=np.asarray(tokens), logits=np.stack(logits), deviation=dev)

@@ -326,3 +326,45 @@ def test_engine_push_over_torch_symmetric_memory():
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_tp_graph_worker.py")
     r = subprocess.run([sys.executable, worker, "push", str(port)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "TP_PUSH_SYMM_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
+
+
+def test_peer_bcast_and_argmax_between_two_streams(af):
+    """`af_peer_bcast` (rank 0's decision record into every rank's slot) and `af_peer_argmax` (every rank's (value, index)
+    pair to every rank; largest value, lowest index on ties) with two streams playing the ranks over two regions of
+    one allocation, three rounds (the counters are monotonic; the epochs live on the device)."""
+    from paper_2603_11873_b200.adapters import peer_argmax, peer_bcast
+
+    tp = 2
+    region = 64                                              # int64 words per rank: counters | 16-word slot | pair slots
+    shared = torch.zeros(tp * region, dtype=torch.int64, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(tp)]
+    epochs = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(tp)]
+    regs = [shared[r * region: (r + 1) * region] for r in range(tp)]
+    offs = [[(q - r) * region * 8 for q in range(tp)] for r in range(tp)]
+    src = torch.zeros(3, 16, dtype=torch.int64, device="cuda")
+    for rnd in range(3):
+        src[rnd] = torch.arange(16, device="cuda") * 7 + rnd * 1000 + 1
+    dst = [torch.zeros(3, 16, dtype=torch.int64, device="cuda") for _ in range(tp)]
+    # round -> (values, indices) per rank; round 1 is a tie in value: the lower index wins
+    vals = [[1.5, 2.5], [3.0, 3.0], [-1.0, -2.0]]
+    idxs = [[7, 300], [400, 9], [5, 600]]
+    want = [300, 9, 5]
+    val_t = [[torch.tensor([vals[rnd][r]], dtype=torch.float32, device="cuda") for r in range(tp)] for rnd in range(3)]
+    idx_t = [[torch.tensor([idxs[rnd][r]], dtype=torch.int32, device="cuda") for r in range(tp)] for rnd in range(3)]
+    out = [torch.zeros(3, dtype=torch.int32, device="cuda") for _ in range(tp)]
+    torch.cuda.synchronize()
+    for rnd in range(3):
+        for r in range(tp):                                  # (calls that wait for each other are enqueued back to back)
+            with torch.cuda.stream(streams[r]):
+                c32 = regs[r][:1].view(torch.int32)
+                peer_bcast(src[rnd] if r == 0 else None, regs[r][2:18], dst[r][rnd], r == 0, c32[0:1], epochs[r][0:1], offs[r])
+        for r in range(tp):
+            with torch.cuda.stream(streams[r]):
+                c32 = regs[r][:1].view(torch.int32)
+                peer_argmax(val_t[rnd][r], idx_t[rnd][r], regs[r][18:26], r, c32[1:2], epochs[r][1:2], offs[r], out[r][rnd: rnd + 1])
+    torch.cuda.synchronize()
+    for r in range(tp):
+        assert torch.equal(dst[r], src), r
+        assert out[r].tolist() == want, (r, out[r].tolist())
+        assert epochs[r].tolist() == [3, 3]
+        assert regs[r][:1].view(torch.int32).tolist() == [3, 3 * tp]     # one bump per broadcast (the root's), tp per gather

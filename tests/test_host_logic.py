@@ -346,3 +346,5 @@ def test_peer_buffer_contract_and_peer_calls_validate_without_a_device():
     assert L.af_group_set_peers(None, 2, offs, 1) == _capi.AF_EVALUE             # no group
     assert L.af_peer_barrier(None, None, 2, offs, None, None) == _capi.AF_EVALUE
     assert L.af_peer_wait(None, 1, None, None) == _capi.AF_EVALUE
+    assert L.af_peer_bcast(None, None, None, 128, 1, None, None, 2, offs, None, None) == _capi.AF_EVALUE
+    assert L.af_peer_argmax(None, None, None, 0, None, None, 2, offs, None, None, None) == _capi.AF_EVALUE
