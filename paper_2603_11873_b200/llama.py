@@ -268,33 +268,30 @@ class PeerBuffer:
         dist.barrier(group=group)                      # every region is zeroed before anybody pushes into it
         return cls(t, [p - ptrs[hdl.rank] for p in ptrs], keep=hdl)
 
+    @classmethod
+    def ipc(cls, n_words: int, device, group=None) -> "PeerBuffer":
+        """One buffer per rank of `group`, mapped by the other ranks through CUDA IPC handles exchanged over the process
+        group (any backend): the ranks of one node -- on different GPUs with peer access, or, for tests, on the SAME
+        GPU, which torch symmetric memory refuses.  A collective call."""
+        import torch.distributed as dist
 
-def _ipc_peer_buffer(cls, n_words: int, device, group=None):
-    import torch.distributed as dist
-
-    t = torch.zeros(n_words, dtype=torch.int64, device=device)
-    meta = t.untyped_storage()._share_cuda_()          # cudaIpcGetMemHandle of the block + this storage's offset in it
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    metas = [None] * world
-    dist.all_gather_object(metas, meta, group=group)
-    views, offsets = [], []
-    for w, m in enumerate(metas):
-        if w == rank:
-            offsets.append(0)
-            continue
-        storage = torch.UntypedStorage._new_shared_cuda(*m)     # cudaIpcOpenMemHandle (peer access enabled lazily)
-        view = torch.empty(0, dtype=torch.int64, device=device).set_(storage)
-        views.append(view)
-        offsets.append(view.data_ptr() - t.data_ptr())
-    torch.cuda.synchronize(device)
-    dist.barrier(group=group)                          # every region exists, is zeroed and is mapped everywhere
-    return cls(t, offsets, keep=views)
-
-
-PeerBuffer.ipc = classmethod(_ipc_peer_buffer)
-PeerBuffer.ipc.__func__.__doc__ = """One buffer per rank of `group`, mapped by the other ranks through CUDA IPC handles exchanged over the
-process group (any backend): the ranks of one node -- on different GPUs with peer access, or, for tests, on the SAME
-GPU, which torch symmetric memory refuses.  A collective call."""
+        t = torch.zeros(n_words, dtype=torch.int64, device=device)
+        meta = t.untyped_storage()._share_cuda_()          # cudaIpcGetMemHandle of the block + this storage's offset in it
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        metas = [None] * world
+        dist.all_gather_object(metas, meta, group=group)
+        views, offsets = [], []
+        for w, m in enumerate(metas):
+            if w == rank:
+                offsets.append(0)
+                continue
+            storage = torch.UntypedStorage._new_shared_cuda(*m)     # cudaIpcOpenMemHandle (peer access enabled lazily)
+            view = torch.empty(0, dtype=torch.int64, device=device).set_(storage)
+            views.append(view)
+            offsets.append(view.data_ptr() - t.data_ptr())
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)                          # every region exists, is zeroed and is mapped everywhere
+        return cls(t, offsets, keep=views)
 
 
 class Collectives:
