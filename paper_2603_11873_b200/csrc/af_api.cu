@@ -1027,6 +1027,8 @@ int af_switch_gemv_chain(af_group* g, const af_decision* prev_dev, const af_deci
         return fail(AF_ESTATE, "FROM_PRISTINE needs a pristine copy of every segment");
     if (!phases || n_phases != g->n_phases) return fail(AF_EDIM, "one af_gemv_phase per phase of the chain");
     if (n_phases > 1 && !phase_done_dev) return fail(AF_EVALUE, "a chain of several phases needs its phase_done counters");
+    if (g->n_peers > 0 && ((g->reduce_mask >> (n_phases - 1)) & 1) && !phase_done_dev)
+        return fail(AF_EVALUE, "a last phase that is pushed to the peers reports on phase_done[n_phases - 1]: counters needed");
     for (int ph = 0; ph < n_phases; ++ph) {
         const af_gemv_phase& f = phases[ph];
         if (f.prologue < AF_PRO_NONE || f.prologue > AF_PRO_RMSNORM_DEFERRED) return fail(AF_EVALUE, "unknown prologue");

@@ -368,3 +368,23 @@ def test_peer_bcast_and_argmax_between_two_streams(af):
         assert out[r].tolist() == want, (r, out[r].tolist())
         assert epochs[r].tolist() == [3, 3]
         assert regs[r][:1].view(torch.int32).tolist() == [3, 3 * tp]     # one bump per broadcast (the root's), tp per gather
+
+
+def test_single_phase_group_with_peers_needs_its_counter(af):
+    """A one-projection group whose only phase is pushed to the peers reports on phase_done[0]; without counters the
+    launch is refused before anything runs."""
+    from paper_2603_11873_b200.adapters import SegmentGroup
+
+    shapes, w, down, up = _full_model(seed=14)
+    tg, tab = _table(w, down, up)
+    grp = SegmentGroup(tab, [0])
+    grp.set_peers([0], reduce_phases=[0])
+    acc = torch.zeros(D, dtype=torch.int64, device="cuda")
+    x = torch.ones(D, device="cuda")
+    cur = _decision((1, 2), (0.5, 0.5))
+    with pytest.raises(Exception):
+        grp.switch_gemv(None, cur, acc, xin=x, max_k=2)                     # no counters at all
+    done = torch.zeros(1, dtype=torch.int32, device="cuda")
+    grp.switch_gemv_chain(None, cur, [dict(acc_out=acc, xin=x)], done, max_k=2)
+    tab.status()
+    assert done.item() == grp.grid and float(acc.abs().max()) > 0
