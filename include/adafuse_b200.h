@@ -416,7 +416,9 @@ int af_peer_bcast(const void* src_dev, void* slot_dev, void* dst_dev, int32_t by
 int af_peer_argmax(const float* val_dev, const int32_t* idx_dev, void* slots_dev, int32_t my_slot, int32_t* counter_dev,
                    int32_t* epoch_dev, int32_t n_peers, const int64_t* peer_offset_bytes, int32_t* out_idx_dev,
                    int32_t* err_flag_dev, void* stream);
-/* Stream-ordered wait until *counter_dev >= target (system-scope acquire); ~2 s -> AF_ECUDA in *err_flag_dev. */
+/* Stream-ordered wait until *counter_dev >= target (system-scope acquire); ~2 s -> AF_ECUDA in *err_flag_dev.  Every
+ * cross-rank wait of the library (this one, af_peer_barrier / _bcast / _argmax, the phase barriers of a launch with
+ * peers) gives up after ~2 ms once *err_flag_dev is already non-zero: a dead rank fails the step in seconds. */
 int af_peer_wait(const int32_t* counter_dev, int32_t target, int32_t* err_flag_dev, void* stream);
 /* adapters.py:188-233 (`concat_gated` + `build_switch` bookkeeping) once per token: turns the two
  * device decisions into the table's block list (experts present on both sides collapse to one block

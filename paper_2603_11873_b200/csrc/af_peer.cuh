@@ -26,10 +26,13 @@ __device__ __forceinline__ bool peer_spin_until(const int* counter, long long ta
     do {
         asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
         if ((long long)seen >= target) return true;
-        if (clock64() - t0 > (1ll << 32)) {
+        const long long waited = clock64() - t0;
+        if (waited > (1ll << 32)) {
             if (err_flag) atomicExch(err_flag, AF_ECUDA);
             return false;
         }
+        // an error already raised (an earlier timeout) ends later waits after ~2 ms instead of ~2 s each
+        if (waited > (1ll << 22) && err_flag && *reinterpret_cast<volatile int*>(err_flag) != 0) return false;
     } while (true);
 }
 

@@ -700,10 +700,14 @@ __global__ void __launch_bounds__(kUThreads, 1) switch_umma_kernel(const __grid_
                                 else
                                     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(mp.phase_done + ph - 1) : "memory");
                                 if (seen >= target) break;
-                                if (clock64() - t0 > (1ll << 32)) {
+                                const long long waited = clock64() - t0;
+                                if (waited > (1ll << 32)) {
                                     if (p.err_flag) atomicExch(p.err_flag, AF_ECUDA);
                                     break;
                                 }
+                                // (an error already raised -- an earlier launch's timeout, a rank that gave up -- ends later waits
+                                //  after ~2 ms instead of ~2 s each: a dead peer fails the step in seconds, not minutes)
+                                if (waited > (1ll << 22) && p.err_flag && *reinterpret_cast<volatile int*>(p.err_flag) != 0) break;
                             } while (true);
                         }
                         named_bar_sync(1, kUEpi);

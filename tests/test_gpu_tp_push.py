@@ -217,8 +217,8 @@ def test_last_phase_reduced_needs_its_own_counter_and_wait(af):
 
 def test_peer_barrier_between_two_streams(af):
     """`af_peer_barrier`: a monotonic counter every rank bumps on every rank; round k completes when the own counter
-    has reached k * n_peers.  Two streams play the ranks; a rank that is alone times out with an error flag instead of
-    hanging -- not exercised here (2 s), only the happy path over several rounds."""
+    has reached k * n_peers.  Two streams play the ranks, several rounds (the time-out of a rank left alone:
+    test_a_missing_peer_times_out_and_later_waits_fail_fast)."""
     from paper_2603_11873_b200.adapters import peer_barrier
 
     tp = 2
@@ -388,3 +388,30 @@ def test_single_phase_group_with_peers_needs_its_counter(af):
     grp.switch_gemv_chain(None, cur, [dict(acc_out=acc, xin=x)], done, max_k=2)
     tab.status()
     assert done.item() == grp.grid and float(acc.abs().max()) > 0
+
+
+def test_a_missing_peer_times_out_and_later_waits_fail_fast(af):
+    """A wait for a peer that never arrives raises AF_ECUDA in the caller's status word after ~2 s instead of hanging; with
+    the word already set, later waits give up after ~2 ms each -- a dead rank fails a step in seconds, not minutes."""
+    import time
+
+    from paper_2603_11873_b200 import _capi
+    from paper_2603_11873_b200.adapters import peer_barrier, peer_wait
+
+    counter = torch.zeros(2, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    t0 = time.time()
+    peer_wait(counter[0:1], 1, err)                              # nobody bumps it
+    torch.cuda.synchronize()
+    first = time.time() - t0
+    assert err.item() == _capi.AF_ECUDA and 1.0 < first < 10.0, (err.item(), first)
+    t0 = time.time()
+    for _ in range(20):
+        peer_wait(counter[0:1], 1, err)
+    epoch = torch.zeros(1, dtype=torch.int32, device="cuda")
+    peer_barrier(counter[1:2], epoch, [0, 8], err)               # a "second rank" (the next word) that never joins
+    torch.cuda.synchronize()
+    later = time.time() - t0
+    assert later < 1.0, later
+    assert counter[1].item() == 1 and epoch.item() == 1          # this rank did its part of the barrier
