@@ -5,7 +5,7 @@
 // spend ~130 instructions per warp and 16 KB tile feeding the tensor pipe (ldmatrix of UP, B
 // fragments in registers, 16 HMMA, fragment bookkeeping) -- 0.8 us per tile against 0.72 us of HBM
 // time.  Here the product  D[128 x 128] = U[128 x 8 n_blocks] . (hi + lo)(g A)[8 n_blocks x 128]  is
-// 2 * ceil(n_blocks / 2) tcgen05.mma instructions from one thread, straight from shared memory:
+// 2 * ceil(n_blocks / 2) tcgen05.mma instructions from one warp (an elected lane), straight from shared memory:
 //   A = the UP ring as it is loaded -- one expert block (128 rows x 8 ranks) is a contiguous
 //       [128][16 B] slab = one K-chunk of the K-major no-swizzle canonical layout (LBO = slab
 //       stride, SBO = 128 B);
