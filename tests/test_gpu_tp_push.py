@@ -405,7 +405,8 @@ def test_a_missing_peer_times_out_and_later_waits_fail_fast(af):
     peer_wait(counter[0:1], 1, err)                              # nobody bumps it
     torch.cuda.synchronize()
     first = time.time() - t0
-    assert err.item() == _capi.AF_ECUDA and 1.0 < first < 10.0, (err.item(), first)
+    # (2^32 SM cycles: 2.2 s at 1965 MHz, longer if the clocks have not ramped up for a one-thread kernel)
+    assert err.item() == _capi.AF_ECUDA and 1.0 < first < 90.0, (err.item(), first)
     t0 = time.time()
     for _ in range(20):
         peer_wait(counter[0:1], 1, err)
@@ -413,5 +414,5 @@ def test_a_missing_peer_times_out_and_later_waits_fail_fast(af):
     peer_barrier(counter[1:2], epoch, [0, 8], err)               # a "second rank" (the next word) that never joins
     torch.cuda.synchronize()
     later = time.time() - t0
-    assert later < 1.0, later
+    assert later < max(1.0, first / 2), (later, first)            # 21 waits of ~2 ms (2^22 cycles) each, not 21 time-outs
     assert counter[1].item() == 1 and epoch.item() == 1          # this rank did its part of the barrier
